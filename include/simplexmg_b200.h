@@ -1,0 +1,153 @@
+/*
+ * simplexmg_b200.h -- C-ABI of the B200-native combined-smoother hot path.
+ *
+ * A drop-in for the compiled arithmetic the reference (`simplexmg`, arXiv
+ * 2402.12947; paths relative to /root/reference/pkg/src/simplexmg) reaches on
+ * its V-cycle hot path.  The reference is pure Python over scipy/LAPACK and has
+ * no FFI of its own; each entry point below names the reference function it
+ * replaces, and INTEGRATION.md shows the ctypes binding a maintainer adds.
+ *
+ * Conventions
+ *   - Plain C types only.  Matrices enter as HOST arrays in the reference's
+ *     canonical CSR layout (int64 row offsets and column indices, float64
+ *     values; sparse.py:47-84); the library keeps its own device copies.
+ *   - Vectors are DEVICE pointers (float64) unless the name ends in _host.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - Every call returns SMG_OK or an error code; smg_last_error() gives the
+ *     message (thread-local).  Error codes map onto the reference's typed
+ *     exceptions (sparse.py:23-44, smoothers.py:27-30).
+ *   - No CPU fallback: every compute entry point launches sm_100a kernels.
+ */
+#ifndef SIMPLEXMG_B200_H
+#define SIMPLEXMG_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SMG_API __attribute__((visibility("default")))
+#else
+#define SMG_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SMG_ABI_VERSION 1
+
+#define SMG_OK 0
+#define SMG_ERR_INVALID 1        /* ValueError (bad arguments / layout)               */
+#define SMG_ERR_DIMENSION 2      /* ValueError "dimension mismatch" (sparse.py:139)   */
+#define SMG_ERR_CUDA 3           /* RuntimeError from the CUDA runtime                */
+#define SMG_ERR_ZERO_DIAGONAL 4  /* ZeroDiagonalError(row) (smoothers.py:112-114)     */
+#define SMG_ERR_INDEFINITE 5     /* IndefiniteOperatorError (sparse.py:199-200)       */
+#define SMG_ERR_UNSUPPORTED 6    /* NotImplementedError (e.g. SGS smoother)           */
+
+/* smoother kinds (smoothers.py:33-59).  SMG_SMOOTHER_CHEBYSHEV with
+ * lambda_min_fraction == 1 is the reference's damped-Jacobi branch
+ * (smoothers.py:120-124; omega = 1/lambda_max). */
+#define SMG_SMOOTHER_CHEBYSHEV 0
+#define SMG_SMOOTHER_SGS 1       /* not on the GPU hot path: SMG_ERR_UNSUPPORTED */
+
+typedef struct smg_operator smg_operator;
+typedef struct smg_correction smg_correction;
+typedef struct smg_hierarchy smg_hierarchy;
+
+SMG_API int smg_abi_version(void);
+SMG_API const char *smg_last_error(void);
+SMG_API int smg_device_info(int *sm_count, int64_t *l2_bytes, int *cc_major, int *cc_minor);
+
+/* ---- operators: CsrMatrix (sparse.py:47-132) ------------------------------
+ * Canonical CSR (sorted, unique columns per row).  with_transpose != 0 also
+ * stores CSR(A^T) so the operator can serve as a prolongation P (restriction
+ * P^T r, mg.py:142). */
+SMG_API int smg_operator_create(int64_t nrows, int64_t ncols, const int64_t *row_offsets,
+                        const int64_t *col_indices, const double *values,
+                        int with_transpose, smg_operator **out);
+SMG_API int smg_operator_destroy(smg_operator *op);
+/* first_zero_diag = first row whose diagonal is 0 or absent, -1 if none */
+SMG_API int smg_operator_info(const smg_operator *op, int64_t *nrows, int64_t *ncols, int64_t *nnz,
+                      int64_t *first_zero_diag, int64_t *device_bytes);
+
+/* y = A x                       (sparse.py:135-140 spmv; bitwise)                */
+SMG_API int smg_spmv(const smg_operator *a, const double *x, double *y, void *stream);
+/* r = b - A u                   (smoothers.py:263,266; mg.py:141; bitwise)       */
+SMG_API int smg_residual(const smg_operator *a, const double *b, const double *u, double *r,
+                 void *stream);
+/* y = P^T r                     (transfer.py:158-162 restrict_residual, mg.py:142;
+ *                                bitwise vs scipy csc_matvec)                     */
+SMG_API int smg_spmv_transpose(const smg_operator *p, const double *r, double *y, void *stream);
+/* u_fine += P u_coarse          (transfer.py:165-172 prolong_add, mg.py:149)     */
+SMG_API int smg_prolong_add(const smg_operator *p, const double *u_coarse, double *u_fine,
+                    void *stream);
+
+/* Chebyshev / damped-Jacobi smoother in place on u (smoothers.py:99-136;
+ * bitwise).  work: 2*n device doubles, or NULL for a library allocation. */
+SMG_API int smg_chebyshev_smooth(const smg_operator *a, const double *b, double *u, int sweeps,
+                         double lambda_max, double lambda_min_fraction, double *work,
+                         void *stream);
+
+/* ---- local correction: LocalCorrection (smoothers.py:139-200) ------------
+ * Region d owns the sorted dofs[region_offsets[d] .. region_offsets[d+1]) and
+ * the dense row-major n_d x n_d array factors[factor_offsets[d] ..] whose
+ * LOWER triangle is the Cholesky factor (scipy cho_factor(lower=True),
+ * sparse.py:248; the upper triangle is ignored).  Regions must be disjoint. */
+SMG_API int smg_correction_create(const smg_operator *a, int64_t n_regions,
+                          const int64_t *region_offsets, const int64_t *dofs,
+                          const int64_t *factor_offsets, const double *factors,
+                          smg_correction **out);
+SMG_API int smg_correction_destroy(smg_correction *c);
+SMG_API int smg_correction_info(const smg_correction *c, int64_t *n_regions, int64_t *covered_dofs,
+                        int *coupled, int64_t *device_bytes);
+/* out = S_c r, zero outside the regions (smoothers.py:203-211)                    */
+SMG_API int smg_apply_local_correction(const smg_correction *c, const double *r, double *out,
+                               void *stream);
+/* u += S_c (b - A u)            (smoothers.py:263 / :266)                          */
+SMG_API int smg_local_correct(const smg_correction *c, const double *b, double *u, void *stream);
+/* sandwich smoother             (smoothers.py:252-267); c may be NULL             */
+SMG_API int smg_combined_smooth(const smg_operator *a, const double *b, double *u,
+                        const smg_correction *c, int kind, int sweeps, double lambda_max,
+                        double lambda_min_fraction, double *work, void *stream);
+
+/* ---- hierarchy and solvers: Hierarchy / vcycle (mg.py:51-184) -------------
+ * Level l (0 = finest) has operator a[l], prolongation p[l] (from level l+1
+ * into l; created with_transpose; ignored on the coarsest level), optional
+ * correction[l] and smoother parameters.  The coarsest level is solved with
+ * the dense operator coarse_inverse = A_L^{-1} (n_coarse x n_coarse row-major,
+ * e.g. LAPACK dpotri on the reference's coarse_factor, mg.py:123);
+ * coarse_refine != 0 adds one refinement step with a[n_levels-1].
+ * The hierarchy borrows (does not own) the operators and corrections. */
+SMG_API int smg_hierarchy_create(int n_levels, const smg_operator *const *a,
+                         const smg_operator *const *p, const smg_correction *const *corrections,
+                         const int *kinds, const int *sweeps, const double *lambda_max,
+                         const double *lambda_min_fraction, int64_t n_coarse,
+                         const double *coarse_inverse, int coarse_refine,
+                         smg_hierarchy **out);
+SMG_API int smg_hierarchy_destroy(smg_hierarchy *h);
+/* enable != 0: capture each V-cycle once per (b, u) pointer pair as a CUDA graph */
+SMG_API int smg_hierarchy_set_graphs(smg_hierarchy *h, int enable);
+/* kernels one V-cycle launches (for launch accounting) */
+SMG_API int smg_hierarchy_launches_per_vcycle(const smg_hierarchy *h, int64_t *launches);
+
+/* u <- one V-cycle on u (mg.py:127-151; in place)                                 */
+SMG_API int smg_vcycle(smg_hierarchy *h, const double *b, double *u, void *stream);
+/* same with HOST b/u: H2D copies, V-cycle, D2H of u (the e2e path)                */
+SMG_API int smg_vcycle_host(smg_hierarchy *h, const double *b_host, double *u_host, void *stream);
+/* stationary MG (mg.py:154-175): u holds u0 on entry and the result on exit.
+ * history: capacity max_cycles + 1 host doubles; *n_history entries written.  */
+SMG_API int smg_solve_stationary(smg_hierarchy *h, const double *b, double *u, double rtol,
+                         int max_cycles, double *history, int *n_history, void *stream);
+/* MG-preconditioned CG (sparse.py:168-211 with mg.py:178-184 as precond).
+ * h == NULL: unpreconditioned.  x holds x0 on entry when x0_given != 0, else
+ * it is zeroed.  history: capacity maxit + 1.  On SMG_ERR_INDEFINITE,
+ * *bad_iteration / *bad_curvature describe the failure. */
+SMG_API int smg_cg(smg_hierarchy *h, const smg_operator *a, const double *b, double *x, int x0_given,
+           double rtol, int maxit, double *history, int *n_history, int64_t *bad_iteration,
+           double *bad_curvature, void *stream);
+/* deterministic fixed-order dot product, result to host */
+SMG_API int smg_dot(int64_t n, const double *x, const double *y, double *result_host, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SIMPLEXMG_B200_H */

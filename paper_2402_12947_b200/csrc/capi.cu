@@ -1,0 +1,999 @@
+// C-ABI implementation: device-resident operators, patch sets and the V-cycle
+// runtime (graph-captured) behind include/simplexmg_b200.h.
+//
+// Host arithmetic for smoother scalars follows smoothers.py:109-135 exactly
+// (compiled with -ffp-contract=off), so the scalars fed to the kernels equal
+// the Python floats the reference computes.
+#include "../../include/simplexmg_b200.h"
+#include "smg_internal.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <utility>
+
+namespace smg {
+
+cudaError_t configure_patch_solve_smem(size_t bytes);
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+int fail(const std::string& msg)
+{
+  set_error(msg);
+  return SMG_ERR_INVALID;
+}
+int check_cuda(cudaError_t e, const char* what)
+{
+  if (e == cudaSuccess) return SMG_OK;
+  set_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return SMG_ERR_CUDA;
+}
+
+#define SMG_TRY(expr)                      \
+  do {                                     \
+    int _rc = (expr);                      \
+    if (_rc != SMG_OK) return _rc;         \
+  } while (0)
+#define SMG_CUDA(expr) SMG_TRY(check_cuda((expr), #expr))
+
+template <typename T>
+static int dev_upload(std::vector<void*>& allocs, int64_t& bytes, const T* host, size_t n,
+                      T** out)
+{
+  *out = nullptr;
+  if (n == 0) return SMG_OK;
+  void* p = nullptr;
+  SMG_CUDA(cudaMalloc(&p, n * sizeof(T)));
+  allocs.push_back(p);
+  bytes += (int64_t)(n * sizeof(T));
+  if (host) SMG_CUDA(cudaMemcpy(p, host, n * sizeof(T), cudaMemcpyHostToDevice));
+  *out = static_cast<T*>(p);
+  return SMG_OK;
+}
+
+template <typename T>
+static int dev_alloc(std::vector<void*>& allocs, int64_t& bytes, size_t n, T** out)
+{
+  return dev_upload<T>(allocs, bytes, nullptr, n, out);
+}
+
+static void free_all(std::vector<void*>& allocs)
+{
+  for (void* p : allocs) cudaFree(p);
+  allocs.clear();
+}
+
+// Greedy tile partition: consecutive rows, <= kRowsPerTile rows, <= kTileNnz
+// nonzeros unless a single row is longer.
+static std::vector<int32_t> make_tiles(int64_t nrows, const int64_t* rowptr)
+{
+  std::vector<int32_t> t;
+  t.reserve((size_t)(nrows / 64 + 2));
+  t.push_back(0);
+  int64_t r = 0;
+  while (r < nrows) {
+    const int64_t start = r;
+    const int64_t base = rowptr[r];
+    ++r;
+    while (r < nrows && r - start < kRowsPerTile && rowptr[r + 1] - base <= kTileNnz) ++r;
+    t.push_back((int32_t)r);
+  }
+  return t;
+}
+
+static int build_devcsr(std::vector<void*>& allocs, int64_t& bytes, int64_t nrows, int64_t ncols,
+                        const int64_t* rowptr, const int64_t* col64, const double* val,
+                        DevCsr* out)
+{
+  const int64_t nnz = rowptr[nrows];
+  std::vector<int32_t> col32((size_t)nnz);
+  for (int64_t j = 0; j < nnz; ++j) col32[(size_t)j] = (int32_t)col64[j];
+  std::vector<int32_t> tiles = make_tiles(nrows, rowptr);
+  DevCsr d;
+  d.nrows = nrows;
+  d.ncols = ncols;
+  d.nnz = nnz;
+  d.ntiles = (int32_t)(tiles.size() - 1);
+  int64_t* rp = nullptr;
+  int32_t* c = nullptr;
+  double* v = nullptr;
+  int32_t* tr = nullptr;
+  SMG_TRY(dev_upload(allocs, bytes, rowptr, (size_t)nrows + 1, &rp));
+  SMG_TRY(dev_upload(allocs, bytes, col32.data(), (size_t)nnz, &c));
+  SMG_TRY(dev_upload(allocs, bytes, val, (size_t)nnz, &v));
+  SMG_TRY(dev_upload(allocs, bytes, tiles.data(), tiles.size(), &tr));
+  d.rowptr = rp;
+  d.col = c;
+  d.val = v;
+  d.tile_row = tr;
+  *out = d;
+  return SMG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// smoother scalars, smoothers.py:109-135
+struct ChebScalars {
+  bool collapsed = false;
+  double theta = 0, delta = 0, sigma = 0;
+  std::vector<std::pair<double, double>> steps;  // (c1, c2) for sweeps 2..k
+};
+
+static int cheb_scalars(int sweeps, double lambda_max, double frac, ChebScalars* out)
+{
+  if (!(lambda_max > 0.0)) {
+    set_error("chebyshev_smooth requires a positive cfg.lambda_max");
+    return SMG_ERR_INVALID;
+  }
+  if (sweeps < 1) return fail("sweeps must be at least 1");
+  const double lam_max = lambda_max;
+  const double lam_min = frac * lam_max;
+  ChebScalars s;
+  s.theta = 0.5 * (lam_max + lam_min);
+  s.delta = 0.5 * (lam_max - lam_min);
+  if (s.delta == 0.0) {
+    s.collapsed = true;
+  } else {
+    s.sigma = s.theta / s.delta;
+    double rho = 1.0 / s.sigma;
+    for (int k = 1; k < sweeps; ++k) {
+      const double rho_next = 1.0 / (2.0 * s.sigma - rho);
+      const double c1 = rho_next * rho;
+      const double c2 = 2.0 * rho_next / s.delta;
+      s.steps.emplace_back(c1, c2);
+      rho = rho_next;
+    }
+  }
+  *out = s;
+  return SMG_OK;
+}
+
+// k steps ping-ponging between *cur and *alt (the reference computes the full
+// A u before updating u, so the gathering SpMV never writes its own input).
+static int enqueue_global_smooth(const Operator& op, const double* b, double** cur, double** alt,
+                                 double* d, int sweeps, const ChebScalars& cs, cudaStream_t st,
+                                 int64_t* launches)
+{
+  EpiArgs ea;
+  ea.b = b;
+  ea.theta = cs.theta;
+  ea.d = d;
+  if (cs.collapsed) {
+    for (int k = 0; k < sweeps; ++k) {
+      ea.u_in = *cur;
+      ea.out = *alt;
+      SMG_CUDA(launch_csr_stream(op.a, *cur, Epi::kJacobi, ea, st));
+      std::swap(*cur, *alt);
+      ++*launches;
+    }
+    return SMG_OK;
+  }
+  ea.u_in = *cur;
+  ea.out = *alt;
+  SMG_CUDA(launch_csr_stream(op.a, *cur, Epi::kChebFirst, ea, st));
+  std::swap(*cur, *alt);
+  ++*launches;
+  for (size_t k = 0; k < cs.steps.size(); ++k) {
+    ea.u_in = *cur;
+    ea.out = *alt;
+    ea.c1 = cs.steps[k].first;
+    ea.c2 = cs.steps[k].second;
+    SMG_CUDA(launch_csr_stream(op.a, *cur, Epi::kChebNext, ea, st));
+    std::swap(*cur, *alt);
+    ++*launches;
+  }
+  return SMG_OK;
+}
+
+static int enqueue_local_correct(const Correction& c, const double* b, double* u, cudaStream_t st,
+                                 int64_t* launches)
+{
+  if (c.n_regions == 0) return SMG_OK;
+  SMG_CUDA(launch_patch_residual(c.op->a, c, b, u, st));
+  SMG_CUDA(launch_patch_solve(c, u, nullptr, st));
+  *launches += 2;
+  return SMG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// scratch for free-standing reductions
+struct DotScratch {
+  double* partials = nullptr;
+  unsigned int* counter = nullptr;
+  double* result = nullptr;
+  double* host = nullptr;  // pinned
+  std::vector<void*> allocs;
+  int64_t bytes = 0;
+  int init()
+  {
+    if (partials) return SMG_OK;
+    SMG_TRY(dev_alloc(allocs, bytes, kDotBlocks, &partials));
+    SMG_TRY(dev_alloc(allocs, bytes, 1, &counter));
+    SMG_TRY(dev_alloc(allocs, bytes, 1, &result));
+    SMG_CUDA(cudaMemset(counter, 0, sizeof(unsigned int)));
+    SMG_CUDA(cudaMallocHost(&host, sizeof(double)));
+    return SMG_OK;
+  }
+  void release()
+  {
+    free_all(allocs);
+    if (host) cudaFreeHost(host);
+    host = nullptr;
+    partials = nullptr;
+  }
+  int dot(int64_t n, const double* x, const double* y, cudaStream_t st, double* out)
+  {
+    SMG_TRY(init());
+    SMG_CUDA(launch_dot(n, x, y, partials, counter, result, st));
+    SMG_CUDA(cudaMemcpyAsync(host, result, sizeof(double), cudaMemcpyDeviceToHost, st));
+    SMG_CUDA(cudaStreamSynchronize(st));
+    *out = *host;
+    return SMG_OK;
+  }
+};
+
+// ---------------------------------------------------------------------------
+struct HLevel {
+  const Operator* a = nullptr;
+  const Operator* p = nullptr;
+  const Correction* lc = nullptr;
+  int kind = kChebyshev;
+  int sweeps = 1;
+  double lambda_max = 0, frac = 0.1;
+  ChebScalars cs;
+  int64_t n = 0;
+  double* b = nullptr;   // levels >= 1
+  double* u = nullptr;   // levels >= 1
+  double* t = nullptr;   // ping-pong partner
+  double* d = nullptr;   // Chebyshev direction
+  double* r = nullptr;   // residual
+};
+
+struct Hierarchy {
+  std::vector<HLevel> lv;
+  int64_t n_coarse = 0;
+  double* coarse_inv = nullptr;
+  int coarse_refine = 0;
+  double* coarse_r = nullptr;
+  double* coarse_x = nullptr;
+  std::vector<void*> allocs;
+  int64_t bytes = 0;
+  bool use_graphs = true;
+  std::map<std::pair<const void*, void*>, cudaGraphExec_t> graphs;
+  cudaStream_t capture_stream = nullptr;
+  int64_t launches = 0;
+  double* stage_b = nullptr;  // device copies for the host-buffer path
+  double* stage_u = nullptr;
+  DotScratch dots;
+
+  ~Hierarchy()
+  {
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    if (capture_stream) cudaStreamDestroy(capture_stream);
+    dots.release();
+    free_all(allocs);
+  }
+};
+
+static int enqueue_smooth(HLevel& L, const double* b, double** cur, double** alt, cudaStream_t st,
+                          int64_t* launches)
+{
+  const bool active = L.lc && L.lc->n_regions > 0;
+  if (active) SMG_TRY(enqueue_local_correct(*L.lc, b, *cur, st, launches));
+  SMG_TRY(enqueue_global_smooth(*L.a, b, cur, alt, L.d, L.sweeps, L.cs, st, launches));
+  if (active) SMG_TRY(enqueue_local_correct(*L.lc, b, *cur, st, launches));
+  return SMG_OK;
+}
+
+// mg.py:127-151
+static int enqueue_vcycle(Hierarchy& h, const double* b0, double* u0, cudaStream_t st,
+                          int64_t* launches)
+{
+  const int nl = (int)h.lv.size();
+  std::vector<double*> cur(nl), alt(nl);
+  std::vector<const double*> bl(nl);
+  bl[0] = b0;
+  cur[0] = u0;
+  alt[0] = h.lv[0].t;
+  for (int l = 1; l < nl; ++l) {
+    bl[l] = h.lv[l].b;
+    cur[l] = h.lv[l].u;
+    alt[l] = h.lv[l].t;
+  }
+  for (int l = 0; l < nl - 1; ++l) {
+    HLevel& L = h.lv[l];
+    SMG_TRY(enqueue_smooth(L, bl[l], &cur[l], &alt[l], st, launches));
+    EpiArgs ea;
+    ea.b = bl[l];
+    ea.out = L.r;
+    SMG_CUDA(launch_csr_stream(L.a->a, cur[l], Epi::kResidual, ea, st));
+    EpiArgs er;
+    er.out = h.lv[l + 1].b;
+    SMG_CUDA(launch_csr_stream(L.p->t, L.r, Epi::kSpmv, er, st));
+    SMG_CUDA(cudaMemsetAsync(cur[l + 1], 0, sizeof(double) * (size_t)h.lv[l + 1].n, st));
+    *launches += 2;
+  }
+  // coarse solve
+  {
+    HLevel& C = h.lv[nl - 1];
+    SMG_CUDA(launch_dense_gemv(h.n_coarse, h.coarse_inv, bl[nl - 1], cur[nl - 1], st));
+    ++*launches;
+    if (h.coarse_refine) {
+      EpiArgs ea;
+      ea.b = bl[nl - 1];
+      ea.out = h.coarse_r;
+      SMG_CUDA(launch_csr_stream(C.a->a, cur[nl - 1], Epi::kResidual, ea, st));
+      SMG_CUDA(launch_dense_gemv_add(h.n_coarse, h.coarse_inv, h.coarse_r, cur[nl - 1], st));
+      *launches += 2;
+    }
+  }
+  for (int l = nl - 2; l >= 0; --l) {
+    HLevel& L = h.lv[l];
+    EpiArgs ea;
+    ea.out = cur[l];
+    SMG_CUDA(launch_csr_stream(L.p->a, cur[l + 1], Epi::kAddTo, ea, st));
+    ++*launches;
+    SMG_TRY(enqueue_smooth(L, bl[l], &cur[l], &alt[l], st, launches));
+  }
+  if (cur[0] != u0) {
+    SMG_CUDA(cudaMemcpyAsync(u0, cur[0], sizeof(double) * (size_t)h.lv[0].n,
+                             cudaMemcpyDeviceToDevice, st));
+  }
+  return SMG_OK;
+}
+
+static int run_vcycle(Hierarchy& h, const double* b, double* u, cudaStream_t st)
+{
+  if (!h.use_graphs) {
+    int64_t n = 0;
+    SMG_TRY(enqueue_vcycle(h, b, u, st, &n));
+    h.launches = n;
+    return SMG_OK;
+  }
+  auto key = std::make_pair((const void*)b, (void*)u);
+  auto it = h.graphs.find(key);
+  if (it == h.graphs.end()) {
+    if (!h.capture_stream)
+      SMG_CUDA(cudaStreamCreateWithFlags(&h.capture_stream, cudaStreamNonBlocking));
+    SMG_CUDA(cudaStreamBeginCapture(h.capture_stream, cudaStreamCaptureModeThreadLocal));
+    int64_t n = 0;
+    int rc = enqueue_vcycle(h, b, u, h.capture_stream, &n);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(h.capture_stream, &g);
+    if (rc != SMG_OK) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    SMG_CUDA(e);
+    cudaGraphExec_t ex = nullptr;
+    e = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    SMG_CUDA(e);
+    if (h.graphs.size() > 64) {  // bound the cache
+      for (auto& kv : h.graphs) cudaGraphExecDestroy(kv.second);
+      h.graphs.clear();
+    }
+    it = h.graphs.emplace(key, ex).first;
+    h.launches = n;
+  }
+  SMG_CUDA(cudaGraphLaunch(it->second, st));
+  return SMG_OK;
+}
+
+static std::mutex g_scratch_mu;
+static DotScratch g_dots;
+
+}  // namespace smg
+
+using namespace smg;
+
+struct smg_operator {
+  Operator o;
+};
+struct smg_correction {
+  Correction c;
+};
+struct smg_hierarchy {
+  Hierarchy h;
+};
+
+static cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+extern "C" {
+
+int smg_abi_version(void) { return SMG_ABI_VERSION; }
+
+const char* smg_last_error(void) { return g_last_error.c_str(); }
+
+int smg_device_info(int* sm_count, int64_t* l2_bytes, int* cc_major, int* cc_minor)
+{
+  int dev = 0;
+  SMG_CUDA(cudaGetDevice(&dev));
+  cudaDeviceProp p;
+  SMG_CUDA(cudaGetDeviceProperties(&p, dev));
+  if (sm_count) *sm_count = p.multiProcessorCount;
+  if (l2_bytes) *l2_bytes = p.l2CacheSize;
+  if (cc_major) *cc_major = p.major;
+  if (cc_minor) *cc_minor = p.minor;
+  return SMG_OK;
+}
+
+int smg_operator_create(int64_t nrows, int64_t ncols, const int64_t* rowptr, const int64_t* col,
+                        const double* val, int with_transpose, smg_operator** out)
+{
+  if (!out) return fail("out is NULL");
+  *out = nullptr;
+  if (nrows < 0 || ncols < 0) return fail("negative dimensions");
+  if (nrows >= INT32_MAX || ncols >= INT32_MAX) return fail("dimensions exceed int32 indexing");
+  if (!rowptr) return fail("row_offsets is NULL");
+  if (rowptr[0] != 0) return fail("row_offsets must be monotone from 0 to nnz");
+  for (int64_t i = 0; i < nrows; ++i)
+    if (rowptr[i + 1] < rowptr[i]) return fail("row_offsets must be monotone from 0 to nnz");
+  const int64_t nnz = rowptr[nrows];
+  for (int64_t i = 0; i < nrows; ++i) {
+    for (int64_t j = rowptr[i]; j < rowptr[i + 1]; ++j) {
+      if (col[j] < 0 || col[j] >= ncols) return fail("column index out of range");
+      if (j > rowptr[i] && col[j] <= col[j - 1])
+        return fail("column indices must be strictly increasing within rows");
+    }
+  }
+  auto* op = new smg_operator();
+  Operator& o = op->o;
+  int rc = build_devcsr(o.allocs, o.device_bytes, nrows, ncols, rowptr, col, val, &o.a);
+  if (rc != SMG_OK) {
+    free_all(o.allocs);
+    delete op;
+    return rc;
+  }
+  // first zero / missing diagonal (smoothers.py:111-114 via a.diagonal())
+  o.first_zero_diag = -1;
+  const int64_t nd = std::min(nrows, ncols);
+  for (int64_t i = 0; i < nd && o.first_zero_diag < 0; ++i) {
+    double dv = 0.0;
+    const int64_t* b = col + rowptr[i];
+    const int64_t* e = col + rowptr[i + 1];
+    const int64_t* f = std::lower_bound(b, e, i);
+    if (f != e && *f == i) dv = val[rowptr[i] + (f - b)];
+    if (dv == 0.0) o.first_zero_diag = i;
+  }
+  if (with_transpose) {
+    // CSR(A^T) with ascending source rows in each row (counting sort is stable)
+    std::vector<int64_t> tptr((size_t)ncols + 1, 0);
+    for (int64_t j = 0; j < nnz; ++j) ++tptr[(size_t)col[j] + 1];
+    for (int64_t c = 0; c < ncols; ++c) tptr[(size_t)c + 1] += tptr[(size_t)c];
+    std::vector<int64_t> fill(tptr.begin(), tptr.end() - 1);
+    std::vector<int64_t> tcol((size_t)nnz);
+    std::vector<double> tval((size_t)nnz);
+    for (int64_t i = 0; i < nrows; ++i)
+      for (int64_t j = rowptr[i]; j < rowptr[i + 1]; ++j) {
+        const int64_t pos = fill[(size_t)col[j]]++;
+        tcol[(size_t)pos] = i;
+        tval[(size_t)pos] = val[j];
+      }
+    rc = build_devcsr(o.allocs, o.device_bytes, ncols, nrows, tptr.data(), tcol.data(),
+                      tval.data(), &o.t);
+    if (rc != SMG_OK) {
+      free_all(o.allocs);
+      delete op;
+      return rc;
+    }
+    o.has_t = true;
+  }
+  *out = op;
+  return SMG_OK;
+}
+
+int smg_operator_destroy(smg_operator* op)
+{
+  if (!op) return SMG_OK;
+  free_all(op->o.allocs);
+  delete op;
+  return SMG_OK;
+}
+
+int smg_operator_info(const smg_operator* op, int64_t* nrows, int64_t* ncols, int64_t* nnz,
+                      int64_t* first_zero_diag, int64_t* device_bytes)
+{
+  if (!op) return fail("operator is NULL");
+  if (nrows) *nrows = op->o.a.nrows;
+  if (ncols) *ncols = op->o.a.ncols;
+  if (nnz) *nnz = op->o.a.nnz;
+  if (first_zero_diag) *first_zero_diag = op->o.first_zero_diag;
+  if (device_bytes) *device_bytes = op->o.device_bytes;
+  return SMG_OK;
+}
+
+int smg_spmv(const smg_operator* a, const double* x, double* y, void* stream)
+{
+  if (!a) return fail("operator is NULL");
+  EpiArgs ea;
+  ea.out = y;
+  SMG_CUDA(launch_csr_stream(a->o.a, x, Epi::kSpmv, ea, as_stream(stream)));
+  return SMG_OK;
+}
+
+int smg_residual(const smg_operator* a, const double* b, const double* u, double* r, void* stream)
+{
+  if (!a) return fail("operator is NULL");
+  EpiArgs ea;
+  ea.b = b;
+  ea.out = r;
+  SMG_CUDA(launch_csr_stream(a->o.a, u, Epi::kResidual, ea, as_stream(stream)));
+  return SMG_OK;
+}
+
+int smg_spmv_transpose(const smg_operator* p, const double* r, double* y, void* stream)
+{
+  if (!p) return fail("operator is NULL");
+  if (!p->o.has_t) return fail("operator was created without its transpose");
+  EpiArgs ea;
+  ea.out = y;
+  SMG_CUDA(launch_csr_stream(p->o.t, r, Epi::kSpmv, ea, as_stream(stream)));
+  return SMG_OK;
+}
+
+int smg_prolong_add(const smg_operator* p, const double* uc, double* uf, void* stream)
+{
+  if (!p) return fail("operator is NULL");
+  EpiArgs ea;
+  ea.out = uf;
+  SMG_CUDA(launch_csr_stream(p->o.a, uc, Epi::kAddTo, ea, as_stream(stream)));
+  return SMG_OK;
+}
+
+static int check_square_diag(const Operator& o)
+{
+  if (o.a.nrows != o.a.ncols) return fail("smoother needs a square operator");
+  if (o.first_zero_diag >= 0) {
+    set_error("zero diagonal entry in row " + std::to_string(o.first_zero_diag));
+    return SMG_ERR_ZERO_DIAGONAL;
+  }
+  return SMG_OK;
+}
+
+static int smooth_standalone(const Operator& o, const double* b, double* u, const Correction* c,
+                             int kind, int sweeps, double lmax, double frac, double* work,
+                             cudaStream_t st)
+{
+  if (kind == SMG_SMOOTHER_SGS) {
+    set_error("symmetric Gauss-Seidel is outside the GPU hot path");
+    return SMG_ERR_UNSUPPORTED;
+  }
+  if (kind != SMG_SMOOTHER_CHEBYSHEV) return fail("unknown smoother kind");
+  ChebScalars cs;
+  SMG_TRY(cheb_scalars(sweeps, lmax, frac, &cs));
+  SMG_TRY(check_square_diag(o));
+  const int64_t n = o.a.nrows;
+  std::vector<void*> tmp;
+  int64_t bytes = 0;
+  double* w = work;
+  if (!w && n > 0) SMG_TRY(dev_alloc(tmp, bytes, (size_t)(2 * n), &w));
+  double* cur = u;
+  double* alt = w;
+  double* d = w ? w + n : nullptr;
+  int64_t launches = 0;
+  int rc = SMG_OK;
+  const bool active = c && c->n_regions > 0;
+  if (active) rc = enqueue_local_correct(*c, b, cur, st, &launches);
+  if (rc == SMG_OK) rc = enqueue_global_smooth(o, b, &cur, &alt, d, sweeps, cs, st, &launches);
+  if (rc == SMG_OK && active) rc = enqueue_local_correct(*c, b, cur, st, &launches);
+  if (rc == SMG_OK && cur != u && n > 0)
+    rc = check_cuda(cudaMemcpyAsync(u, cur, sizeof(double) * (size_t)n, cudaMemcpyDeviceToDevice, st),
+                    "copy back");
+  if (!tmp.empty()) {
+    cudaStreamSynchronize(st);
+    free_all(tmp);
+  }
+  return rc;
+}
+
+int smg_chebyshev_smooth(const smg_operator* a, const double* b, double* u, int sweeps,
+                         double lambda_max, double frac, double* work, void* stream)
+{
+  if (!a) return fail("operator is NULL");
+  return smooth_standalone(a->o, b, u, nullptr, SMG_SMOOTHER_CHEBYSHEV, sweeps, lambda_max, frac,
+                           work, as_stream(stream));
+}
+
+int smg_correction_create(const smg_operator* a, int64_t n_regions, const int64_t* roff,
+                          const int64_t* dofs, const int64_t* foff, const double* factors,
+                          smg_correction** out)
+{
+  if (!out) return fail("out is NULL");
+  *out = nullptr;
+  if (!a) return fail("operator is NULL");
+  const Operator& o = a->o;
+  const int64_t n = o.a.nrows;
+  if (n_regions < 0) return fail("negative region count");
+  if (n_regions > 0 && (!roff || !dofs || !foff || !factors)) return fail("NULL region arrays");
+  std::vector<int32_t> owner((size_t)n, -1);
+  const int64_t m = n_regions > 0 ? roff[n_regions] : 0;
+  std::vector<int32_t> pptr((size_t)n_regions + 1);
+  std::vector<int32_t> dof32((size_t)m);
+  std::vector<int64_t> poff((size_t)n_regions + 1, 0);
+  int32_t max_dofs = 0;
+  for (int64_t r = 0; r < n_regions; ++r) {
+    const int64_t nd = roff[r + 1] - roff[r];
+    if (nd <= 0) return fail("region " + std::to_string(r) + " is empty");
+    max_dofs = std::max<int32_t>(max_dofs, (int32_t)nd);
+    pptr[(size_t)r] = (int32_t)roff[r];
+    poff[(size_t)r + 1] = poff[(size_t)r] + nd * (nd + 1) / 2;
+    for (int64_t k = roff[r]; k < roff[r + 1]; ++k) {
+      const int64_t g = dofs[k];
+      if (g < 0 || g >= n)
+        return fail("region " + std::to_string(r) + " has dof indices outside 0.." +
+                    std::to_string(n - 1));
+      if (k > roff[r] && g <= dofs[k - 1])
+        return fail("region " + std::to_string(r) + " dofs must be sorted and unique");
+      if (owner[(size_t)g] >= 0)
+        return fail("region " + std::to_string(r) + " overlaps a previous region's dofs");
+      owner[(size_t)g] = (int32_t)r;
+      dof32[(size_t)k] = (int32_t)g;
+    }
+  }
+  pptr[(size_t)n_regions] = (int32_t)m;
+  // pack lower triangles (row-major)
+  std::vector<double> packed((size_t)poff[(size_t)n_regions]);
+  for (int64_t r = 0; r < n_regions; ++r) {
+    const int64_t nd = roff[r + 1] - roff[r];
+    const double* f = factors + foff[r];
+    double* dst = packed.data() + poff[(size_t)r];
+    for (int64_t i = 0; i < nd; ++i)
+      for (int64_t j = 0; j <= i; ++j) *dst++ = f[i * nd + j];
+  }
+  auto* cc = new smg_correction();
+  Correction& c = cc->c;
+  c.n_global = n;
+  c.n_regions = (int32_t)n_regions;
+  c.m = m;
+  c.max_dofs = max_dofs;
+  c.op = &o;
+  // coupling through A between different regions
+  c.coupled = false;
+  {
+    std::vector<int64_t> hrp((size_t)n + 1);
+    std::vector<int32_t> hcol((size_t)o.a.nnz);
+    cudaMemcpy(hrp.data(), o.a.rowptr, sizeof(int64_t) * (size_t)(n + 1), cudaMemcpyDeviceToHost);
+    cudaMemcpy(hcol.data(), o.a.col, sizeof(int32_t) * (size_t)o.a.nnz, cudaMemcpyDeviceToHost);
+    for (int64_t k = 0; k < m && !c.coupled; ++k) {
+      const int32_t g = dof32[(size_t)k];
+      for (int64_t j = hrp[(size_t)g]; j < hrp[(size_t)g + 1]; ++j) {
+        const int32_t own = owner[(size_t)hcol[(size_t)j]];
+        if (own >= 0 && own != owner[(size_t)g]) {
+          c.coupled = true;
+          break;
+        }
+      }
+    }
+  }
+  int32_t* dp = nullptr;
+  int32_t* dd = nullptr;
+  int64_t* df = nullptr;
+  double* dl = nullptr;
+  int rc = SMG_OK;
+  if (n_regions > 0) {
+    rc = dev_upload(c.allocs, c.device_bytes, pptr.data(), pptr.size(), &dp);
+    if (rc == SMG_OK) rc = dev_upload(c.allocs, c.device_bytes, dof32.data(), dof32.size(), &dd);
+    if (rc == SMG_OK) rc = dev_upload(c.allocs, c.device_bytes, poff.data(), poff.size(), &df);
+    if (rc == SMG_OK) rc = dev_upload(c.allocs, c.device_bytes, packed.data(), packed.size(), &dl);
+    if (rc == SMG_OK) rc = dev_alloc(c.allocs, c.device_bytes, (size_t)m, &c.rbuf);
+    if (rc == SMG_OK && (size_t)max_dofs * sizeof(double) > 48 * 1024)
+      rc = check_cuda(configure_patch_solve_smem((size_t)max_dofs * sizeof(double)),
+                      "patch solve shared memory");
+  }
+  if (rc != SMG_OK) {
+    free_all(c.allocs);
+    delete cc;
+    return rc;
+  }
+  c.pptr = dp;
+  c.dofs = dd;
+  c.foff = df;
+  c.lfac = dl;
+  *out = cc;
+  return SMG_OK;
+}
+
+int smg_correction_destroy(smg_correction* c)
+{
+  if (!c) return SMG_OK;
+  free_all(c->c.allocs);
+  delete c;
+  return SMG_OK;
+}
+
+int smg_correction_info(const smg_correction* c, int64_t* n_regions, int64_t* covered, int* coupled,
+                        int64_t* device_bytes)
+{
+  if (!c) return fail("correction is NULL");
+  if (n_regions) *n_regions = c->c.n_regions;
+  if (covered) *covered = c->c.m;
+  if (coupled) *coupled = c->c.coupled ? 1 : 0;
+  if (device_bytes) *device_bytes = c->c.device_bytes;
+  return SMG_OK;
+}
+
+int smg_apply_local_correction(const smg_correction* c, const double* r, double* out, void* stream)
+{
+  if (!c) return fail("correction is NULL");
+  const Correction& cc = c->c;
+  cudaStream_t st = as_stream(stream);
+  if (cc.n_global > 0) SMG_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * (size_t)cc.n_global, st));
+  if (cc.n_regions == 0) return SMG_OK;
+  // rbuf[k] = r[dofs[k]], then the batched solves scatter into out
+  SMG_CUDA(launch_gather(cc.dofs, cc.m, r, cc.rbuf, st));
+  SMG_CUDA(launch_patch_solve(cc, nullptr, out, st));
+  return SMG_OK;
+}
+
+int smg_local_correct(const smg_correction* c, const double* b, double* u, void* stream)
+{
+  if (!c) return fail("correction is NULL");
+  int64_t n = 0;
+  return enqueue_local_correct(c->c, b, u, as_stream(stream), &n);
+}
+
+int smg_combined_smooth(const smg_operator* a, const double* b, double* u, const smg_correction* c,
+                        int kind, int sweeps, double lambda_max, double frac, double* work,
+                        void* stream)
+{
+  if (!a) return fail("operator is NULL");
+  return smooth_standalone(a->o, b, u, c ? &c->c : nullptr, kind, sweeps, lambda_max, frac, work,
+                           as_stream(stream));
+}
+
+int smg_hierarchy_create(int n_levels, const smg_operator* const* a, const smg_operator* const* p,
+                         const smg_correction* const* corrections, const int* kinds,
+                         const int* sweeps, const double* lambda_max, const double* frac,
+                         int64_t n_coarse, const double* coarse_inverse, int coarse_refine,
+                         smg_hierarchy** out)
+{
+  if (!out) return fail("out is NULL");
+  *out = nullptr;
+  if (n_levels < 2) return fail("a hierarchy needs at least 2 levels, got " + std::to_string(n_levels));
+  if (!a || !p || !kinds || !sweeps || !lambda_max || !frac) return fail("NULL level arrays");
+  auto* hh = new smg_hierarchy();
+  Hierarchy& h = hh->h;
+  auto bail = [&](int rc) {
+    delete hh;
+    return rc;
+  };
+  h.lv.resize((size_t)n_levels);
+  for (int l = 0; l < n_levels; ++l) {
+    HLevel& L = h.lv[(size_t)l];
+    if (!a[l]) return bail(fail("level operator is NULL"));
+    L.a = &a[l]->o;
+    L.n = L.a->a.nrows;
+    if (L.a->a.nrows != L.a->a.ncols) return bail(fail("level operators must be square"));
+    if (l < n_levels - 1) {
+      if (!p[l]) return bail(fail("prolongation is NULL"));
+      L.p = &p[l]->o;
+      if (!L.p->has_t) return bail(fail("prolongations must be created with_transpose"));
+      if (L.p->a.nrows != L.n || L.p->a.ncols != a[l + 1]->o.a.nrows)
+        return bail(fail("dimension mismatch between prolongation and level operators"));
+      L.lc = corrections ? (corrections[l] ? &corrections[l]->c : nullptr) : nullptr;
+      L.kind = kinds[l];
+      L.sweeps = sweeps[l];
+      L.lambda_max = lambda_max[l];
+      L.frac = frac[l];
+      if (L.kind == SMG_SMOOTHER_SGS) {
+        set_error("symmetric Gauss-Seidel is outside the GPU hot path");
+        return bail(SMG_ERR_UNSUPPORTED);
+      }
+      int rc = cheb_scalars(L.sweeps, L.lambda_max, L.frac, &L.cs);
+      if (rc != SMG_OK) return bail(rc);
+      rc = check_square_diag(*L.a);
+      if (rc != SMG_OK) return bail(rc);
+    }
+  }
+  if (n_coarse != h.lv.back().n) return bail(fail("coarse inverse size does not match the coarsest level"));
+  if (!coarse_inverse) return bail(fail("coarse_inverse is NULL"));
+  int rc = SMG_OK;
+  for (int l = 0; l < n_levels && rc == SMG_OK; ++l) {
+    HLevel& L = h.lv[(size_t)l];
+    const size_t n = (size_t)L.n;
+    if (l > 0) {
+      rc = dev_alloc(h.allocs, h.bytes, n, &L.b);
+      if (rc == SMG_OK) rc = dev_alloc(h.allocs, h.bytes, n, &L.u);
+    }
+    if (rc == SMG_OK && l < n_levels - 1) {
+      rc = dev_alloc(h.allocs, h.bytes, n, &L.t);
+      if (rc == SMG_OK) rc = dev_alloc(h.allocs, h.bytes, n, &L.d);
+      if (rc == SMG_OK) rc = dev_alloc(h.allocs, h.bytes, n, &L.r);
+    }
+  }
+  if (rc == SMG_OK)
+    rc = dev_upload(h.allocs, h.bytes, coarse_inverse, (size_t)(n_coarse * n_coarse), &h.coarse_inv);
+  h.n_coarse = n_coarse;
+  h.coarse_refine = coarse_refine;
+  if (rc == SMG_OK && coarse_refine) rc = dev_alloc(h.allocs, h.bytes, (size_t)n_coarse, &h.coarse_r);
+  if (rc == SMG_OK) rc = dev_alloc(h.allocs, h.bytes, (size_t)h.lv[0].n, &h.stage_b);
+  if (rc == SMG_OK) rc = dev_alloc(h.allocs, h.bytes, (size_t)h.lv[0].n, &h.stage_u);
+  if (rc != SMG_OK) return bail(rc);
+  *out = hh;
+  return SMG_OK;
+}
+
+int smg_hierarchy_destroy(smg_hierarchy* h)
+{
+  delete h;
+  return SMG_OK;
+}
+
+int smg_hierarchy_set_graphs(smg_hierarchy* h, int enable)
+{
+  if (!h) return fail("hierarchy is NULL");
+  h->h.use_graphs = enable != 0;
+  return SMG_OK;
+}
+
+int smg_hierarchy_launches_per_vcycle(const smg_hierarchy* h, int64_t* launches)
+{
+  if (!h || !launches) return fail("NULL argument");
+  *launches = h->h.launches;
+  return SMG_OK;
+}
+
+int smg_vcycle(smg_hierarchy* h, const double* b, double* u, void* stream)
+{
+  if (!h) return fail("hierarchy is NULL");
+  return run_vcycle(h->h, b, u, as_stream(stream));
+}
+
+int smg_vcycle_host(smg_hierarchy* h, const double* b_host, double* u_host, void* stream)
+{
+  if (!h) return fail("hierarchy is NULL");
+  Hierarchy& H = h->h;
+  cudaStream_t st = as_stream(stream);
+  const size_t bytes = sizeof(double) * (size_t)H.lv[0].n;
+  SMG_CUDA(cudaMemcpyAsync(H.stage_b, b_host, bytes, cudaMemcpyHostToDevice, st));
+  SMG_CUDA(cudaMemcpyAsync(H.stage_u, u_host, bytes, cudaMemcpyHostToDevice, st));
+  SMG_TRY(run_vcycle(H, H.stage_b, H.stage_u, st));
+  SMG_CUDA(cudaMemcpyAsync(u_host, H.stage_u, bytes, cudaMemcpyDeviceToHost, st));
+  SMG_CUDA(cudaStreamSynchronize(st));
+  return SMG_OK;
+}
+
+int smg_solve_stationary(smg_hierarchy* h, const double* b, double* u, double rtol, int max_cycles,
+                         double* history, int* n_history, void* stream)
+{
+  if (!h || !history || !n_history) return fail("NULL argument");
+  Hierarchy& H = h->h;
+  cudaStream_t st = as_stream(stream);
+  HLevel& L0 = H.lv[0];
+  const int64_t n = L0.n;
+  double rr = 0, bb = 0;
+  EpiArgs ea;
+  ea.b = b;
+  ea.out = L0.r;
+  SMG_CUDA(launch_csr_stream(L0.a->a, u, Epi::kResidual, ea, st));
+  SMG_TRY(H.dots.dot(n, L0.r, L0.r, st, &rr));
+  SMG_TRY(H.dots.dot(n, b, b, st, &bb));
+  const double residual = std::sqrt(rr);
+  const double norm_b = std::sqrt(bb);
+  const double denom = norm_b > 0 ? norm_b : residual;
+  int cnt = 0;
+  if (denom == 0.0) {
+    history[cnt++] = 0.0;
+    *n_history = cnt;
+    return SMG_OK;
+  }
+  history[cnt++] = residual / denom;
+  for (int k = 0; k < max_cycles; ++k) {
+    if (history[cnt - 1] <= rtol) break;
+    SMG_TRY(run_vcycle(H, b, u, st));
+    SMG_CUDA(launch_csr_stream(L0.a->a, u, Epi::kResidual, ea, st));
+    SMG_TRY(H.dots.dot(n, L0.r, L0.r, st, &rr));
+    history[cnt++] = std::sqrt(rr) / denom;
+  }
+  *n_history = cnt;
+  return SMG_OK;
+}
+
+int smg_cg(smg_hierarchy* h, const smg_operator* a, const double* b, double* x, int x0_given,
+           double rtol, int maxit, double* history, int* n_history, int64_t* bad_iteration,
+           double* bad_curvature, void* stream)
+{
+  if (!a || !history || !n_history) return fail("NULL argument");
+  const Operator& A = a->o;
+  const int64_t n = A.a.nrows;
+  cudaStream_t st = as_stream(stream);
+  std::vector<void*> tmp;
+  int64_t bytes = 0;
+  double *r = nullptr, *z = nullptr, *d = nullptr, *q = nullptr;
+  SMG_TRY(dev_alloc(tmp, bytes, (size_t)n, &r));
+  SMG_TRY(dev_alloc(tmp, bytes, (size_t)n, &z));
+  SMG_TRY(dev_alloc(tmp, bytes, (size_t)n, &d));
+  SMG_TRY(dev_alloc(tmp, bytes, (size_t)n, &q));
+  DotScratch local;
+  DotScratch& dots = h ? h->h.dots : local;
+  struct Guard {
+    std::vector<void*>& t;
+    DotScratch& l;
+    cudaStream_t s;
+    ~Guard()
+    {
+      cudaStreamSynchronize(s);
+      free_all(t);
+      l.release();
+    }
+  } guard{tmp, local, st};
+
+  auto precond = [&](const double* rin, double* zout) -> int {
+    if (!h) {
+      SMG_CUDA(cudaMemcpyAsync(zout, rin, sizeof(double) * (size_t)n, cudaMemcpyDeviceToDevice, st));
+      return SMG_OK;
+    }
+    SMG_CUDA(cudaMemsetAsync(zout, 0, sizeof(double) * (size_t)n, st));
+    return run_vcycle(h->h, rin, zout, st);
+  };
+  if (!x0_given) SMG_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * (size_t)n, st));
+  EpiArgs ea;
+  ea.b = b;
+  ea.out = r;
+  SMG_CUDA(launch_csr_stream(A.a, x, Epi::kResidual, ea, st));
+  double bb = 0, rr = 0;
+  SMG_TRY(dots.dot(n, b, b, st, &bb));
+  SMG_TRY(dots.dot(n, r, r, st, &rr));
+  const double norm_b = std::sqrt(bb);
+  const double denom = norm_b > 0 ? norm_b : std::sqrt(rr);
+  int cnt = 0;
+  if (denom == 0.0) {
+    history[cnt++] = 0.0;
+    *n_history = cnt;
+    return SMG_OK;
+  }
+  history[cnt++] = std::sqrt(rr) / denom;
+  if (history[0] <= rtol) {
+    *n_history = cnt;
+    return SMG_OK;
+  }
+  SMG_TRY(precond(r, z));
+  SMG_CUDA(cudaMemcpyAsync(d, z, sizeof(double) * (size_t)n, cudaMemcpyDeviceToDevice, st));
+  double rz = 0;
+  SMG_TRY(dots.dot(n, r, z, st, &rz));
+  for (int k = 0; k < maxit; ++k) {
+    EpiArgs em;
+    em.out = q;
+    SMG_CUDA(launch_csr_stream(A.a, d, Epi::kSpmv, em, st));
+    double curvature = 0;
+    SMG_TRY(dots.dot(n, d, q, st, &curvature));
+    if (curvature <= 0.0) {
+      if (bad_iteration) *bad_iteration = k;
+      if (bad_curvature) *bad_curvature = curvature;
+      *n_history = cnt;
+      char buf[160];
+      snprintf(buf, sizeof buf,
+               "non-positive curvature p'Ap = %.6e at CG iteration %d; operator is not positive definite",
+               curvature, k);
+      set_error(buf);
+      return SMG_ERR_INDEFINITE;
+    }
+    const double alpha = rz / curvature;
+    SMG_CUDA(launch_axpby(n, alpha, d, 0.0, x, 0, st));
+    SMG_CUDA(launch_axpby(n, alpha, q, 0.0, r, 1, st));
+    SMG_TRY(dots.dot(n, r, r, st, &rr));
+    history[cnt++] = std::sqrt(rr) / denom;
+    if (history[cnt - 1] <= rtol) break;
+    SMG_TRY(precond(r, z));
+    double rz_new = 0;
+    SMG_TRY(dots.dot(n, r, z, st, &rz_new));
+    SMG_CUDA(launch_axpby(n, 0.0, z, rz_new / rz, d, 2, st));
+    rz = rz_new;
+  }
+  *n_history = cnt;
+  return SMG_OK;
+}
+
+int smg_dot(int64_t n, const double* x, const double* y, double* result_host, void* stream)
+{
+  if (!result_host) return fail("result is NULL");
+  std::lock_guard<std::mutex> lk(g_scratch_mu);
+  return g_dots.dot(n, x, y, as_stream(stream), result_host);
+}
+
+}  // extern "C"

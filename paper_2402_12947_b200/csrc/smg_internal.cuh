@@ -1,0 +1,115 @@
+// Internal types shared by the sm_100a kernels and the C-ABI layer.
+// Nothing here crosses the library boundary (include/simplexmg_b200.h is the
+// only public surface).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace smg {
+
+// ---------------------------------------------------------------------------
+// CSR-stream partition.  A "tile" is a run of consecutive rows owned by one
+// CTA: at most kRowsPerTile rows and (unless a single row is longer) at most
+// kTileNnz nonzeros.  The CTA streams the tile's values/columns with
+// coalesced loads into shared memory as exact products val*x[col], then every
+// thread sums its own row sequentially in column order -- the order scipy's
+// csr_matvec uses -- so results are bit-identical to the reference.
+constexpr int kThreads = 256;        // one row per thread at most
+constexpr int kRowsPerTile = kThreads;
+constexpr int kTileNnz = 2048;       // products staged per pass (16 KB smem)
+constexpr int kItems = kTileNnz / kThreads;
+
+struct DevCsr {
+  int64_t nrows = 0, ncols = 0, nnz = 0;
+  const int64_t* rowptr = nullptr;   // nrows + 1
+  const int32_t* col = nullptr;      // nnz
+  const double* val = nullptr;       // nnz
+  const int32_t* tile_row = nullptr; // ntiles + 1 (row boundaries of tiles)
+  int32_t ntiles = 0;
+};
+
+// Host-side owner of one operator's device arrays.
+struct Operator {
+  DevCsr a;                 // the matrix
+  bool has_t = false;
+  DevCsr t;                 // CSR of the transpose (restriction P^T), fine index ascending
+  int64_t first_zero_diag = -1;   // -1: every row has a nonzero diagonal
+  int64_t device_bytes = 0;
+  std::vector<void*> allocs;
+};
+
+struct Correction {
+  int64_t n_global = 0;
+  int32_t n_regions = 0;
+  int64_t m = 0;                 // total patch dofs
+  int32_t max_dofs = 0;
+  const int32_t* pptr = nullptr;   // n_regions + 1
+  const int32_t* dofs = nullptr;   // m (global dof of each patch slot)
+  const int64_t* foff = nullptr;   // n_regions + 1, offsets into packed factors
+  const double* lfac = nullptr;    // packed lower factors, row-major
+  double* rbuf = nullptr;          // m scratch (patch residual / correction)
+  bool coupled = true;             // some A[B_d, B_d'] != 0 (d != d')
+  const Operator* op = nullptr;
+  int64_t device_bytes = 0;
+  std::vector<void*> allocs;
+};
+
+enum SmootherKind : int { kChebyshev = 0, kJacobi = 1 };
+
+struct Smoother {
+  int kind = kChebyshev;
+  int sweeps = 1;
+  double lambda_max = 0.0;
+  double lambda_min_fraction = 0.1;
+};
+
+// error reporting (thread-local last error)
+void set_error(const std::string& msg);
+int fail(const std::string& msg);
+int check_cuda(cudaError_t e, const char* what);
+
+// ---------------------------------------------------------------------------
+// kernel launchers (spmv_kernels.cu)
+enum class Epi : int {
+  kSpmv = 0,       // y = s
+  kResidual,       // y = b - s
+  kJacobi,         // u_out = u_in + (inv_d * (b - s)) / theta
+  kChebFirst,      // d = (inv_d * (b - s)) / theta ; u_out = u_in + d
+  kChebNext,       // z = inv_d * (b - s) ; d = c1*d + c2*z ; u_out = u_in + d
+  kAddTo,          // y = y + s  (prolong-add)
+};
+
+struct EpiArgs {
+  const double* b = nullptr;
+  const double* u_in = nullptr;
+  double* out = nullptr;   // y / r / u_out
+  double* d = nullptr;
+  double theta = 1.0, c1 = 0.0, c2 = 0.0;
+};
+
+cudaError_t launch_csr_stream(const DevCsr& m, const double* x, Epi epi, const EpiArgs& ea,
+                              cudaStream_t s);
+
+// patch kernels (patch_kernels.cu)
+cudaError_t launch_patch_residual(const DevCsr& a, const Correction& c, const double* b,
+                                  const double* u, cudaStream_t s);
+cudaError_t launch_gather(const int32_t* idx, int64_t m, const double* src, double* dst,
+                          cudaStream_t s);
+cudaError_t launch_patch_solve(const Correction& c, double* u_add, double* out_scatter,
+                               cudaStream_t s);
+
+// dense / reduction kernels (dense_kernels.cu)
+cudaError_t launch_dense_gemv(int64_t n, const double* m, const double* x, double* y,
+                              cudaStream_t s);
+cudaError_t launch_dense_gemv_add(int64_t n, const double* m, const double* x, double* y,
+                                  cudaStream_t s);
+cudaError_t launch_dot(int64_t n, const double* a, const double* b, double* partials,
+                       unsigned int* counter, double* result, cudaStream_t s);
+cudaError_t launch_axpby(int64_t n, double alpha, const double* x, double beta, double* y,
+                         int mode, cudaStream_t s);
+constexpr int kDotBlocks = 296;   // fixed grid => deterministic reduction order
+
+}  // namespace smg

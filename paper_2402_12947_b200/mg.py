@@ -1,0 +1,341 @@
+"""Multigrid hierarchy and V-cycle solvers behind the reference's ``simplexmg.mg`` API.
+
+Mirrors ``pkg/src/simplexmg/mg.py`` (paths relative to
+/root/reference/pkg/src/simplexmg): ``Level`` / ``Hierarchy`` (:30-69),
+``build_hierarchy`` (:72-124, setup on the host), ``vcycle`` (:127-151),
+``solve_stationary`` (:154-175) and ``as_preconditioner`` (:178-184).
+
+The solvers run entirely on the GPU through the C-ABI's device hierarchy
+(``smg_hierarchy``): every level's operator, CSR(P^T) restriction, packed
+patch factors and the dense coarse inverse live in HBM, and one V-cycle is a
+single CUDA-graph launch.  ``DeviceHierarchy.from_reference(h)`` accepts the
+reference's own ``Hierarchy`` object (duck-typed), so a reference user swaps
+``simplexmg.mg.vcycle`` for ``paper_2402_12947_b200.mg.vcycle`` unchanged.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import weakref
+from dataclasses import dataclass, field, replace
+from typing import Callable, List, Optional, Sequence, Tuple
+
+import numpy as np
+import scipy.linalg
+
+from . import _lib
+from . import device as _dev
+from .sparse import CsrMatrix, DenseFactor, dense_factor
+from .smoothers import (KIND_CODE, LocalCorrection, SmootherConfig, ZeroDiagonalError,
+                        combined_smooth)
+
+_f64p = ctypes.POINTER(ctypes.c_double)
+
+
+@dataclass(frozen=True, eq=False)
+class Prolongation:
+    """Interpolation matrix from a coarse dof space into a finer one (transfer.py:104-114)."""
+
+    matrix: CsrMatrix
+    fine_level: Optional[int] = None
+    coarse_level: Optional[int] = None
+
+    @property
+    def shape(self) -> tuple:
+        return self.matrix.shape
+
+
+@dataclass(eq=False)
+class Level:
+    """One grid level (mg.py:30-48)."""
+
+    index: int
+    mesh: object
+    dofmap: object
+    a: CsrMatrix
+    prolongation: Optional[Prolongation]
+    smoother: SmootherConfig
+    regions: object
+    local_correction: Optional[LocalCorrection]
+    sgs: object = None
+    lambda_max: Optional[float] = None
+    lambda_max_adjusted: Optional[float] = None
+
+    def smooth(self, b, u):
+        return combined_smooth(self.a, b, u, self.local_correction, self.smoother, self.sgs)
+
+
+@dataclass(eq=False)
+class Hierarchy:
+    """Levels fine to coarse plus the factored coarsest operator (mg.py:51-69)."""
+
+    levels: List[Level]
+    coarse_factor: DenseFactor
+    system: object = None
+    coarse_refine: bool = False
+
+    @property
+    def n_levels(self) -> int:
+        return len(self.levels)
+
+    @property
+    def fine(self) -> Level:
+        return self.levels[0]
+
+    @property
+    def rhs(self) -> np.ndarray:
+        return self.system.b
+
+    def device(self) -> "DeviceHierarchy":
+        return _device_for(self)
+
+
+def coarse_inverse(coarse_factor) -> np.ndarray:
+    """Dense A_L^{-1} from the reference's Cholesky factor (mg.py:123) via
+    LAPACK dpotri (setup).  ``coarse_factor.factor = (c, lower)``."""
+    f = getattr(coarse_factor, "factor", coarse_factor)
+    kind = getattr(coarse_factor, "kind", "cholesky")
+    if kind != "cholesky":
+        raise NotImplementedError("coarse operator is not SPD (LU fallback): not on the GPU hot path")
+    c, lower = f
+    c = np.asarray(c, dtype=np.float64)
+    lo = np.asfortranarray(np.tril(c) if lower else np.triu(c).T)
+    inv, info = scipy.linalg.lapack.dpotri(lo, lower=1)
+    if info != 0:
+        raise RuntimeError(f"dpotri failed with info={info}")
+    tri = np.tril(inv)
+    full = tri + tri.T
+    full[np.diag_indices_from(full)] = np.diag(tri)
+    return np.ascontiguousarray(full)
+
+
+class DeviceHierarchy:
+    """Device-resident hierarchy (smg_hierarchy): the object the solvers run on."""
+
+    def __init__(self, levels, coarse_factor, coarse_refine: bool = False, use_graphs: bool = True,
+                 coarse_inv: Optional[np.ndarray] = None):
+        _dev.require_cuda()
+        lib = _lib.load()
+        nl = len(levels)
+        if nl < 2:
+            raise ValueError(f"a hierarchy needs at least 2 meshes, got {nl}")
+        self.ops, self.prols, self.corrs = [], [], []
+        kinds, sweeps, lmax, frac = [], [], [], []
+        for l, lv in enumerate(levels):
+            op = _dev.device_operator(lv.a)
+            self.ops.append(op)
+            if l < nl - 1:
+                self.prols.append(_dev.device_operator(lv.prolongation.matrix, with_transpose=True))
+                lc = lv.local_correction
+                self.corrs.append(_dev.device_correction(lv.a, lc)
+                                  if lc is not None and len(lc.regions) > 0 else None)
+                cfg = SmootherConfig.from_any(lv.smoother)
+                if cfg.kind == "sgs":
+                    raise NotImplementedError("symmetric Gauss-Seidel is outside the GPU hot path")
+                lm, fr = cfg.chebyshev_parameters()
+                if lm is None or lm <= 0:
+                    raise ValueError("chebyshev_smooth requires a positive cfg.lambda_max")
+                if op.first_zero_diag >= 0:
+                    raise ZeroDiagonalError(int(op.first_zero_diag))
+                kinds.append(KIND_CODE[cfg.kind])
+                sweeps.append(int(cfg.sweeps))
+                lmax.append(float(lm))
+                frac.append(float(fr))
+            else:
+                self.prols.append(None)
+                self.corrs.append(None)
+                kinds.append(0)
+                sweeps.append(1)
+                lmax.append(1.0)
+                frac.append(0.1)
+        self.n = [op.nrows for op in self.ops]
+        inv = coarse_inverse(coarse_factor) if coarse_inv is None else coarse_inv
+        n_c = self.n[-1]
+        if inv.shape != (n_c, n_c):
+            raise ValueError("coarse factor does not match the coarsest operator")
+        self.coarse_inv = np.ascontiguousarray(inv)
+        VP = ctypes.c_void_p * nl
+        a_arr = VP(*[op.handle.value for op in self.ops])
+        p_arr = VP(*[(p.handle.value if p is not None else None) for p in self.prols])
+        c_arr = VP(*[(c.handle.value if c is not None else None) for c in self.corrs])
+        IA = ctypes.c_int * nl
+        DA = ctypes.c_double * nl
+        h = ctypes.c_void_p()
+        _lib.check(lib.smg_hierarchy_create(
+            nl, ctypes.cast(a_arr, ctypes.POINTER(ctypes.c_void_p)),
+            ctypes.cast(p_arr, ctypes.POINTER(ctypes.c_void_p)),
+            ctypes.cast(c_arr, ctypes.POINTER(ctypes.c_void_p)),
+            IA(*kinds), IA(*sweeps), DA(*lmax), DA(*frac), n_c,
+            self.coarse_inv.ctypes.data_as(_f64p), 1 if coarse_refine else 0, ctypes.byref(h)))
+        self.handle = h
+        self._finalizer = weakref.finalize(self, lib.smg_hierarchy_destroy, h)
+        self.set_graphs(use_graphs)
+
+    @classmethod
+    def from_reference(cls, h, coarse_refine: bool = False, use_graphs: bool = True):
+        """Upload a reference ``simplexmg.mg.Hierarchy`` (or this package's)."""
+        return cls(h.levels, h.coarse_factor, coarse_refine=coarse_refine, use_graphs=use_graphs)
+
+    def set_graphs(self, enable: bool) -> None:
+        _lib.check(_lib.load().smg_hierarchy_set_graphs(self.handle, 1 if enable else 0))
+
+    def launches_per_vcycle(self) -> int:
+        n = ctypes.c_int64()
+        _lib.check(_lib.load().smg_hierarchy_launches_per_vcycle(self.handle, ctypes.byref(n)))
+        return int(n.value)
+
+    @property
+    def n_levels(self) -> int:
+        return len(self.ops)
+
+    # -- solvers --------------------------------------------------------------
+    def vcycle(self, b, u):
+        n0 = self.n[0]
+        lib = _lib.load()
+        t = _dev.torch()
+        if isinstance(u, t.Tensor):
+            bt, _ = _dev.as_device_vector(b, n0, "b")
+            ut, _ = _dev.as_device_vector(u, n0, "u")
+            _lib.check(lib.smg_vcycle(self.handle, _dev.ptr(bt), _dev.ptr(ut),
+                                      _dev.stream_handle()))
+            return u
+        bh = np.ascontiguousarray(np.asarray(b, dtype=np.float64))
+        if bh.shape != (n0,) or np.shape(u) != (n0,):
+            raise ValueError(f"dimension mismatch: fine level has {n0} dofs")
+        if not (isinstance(u, np.ndarray) and u.dtype == np.float64 and u.flags.c_contiguous):
+            raise ValueError("u must be a contiguous float64 numpy array (updated in place)")
+        _lib.check(lib.smg_vcycle_host(self.handle, bh.ctypes.data_as(_f64p),
+                                       u.ctypes.data_as(_f64p), _dev.stream_handle()))
+        return u
+
+    def solve_stationary(self, b, u0, rtol: float = 1e-10, max_cycles: int = 100):
+        n0 = self.n[0]
+        t = _dev.torch()
+        bt, host = _dev.as_device_vector(b, n0, "b")
+        u0t, _ = _dev.as_device_vector(u0, n0, "u0")
+        u = u0t.clone()
+        hist = np.zeros(max_cycles + 2)
+        nh = ctypes.c_int()
+        _lib.check(_lib.load().smg_solve_stationary(
+            self.handle, _dev.ptr(bt), _dev.ptr(u), float(rtol), int(max_cycles),
+            hist.ctypes.data_as(_f64p), ctypes.byref(nh), _dev.stream_handle()))
+        history = [float(v) for v in hist[:nh.value]]
+        if host is not None or not isinstance(u0, t.Tensor):
+            return u.cpu().numpy(), history
+        return u, history
+
+    def as_preconditioner(self) -> Callable:
+        return as_preconditioner(self)
+
+
+def _signature(h) -> tuple:
+    sig = []
+    for lv in h.levels:
+        cfg = lv.smoother
+        sig.append((id(lv.a), id(lv.prolongation) if lv.prolongation is not None else None,
+                    id(lv.local_correction), cfg.kind, cfg.sweeps, cfg.lambda_max,
+                    cfg.lambda_min_fraction, getattr(cfg, "omega", None)))
+    sig.append(id(h.coarse_factor))
+    sig.append(bool(getattr(h, "coarse_refine", False)))
+    return tuple(sig)
+
+
+_dev_cache = {}
+
+
+def _device_for(h) -> DeviceHierarchy:
+    key = id(h)
+    sig = _signature(h)
+    hit = _dev_cache.get(key)
+    if hit is not None and hit[0]() is h and hit[1] == sig:
+        return hit[2]
+    dh = DeviceHierarchy(h.levels, h.coarse_factor,
+                         coarse_refine=bool(getattr(h, "coarse_refine", False)))
+    try:
+        ref = weakref.ref(h, lambda _r, k=key: _dev_cache.pop(k, None))
+    except TypeError:
+        ref = (lambda o=h: o)
+    _dev_cache[key] = (ref, sig, dh)
+    return dh
+
+
+def _as_device_hierarchy(obj) -> Optional[DeviceHierarchy]:
+    if isinstance(obj, DeviceHierarchy):
+        return obj
+    dh = getattr(obj, "_smg_device_hierarchy", None)
+    if dh is not None:
+        return dh
+    if hasattr(obj, "levels") and hasattr(obj, "coarse_factor"):
+        return _device_for(obj)
+    return None
+
+
+def vcycle(h, b, u):
+    """One V-cycle, ``u`` updated in place (mg.py:127-151)."""
+    return _as_device_hierarchy(h).vcycle(b, u)
+
+
+def solve_stationary(h, b, u0, rtol: float = 1e-10,
+                     max_cycles: int = 100) -> Tuple[np.ndarray, List[float]]:
+    """Repeat V-cycles until the relative residual drops below rtol (mg.py:154-175)."""
+    return _as_device_hierarchy(h).solve_stationary(b, u0, rtol, max_cycles)
+
+
+def as_preconditioner(h) -> Callable:
+    """r -> vcycle(0; r) (mg.py:178-184).  The callable carries its device
+    hierarchy so :func:`paper_2402_12947_b200.sparse.cg` runs it on-device."""
+    dh = _as_device_hierarchy(h)
+
+    def apply(r):
+        t = _dev.torch()
+        if isinstance(r, t.Tensor):
+            z = t.zeros_like(r)
+        else:
+            z = np.zeros_like(np.asarray(r, dtype=np.float64))
+        dh.vcycle(r, z)
+        return z
+
+    apply._smg_device_hierarchy = dh
+    return apply
+
+
+# ---------------------------------------------------------------------------
+# setup (host): mg.py:72-124 restated over this package's vectorised builders
+
+def build_hierarchy(meshes: Sequence, smoother: SmootherConfig, use_local_correction: bool,
+                    quality_threshold: float = 0.1, element_degree: int = 1,
+                    source=None, region_layers: int = 1,
+                    lambda_tol: float = 1e-8, coarse_refine: bool = False) -> Hierarchy:
+    """Poisson with homogeneous Dirichlet on every box face; fine to coarse meshes."""
+    from .fem import assemble_poisson, build_dofmap
+    from .mesh import identify_regions
+    from .smoothers import (adjusted_lambda_max, build_local_correction, dofs_for_regions,
+                            jacobi_lambda_max)
+    from .transfer import build_prolongation, coarsen_system
+    if len(meshes) < 2:
+        raise ValueError(f"a hierarchy needs at least 2 meshes, got {len(meshes)}")
+    dofmaps = [build_dofmap(m, element_degree) for m in meshes]
+    system = assemble_poisson(meshes[0], dofmaps[0], source)
+    operators = [system.a]
+    prolongations = []
+    for l in range(len(meshes) - 1):
+        p = build_prolongation(dofmaps[l], meshes[l + 1], dofmaps[l + 1])
+        prolongations.append(Prolongation(p, l, l + 1))
+        operators.append(coarsen_system(operators[l], p))
+    levels = []
+    for l, (mesh, dofmap, a) in enumerate(zip(meshes, dofmaps, operators)):
+        regions = identify_regions(mesh, quality_threshold, layers=region_layers)
+        dof_sets = dofs_for_regions(dofmap, mesh, regions)
+        correction = None
+        if use_local_correction and dof_sets:
+            correction = build_local_correction(a, dof_sets)
+        lam = lam_adj = None
+        cfg = smoother
+        if smoother.kind == "chebyshev":
+            lam = jacobi_lambda_max(a, lambda_tol)
+            lam_adj = adjusted_lambda_max(a, dof_sets, lambda_tol) if dof_sets else lam
+            cfg = replace(smoother, lambda_max=lam_adj if smoother.adjusted else lam)
+        prol = prolongations[l] if l < len(prolongations) else None
+        levels.append(Level(l, mesh, dofmap, a, prol, cfg, regions, correction, None, lam, lam_adj))
+    coarse = dense_factor(operators[-1].to_dense())
+    return Hierarchy(levels, coarse, system, coarse_refine)

@@ -1,0 +1,74 @@
+"""Host setup (vectorised mesh / FEM / transfer / regions) against the
+reference-built hierarchies stored in tests/golden (c1s, c2s, c3s were
+assembled, transferred and Galerkin-coarsened by the reference itself from
+the same meshes).  Setup is not the hot path; these tests pin that the
+bench's full-size hierarchies are the ones the reference would build."""
+
+import numpy as np
+import pytest
+
+from paper_2402_12947_b200 import configs
+from paper_2402_12947_b200.mesh import generate_simplex_grid, identify_regions, radius_ratios
+from tests.golden import fixtures, refshim
+
+CASES = [("c1s", configs.C1.scaled(4), 1), ("c2s", configs.C2.scaled(8), 2),
+         ("c3s", configs.C3.scaled(4), 1)]
+
+
+def _rel_csr(m, ref):
+    assert m.nrows == ref.nrows and m.ncols == ref.ncols
+    assert np.array_equal(m.row_offsets, ref.row_offsets)
+    assert np.array_equal(m.col_indices, ref.col_indices)
+    return float(np.max(np.abs(m.values - ref.values)) / np.max(np.abs(ref.values)))
+
+
+@pytest.mark.parametrize("name,wl,layers", CASES)
+def test_own_setup_matches_reference_hierarchy(name, wl, layers):
+    z, ref = fixtures.load(name)
+    h, b, u0 = configs.build(wl)
+    assert len(h.levels) == len(ref.levels)
+    for lv, rl in zip(h.levels, ref.levels):
+        assert _rel_csr(lv.a, rl.a) <= 1e-12
+        if rl.prolongation is not None:
+            assert _rel_csr(lv.prolongation.matrix, rl.prolongation.matrix) <= 1e-13
+        nref = 0 if rl.local_correction is None else len(rl.local_correction.regions)
+        nown = 0 if lv.local_correction is None else len(lv.local_correction.regions)
+        assert nref == nown
+        for (i1, _), (i2, _) in zip(lv.local_correction.regions if nown else [],
+                                    rl.local_correction.regions if nref else []):
+            assert np.array_equal(i1, i2)
+    assert np.array_equal(b, z["g/b"])
+
+
+@pytest.mark.skipif(not refshim.available(), reason="reference not present")
+@pytest.mark.parametrize("dim,n", [(2, 1), (2, 5), (3, 1), (3, 3)])
+def test_grid_matches_reference(dim, n):
+    sm = refshim.import_reference()
+    r = sm.mesh.generate_simplex_grid(dim, n)
+    m = generate_simplex_grid(dim, n)
+    assert np.array_equal(m.vertices, r.vertices)
+    assert np.array_equal(m.cells, r.cells)
+    assert np.array_equal(m.boundary_facets, r.boundary_facets)
+    assert np.array_equal(m.facet_markers, r.facet_markers)
+    np.testing.assert_allclose(radius_ratios(m), sm.mesh.radius_ratios(r), rtol=1e-14)
+
+
+@pytest.mark.skipif(not refshim.available(), reason="reference not present")
+def test_regions_match_reference():
+    sm = refshim.import_reference()
+    wl = configs.C1.scaled(4)
+    mesh = configs.build_meshes(wl)[0]
+    rmesh = sm.mesh.SimplexMesh(mesh.dim, mesh.vertices, mesh.cells, mesh.boundary_facets,
+                                mesh.facet_markers)
+    ref = sm.mesh.identify_regions(rmesh, 0.1)
+    own = identify_regions(mesh, 0.1)
+    assert set(own.omega_b.tolist()) == set(ref.omega_b)
+    assert [sorted(r.tolist()) for r in own.omega_B_regions] == [sorted(r) for r in ref.omega_B_regions]
+
+
+def test_workload_shapes():
+    """The full-size constructions have the BASELINE sizes (grid arithmetic only)."""
+    assert (2 * configs.C2.grids[0] + 1) ** 2 == 1050625
+    assert (configs.C1.grids[0] + 1) ** 2 == 16641
+    assert (configs.C3.grids[0] + 1) ** 3 == 274625
+    assert (2 * configs.C4.grids[0] + 1) ** 3 == 7189057
