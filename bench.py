@@ -1,0 +1,377 @@
+#!/usr/bin/env python
+"""Benchmark: combined-smoother V-cycles on one B200 (BASELINE.json configs[1] = C2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C2] [--impl reference]
+
+A step is one V-cycle (mg.py:127-151) of the C2 hierarchy (2D P2, 1,050,625
+fine DOFs, 5 levels, Chebyshev degree 3, 20 two-layer local-correction
+patches) with b and u resident in HBM; the whole cycle is one CUDA-graph
+launch through the C-ABI (smg_vcycle).  Every V-cycle touches ~3 GB, far more
+than the 126 MB L2, so no flush is needed between steps.
+
+Also measured in the same run (all reported in the one JSON line):
+  * roofline: the dominant kernel, the fine-level Chebyshev step
+    (csr_stream_kernel<ChebNext>, 12z + 44n algorithmic bytes per launch),
+    timed with CUDA events on the launching stream;
+  * sweeps_per_s: fine-level smoother sweeps/s (same loop);
+  * lc_share: fine-level local-correction applications' share of a V-cycle;
+  * e2e: V-cycles/s through smg_vcycle_host with HOST buffers (H2D of b and
+    u, V-cycle, D2H of u inside the timed region);
+  * cpu_baseline: the CPU oracle (oracle/, the reference algorithm restated
+    in numpy + C, bit-identical sparse arithmetic) on the host cores.
+`--impl reference` times that CPU implementation alone (rank 0; other ranks
+exit 0).  N > 1 GPUs run independent replicas (the path does not shard;
+DESIGN.md), timed on the device, max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "V-cycles/sec & smoother sweeps/sec (fp64) at 1 B200; SpMV HBM GB/s vs peak"
+UNIT = "V-cycles/s"
+
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.gpu)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sms, maxs, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sms.append(float(parts[1]))
+                maxs.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sms)) if sms else None,
+                "sm_max_mhz": max(maxs) if maxs else None,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _cheb_steps(cfg):
+    """(theta, [(c1, c2), ...]) exactly as smoothers.py:109-135 computes them."""
+    lam_max, frac = cfg.chebyshev_parameters()
+    lam_min = frac * lam_max
+    theta = 0.5 * (lam_max + lam_min)
+    delta = 0.5 * (lam_max - lam_min)
+    if delta == 0.0:
+        return theta, None
+    sigma = theta / delta
+    rho = 1.0 / sigma
+    out = []
+    for _ in range(cfg.sweeps - 1):
+        rho_next = 1.0 / (2.0 * sigma - rho)
+        out.append((rho_next * rho, 2.0 * rho_next / delta))
+        rho = rho_next
+    return theta, out
+
+
+def cpu_baseline(h, b, budget_s: float, threads: int):
+    """Oracle V-cycles on the host for ~budget_s seconds (at least one)."""
+    from oracle import oracle as O
+    O.set_threads(threads)
+    u = np.zeros(len(b))
+    O.vcycle(h, b, u)  # warm (builds transposes / caches)
+    n, t0 = 0, time.perf_counter()
+    while True:
+        O.vcycle(h, b, u)
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s:
+            break
+    return n / el, n, el, O.num_threads()
+
+
+def run_reference(args):
+    ws, rank, local = _dist()
+    if rank != 0:
+        return 0
+    from paper_2402_12947_b200 import configs
+    from oracle import oracle as O
+    wl = configs.WORKLOADS[args.workload]
+    h, b, u0 = configs.build(wl)
+    threads = len(os.sched_getaffinity(0))
+    O.set_threads(threads)
+    u = u0.copy()
+    t0 = time.perf_counter()
+    O.vcycle(h, b, u)
+    t_one = time.perf_counter() - t0
+    warm = min(args.warmup, 1)
+    for _ in range(warm):
+        O.vcycle(h, b, u)
+    steps = max(1, min(args.steps, int(90.0 / max(t_one, 1e-3))))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        O.vcycle(h, b, u)
+    el = time.perf_counter() - t0
+    value = steps / el
+    sample = (f"{steps} oracle V-cycles of {args.workload} (bounded sample of the {args.steps} "
+              f"requested; ~90 s cap), after {warm} warm-up")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+        "steps": steps, "warmup": warm, "ms_per_step": 1e3 * el / steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE C2 construction)",
+        "config": _config(wl, h),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": O.num_threads(), "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def _config(wl, h):
+    return {
+        "workload": f"{wl.name}: BASELINE configs[1] (2D Poisson P2, 513x513 vertex grid, "
+                    "jitter 0.2h, 20 collapsed-node clusters, 2-layer patches, Chebyshev "
+                    "degree 3, random N(0,1) RHS, 5-level non-nested Galerkin hierarchy)",
+        "levels_dofs": [lv.a.nrows for lv in h.levels],
+        "levels_nnz": [lv.a.nnz for lv in h.levels],
+        "patches": [0 if lv.local_correction is None else len(lv.local_correction.regions)
+                    for lv in h.levels],
+        "patch_dofs": int(sum(len(i) for i, _ in h.levels[0].local_correction.regions))
+        if h.levels[0].local_correction is not None else 0,
+        "l2": "no flush: inputs larger than L2 (~3 GB touched per V-cycle vs 126 MB L2)",
+        "parallelism": "replicas (one independent hierarchy per GPU)",
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--workload", default="C2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2402_12947_b200 as P
+    from paper_2402_12947_b200 import _lib, configs, device as D
+    from paper_2402_12947_b200.mg import DeviceHierarchy
+
+    wl = configs.WORKLOADS[args.workload]
+    t_setup = time.perf_counter()
+    h, b_host, u0 = configs.build(wl)
+    dh = DeviceHierarchy(h.levels, h.coarse_factor)
+    t_setup = time.perf_counter() - t_setup
+    lib = _lib.load()
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+    b = torch.from_numpy(b_host).cuda()
+    u = torch.zeros_like(b)
+    n0 = len(b_host)
+
+    # ---- headline: V-cycles with inputs resident in HBM
+    for _ in range(args.warmup):
+        _lib.check(lib.smg_vcycle(dh.handle, D.ptr(b), D.ptr(u), sh))
+    launches = dh.launches_per_vcycle()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        _lib.check(lib.smg_vcycle(dh.handle, D.ptr(b), D.ptr(u), sh))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1)
+    if ws > 1:
+        tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    ms_per_step = ms / args.steps
+    value = ws * args.steps / (ms / 1e3)
+
+    # ---- dominant kernel: fine-level Chebyshev step (K3), CUDA events on its stream
+    lv = h.levels[0]
+    op = dh.ops[0]
+    theta, steps = _cheb_steps(P.SmootherConfig.from_any(lv.smoother))
+    z, nn = op.nnz, op.nrows
+    ua = torch.randn(nn, dtype=torch.float64, device="cuda")
+    ub = torch.empty_like(ua)
+    dbuf = torch.zeros_like(ua)
+    reps = 300
+    if steps:
+        c1, c2 = steps[-1]
+        step_kind, bytes_per = 2, 12 * z + 44 * nn
+    else:
+        c1 = c2 = 0.0
+        step_kind, bytes_per = 0, 12 * z + 28 * nn
+    for i in range(10):
+        _lib.check(lib.smg_smoother_step(op.handle, D.ptr(b), D.ptr(ua), D.ptr(ub), D.ptr(dbuf),
+                                         step_kind, theta, c1, c2, sh))
+        ua, ub = ub, ua
+    torch.cuda.synchronize()
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k0.record(stream)
+    for i in range(reps):
+        _lib.check(lib.smg_smoother_step(op.handle, D.ptr(b), D.ptr(ua), D.ptr(ub), D.ptr(dbuf),
+                                         step_kind, theta, c1, c2, sh))
+        ua, ub = ub, ua
+    k1.record(stream)
+    torch.cuda.synchronize()
+    k_ms = k0.elapsed_time(k1) / reps
+    peak, peak_src = _peaks()
+    achieved = bytes_per / (k_ms / 1e3) / 1e9
+    sweeps_per_s = 1e3 / k_ms
+
+    # ---- fine-level local-correction share of a V-cycle (4 applications per cycle)
+    lc_share = None
+    if dh.corrs[0] is not None:
+        for _ in range(5):
+            _lib.check(lib.smg_local_correct(dh.corrs[0].handle, D.ptr(b), D.ptr(ua), sh))
+        torch.cuda.synchronize()
+        k0.record(stream)
+        for _ in range(reps):
+            _lib.check(lib.smg_local_correct(dh.corrs[0].handle, D.ptr(b), D.ptr(ua), sh))
+        k1.record(stream)
+        torch.cuda.synchronize()
+        lc_ms = k0.elapsed_time(k1) / reps
+        lc_share = 4 * lc_ms / ms_per_step
+
+    # ---- e2e through the host-buffer C-ABI call (pinned host memory)
+    bh = torch.from_numpy(b_host).pin_memory()
+    uh = torch.zeros(n0, dtype=torch.float64).pin_memory()
+    bnp, unp = bh.numpy(), uh.numpy()
+    e2e_steps = max(20, min(args.steps, 200))
+    for _ in range(3):
+        dh.vcycle(bnp, unp)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        dh.vcycle(bnp, unp)
+    e2e_s = time.perf_counter() - t0
+    e2e_val = e2e_s
+    if ws > 1:
+        tt = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_val = float(tt.item())
+    e2e = {"value": ws * e2e_steps / e2e_val, "unit": UNIT,
+           "h2d_bytes_per_step": 2 * 8 * n0, "d2h_bytes_per_step": 8 * n0,
+           "steps": e2e_steps, "path": "smg_vcycle_host (pinned numpy b, u)"}
+
+    # ---- CPU baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        threads = len(os.sched_getaffinity(0))
+        val, n_done, el, cores = cpu_baseline(h, b_host, args.cpu_budget, threads)
+        cpu = {"value": val, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"{n_done} oracle V-cycles of {args.workload} in {el:.1f} s "
+                         f"(sparse rows on {cores} OpenMP threads, numpy elementwise 1 thread)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded BASELINE C2 construction; random-N(0,1) RHS)",
+            "config": _config(wl, h),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "csr_stream_kernel<ChebNext> on the fine level",
+                         "bytes_per_launch": bytes_per, "us_per_launch": 1e3 * k_ms,
+                         "peak_source": peak_src, "nnz": z, "rows": nn,
+                         "nnz_per_row": z / nn},
+            "sweeps_per_s": sweeps_per_s,
+            "lc_share": lc_share,
+            "e2e": e2e,
+            "gpu_launches": launches * args.steps,
+            "launches_per_vcycle": launches,
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+            "setup_s": t_setup,
+        }
+        print(json.dumps(line))
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -87,6 +87,19 @@ SMG_API int smg_chebyshev_smooth(const smg_operator *a, const double *b, double 
                          double lambda_max, double lambda_min_fraction, double *work,
                          void *stream);
 
+/* One fused smoother step (the loop body of smoothers.py:120-135), for
+ * callers that drive the recurrence themselves and for per-kernel timing:
+ *   step 0: u_out = u_in + (D^-1 (b - A u_in)) / theta              (:123)
+ *   step 1: d = (D^-1 (b - A u_in)) / theta; u_out = u_in + d       (:128-129)
+ *   step 2: d = c1 d + c2 D^-1 (b - A u_in); u_out = u_in + d       (:132-134)
+ * u_out must not alias u_in (the reference forms A u before updating u). */
+#define SMG_STEP_JACOBI 0
+#define SMG_STEP_CHEB_FIRST 1
+#define SMG_STEP_CHEB_NEXT 2
+SMG_API int smg_smoother_step(const smg_operator *a, const double *b, const double *u_in,
+                              double *u_out, double *d, int step, double theta, double c1,
+                              double c2, void *stream);
+
 /* ---- local correction: LocalCorrection (smoothers.py:139-200) ------------
  * Region d owns the sorted dofs[region_offsets[d] .. region_offsets[d+1]) and
  * the dense row-major n_d x n_d array factors[factor_offsets[d] ..] whose

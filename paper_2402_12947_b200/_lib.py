@@ -43,6 +43,8 @@ PROTOTYPES = {
     "smg_prolong_add": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "smg_chebyshev_smooth": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, ctypes.c_double,
                                             ctypes.c_double, _vp, _vp]),
+    "smg_smoother_step": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, ctypes.c_int, ctypes.c_double,
+                                         ctypes.c_double, ctypes.c_double, _vp]),
     "smg_correction_create": (ctypes.c_int, [_vp, _i64, _i64p, _i64p, _i64p, _f64p, _pp]),
     "smg_correction_destroy": (ctypes.c_int, [_vp]),
     "smg_correction_info": (ctypes.c_int, [_vp, _i64p, _i64p, _intp, _i64p]),

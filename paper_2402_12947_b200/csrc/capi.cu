@@ -545,6 +545,31 @@ int smg_prolong_add(const smg_operator* p, const double* uc, double* uf, void* s
   return SMG_OK;
 }
 
+int smg_smoother_step(const smg_operator* a, const double* b, const double* u_in, double* u_out,
+                      double* d, int step, double theta, double c1, double c2, void* stream)
+{
+  if (!a) return fail("operator is NULL");
+  if (u_in == u_out) return fail("u_out must not alias u_in");
+  if (a->o.first_zero_diag >= 0) {
+    set_error("zero diagonal entry in row " + std::to_string(a->o.first_zero_diag));
+    return SMG_ERR_ZERO_DIAGONAL;
+  }
+  EpiArgs ea;
+  ea.b = b;
+  ea.u_in = u_in;
+  ea.out = u_out;
+  ea.d = d;
+  ea.theta = theta;
+  ea.c1 = c1;
+  ea.c2 = c2;
+  Epi e = step == SMG_STEP_JACOBI ? Epi::kJacobi
+          : step == SMG_STEP_CHEB_FIRST ? Epi::kChebFirst
+          : step == SMG_STEP_CHEB_NEXT ? Epi::kChebNext : Epi::kSpmv;
+  if (e == Epi::kSpmv) return fail("unknown smoother step");
+  SMG_CUDA(launch_csr_stream(a->o.a, u_in, e, ea, as_stream(stream)));
+  return SMG_OK;
+}
+
 static int check_square_diag(const Operator& o)
 {
   if (o.a.nrows != o.a.ncols) return fail("smoother needs a square operator");

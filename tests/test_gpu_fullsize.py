@@ -1,0 +1,107 @@
+"""BASELINE-size parity: C1 (16,641 DOFs) and C2 (1,050,625 DOFs) hierarchies
+built by this repo's setup, GPU path vs the CPU oracle on identical inputs,
+plus size-independent properties of the V-cycle.
+
+Bars: per-sweep vectors, restriction and prolongation bitwise; V-cycle
+<= 1e-12 relative; identical stationary and CG iteration counts (rtol 1e-10);
+linearity and exact-solution fixed point of the V-cycle.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.fixture(scope="module", params=["C1", "C2"])
+def case(request):
+    from paper_2402_12947_b200 import configs
+    h, b, u0 = configs.build(configs.WORKLOADS[request.param])
+    return request.param, h, b, u0
+
+
+def test_fine_level_sweeps_bitwise(case):
+    import paper_2402_12947_b200 as P
+    from oracle import oracle as O
+    name, h, b, u0 = case
+    lv = h.levels[0]
+    ur = np.random.default_rng(5).standard_normal(lv.a.nrows)
+    for k in range(1, lv.smoother.sweeps + 1):
+        u = ur.copy()
+        P.chebyshev_smooth(lv.a, b, u, k, lv.smoother)
+        ref = O.global_smooth(lv.a, b, ur.copy(), type(lv.smoother)(
+            lv.smoother.kind, k, lv.smoother.lambda_max, lv.smoother.lambda_min_fraction,
+            omega=lv.smoother.omega))
+        assert np.array_equal(u, ref), f"{name} sweep {k}"
+
+
+def test_transfers_bitwise(case):
+    import torch
+    from oracle import oracle as O
+    from paper_2402_12947_b200 import _lib, device as D
+    name, h, b, u0 = case
+    lib = _lib.load()
+    for lv in h.levels[:-1]:
+        pm = lv.prolongation.matrix
+        op = D.device_operator(pm, with_transpose=True)
+        r = np.random.default_rng(lv.index).standard_normal(pm.nrows)
+        uc = np.random.default_rng(100 + lv.index).standard_normal(pm.ncols)
+        rt, uct = torch.from_numpy(r).cuda(), torch.from_numpy(uc).cuda()
+        y = torch.empty(pm.ncols, dtype=torch.float64, device="cuda")
+        _lib.check(lib.smg_spmv_transpose(op.handle, D.ptr(rt), D.ptr(y), D.stream_handle()))
+        assert np.array_equal(y.cpu().numpy(), O.spmv_transpose(pm, r))
+        _lib.check(lib.smg_prolong_add(op.handle, D.ptr(uct), D.ptr(rt), D.stream_handle()))
+        ref = r.copy()
+        ref += O.spmv(pm, uc)
+        assert np.array_equal(rt.cpu().numpy(), ref)
+
+
+def test_vcycle_matches_oracle(case):
+    import paper_2402_12947_b200 as P
+    from oracle import oracle as O
+    name, h, b, u0 = case
+    ur = np.random.default_rng(6).standard_normal(len(b))
+    u = ur.copy()
+    P.vcycle(h, b, u)
+    assert rel(u, O.vcycle(h, b, ur.copy())) <= 1e-12
+
+
+def test_iteration_counts_match_oracle(case):
+    import paper_2402_12947_b200 as P
+    from oracle import oracle as O
+    name, h, b, u0 = case
+    _, hg = P.solve_stationary(h, b, u0, 1e-10, 100)
+    _, ho = O.solve_stationary(h, b, u0, 1e-10, 100)
+    assert len(hg) == len(ho) and hg[-1] <= 1e-10
+    np.testing.assert_allclose(hg, ho, rtol=1e-3)
+    _, cg_g = P.cg(h.levels[0].a, b, precond=P.as_preconditioner(h), rtol=1e-10, maxit=200)
+    _, cg_o = O.cg(h.levels[0].a, b, O.as_preconditioner(h), 1e-10, 200)
+    assert len(cg_g) == len(cg_o)
+
+
+def test_vcycle_linearity_and_fixed_point(case):
+    """mg.py:127-151 is affine in (b, u): E(u) = M u + N b.  Zero-initial-guess
+    V-cycles are linear in b (test_mg.py:132-142 analogue), and the exact
+    solution is a fixed point (test_mg.py:111-118)."""
+    import torch
+    import paper_2402_12947_b200 as P
+    name, h, b, u0 = case
+    dh = h.device()
+    n = len(b)
+    g = np.random.default_rng(8)
+    b1, b2 = g.standard_normal(n), g.standard_normal(n)
+    z1, z2, z12 = np.zeros(n), np.zeros(n), np.zeros(n)
+    dh.vcycle(b1, z1)
+    dh.vcycle(b2, z2)
+    dh.vcycle(2.0 * b1 - 3.0 * b2, z12)
+    assert rel(z12, 2.0 * z1 - 3.0 * z2) <= 1e-12
+    ustar = g.standard_normal(n)
+    ustar[h.system.dirichlet_dofs] = 0.0
+    bstar = P.spmv(h.levels[0].a, ustar)
+    u = ustar.copy()
+    dh.vcycle(bstar, u)
+    assert rel(u, ustar) <= 1e-11
