@@ -17,7 +17,6 @@
 
 namespace smg {
 
-cudaError_t configure_patch_solve_smem(size_t bytes);
 
 static thread_local std::string g_last_error;
 
@@ -91,9 +90,16 @@ static int build_devcsr(std::vector<void*>& allocs, int64_t& bytes, int64_t nrow
                         DevCsr* out)
 {
   const int64_t nnz = rowptr[nrows];
-  std::vector<int32_t> col32((size_t)nnz);
+  // padded so the TMA ring may read up to 16 B past the last element
+  std::vector<int32_t> col32((size_t)nnz + 4, 0);
   for (int64_t j = 0; j < nnz; ++j) col32[(size_t)j] = (int32_t)col64[j];
+  std::vector<double> valp((size_t)nnz + 2, 0.0);
+  if (nnz) std::memcpy(valp.data(), val, sizeof(double) * (size_t)nnz);
+  std::vector<int64_t> rpp((size_t)nrows + 3, nnz);
+  std::memcpy(rpp.data(), rowptr, sizeof(int64_t) * (size_t)(nrows + 1));
   std::vector<int32_t> tiles = make_tiles(nrows, rowptr);
+  std::vector<int64_t> tnz(tiles.size());
+  for (size_t i = 0; i < tiles.size(); ++i) tnz[i] = rowptr[tiles[i]];
   DevCsr d;
   d.nrows = nrows;
   d.ncols = ncols;
@@ -103,14 +109,17 @@ static int build_devcsr(std::vector<void*>& allocs, int64_t& bytes, int64_t nrow
   int32_t* c = nullptr;
   double* v = nullptr;
   int32_t* tr = nullptr;
-  SMG_TRY(dev_upload(allocs, bytes, rowptr, (size_t)nrows + 1, &rp));
-  SMG_TRY(dev_upload(allocs, bytes, col32.data(), (size_t)nnz, &c));
-  SMG_TRY(dev_upload(allocs, bytes, val, (size_t)nnz, &v));
+  int64_t* tz = nullptr;
+  SMG_TRY(dev_upload(allocs, bytes, rpp.data(), rpp.size(), &rp));
+  SMG_TRY(dev_upload(allocs, bytes, col32.data(), col32.size(), &c));
+  SMG_TRY(dev_upload(allocs, bytes, valp.data(), valp.size(), &v));
   SMG_TRY(dev_upload(allocs, bytes, tiles.data(), tiles.size(), &tr));
+  SMG_TRY(dev_upload(allocs, bytes, tnz.data(), tnz.size(), &tz));
   d.rowptr = rp;
   d.col = c;
   d.val = v;
   d.tile_row = tr;
+  d.tile_nz = tz;
   *out = d;
   return SMG_OK;
 }
@@ -193,9 +202,15 @@ static int enqueue_local_correct(const Correction& c, const double* b, double* u
                                  int64_t* launches)
 {
   if (c.n_regions == 0) return SMG_OK;
-  SMG_CUDA(launch_patch_residual(c.op->a, c, b, u, st));
-  SMG_CUDA(launch_patch_solve(c, u, nullptr, st));
-  *launches += 2;
+  if (c.coupled) {
+    // all residuals must see the pre-correction u: separate gather pass
+    SMG_CUDA(launch_patch_residual(c.op->a, c, b, u, st));
+    SMG_CUDA(launch_patch_solve(c, b, u, u, nullptr, false, st));
+    *launches += 2;
+  } else {
+    SMG_CUDA(launch_patch_solve(c, b, u, u, nullptr, true, st));
+    *launches += 1;
+  }
   return SMG_OK;
 }
 
@@ -706,9 +721,13 @@ int smg_correction_create(const smg_operator* a, int64_t n_regions, const int64_
     if (rc == SMG_OK) rc = dev_upload(c.allocs, c.device_bytes, poff.data(), poff.size(), &df);
     if (rc == SMG_OK) rc = dev_upload(c.allocs, c.device_bytes, packed.data(), packed.size(), &dl);
     if (rc == SMG_OK) rc = dev_alloc(c.allocs, c.device_bytes, (size_t)m, &c.rbuf);
-    if (rc == SMG_OK && (size_t)max_dofs * sizeof(double) > 48 * 1024)
-      rc = check_cuda(configure_patch_solve_smem((size_t)max_dofs * sizeof(double)),
-                      "patch solve shared memory");
+    if (rc == SMG_OK) {
+      c.pptr = dp;
+      c.dofs = dd;
+      c.foff = df;
+      c.lfac = dl;
+      rc = check_cuda(configure_patch_solve_smem(c), "patch solve shared memory");
+    }
   }
   if (rc != SMG_OK) {
     free_all(c.allocs);
@@ -751,7 +770,7 @@ int smg_apply_local_correction(const smg_correction* c, const double* r, double*
   if (cc.n_regions == 0) return SMG_OK;
   // rbuf[k] = r[dofs[k]], then the batched solves scatter into out
   SMG_CUDA(launch_gather(cc.dofs, cc.m, r, cc.rbuf, st));
-  SMG_CUDA(launch_patch_solve(cc, nullptr, out, st));
+  SMG_CUDA(launch_patch_solve(cc, nullptr, nullptr, nullptr, out, false, st));
   return SMG_OK;
 }
 

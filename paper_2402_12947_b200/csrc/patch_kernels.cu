@@ -52,21 +52,48 @@ constexpr int kSolveThreads = 256;
 constexpr int kSolveWarps = kSolveThreads / 32;
 
 // mode 0: u[dofs] += x ;  mode 1: out[dofs] = x
+// kFused: the CTA forms its own patch residual b - A u on its rows first
+// (valid when no other region's rows couple to this one through A, checked
+// at upload); otherwise the residuals come from patch_residual_kernel (rbuf).
+// The packed factor is staged in shared memory when it fits (<= ~236 dofs),
+// so the sequential panel solves never wait on HBM/L2; larger factors are
+// read through the same generic pointer from global memory.
+template <bool kFused>
 __global__ void __launch_bounds__(kSolveThreads)
-patch_solve_kernel(const int32_t* __restrict__ pptr, const int32_t* __restrict__ dofs,
-                   const int64_t* __restrict__ foff, const double* __restrict__ lfac,
-                   const double* __restrict__ rbuf, double* __restrict__ target, int mode)
+patch_solve_kernel(const DevCsr a, const int32_t* __restrict__ pptr,
+                   const int32_t* __restrict__ dofs, const int64_t* __restrict__ foff,
+                   const double* __restrict__ lfac, const double* __restrict__ b,
+                   const double* u_res, const double* __restrict__ rbuf,
+                   double* target, int mode, int64_t smem_tri_cap)
 {
-  extern __shared__ double s_x[];
+  extern __shared__ double s_dyn[];
   __shared__ double s_red[kSolveWarps][32];
   const int p = blockIdx.x;
   const int32_t k0 = pptr[p];
   const int n = pptr[p + 1] - k0;
-  const double* __restrict__ L = lfac + foff[p];
+  const double* __restrict__ Lg = lfac + foff[p];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
+  double* s_x = s_dyn;
+  const int64_t ntri = tri(n);
+  const bool staged = ntri <= smem_tri_cap;
+  double* s_L = s_dyn + ((n + 1) & ~1);
+  const double* L = staged ? s_L : Lg;
 
-  for (int i = threadIdx.x; i < n; i += kSolveThreads) s_x[i] = rbuf[k0 + i];
+  if (staged)
+    for (int64_t i = threadIdx.x; i < ntri; i += kSolveThreads) s_L[i] = __ldg(Lg + i);
+  if (kFused) {
+    for (int i = threadIdx.x; i < n; i += kSolveThreads) {
+      const int32_t g = dofs[k0 + i];
+      double sum = 0.0;
+      const int64_t e = a.rowptr[g + 1];
+      for (int64_t j = a.rowptr[g]; j < e; ++j)
+        sum = __dadd_rn(sum, __dmul_rn(__ldg(a.val + j), u_res[__ldg(a.col + j)]));
+      s_x[i] = __dsub_rn(b[g], sum);
+    }
+  } else {
+    for (int i = threadIdx.x; i < n; i += kSolveThreads) s_x[i] = rbuf[k0 + i];
+  }
   __syncthreads();
 
   // ---- forward: L y = r (left-looking over 32-row panels)
@@ -178,22 +205,46 @@ cudaError_t launch_gather(const int32_t* idx, int64_t m, const double* src, doub
   return cudaGetLastError();
 }
 
-// mode: u_add != nullptr -> u += x ; else out_scatter[dofs] = x
-cudaError_t launch_patch_solve(const Correction& c, double* u_add, double* out_scatter,
-                               cudaStream_t s)
+constexpr int64_t kSmemBudget = 220 * 1024;   // dynamic smem per CTA (of 227 KB)
+
+static size_t solve_smem(const Correction& c, int64_t* tri_cap)
+{
+  const int64_t xb = ((c.max_dofs + 1) & ~1) * (int64_t)sizeof(double);
+  int64_t cap = (kSmemBudget - xb) / (int64_t)sizeof(double);
+  const int64_t need = (int64_t)c.max_dofs * (c.max_dofs + 1) / 2;
+  if (cap < 0) cap = 0;
+  *tri_cap = cap;
+  const int64_t use = need < cap ? need : cap;
+  return (size_t)(xb + use * (int64_t)sizeof(double));
+}
+
+// u_add != nullptr -> u += x ; else out_scatter[dofs] = x.  fused: residual in-kernel.
+cudaError_t launch_patch_solve(const Correction& c, const double* b, const double* u_res,
+                               double* u_add, double* out_scatter, bool fused, cudaStream_t s)
 {
   if (c.n_regions == 0) return cudaSuccess;
-  const size_t smem = (size_t)c.max_dofs * sizeof(double);
+  int64_t cap = 0;
+  const size_t smem = solve_smem(c, &cap);
   const int mode = u_add ? 0 : 1;
-  patch_solve_kernel<<<c.n_regions, kSolveThreads, smem, s>>>(
-      c.pptr, c.dofs, c.foff, c.lfac, c.rbuf, u_add ? u_add : out_scatter, mode);
+  double* tgt = u_add ? u_add : out_scatter;
+  if (fused)
+    patch_solve_kernel<true><<<c.n_regions, kSolveThreads, smem, s>>>(
+        c.op->a, c.pptr, c.dofs, c.foff, c.lfac, b, u_res, c.rbuf, tgt, mode, cap);
+  else
+    patch_solve_kernel<false><<<c.n_regions, kSolveThreads, smem, s>>>(
+        c.op->a, c.pptr, c.dofs, c.foff, c.lfac, b, u_res, c.rbuf, tgt, mode, cap);
   return cudaGetLastError();
 }
 
-cudaError_t configure_patch_solve_smem(size_t bytes)
+cudaError_t configure_patch_solve_smem(const Correction& c)
 {
-  return cudaFuncSetAttribute(patch_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)bytes);
+  int64_t cap = 0;
+  const size_t smem = solve_smem(c, &cap);
+  cudaError_t e = cudaFuncSetAttribute(patch_solve_kernel<true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(patch_solve_kernel<false>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
 }  // namespace smg

@@ -21,6 +21,8 @@ constexpr int kThreads = 256;        // one row per thread at most
 constexpr int kRowsPerTile = kThreads;
 constexpr int kTileNnz = 2048;       // products staged per pass (16 KB smem)
 constexpr int kItems = kTileNnz / kThreads;
+constexpr int kStages = 3;           // TMA ring depth (tiles in flight per CTA)
+constexpr int kCtasPerSm = 2;        // persistent grid: 2 CTAs per SM
 
 struct DevCsr {
   int64_t nrows = 0, ncols = 0, nnz = 0;
@@ -28,6 +30,7 @@ struct DevCsr {
   const int32_t* col = nullptr;      // nnz
   const double* val = nullptr;       // nnz
   const int32_t* tile_row = nullptr; // ntiles + 1 (row boundaries of tiles)
+  const int64_t* tile_nz = nullptr;  // ntiles + 1 (rowptr at the tile boundaries)
   int32_t ntiles = 0;
 };
 
@@ -98,8 +101,9 @@ cudaError_t launch_patch_residual(const DevCsr& a, const Correction& c, const do
                                   const double* u, cudaStream_t s);
 cudaError_t launch_gather(const int32_t* idx, int64_t m, const double* src, double* dst,
                           cudaStream_t s);
-cudaError_t launch_patch_solve(const Correction& c, double* u_add, double* out_scatter,
-                               cudaStream_t s);
+cudaError_t launch_patch_solve(const Correction& c, const double* b, const double* u_res,
+                               double* u_add, double* out_scatter, bool fused, cudaStream_t s);
+cudaError_t configure_patch_solve_smem(const Correction& c);
 
 // dense / reduction kernels (dense_kernels.cu)
 cudaError_t launch_dense_gemv(int64_t n, const double* m, const double* x, double* y,

@@ -12,122 +12,281 @@
 //   (restriction P^T r runs kSpmv over the stored CSR(P^T), mg.py:142)
 //
 // Bitwise parity with the reference (scipy csr_matvec: per-row sequential sum
-// in column order, separately rounded multiply and add) drives the design:
-//   * phase 1: the CTA streams its tile's values and column indices with
-//     coalesced loads and stages the exact products val*x[col] (__dmul_rn) in
-//     shared memory -- independent roundings, so any thread may compute them;
+// in column order, separately rounded multiply and add):
+//   * phase 1: the tile's exact products val*x[col] (__dmul_rn) are formed by
+//     all threads and staged in shared memory -- products are independently
+//     rounded, so any thread may form any of them;
 //   * phase 2: each thread owns one row and adds that row's products in
 //     column order with __dadd_rn (no FMA contraction anywhere);
 //   * the epilogue reproduces numpy's elementwise expression order, with IEEE
 //     division (__ddiv_rn) for 1/a_ii and /theta.
-// The diagonal is picked from the row during phase 2 (no separate inv-diag
-// array is read).  Rows of any length are handled: a tile whose nonzeros
-// exceed kTileNnz is streamed in several passes, each thread continuing its
-// running sum, which keeps the column order.
+//
+// B200 data movement: the kernel is persistent (2 CTAs per SM, static
+// round-robin over tiles) and streams every tile's values, column indices and
+// row offsets HBM -> shared memory with 1D TMA bulk copies
+// (cp.async.bulk ... mbarrier::complete_tx) into a kStages-deep ring, issued
+// kStages tiles ahead by one elected thread, so HBM latency is overlapped with
+// the gather / sum / epilogue of earlier tiles.  Only the x gathers (L2/L1
+// resident) and the per-row epilogue vectors go through the LSU; the
+// epilogue operands are prefetched into registers before the tile's barrier
+// wait.  Tiles whose nonzeros exceed kTileNnz (a single row longer than the
+// ring slot) take a chunked fallback that reads global memory directly.
 #include "smg_internal.cuh"
 
 namespace smg {
 
+// ---------------------------------------------------------------------------
+// PTX helpers (mbarrier + 1D bulk TMA)
+__device__ __forceinline__ uint32_t smem_u32(const void* p)
+{
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count)
+{
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init()
+{
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes)
+{
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
+{
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
+{
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async()
+{
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
 template <Epi E>
-struct EpiNeedsDiag {
-  static constexpr bool value = (E == Epi::kJacobi || E == Epi::kChebFirst || E == Epi::kChebNext);
+struct EpiTraits {
+  static constexpr bool kDiag = (E == Epi::kJacobi || E == Epi::kChebFirst || E == Epi::kChebNext);
+  static constexpr bool kB = (E != Epi::kSpmv && E != Epi::kAddTo);
+  static constexpr bool kU = (E == Epi::kJacobi || E == Epi::kChebFirst || E == Epi::kChebNext);
+  static constexpr bool kD = (E == Epi::kChebNext);
+  static constexpr bool kOut = (E == Epi::kAddTo);
 };
 
+// ring-slot geometry (bytes are multiples of 16 as cp.async.bulk requires)
+constexpr int kValCap = kTileNnz + 2;        // doubles (start aligned down to 16 B)
+constexpr int kColCap = kTileNnz + 4;        // int32
+constexpr int kRpCap = kRowsPerTile + 4;     // int64 (rows r0..r1 inclusive + alignment)
+constexpr int kSlotBytes = kValCap * 8 + kColCap * 4 + kRpCap * 8;
+static_assert(kSlotBytes % 16 == 0, "slot must keep 16-byte alignment");
+constexpr int kSmemBytes = kStages * kSlotBytes + kTileNnz * 8;
+
 template <Epi E>
-__global__ void __launch_bounds__(kThreads)
-csr_stream_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea)
+__device__ __forceinline__ void epilogue(const DevCsr& m, const EpiArgs& ea, int32_t row, double sum,
+                                         double dg, double bv, double uv, double dv, double ov)
 {
-  constexpr bool kDiag = EpiNeedsDiag<E>::value;
-  __shared__ double s_prod[kTileNnz];
-  __shared__ int32_t s_col[kDiag ? kTileNnz : 1];
-
-  const int tile = blockIdx.x;
-  const int32_t r0 = m.tile_row[tile];
-  const int32_t r1 = m.tile_row[tile + 1];
-  const int32_t row = r0 + (int32_t)threadIdx.x;
-  const bool has_row = row < r1;
-  const int64_t base = m.rowptr[r0];
-  const int64_t end = m.rowptr[r1];
-  int64_t lo = 0, hi = 0;
-  if (has_row) {
-    lo = m.rowptr[row];
-    hi = m.rowptr[row + 1];
-  }
-
-  double sum = 0.0;
-  int64_t jdiag = -1;
-  for (int64_t cs = base; cs < end; cs += kTileNnz) {
-    const int64_t rem = end - cs;
-    const int cnt = rem < (int64_t)kTileNnz ? (int)rem : kTileNnz;
-    const int32_t* __restrict__ colp = m.col + cs;
-    const double* __restrict__ valp = m.val + cs;
-    // phase 1: coalesced streaming of (col, val), gather x, exact products
-    int32_t c[kItems];
-    double v[kItems];
-#pragma unroll
-    for (int it = 0; it < kItems; ++it) {
-      const int k = it * kThreads + (int)threadIdx.x;
-      c[it] = 0;
-      v[it] = 0.0;
-      if (k < cnt) {
-        c[it] = __ldg(colp + k);
-        v[it] = __ldg(valp + k);
-      }
-    }
-#pragma unroll
-    for (int it = 0; it < kItems; ++it) {
-      const int k = it * kThreads + (int)threadIdx.x;
-      if (k < cnt) {
-        const double xv = __ldg(x + c[it]);
-        s_prod[k] = __dmul_rn(v[it], xv);
-        if constexpr (kDiag) s_col[k] = c[it];
-      }
-    }
-    __syncthreads();
-    // phase 2: sequential per-row sum in column order
-    if (has_row) {
-      const int64_t a = lo > cs ? lo : cs;
-      const int64_t bnd = hi < cs + cnt ? hi : cs + cnt;
-      for (int64_t j = a; j < bnd; ++j) {
-        sum = __dadd_rn(sum, s_prod[j - cs]);
-        if constexpr (kDiag) {
-          if (s_col[j - cs] == row) jdiag = j;
-        }
-      }
-    }
-    __syncthreads();
-  }
-  if (!has_row) return;
-
   if constexpr (E == Epi::kSpmv) {
     ea.out[row] = sum;
   } else if constexpr (E == Epi::kResidual) {
-    ea.out[row] = __dsub_rn(ea.b[row], sum);
+    ea.out[row] = __dsub_rn(bv, sum);
   } else if constexpr (E == Epi::kAddTo) {
-    ea.out[row] = __dadd_rn(ea.out[row], sum);
+    ea.out[row] = __dadd_rn(ov, sum);
   } else {
-    const double dg = jdiag >= 0 ? m.val[jdiag] : 0.0;
     const double inv = __ddiv_rn(1.0, dg);
-    const double t = __dmul_rn(inv, __dsub_rn(ea.b[row], sum));
+    const double t = __dmul_rn(inv, __dsub_rn(bv, sum));
     if constexpr (E == Epi::kJacobi) {
-      ea.out[row] = __dadd_rn(ea.u_in[row], __ddiv_rn(t, ea.theta));
+      ea.out[row] = __dadd_rn(uv, __ddiv_rn(t, ea.theta));
     } else if constexpr (E == Epi::kChebFirst) {
       const double d = __ddiv_rn(t, ea.theta);
       ea.d[row] = d;
-      ea.out[row] = __dadd_rn(ea.u_in[row], d);
+      ea.out[row] = __dadd_rn(uv, d);
     } else {  // kChebNext
-      const double d = __dadd_rn(__dmul_rn(ea.c1, ea.d[row]), __dmul_rn(ea.c2, t));
+      const double d = __dadd_rn(__dmul_rn(ea.c1, dv), __dmul_rn(ea.c2, t));
       ea.d[row] = d;
-      ea.out[row] = __dadd_rn(ea.u_in[row], d);
+      ea.out[row] = __dadd_rn(uv, d);
     }
   }
 }
+
+// producer: issue the bulk copies of tile t into ring slot s
+__device__ __forceinline__ void issue_tile(const DevCsr& m, int t, unsigned char* slot,
+                                           uint64_t* bar)
+{
+  const int32_t r0 = m.tile_row[t];
+  const int32_t r1 = m.tile_row[t + 1];
+  const int64_t e0 = m.tile_nz[t];
+  const int64_t e1 = m.tile_nz[t + 1];
+  if (e1 - e0 > kTileNnz) {  // long tile: consumer reads global memory directly
+    mbar_arrive_expect_tx(bar, 0);
+    return;
+  }
+  const int64_t va = e0 & ~int64_t(1), vb = (e1 + 1) & ~int64_t(1);
+  const int64_t ca = e0 & ~int64_t(3), cb = (e1 + 3) & ~int64_t(3);
+  const int64_t ra = r0 & ~1, rb = (int64_t(r1) + 2) & ~int64_t(1);
+  const uint32_t bv = (uint32_t)((vb - va) * 8), bc = (uint32_t)((cb - ca) * 4),
+                 br = (uint32_t)((rb - ra) * 8);
+  mbar_arrive_expect_tx(bar, bv + bc + br);
+  double* sval = reinterpret_cast<double*>(slot);
+  int32_t* scol = reinterpret_cast<int32_t*>(slot + kValCap * 8);
+  int64_t* srp = reinterpret_cast<int64_t*>(slot + kValCap * 8 + kColCap * 4);
+  if (bv) bulk_g2s(sval, m.val + va, bv, bar);
+  if (bc) bulk_g2s(scol, m.col + ca, bc, bar);
+  bulk_g2s(srp, m.rowptr + ra, br, bar);
+}
+
+template <Epi E>
+__global__ void __launch_bounds__(kThreads, kCtasPerSm)
+csr_stream_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea)
+{
+  using T = EpiTraits<E>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint64_t bars[kStages];
+  double* s_prod = reinterpret_cast<double*>(smem + kStages * kSlotBytes);
+
+  const int ntiles = m.ntiles;
+  const int G = gridDim.x;
+  const int first = blockIdx.x;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      const int t = first + s * G;
+      if (t < ntiles) issue_tile(m, t, smem + s * kSlotBytes, &bars[s]);
+    }
+  }
+
+  int it = 0;
+  for (int t = first; t < ntiles; t += G, ++it) {
+    const int s = it % kStages;
+    const uint32_t parity = (uint32_t)((it / kStages) & 1);
+    unsigned char* slot = smem + s * kSlotBytes;
+    const int32_t r0 = m.tile_row[t];
+    const int32_t r1 = m.tile_row[t + 1];
+    const int32_t row = r0 + tid;
+    const bool has_row = row < r1;
+    // prefetch the row's epilogue operands while the tile is in flight
+    double bv = 0.0, uv = 0.0, dv = 0.0, ov = 0.0;
+    if (has_row) {
+      if constexpr (T::kB) bv = ea.b[row];
+      if constexpr (T::kU) uv = ea.u_in[row];
+      if constexpr (T::kD) dv = ea.d[row];
+      if constexpr (T::kOut) ov = ea.out[row];
+    }
+    const int64_t e0 = m.tile_nz[t];
+    const int64_t e1 = m.tile_nz[t + 1];
+    double sum = 0.0;
+    double dg = 0.0;
+    mbar_wait(&bars[s], parity);
+    if (e1 - e0 <= kTileNnz) {
+      const double* sval = reinterpret_cast<const double*>(slot) + (e0 & 1);
+      const int32_t* scol = reinterpret_cast<const int32_t*>(slot + kValCap * 8) + (e0 & 3);
+      const int64_t* srp =
+          reinterpret_cast<const int64_t*>(slot + kValCap * 8 + kColCap * 4) + (r0 & 1);
+      const int cnt = (int)(e1 - e0);
+      // phase 1: gather x, exact products
+#pragma unroll
+      for (int i = 0; i < kItems; ++i) {
+        const int k = i * kThreads + tid;
+        if (k < cnt) s_prod[k] = __dmul_rn(sval[k], __ldg(x + scol[k]));
+      }
+      __syncthreads();
+      // phase 2: sequential per-row sum in column order
+      if (has_row) {
+        const int a = (int)(srp[tid] - e0);
+        const int bnd = (int)(srp[tid + 1] - e0);
+        int jd = -1;
+        for (int j = a; j < bnd; ++j) {
+          sum = __dadd_rn(sum, s_prod[j]);
+          if constexpr (T::kDiag) {
+            if (scol[j] == row) jd = j;
+          }
+        }
+        if constexpr (T::kDiag) dg = jd >= 0 ? sval[jd] : 0.0;
+      }
+    } else {
+      // long tile (a row longer than one ring slot): chunked, global reads
+      int64_t lo = 0, hi = 0;
+      if (has_row) {
+        lo = m.rowptr[row];
+        hi = m.rowptr[row + 1];
+      }
+      int64_t jd = -1;
+      for (int64_t cs = e0; cs < e1; cs += kTileNnz) {
+        const int64_t rem = e1 - cs;
+        const int cnt = rem < (int64_t)kTileNnz ? (int)rem : kTileNnz;
+        for (int k = tid; k < cnt; k += kThreads)
+          s_prod[k] = __dmul_rn(__ldg(m.val + cs + k), __ldg(x + __ldg(m.col + cs + k)));
+        __syncthreads();
+        if (has_row) {
+          const int64_t a = lo > cs ? lo : cs;
+          const int64_t bnd = hi < cs + cnt ? hi : cs + cnt;
+          for (int64_t j = a; j < bnd; ++j) {
+            sum = __dadd_rn(sum, s_prod[j - cs]);
+            if constexpr (T::kDiag) {
+              if (__ldg(m.col + j) == row) jd = j;
+            }
+          }
+        }
+        __syncthreads();
+      }
+      if constexpr (T::kDiag) dg = jd >= 0 ? __ldg(m.val + jd) : 0.0;
+    }
+    if (has_row) epilogue<E>(m, ea, row, sum, dg, bv, uv, dv, ov);
+    __syncthreads();  // slot s and s_prod are free again
+    if (tid == 0) {
+      const int tn = t + kStages * G;
+      if (tn < ntiles) {
+        fence_proxy_async();
+        issue_tile(m, tn, slot, &bars[s]);
+      }
+    }
+  }
+}
+
+static int g_sm_count = 0;
 
 template <Epi E>
 static cudaError_t launch_t(const DevCsr& m, const double* x, const EpiArgs& ea, cudaStream_t s)
 {
   if (m.ntiles == 0) return cudaSuccess;
-  csr_stream_kernel<E><<<m.ntiles, kThreads, 0, s>>>(m, x, ea);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(csr_stream_kernel<E>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  if (g_sm_count == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sm_count <= 0) g_sm_count = 148;
+  }
+  int grid = g_sm_count * kCtasPerSm;
+  if (grid > m.ntiles) grid = m.ntiles;
+  csr_stream_kernel<E><<<grid, kThreads, kSmemBytes, s>>>(m, x, ea);
   return cudaGetLastError();
 }
 
