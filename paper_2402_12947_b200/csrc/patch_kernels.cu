@@ -6,38 +6,27 @@
 // the principal submatrix A[B_d, B_d] (smoothers.py:176-200, LAPACK dpotrs
 // via sparse.py:225-231).
 //
-// Two kernels, because regions are DOF-disjoint but may be coupled through A
-// (SURVEY.md section 8(a) A4): every patch residual must see the
-// pre-correction u.
-//   patch_residual_kernel  rbuf[k] = b[i] - (A u)[i] for every patch dof
-//                          i = dofs[k]; per-row sequential sum in column order
-//                          (bit-identical to the reference's full residual
-//                          restricted to patch rows).
-//   patch_solve_kernel     one CTA per region: forward substitution with the
-//                          packed row-major L_d, back substitution with L_d^T,
-//                          then u[i] += x (or out[i] = x).  32-wide panels:
-//                          off-panel updates are warp-cooperative, coalesced
-//                          reads of factor row segments; the panel triangle
-//                          is solved by one warp from registers with shuffles.
-// Dense solves are tolerance-parity (<= 1e-13 relative vs the oracle), not
+// One CTA per region.  Each CTA
+//   1. stages the packed lower factor L_d in shared memory when it fits
+//      (larger factors are read through the same generic pointer from HBM);
+//   2. forms the patch residual b - A u on its rows (the reference computes a
+//      full-length residual and keeps only these rows -- identical values):
+//      row bounds -> block scan -> all threads stream the rows' (val, col)
+//      segments and form exact products in shared memory -> each row is then
+//      summed sequentially in column order (bit-identical to scipy);
+//   3. forward substitution with L, back substitution with L^T, 32-row panels:
+//      off-panel updates are coalesced warp dot products, the panel triangle
+//      is solved by one warp from registers with shuffles;
+//   4. u[B_d] += x (or out[B_d] = x for apply_local_correction).
+// Regions are DOF-disjoint but may be coupled through A: when
+// the upload-time check finds coupling, the residuals of ALL regions are
+// formed first by a residual-only launch (every region sees the
+// pre-correction u), then the solve launch reads them from rbuf.
+// Dense solves are tolerance-parity (~1e-15 relative vs the oracle), not
 // bitwise: LAPACK's blocked order is not reproducible.
 #include "smg_internal.cuh"
 
 namespace smg {
-
-__global__ void patch_residual_kernel(const DevCsr a, const int32_t* __restrict__ dofs, int64_t m,
-                                      const double* __restrict__ b,
-                                      const double* __restrict__ u, double* __restrict__ rbuf)
-{
-  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= m) return;
-  const int32_t i = dofs[k];
-  double sum = 0.0;
-  const int64_t e = a.rowptr[i + 1];
-  for (int64_t j = a.rowptr[i]; j < e; ++j)
-    sum = __dadd_rn(sum, __dmul_rn(a.val[j], __ldg(u + a.col[j])));
-  rbuf[k] = __dsub_rn(b[i], sum);
-}
 
 __device__ __forceinline__ double warp_sum(double v)
 {
@@ -46,55 +35,148 @@ __device__ __forceinline__ double warp_sum(double v)
   return v;
 }
 
-__device__ __forceinline__ int64_t tri(int64_t i) { return i * (i + 1) / 2; }
+__host__ __device__ __forceinline__ int64_t tri(int64_t i) { return i * (i + 1) / 2; }
 
 constexpr int kSolveThreads = 256;
 constexpr int kSolveWarps = kSolveThreads / 32;
+constexpr int kProdCap = 2048;                 // residual products staged per pass
+constexpr int64_t kSmemBudget = 220 * 1024;    // dynamic smem per CTA (of 227 KB)
 
-// mode 0: u[dofs] += x ;  mode 1: out[dofs] = x
-// kFused: the CTA forms its own patch residual b - A u on its rows first
-// (valid when no other region's rows couple to this one through A, checked
-// at upload); otherwise the residuals come from patch_residual_kernel (rbuf).
-// The packed factor is staged in shared memory when it fits (<= ~236 dofs),
-// so the sequential panel solves never wait on HBM/L2; larger factors are
-// read through the same generic pointer from global memory.
-template <bool kFused>
-__global__ void __launch_bounds__(kSolveThreads)
-patch_solve_kernel(const DevCsr a, const int32_t* __restrict__ pptr,
-                   const int32_t* __restrict__ dofs, const int64_t* __restrict__ foff,
-                   const double* __restrict__ lfac, const double* __restrict__ b,
-                   const double* u_res, const double* __restrict__ rbuf,
-                   double* target, int mode, int64_t smem_tri_cap)
+enum PatchMode : int { kAddResidualSolve = 0, kSolveFromBuf = 1, kResidualOnly = 2 };
+
+// shared-memory carve-up for a region of at most nmax dofs
+struct PatchSmem {
+  int64_t x_off, lo_off, off_off, prod_off, l_off, tri_cap, bytes;
+};
+
+__host__ __device__ inline PatchSmem patch_smem_layout(int nmax)
 {
-  extern __shared__ double s_dyn[];
+  PatchSmem p;
+  const int64_t n2 = (nmax + 2) & ~int64_t(1);
+  p.x_off = 0;                                   // double[n2]
+  p.lo_off = p.x_off + 8 * n2;                   // int64[n2]
+  p.off_off = p.lo_off + 8 * n2;                 // int32[n2 + 2]
+  p.prod_off = p.off_off + ((4 * (n2 + 2) + 15) & ~int64_t(15));  // double[kProdCap]
+  p.l_off = p.prod_off + 8 * kProdCap;
+  int64_t cap = (kSmemBudget - p.l_off) / 8;
+  if (cap < 0) cap = 0;
+  p.tri_cap = cap;
+  const int64_t need = tri(nmax);
+  p.bytes = p.l_off + 8 * (need < cap ? need : cap);
+  return p;
+}
+
+// exclusive scan of len[0..n) into off[0..n], returns the total (block-wide)
+__device__ int block_scan(const int32_t* len, int32_t* off, int n, int* s_carry)
+{
+  __shared__ int s_warp[kSolveWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) *s_carry = 0;
+  __syncthreads();
+  for (int base = 0; base < n; base += kSolveThreads) {
+    const int i = base + threadIdx.x;
+    const int v = i < n ? len[i] : 0;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    int wpre = 0;
+    for (int w = 0; w < warp; ++w) wpre += s_warp[w];
+    int tot = 0;
+    for (int w = 0; w < kSolveWarps; ++w) tot += s_warp[w];
+    const int carry = *s_carry;
+    if (i < n) off[i] = carry + wpre + incl - v;
+    __syncthreads();
+    if (threadIdx.x == 0) *s_carry = carry + tot;
+    __syncthreads();
+  }
+  const int total = *s_carry;
+  if (threadIdx.x == 0) off[n] = total;
+  __syncthreads();
+  return total;
+}
+
+template <int kMode>
+__global__ void __launch_bounds__(kSolveThreads)
+patch_kernel(const DevCsr a, const int32_t* __restrict__ pptr, const int32_t* __restrict__ dofs,
+             const int64_t* __restrict__ foff, const double* __restrict__ lfac,
+             const double* __restrict__ b, const double* u_res, double* rbuf, double* target,
+             int scatter_add, int nmax)
+{
+  extern __shared__ __align__(16) unsigned char psm[];
   __shared__ double s_red[kSolveWarps][32];
+  __shared__ int s_carry;
+  const PatchSmem L_ = patch_smem_layout(nmax);
+  double* s_x = reinterpret_cast<double*>(psm + L_.x_off);
+  int64_t* s_lo = reinterpret_cast<int64_t*>(psm + L_.lo_off);
+  int32_t* s_off = reinterpret_cast<int32_t*>(psm + L_.off_off);
+  double* s_prod = reinterpret_cast<double*>(psm + L_.prod_off);
+  double* s_L = reinterpret_cast<double*>(psm + L_.l_off);
+
   const int p = blockIdx.x;
   const int32_t k0 = pptr[p];
   const int n = pptr[p + 1] - k0;
-  const double* __restrict__ Lg = lfac + foff[p];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  double* s_x = s_dyn;
   const int64_t ntri = tri(n);
-  const bool staged = ntri <= smem_tri_cap;
-  double* s_L = s_dyn + ((n + 1) & ~1);
-  const double* L = staged ? s_L : Lg;
+  const bool staged = kMode != kResidualOnly && ntri <= L_.tri_cap;
+  const double* __restrict__ Lg = lfac + foff[p];
 
-  if (staged)
-    for (int64_t i = threadIdx.x; i < ntri; i += kSolveThreads) s_L[i] = __ldg(Lg + i);
-  if (kFused) {
+  if (kMode != kSolveFromBuf) {
+    // ---- residual rows: bounds, scan, streamed products, ordered sums
+    int32_t* s_len = reinterpret_cast<int32_t*>(s_prod);  // temporary
     for (int i = threadIdx.x; i < n; i += kSolveThreads) {
       const int32_t g = dofs[k0 + i];
-      double sum = 0.0;
-      const int64_t e = a.rowptr[g + 1];
-      for (int64_t j = a.rowptr[g]; j < e; ++j)
-        sum = __dadd_rn(sum, __dmul_rn(__ldg(a.val + j), u_res[__ldg(a.col + j)]));
-      s_x[i] = __dsub_rn(b[g], sum);
+      const int64_t lo = a.rowptr[g];
+      s_lo[i] = lo;
+      s_len[i] = (int32_t)(a.rowptr[g + 1] - lo);
+      s_x[i] = 0.0;
     }
+    __syncthreads();
+    const int total = block_scan(s_len, s_off, n, &s_carry);
+    // stage the factor while the residual streams (independent loads)
+    if (staged)
+      for (int64_t i = threadIdx.x; i < ntri; i += kSolveThreads) s_L[i] = __ldg(Lg + i);
+    for (int c0 = 0; c0 < total; c0 += kProdCap) {
+      const int cnt = min(kProdCap, total - c0);
+      for (int e = threadIdx.x; e < cnt; e += kSolveThreads) {
+        const int eg = c0 + e;
+        int lo = 0, hi = n;  // last row r with s_off[r] <= eg
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (s_off[mid] <= eg) lo = mid; else hi = mid;
+        }
+        const int64_t j = s_lo[lo] + (eg - s_off[lo]);
+        s_prod[e] = __dmul_rn(__ldg(a.val + j), u_res[__ldg(a.col + j)]);
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < n; i += kSolveThreads) {
+        const int a0 = max(s_off[i], c0), a1 = min(s_off[i + 1], c0 + cnt);
+        double sum = s_x[i];
+        for (int e = a0; e < a1; ++e) sum = __dadd_rn(sum, s_prod[e - c0]);
+        s_x[i] = sum;
+      }
+      __syncthreads();
+    }
+    for (int i = threadIdx.x; i < n; i += kSolveThreads) {
+      const double r = __dsub_rn(b[dofs[k0 + i]], s_x[i]);
+      if (kMode == kResidualOnly)
+        rbuf[k0 + i] = r;
+      else
+        s_x[i] = r;
+    }
+    if (kMode == kResidualOnly) return;
   } else {
+    if (staged)
+      for (int64_t i = threadIdx.x; i < ntri; i += kSolveThreads) s_L[i] = __ldg(Lg + i);
     for (int i = threadIdx.x; i < n; i += kSolveThreads) s_x[i] = rbuf[k0 + i];
   }
   __syncthreads();
+  const double* L = staged ? s_L : Lg;
 
   // ---- forward: L y = r (left-looking over 32-row panels)
   for (int p0 = 0; p0 < n; p0 += 32) {
@@ -173,21 +255,11 @@ patch_solve_kernel(const DevCsr a, const int32_t* __restrict__ pptr,
 
   for (int i = threadIdx.x; i < n; i += kSolveThreads) {
     const int32_t g = dofs[k0 + i];
-    if (mode == 0)
+    if (scatter_add)
       target[g] = __dadd_rn(target[g], s_x[i]);
     else
       target[g] = s_x[i];
   }
-}
-
-cudaError_t launch_patch_residual(const DevCsr& a, const Correction& c, const double* b,
-                                  const double* u, cudaStream_t s)
-{
-  if (c.m == 0) return cudaSuccess;
-  const int threads = 128;
-  const int64_t blocks = (c.m + threads - 1) / threads;
-  patch_residual_kernel<<<(unsigned)blocks, threads, 0, s>>>(a, c.dofs, c.m, b, u, c.rbuf);
-  return cudaGetLastError();
 }
 
 __global__ void gather_kernel(const int32_t* __restrict__ idx, int64_t m,
@@ -205,17 +277,15 @@ cudaError_t launch_gather(const int32_t* idx, int64_t m, const double* src, doub
   return cudaGetLastError();
 }
 
-constexpr int64_t kSmemBudget = 220 * 1024;   // dynamic smem per CTA (of 227 KB)
-
-static size_t solve_smem(const Correction& c, int64_t* tri_cap)
+// residual-only pass (coupled regions): rbuf[k] = (b - A u)[dofs[k]]
+cudaError_t launch_patch_residual(const DevCsr& a, const Correction& c, const double* b,
+                                  const double* u, cudaStream_t s)
 {
-  const int64_t xb = ((c.max_dofs + 1) & ~1) * (int64_t)sizeof(double);
-  int64_t cap = (kSmemBudget - xb) / (int64_t)sizeof(double);
-  const int64_t need = (int64_t)c.max_dofs * (c.max_dofs + 1) / 2;
-  if (cap < 0) cap = 0;
-  *tri_cap = cap;
-  const int64_t use = need < cap ? need : cap;
-  return (size_t)(xb + use * (int64_t)sizeof(double));
+  if (c.n_regions == 0) return cudaSuccess;
+  const PatchSmem L = patch_smem_layout(c.max_dofs);
+  patch_kernel<kResidualOnly><<<c.n_regions, kSolveThreads, (size_t)L.l_off, s>>>(
+      a, c.pptr, c.dofs, c.foff, c.lfac, b, u, c.rbuf, nullptr, 0, c.max_dofs);
+  return cudaGetLastError();
 }
 
 // u_add != nullptr -> u += x ; else out_scatter[dofs] = x.  fused: residual in-kernel.
@@ -223,28 +293,30 @@ cudaError_t launch_patch_solve(const Correction& c, const double* b, const doubl
                                double* u_add, double* out_scatter, bool fused, cudaStream_t s)
 {
   if (c.n_regions == 0) return cudaSuccess;
-  int64_t cap = 0;
-  const size_t smem = solve_smem(c, &cap);
-  const int mode = u_add ? 0 : 1;
+  const PatchSmem L = patch_smem_layout(c.max_dofs);
   double* tgt = u_add ? u_add : out_scatter;
+  const int add = u_add ? 1 : 0;
   if (fused)
-    patch_solve_kernel<true><<<c.n_regions, kSolveThreads, smem, s>>>(
-        c.op->a, c.pptr, c.dofs, c.foff, c.lfac, b, u_res, c.rbuf, tgt, mode, cap);
+    patch_kernel<kAddResidualSolve><<<c.n_regions, kSolveThreads, (size_t)L.bytes, s>>>(
+        c.op->a, c.pptr, c.dofs, c.foff, c.lfac, b, u_res, c.rbuf, tgt, add, c.max_dofs);
   else
-    patch_solve_kernel<false><<<c.n_regions, kSolveThreads, smem, s>>>(
-        c.op->a, c.pptr, c.dofs, c.foff, c.lfac, b, u_res, c.rbuf, tgt, mode, cap);
+    patch_kernel<kSolveFromBuf><<<c.n_regions, kSolveThreads, (size_t)L.bytes, s>>>(
+        c.op->a, c.pptr, c.dofs, c.foff, c.lfac, b, u_res, c.rbuf, tgt, add, c.max_dofs);
   return cudaGetLastError();
 }
 
 cudaError_t configure_patch_solve_smem(const Correction& c)
 {
-  int64_t cap = 0;
-  const size_t smem = solve_smem(c, &cap);
-  cudaError_t e = cudaFuncSetAttribute(patch_solve_kernel<true>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(patch_solve_kernel<false>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const PatchSmem L = patch_smem_layout(c.max_dofs);
+  cudaError_t e = cudaFuncSetAttribute(patch_kernel<kAddResidualSolve>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(patch_kernel<kSolveFromBuf>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(patch_kernel<kResidualOnly>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.l_off);
+  return e;
 }
 
 }  // namespace smg

@@ -33,6 +33,8 @@
 // ring slot) take a chunked fallback that reads global memory directly.
 #include "smg_internal.cuh"
 
+#include <cstdlib>
+
 namespace smg {
 
 // ---------------------------------------------------------------------------
@@ -98,6 +100,7 @@ constexpr int kRpCap = kRowsPerTile + 4;     // int64 (rows r0..r1 inclusive + a
 constexpr int kSlotBytes = kValCap * 8 + kColCap * 4 + kRpCap * 8;
 static_assert(kSlotBytes % 16 == 0, "slot must keep 16-byte alignment");
 constexpr int kSmemBytes = kStages * kSlotBytes + kTileNnz * 8;
+constexpr int kDefaultVariant = 1;
 
 template <Epi E>
 __device__ __forceinline__ void epilogue(const DevCsr& m, const EpiArgs& ea, int32_t row, double sum,
@@ -265,7 +268,152 @@ csr_stream_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea
   }
 }
 
+// ---------------------------------------------------------------------------
+// Non-persistent variants: one tile per CTA.
+//   kTma = false: coalesced LSU loads of (val, col) straight into registers;
+//   kTma = true : one elected thread issues the tile's bulk copies, the other
+//                 threads prefetch the epilogue operands meanwhile.
+// Both start every independent load (row bounds, epilogue vectors, tile
+// values) as early as possible so a tile costs ~3 memory latencies.
+constexpr int kFlatTmaSmem = kSlotBytes + kTileNnz * 8;
+
+template <Epi E, bool kTma>
+__global__ void __launch_bounds__(kThreads)
+csr_flat_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea)
+{
+  using T = EpiTraits<E>;
+  extern __shared__ __align__(128) unsigned char fsmem[];
+  __shared__ uint64_t bar;
+  __shared__ double s_prod_static[kTma ? 1 : kTileNnz];
+  __shared__ int32_t s_col_static[(kTma || !T::kDiag) ? 1 : kTileNnz];
+  const int t = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int32_t r0 = m.tile_row[t];
+  const int32_t r1 = m.tile_row[t + 1];
+  const int64_t e0 = m.tile_nz[t];
+  const int64_t e1 = m.tile_nz[t + 1];
+  const bool longtile = e1 - e0 > kTileNnz;
+  if constexpr (kTma) {
+    if (tid == 0) {
+      mbar_init(&bar, 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid == 0) issue_tile(m, t, fsmem, &bar);
+  }
+  const int32_t row = r0 + tid;
+  const bool has_row = row < r1;
+  int64_t lo = 0, hi = 0;
+  double bv = 0.0, uv = 0.0, dv = 0.0, ov = 0.0;
+  if (has_row) {
+    if (!kTma || longtile) {
+      lo = m.rowptr[row];
+      hi = m.rowptr[row + 1];
+    }
+    if constexpr (T::kB) bv = ea.b[row];
+    if constexpr (T::kU) uv = ea.u_in[row];
+    if constexpr (T::kD) dv = ea.d[row];
+    if constexpr (T::kOut) ov = ea.out[row];
+  }
+  double sum = 0.0;
+  double dg = 0.0;
+  double* s_prod = kTma ? reinterpret_cast<double*>(fsmem + kSlotBytes) : s_prod_static;
+  if (!longtile) {
+    const int cnt = (int)(e1 - e0);
+    const double* vals;
+    const int32_t* cols;
+    if constexpr (kTma) {
+      mbar_wait(&bar, 0);
+      vals = reinterpret_cast<const double*>(fsmem) + (e0 & 1);
+      cols = reinterpret_cast<const int32_t*>(fsmem + kValCap * 8) + (e0 & 3);
+      const int64_t* srp =
+          reinterpret_cast<const int64_t*>(fsmem + kValCap * 8 + kColCap * 4) + (r0 & 1);
+      if (has_row) {
+        lo = srp[tid];
+        hi = srp[tid + 1];
+      }
+#pragma unroll
+      for (int i = 0; i < kItems; ++i) {
+        const int k = i * kThreads + tid;
+        if (k < cnt) s_prod[k] = __dmul_rn(vals[k], __ldg(x + cols[k]));
+      }
+    } else {
+      int32_t c[kItems];
+      double v[kItems];
+#pragma unroll
+      for (int i = 0; i < kItems; ++i) {
+        const int k = i * kThreads + tid;
+        c[i] = 0;
+        v[i] = 0.0;
+        if (k < cnt) {
+          c[i] = __ldg(m.col + e0 + k);
+          v[i] = __ldg(m.val + e0 + k);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < kItems; ++i) {
+        const int k = i * kThreads + tid;
+        if (k < cnt) {
+          s_prod[k] = __dmul_rn(v[i], __ldg(x + c[i]));
+          if constexpr (T::kDiag) s_col_static[k] = c[i];
+        }
+      }
+      cols = s_col_static;
+      vals = nullptr;
+    }
+    __syncthreads();
+    if (has_row) {
+      const int a = (int)(lo - e0);
+      const int bnd = (int)(hi - e0);
+      int jd = -1;
+      for (int j = a; j < bnd; ++j) {
+        sum = __dadd_rn(sum, s_prod[j]);
+        if constexpr (T::kDiag) {
+          if (cols[j] == row) jd = j;
+        }
+      }
+      if constexpr (T::kDiag) {
+        if (jd >= 0) dg = kTma ? vals[jd] : __ldg(m.val + e0 + jd);
+      }
+    }
+  } else {
+    if constexpr (kTma) mbar_wait(&bar, 0);
+    int64_t jd = -1;
+    for (int64_t cs = e0; cs < e1; cs += kTileNnz) {
+      const int64_t rem = e1 - cs;
+      const int cnt = rem < (int64_t)kTileNnz ? (int)rem : kTileNnz;
+      for (int k = tid; k < cnt; k += kThreads)
+        s_prod[k] = __dmul_rn(__ldg(m.val + cs + k), __ldg(x + __ldg(m.col + cs + k)));
+      __syncthreads();
+      if (has_row) {
+        const int64_t a = lo > cs ? lo : cs;
+        const int64_t bnd = hi < cs + cnt ? hi : cs + cnt;
+        for (int64_t j = a; j < bnd; ++j) {
+          sum = __dadd_rn(sum, s_prod[j - cs]);
+          if constexpr (T::kDiag) {
+            if (__ldg(m.col + j) == row) jd = j;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    if constexpr (T::kDiag) dg = jd >= 0 ? __ldg(m.val + jd) : 0.0;
+  }
+  if (has_row) epilogue<E>(m, ea, row, sum, dg, bv, uv, dv, ov);
+}
+
 static int g_sm_count = 0;
+
+static int g_variant = -1;
+
+static int spmv_variant()
+{
+  if (g_variant < 0) {
+    const char* v = getenv("SMG_SPMV_VARIANT");
+    g_variant = v ? atoi(v) : kDefaultVariant;
+  }
+  return g_variant;
+}
 
 template <Epi E>
 static cudaError_t launch_t(const DevCsr& m, const double* x, const EpiArgs& ea, cudaStream_t s)
@@ -275,8 +423,20 @@ static cudaError_t launch_t(const DevCsr& m, const double* x, const EpiArgs& ea,
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(csr_stream_kernel<E>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(csr_flat_kernel<E, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, kFlatTmaSmem);
     if (e != cudaSuccess) return e;
     configured = true;
+  }
+  const int variant = spmv_variant();
+  if (variant == 1) {
+    csr_flat_kernel<E, false><<<m.ntiles, kThreads, 0, s>>>(m, x, ea);
+    return cudaGetLastError();
+  }
+  if (variant == 2) {
+    csr_flat_kernel<E, true><<<m.ntiles, kThreads, kFlatTmaSmem, s>>>(m, x, ea);
+    return cudaGetLastError();
   }
   if (g_sm_count == 0) {
     int dev = 0;
