@@ -14,7 +14,7 @@ Also measured in the same run (all reported in the one JSON line):
     (csr_stream_kernel<ChebNext>, 12z + 44n algorithmic bytes per launch),
     timed with CUDA events on the launching stream;
   * sweeps_per_s: fine-level smoother sweeps/s (same loop);
-  * lc_share: fine-level local-correction applications' share of a V-cycle;
+  * lc_share: (T_vcycle - T_vcycle_without_corrections) / T_vcycle, both graph replays;
   * e2e: V-cycles/s through smg_vcycle_host with HOST buffers (H2D of b and
     u, V-cycle, D2H of u inside the timed region);
   * cpu_baseline: the CPU oracle (oracle/, the reference algorithm restated
@@ -302,19 +302,31 @@ def main():
     achieved = bytes_per / (k_ms / 1e3) / 1e9
     sweeps_per_s = 1e3 / k_ms
 
-    # ---- fine-level local-correction share of a V-cycle (4 applications per cycle)
+    # ---- local-correction share: same hierarchy with the corrections removed,
+    # both timed as graph replays (LC share = (T_with - T_without) / T_with)
     lc_share = None
-    if dh.corrs[0] is not None:
-        for _ in range(5):
-            _lib.check(lib.smg_local_correct(dh.corrs[0].handle, D.ptr(b), D.ptr(ua), sh))
-        torch.cuda.synchronize()
-        k0.record(stream)
-        for _ in range(reps):
-            _lib.check(lib.smg_local_correct(dh.corrs[0].handle, D.ptr(b), D.ptr(ua), sh))
-        k1.record(stream)
-        torch.cuda.synchronize()
-        lc_ms = k0.elapsed_time(k1) / reps
-        lc_share = 4 * lc_ms / ms_per_step
+    lc_us = None
+    if any(c is not None for c in dh.corrs):
+        from paper_2402_12947_b200.mg import Level
+        bare = [Level(lv.index, None, None, lv.a, lv.prolongation, lv.smoother, None, None)
+                for lv in h.levels]
+        dh0 = DeviceHierarchy(bare, h.coarse_factor, coarse_inv=dh.coarse_inv)
+        u2 = torch.zeros_like(b)
+        nrep = min(args.steps, 300)
+        times = {}
+        for name, hh in (("with", dh), ("without", dh0)):
+            for _ in range(5):
+                _lib.check(lib.smg_vcycle(hh.handle, D.ptr(b), D.ptr(u2), sh))
+            torch.cuda.synchronize()
+            k0.record(stream)
+            for _ in range(nrep):
+                _lib.check(lib.smg_vcycle(hh.handle, D.ptr(b), D.ptr(u2), sh))
+            k1.record(stream)
+            torch.cuda.synchronize()
+            times[name] = k0.elapsed_time(k1) / nrep
+        lc_us = 1e3 * (times["with"] - times["without"])
+        lc_share = (times["with"] - times["without"]) / times["with"]
+        del dh0
 
     # ---- e2e through the host-buffer C-ABI call (pinned host memory)
     bh = torch.from_numpy(b_host).pin_memory()
@@ -360,6 +372,7 @@ def main():
                          "nnz_per_row": z / nn},
             "sweeps_per_s": sweeps_per_s,
             "lc_share": lc_share,
+            "lc_us_per_vcycle": lc_us,
             "e2e": e2e,
             "gpu_launches": launches * args.steps,
             "launches_per_vcycle": launches,

@@ -139,6 +139,14 @@ SMG_API int smg_hierarchy_create(int n_levels, const smg_operator *const *a,
 SMG_API int smg_hierarchy_destroy(smg_hierarchy *h);
 /* enable != 0: capture each V-cycle once per (b, u) pointer pair as a CUDA graph */
 SMG_API int smg_hierarchy_set_graphs(smg_hierarchy *h, int enable);
+/* runtime options (each change drops cached graphs):
+ *   SMG_OPT_GRAPHS          1 = capture V-cycles as CUDA graphs (default 1)
+ *   SMG_OPT_FUSE_ZERO_GUESS 1 = fuse each coarse level's restriction with its
+ *                           first smoother sweep from the zero initial guess
+ *                           (mg.py:143; bit-identical, default 1) */
+#define SMG_OPT_GRAPHS 0
+#define SMG_OPT_FUSE_ZERO_GUESS 1
+SMG_API int smg_hierarchy_set_option(smg_hierarchy *h, int option, int value);
 /* kernels one V-cycle launches (for launch accounting) */
 SMG_API int smg_hierarchy_launches_per_vcycle(const smg_hierarchy *h, int64_t *launches);
 

@@ -56,6 +56,7 @@ PROTOTYPES = {
                                             _f64p, _i64, _f64p, ctypes.c_int, _pp]),
     "smg_hierarchy_destroy": (ctypes.c_int, [_vp]),
     "smg_hierarchy_set_graphs": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "smg_hierarchy_set_option": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int]),
     "smg_hierarchy_launches_per_vcycle": (ctypes.c_int, [_vp, _i64p]),
     "smg_vcycle": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "smg_vcycle_host": (ctypes.c_int, [_vp, _f64p, _f64p, _vp]),

@@ -165,14 +165,14 @@ static int cheb_scalars(int sweeps, double lambda_max, double frac, ChebScalars*
 // A u before updating u, so the gathering SpMV never writes its own input).
 static int enqueue_global_smooth(const Operator& op, const double* b, double** cur, double** alt,
                                  double* d, int sweeps, const ChebScalars& cs, cudaStream_t st,
-                                 int64_t* launches)
+                                 int64_t* launches, bool first_done = false)
 {
   EpiArgs ea;
   ea.b = b;
   ea.theta = cs.theta;
   ea.d = d;
   if (cs.collapsed) {
-    for (int k = 0; k < sweeps; ++k) {
+    for (int k = first_done ? 1 : 0; k < sweeps; ++k) {
       ea.u_in = *cur;
       ea.out = *alt;
       SMG_CUDA(launch_csr_stream(op.a, *cur, Epi::kJacobi, ea, st));
@@ -181,11 +181,13 @@ static int enqueue_global_smooth(const Operator& op, const double* b, double** c
     }
     return SMG_OK;
   }
-  ea.u_in = *cur;
-  ea.out = *alt;
-  SMG_CUDA(launch_csr_stream(op.a, *cur, Epi::kChebFirst, ea, st));
-  std::swap(*cur, *alt);
-  ++*launches;
+  if (!first_done) {
+    ea.u_in = *cur;
+    ea.out = *alt;
+    SMG_CUDA(launch_csr_stream(op.a, *cur, Epi::kChebFirst, ea, st));
+    std::swap(*cur, *alt);
+    ++*launches;
+  }
   for (size_t k = 0; k < cs.steps.size(); ++k) {
     ea.u_in = *cur;
     ea.out = *alt;
@@ -278,6 +280,7 @@ struct Hierarchy {
   std::vector<void*> allocs;
   int64_t bytes = 0;
   bool use_graphs = true;
+  bool fuse_zero_guess = true;
   std::map<std::pair<const void*, void*>, cudaGraphExec_t> graphs;
   cudaStream_t capture_stream = nullptr;
   int64_t launches = 0;
@@ -295,11 +298,11 @@ struct Hierarchy {
 };
 
 static int enqueue_smooth(HLevel& L, const double* b, double** cur, double** alt, cudaStream_t st,
-                          int64_t* launches)
+                          int64_t* launches, bool first_done = false)
 {
   const bool active = L.lc && L.lc->n_regions > 0;
   if (active) SMG_TRY(enqueue_local_correct(*L.lc, b, *cur, st, launches));
-  SMG_TRY(enqueue_global_smooth(*L.a, b, cur, alt, L.d, L.sweeps, L.cs, st, launches));
+  SMG_TRY(enqueue_global_smooth(*L.a, b, cur, alt, L.d, L.sweeps, L.cs, st, launches, first_done));
   if (active) SMG_TRY(enqueue_local_correct(*L.lc, b, *cur, st, launches));
   return SMG_OK;
 }
@@ -319,17 +322,35 @@ static int enqueue_vcycle(Hierarchy& h, const double* b0, double* u0, cudaStream
     cur[l] = h.lv[l].u;
     alt[l] = h.lv[l].t;
   }
+  std::vector<char> first_done(nl, 0);
   for (int l = 0; l < nl - 1; ++l) {
     HLevel& L = h.lv[l];
-    SMG_TRY(enqueue_smooth(L, bl[l], &cur[l], &alt[l], st, launches));
+    SMG_TRY(enqueue_smooth(L, bl[l], &cur[l], &alt[l], st, launches, first_done[l] != 0));
     EpiArgs ea;
     ea.b = bl[l];
     ea.out = L.r;
     SMG_CUDA(launch_csr_stream(L.a->a, cur[l], Epi::kResidual, ea, st));
-    EpiArgs er;
-    er.out = h.lv[l + 1].b;
-    SMG_CUDA(launch_csr_stream(L.p->t, L.r, Epi::kSpmv, er, st));
-    SMG_CUDA(cudaMemsetAsync(cur[l + 1], 0, sizeof(double) * (size_t)h.lv[l + 1].n, st));
+    HLevel& N = h.lv[l + 1];
+    const bool next_coarsest = (l + 1 == nl - 1);
+    const bool next_lc = N.lc && N.lc->n_regions > 0;
+    if (!next_coarsest && !next_lc && N.a->all_finite && h.fuse_zero_guess) {
+      // restriction fused with the next level's first sweep from u = 0
+      EpiArgs er;
+      er.out = alt[l + 1];
+      er.b_out = N.b;
+      er.diag = N.a->diag;
+      er.theta = N.cs.theta;
+      er.d = N.cs.collapsed ? nullptr : N.d;
+      SMG_CUDA(launch_csr_stream(L.p->t, L.r, Epi::kRestrictFirst, er, st));
+      std::swap(cur[l + 1], alt[l + 1]);
+      first_done[l + 1] = 1;
+    } else {
+      EpiArgs er;
+      er.out = N.b;
+      SMG_CUDA(launch_csr_stream(L.p->t, L.r, Epi::kSpmv, er, st));
+      if (!next_coarsest)
+        SMG_CUDA(cudaMemsetAsync(cur[l + 1], 0, sizeof(double) * (size_t)N.n, st));
+    }
     *launches += 2;
   }
   // coarse solve
@@ -467,13 +488,27 @@ int smg_operator_create(int64_t nrows, int64_t ncols, const int64_t* rowptr, con
   // first zero / missing diagonal (smoothers.py:111-114 via a.diagonal())
   o.first_zero_diag = -1;
   const int64_t nd = std::min(nrows, ncols);
-  for (int64_t i = 0; i < nd && o.first_zero_diag < 0; ++i) {
+  std::vector<double> diag((size_t)nd, 0.0);
+  for (int64_t i = 0; i < nd; ++i) {
     double dv = 0.0;
     const int64_t* b = col + rowptr[i];
     const int64_t* e = col + rowptr[i + 1];
     const int64_t* f = std::lower_bound(b, e, i);
     if (f != e && *f == i) dv = val[rowptr[i] + (f - b)];
-    if (dv == 0.0) o.first_zero_diag = i;
+    diag[(size_t)i] = dv;
+    if (dv == 0.0 && o.first_zero_diag < 0) o.first_zero_diag = i;
+  }
+  for (int64_t j = 0; j < nnz && o.all_finite; ++j)
+    if (!std::isfinite(val[j])) o.all_finite = false;
+  if (nrows == ncols && nd > 0) {
+    double* dd = nullptr;
+    rc = dev_upload(o.allocs, o.device_bytes, diag.data(), diag.size(), &dd);
+    if (rc != SMG_OK) {
+      free_all(o.allocs);
+      delete op;
+      return rc;
+    }
+    o.diag = dd;
   }
   if (with_transpose) {
     // CSR(A^T) with ascending source rows in each row (counting sort is stable)
@@ -872,6 +907,21 @@ int smg_hierarchy_set_graphs(smg_hierarchy* h, int enable)
 {
   if (!h) return fail("hierarchy is NULL");
   h->h.use_graphs = enable != 0;
+  return SMG_OK;
+}
+
+int smg_hierarchy_set_option(smg_hierarchy* h, int option, int value)
+{
+  if (!h) return fail("hierarchy is NULL");
+  Hierarchy& H = h->h;
+  if (option == SMG_OPT_GRAPHS)
+    H.use_graphs = value != 0;
+  else if (option == SMG_OPT_FUSE_ZERO_GUESS)
+    H.fuse_zero_guess = value != 0;
+  else
+    return fail("unknown hierarchy option");
+  for (auto& kv : H.graphs) cudaGraphExecDestroy(kv.second);
+  H.graphs.clear();
   return SMG_OK;
 }
 

@@ -199,10 +199,15 @@ patch_kernel(const DevCsr a, const int32_t* __restrict__ pptr, const int32_t* __
       for (int j = 0; j < 32; ++j)
         lrow[j] = (lane < pn && j <= lane) ? L[tri(i) + p0 + j] : 0.0;
       double xi = lane < pn ? s_x[i] : 0.0;
+      // one reciprocal per lane, in parallel, instead of 32 serial divisions
+      double rd = 1.0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j == lane && lane < pn) rd = 1.0 / lrow[j];
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         if (j < pn) {
-          if (lane == j) xi = xi / lrow[j];
+          if (lane == j) xi = xi * rd;
           const double yj = __shfl_sync(0xffffffffu, xi, j);
           if (lane > j) xi -= lrow[j] * yj;
         }
@@ -240,10 +245,14 @@ patch_kernel(const DevCsr a, const int32_t* __restrict__ pptr, const int32_t* __
       for (int j = 0; j < 32; ++j)
         lcol[j] = (lane < pn && j < pn && j >= lane) ? L[tri(p0 + j) + p0 + lane] : 0.0;
       double yt = lane < pn ? s_x[p0 + lane] : 0.0;
+      double rd = 1.0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j == lane && lane < pn) rd = 1.0 / lcol[j];
 #pragma unroll
       for (int j = 31; j >= 0; --j) {
         if (j < pn) {
-          if (lane == j) yt = yt / lcol[j];
+          if (lane == j) yt = yt * rd;
           const double xj = __shfl_sync(0xffffffffu, yt, j);
           if (lane < j) yt -= lcol[j] * xj;
         }

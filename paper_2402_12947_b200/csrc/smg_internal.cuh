@@ -40,6 +40,8 @@ struct Operator {
   bool has_t = false;
   DevCsr t;                 // CSR of the transpose (restriction P^T), fine index ascending
   int64_t first_zero_diag = -1;   // -1: every row has a nonzero diagonal
+  bool all_finite = true;          // every stored value is finite
+  const double* diag = nullptr;    // explicit diagonal (0.0 where absent), square ops
   int64_t device_bytes = 0;
   std::vector<void*> allocs;
 };
@@ -83,6 +85,10 @@ enum class Epi : int {
   kChebFirst,      // d = (inv_d * (b - s)) / theta ; u_out = u_in + d
   kChebNext,       // z = inv_d * (b - s) ; d = c1*d + c2*z ; u_out = u_in + d
   kAddTo,          // y = y + s  (prolong-add)
+  kRestrictFirst,  // b_c = s (restriction), then the coarse level's first smoother
+                   // step from a zero initial guess: d = (1/diag * (b_c - 0)) / theta,
+                   // u_c = 0 + d  (A_c 0 sums to +0.0 exactly, so this equals the
+                   // reference's first sweep bit for bit)
 };
 
 struct EpiArgs {
@@ -91,6 +97,8 @@ struct EpiArgs {
   double* out = nullptr;   // y / r / u_out
   double* d = nullptr;
   double theta = 1.0, c1 = 0.0, c2 = 0.0;
+  const double* diag = nullptr;   // kRestrictFirst: coarse operator diagonal
+  double* b_out = nullptr;        // kRestrictFirst: restricted right-hand side
 };
 
 cudaError_t launch_csr_stream(const DevCsr& m, const double* x, Epi epi, const EpiArgs& ea,

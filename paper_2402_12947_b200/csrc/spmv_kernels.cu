@@ -91,6 +91,7 @@ struct EpiTraits {
   static constexpr bool kU = (E == Epi::kJacobi || E == Epi::kChebFirst || E == Epi::kChebNext);
   static constexpr bool kD = (E == Epi::kChebNext);
   static constexpr bool kOut = (E == Epi::kAddTo);
+  static constexpr bool kDiagVec = (E == Epi::kRestrictFirst);
 };
 
 // ring-slot geometry (bytes are multiples of 16 as cp.async.bulk requires)
@@ -112,6 +113,13 @@ __device__ __forceinline__ void epilogue(const DevCsr& m, const EpiArgs& ea, int
     ea.out[row] = __dsub_rn(bv, sum);
   } else if constexpr (E == Epi::kAddTo) {
     ea.out[row] = __dadd_rn(ov, sum);
+  } else if constexpr (E == Epi::kRestrictFirst) {
+    ea.b_out[row] = sum;
+    const double inv = __ddiv_rn(1.0, dg);
+    const double t = __dmul_rn(inv, __dsub_rn(sum, 0.0));
+    const double d = __ddiv_rn(t, ea.theta);
+    if (ea.d) ea.d[row] = d;
+    ea.out[row] = __dadd_rn(0.0, d);
   } else {
     const double inv = __ddiv_rn(1.0, dg);
     const double t = __dmul_rn(inv, __dsub_rn(bv, sum));
@@ -201,6 +209,9 @@ csr_stream_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea
     const int64_t e1 = m.tile_nz[t + 1];
     double sum = 0.0;
     double dg = 0.0;
+    if constexpr (T::kDiagVec) {
+      if (has_row) dg = ea.diag[row];
+    }
     mbar_wait(&bars[s], parity);
     if (e1 - e0 <= kTileNnz) {
       const double* sval = reinterpret_cast<const double*>(slot) + (e0 & 1);
@@ -317,6 +328,9 @@ csr_flat_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea)
   }
   double sum = 0.0;
   double dg = 0.0;
+  if constexpr (T::kDiagVec) {
+    if (has_row) dg = ea.diag[row];
+  }
   double* s_prod = kTma ? reinterpret_cast<double*>(fsmem + kSlotBytes) : s_prod_static;
   if (!longtile) {
     const int cnt = (int)(e1 - e0);
@@ -460,6 +474,7 @@ cudaError_t launch_csr_stream(const DevCsr& m, const double* x, Epi epi, const E
     case Epi::kChebFirst: return launch_t<Epi::kChebFirst>(m, x, ea, s);
     case Epi::kChebNext: return launch_t<Epi::kChebNext>(m, x, ea, s);
     case Epi::kAddTo: return launch_t<Epi::kAddTo>(m, x, ea, s);
+    case Epi::kRestrictFirst: return launch_t<Epi::kRestrictFirst>(m, x, ea, s);
   }
   return cudaErrorInvalidValue;
 }

@@ -179,6 +179,9 @@ class DeviceHierarchy:
     def set_graphs(self, enable: bool) -> None:
         _lib.check(_lib.load().smg_hierarchy_set_graphs(self.handle, 1 if enable else 0))
 
+    def set_option(self, option: int, value: int) -> None:
+        _lib.check(_lib.load().smg_hierarchy_set_option(self.handle, int(option), int(value)))
+
     def launches_per_vcycle(self) -> int:
         n = ctypes.c_int64()
         _lib.check(_lib.load().smg_hierarchy_launches_per_vcycle(self.handle, ctypes.byref(n)))

@@ -134,6 +134,22 @@ def test_graph_and_eager_agree_bitwise(P, fx):
     assert np.array_equal(res[0], res[1])
 
 
+def test_zero_guess_fusion_is_bitwise(P, fx):
+    import torch
+    from paper_2402_12947_b200.mg import DeviceHierarchy
+    name, z, h = fx
+    b = torch.from_numpy(z["g/b"]).cuda()
+    res = []
+    for fuse in (1, 0):
+        dh = DeviceHierarchy(h.levels, h.coarse_factor)
+        dh.set_option(1, fuse)
+        u = torch.from_numpy(z["g/u_rand"]).cuda()
+        dh.vcycle(b, u)
+        dh.vcycle(b, u)
+        res.append(u.cpu().numpy())
+    assert np.array_equal(res[0], res[1])
+
+
 def test_iteration_counts(P, fx):
     name, z, h = fx
     b = z["g/b"]
