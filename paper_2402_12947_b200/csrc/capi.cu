@@ -696,7 +696,8 @@ int smg_correction_create(const smg_operator* a, int64_t n_regions, const int64_
     if (nd <= 0) return fail("region " + std::to_string(r) + " is empty");
     max_dofs = std::max<int32_t>(max_dofs, (int32_t)nd);
     pptr[(size_t)r] = (int32_t)roff[r];
-    poff[(size_t)r + 1] = poff[(size_t)r] + nd * (nd + 1) / 2;
+    // 16-byte aligned, even-length slots so one bulk copy stages a factor
+    poff[(size_t)r + 1] = poff[(size_t)r] + ((nd * (nd + 1) / 2 + 1) & ~int64_t(1));
     for (int64_t k = roff[r]; k < roff[r + 1]; ++k) {
       const int64_t g = dofs[k];
       if (g < 0 || g >= n)

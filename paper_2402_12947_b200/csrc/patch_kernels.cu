@@ -28,6 +28,36 @@
 
 namespace smg {
 
+__device__ __forceinline__ uint32_t psmem_u32(const void* p)
+{
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// 1D bulk copy of a packed factor into shared memory (TMA, mbarrier completion)
+__device__ __forceinline__ void factor_bulk_load(double* dst, const double* src, uint32_t bytes,
+                                                 uint64_t* bar)
+{
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(psmem_u32(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(psmem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(psmem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(psmem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void factor_wait(uint64_t* bar)
+{
+  asm volatile(
+      "{\n.reg .pred p;\nW_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+      "@!p bra W_%=;\n}\n" ::"r"(psmem_u32(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ double warp_sum(double v)
 {
 #pragma unroll
@@ -40,6 +70,7 @@ __host__ __device__ __forceinline__ int64_t tri(int64_t i) { return i * (i + 1) 
 constexpr int kSolveThreads = 256;
 constexpr int kSolveWarps = kSolveThreads / 32;
 constexpr int kProdCap = 2048;                 // residual products staged per pass
+constexpr int kProdItems = kProdCap / kSolveThreads;
 constexpr int64_t kSmemBudget = 220 * 1024;    // dynamic smem per CTA (of 227 KB)
 
 enum PatchMode : int { kAddResidualSolve = 0, kSolveFromBuf = 1, kResidualOnly = 2 };
@@ -61,7 +92,9 @@ __host__ __device__ inline PatchSmem patch_smem_layout(int nmax)
   int64_t cap = (kSmemBudget - p.l_off) / 8;
   if (cap < 0) cap = 0;
   p.tri_cap = cap;
-  const int64_t need = tri(nmax);
+  const int64_t need = (tri(nmax) + 1) & ~int64_t(1);
+  cap &= ~int64_t(1);
+  p.tri_cap = cap;
   p.bytes = p.l_off + 8 * (need < cap ? need : cap);
   return p;
 }
@@ -110,6 +143,7 @@ patch_kernel(const DevCsr a, const int32_t* __restrict__ pptr, const int32_t* __
   extern __shared__ __align__(16) unsigned char psm[];
   __shared__ double s_red[kSolveWarps][32];
   __shared__ int s_carry;
+  __shared__ uint64_t s_bar;
   const PatchSmem L_ = patch_smem_layout(nmax);
   double* s_x = reinterpret_cast<double*>(psm + L_.x_off);
   int64_t* s_lo = reinterpret_cast<int64_t*>(psm + L_.lo_off);
@@ -123,8 +157,12 @@ patch_kernel(const DevCsr a, const int32_t* __restrict__ pptr, const int32_t* __
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int64_t ntri = tri(n);
-  const bool staged = kMode != kResidualOnly && ntri <= L_.tri_cap;
+  const bool staged = kMode != kResidualOnly && ((ntri + 1) & ~int64_t(1)) <= L_.tri_cap;
   const double* __restrict__ Lg = lfac + foff[p];
+  // factors are stored at 16-byte aligned offsets with even lengths, so one
+  // bulk copy stages the whole factor while the residual is formed
+  if (staged && threadIdx.x == 0)
+    factor_bulk_load(s_L, Lg, (uint32_t)(((ntri + 1) & ~int64_t(1)) * 8), &s_bar);
 
   if (kMode != kSolveFromBuf) {
     // ---- residual rows: bounds, scan, streamed products, ordered sums
@@ -138,21 +176,38 @@ patch_kernel(const DevCsr a, const int32_t* __restrict__ pptr, const int32_t* __
     }
     __syncthreads();
     const int total = block_scan(s_len, s_off, n, &s_carry);
-    // stage the factor while the residual streams (independent loads)
-    if (staged)
-      for (int64_t i = threadIdx.x; i < ntri; i += kSolveThreads) s_L[i] = __ldg(Lg + i);
     for (int c0 = 0; c0 < total; c0 += kProdCap) {
       const int cnt = min(kProdCap, total - c0);
-      for (int e = threadIdx.x; e < cnt; e += kSolveThreads) {
-        const int eg = c0 + e;
-        int lo = 0, hi = n;  // last row r with s_off[r] <= eg
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (s_off[mid] <= eg) lo = mid; else hi = mid;
+      // batched: locate all of this thread's elements, then issue every load
+      int64_t jj[kProdItems];
+#pragma unroll
+      for (int it = 0; it < kProdItems; ++it) {
+        const int e = it * kSolveThreads + threadIdx.x;
+        jj[it] = -1;
+        if (e < cnt) {
+          const int eg = c0 + e;
+          int lo = 0, hi = n;  // last row r with s_off[r] <= eg
+          while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (s_off[mid] <= eg) lo = mid; else hi = mid;
+          }
+          jj[it] = s_lo[lo] + (eg - s_off[lo]);
         }
-        const int64_t j = s_lo[lo] + (eg - s_off[lo]);
-        s_prod[e] = __dmul_rn(__ldg(a.val + j), u_res[__ldg(a.col + j)]);
       }
+      int32_t cc[kProdItems];
+      double vv[kProdItems];
+#pragma unroll
+      for (int it = 0; it < kProdItems; ++it) {
+        cc[it] = 0;
+        vv[it] = 0.0;
+        if (jj[it] >= 0) {
+          cc[it] = __ldg(a.col + jj[it]);
+          vv[it] = __ldg(a.val + jj[it]);
+        }
+      }
+#pragma unroll
+      for (int it = 0; it < kProdItems; ++it)
+        if (jj[it] >= 0) s_prod[it * kSolveThreads + threadIdx.x] = __dmul_rn(vv[it], u_res[cc[it]]);
       __syncthreads();
       for (int i = threadIdx.x; i < n; i += kSolveThreads) {
         const int a0 = max(s_off[i], c0), a1 = min(s_off[i + 1], c0 + cnt);
@@ -171,10 +226,9 @@ patch_kernel(const DevCsr a, const int32_t* __restrict__ pptr, const int32_t* __
     }
     if (kMode == kResidualOnly) return;
   } else {
-    if (staged)
-      for (int64_t i = threadIdx.x; i < ntri; i += kSolveThreads) s_L[i] = __ldg(Lg + i);
     for (int i = threadIdx.x; i < n; i += kSolveThreads) s_x[i] = rbuf[k0 + i];
   }
+  if (staged) factor_wait(&s_bar);
   __syncthreads();
   const double* L = staged ? s_L : Lg;
 

@@ -82,6 +82,12 @@ __device__ __forceinline__ void fence_proxy_async()
 {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// programmatic dependent launch: no-ops when launched without the attribute
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger()
+{
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 // ---------------------------------------------------------------------------
 template <Epi E>
@@ -102,6 +108,7 @@ constexpr int kSlotBytes = kValCap * 8 + kColCap * 4 + kRpCap * 8;
 static_assert(kSlotBytes % 16 == 0, "slot must keep 16-byte alignment");
 constexpr int kSmemBytes = kStages * kSlotBytes + kTileNnz * 8;
 constexpr int kDefaultVariant = 1;
+constexpr int kFlatMinBlocks = 6;   // <= 40 registers: 6 CTAs (48 warps) per SM
 
 template <Epi E>
 __device__ __forceinline__ void epilogue(const DevCsr& m, const EpiArgs& ea, int32_t row, double sum,
@@ -288,8 +295,8 @@ csr_stream_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea
 // values) as early as possible so a tile costs ~3 memory latencies.
 constexpr int kFlatTmaSmem = kSlotBytes + kTileNnz * 8;
 
-template <Epi E, bool kTma>
-__global__ void __launch_bounds__(kThreads)
+template <Epi E, bool kTma, int kMinB>
+__global__ void __launch_bounds__(kThreads, kMinB)
 csr_flat_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea)
 {
   using T = EpiTraits<E>;
@@ -299,11 +306,14 @@ csr_flat_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea)
   __shared__ int32_t s_col_static[(kTma || !T::kDiag) ? 1 : kTileNnz];
   const int t = blockIdx.x;
   const int tid = threadIdx.x;
+  // ---- operator data (never written by any kernel): safe before the
+  //      programmatic-dependency wait, so it overlaps the previous kernel's tail
   const int32_t r0 = m.tile_row[t];
   const int32_t r1 = m.tile_row[t + 1];
   const int64_t e0 = m.tile_nz[t];
   const int64_t e1 = m.tile_nz[t + 1];
   const bool longtile = e1 - e0 > kTileNnz;
+  const int cnt = (int)(e1 - e0);
   if constexpr (kTma) {
     if (tid == 0) {
       mbar_init(&bar, 1);
@@ -315,26 +325,40 @@ csr_flat_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea)
   const int32_t row = r0 + tid;
   const bool has_row = row < r1;
   int64_t lo = 0, hi = 0;
-  double bv = 0.0, uv = 0.0, dv = 0.0, ov = 0.0;
-  if (has_row) {
-    if (!kTma || longtile) {
-      lo = m.rowptr[row];
-      hi = m.rowptr[row + 1];
+  if (has_row && (!kTma || longtile)) {
+    lo = m.rowptr[row];
+    hi = m.rowptr[row + 1];
+  }
+  int32_t c[kTma ? 1 : kItems];
+  double v[kTma ? 1 : kItems];
+  if constexpr (!kTma) {
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+      const int k = i * kThreads + tid;
+      c[i] = 0;
+      v[i] = 0.0;
+      if (!longtile && k < cnt) {
+        c[i] = __ldg(m.col + e0 + k);
+        v[i] = __ldg(m.val + e0 + k);
+      }
     }
+  }
+  // ---- vectors produced by earlier kernels: after the dependency wait
+  pdl_wait();
+  pdl_trigger();
+  double bv = 0.0, uv = 0.0, dv = 0.0, ov = 0.0;
+  double sum = 0.0;
+  double dg = 0.0;
+  if (has_row) {
     if constexpr (T::kB) bv = ea.b[row];
     if constexpr (T::kU) uv = ea.u_in[row];
     if constexpr (T::kD) dv = ea.d[row];
     if constexpr (T::kOut) ov = ea.out[row];
-  }
-  double sum = 0.0;
-  double dg = 0.0;
-  if constexpr (T::kDiagVec) {
-    if (has_row) dg = ea.diag[row];
+    if constexpr (T::kDiagVec) dg = ea.diag[row];
   }
   double* s_prod = kTma ? reinterpret_cast<double*>(fsmem + kSlotBytes) : s_prod_static;
   if (!longtile) {
-    const int cnt = (int)(e1 - e0);
-    const double* vals;
+    const double* vals = nullptr;
     const int32_t* cols;
     if constexpr (kTma) {
       mbar_wait(&bar, 0);
@@ -352,18 +376,6 @@ csr_flat_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea)
         if (k < cnt) s_prod[k] = __dmul_rn(vals[k], __ldg(x + cols[k]));
       }
     } else {
-      int32_t c[kItems];
-      double v[kItems];
-#pragma unroll
-      for (int i = 0; i < kItems; ++i) {
-        const int k = i * kThreads + tid;
-        c[i] = 0;
-        v[i] = 0.0;
-        if (k < cnt) {
-          c[i] = __ldg(m.col + e0 + k);
-          v[i] = __ldg(m.val + e0 + k);
-        }
-      }
 #pragma unroll
       for (int i = 0; i < kItems; ++i) {
         const int k = i * kThreads + tid;
@@ -373,7 +385,6 @@ csr_flat_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea)
         }
       }
       cols = s_col_static;
-      vals = nullptr;
     }
     __syncthreads();
     if (has_row) {
@@ -395,13 +406,13 @@ csr_flat_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea)
     int64_t jd = -1;
     for (int64_t cs = e0; cs < e1; cs += kTileNnz) {
       const int64_t rem = e1 - cs;
-      const int cnt = rem < (int64_t)kTileNnz ? (int)rem : kTileNnz;
-      for (int k = tid; k < cnt; k += kThreads)
+      const int cn = rem < (int64_t)kTileNnz ? (int)rem : kTileNnz;
+      for (int k = tid; k < cn; k += kThreads)
         s_prod[k] = __dmul_rn(__ldg(m.val + cs + k), __ldg(x + __ldg(m.col + cs + k)));
       __syncthreads();
       if (has_row) {
         const int64_t a = lo > cs ? lo : cs;
-        const int64_t bnd = hi < cs + cnt ? hi : cs + cnt;
+        const int64_t bnd = hi < cs + cn ? hi : cs + cn;
         for (int64_t j = a; j < bnd; ++j) {
           sum = __dadd_rn(sum, s_prod[j - cs]);
           if constexpr (T::kDiag) {
@@ -429,6 +440,17 @@ static int spmv_variant()
   return g_variant;
 }
 
+static int g_pdl = -1;
+
+static bool use_pdl()
+{
+  if (g_pdl < 0) {
+    const char* v = getenv("SMG_PDL");
+    g_pdl = v ? atoi(v) : 1;
+  }
+  return g_pdl != 0;
+}
+
 template <Epi E>
 static cudaError_t launch_t(const DevCsr& m, const double* x, const EpiArgs& ea, cudaStream_t s)
 {
@@ -438,19 +460,27 @@ static cudaError_t launch_t(const DevCsr& m, const double* x, const EpiArgs& ea,
     cudaError_t e = cudaFuncSetAttribute(csr_stream_kernel<E>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(csr_flat_kernel<E, true>,
+      e = cudaFuncSetAttribute(csr_flat_kernel<E, true, 4>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, kFlatTmaSmem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
   const int variant = spmv_variant();
-  if (variant == 1) {
-    csr_flat_kernel<E, false><<<m.ntiles, kThreads, 0, s>>>(m, x, ea);
-    return cudaGetLastError();
-  }
-  if (variant == 2) {
-    csr_flat_kernel<E, true><<<m.ntiles, kThreads, kFlatTmaSmem, s>>>(m, x, ea);
-    return cudaGetLastError();
+  if (variant >= 1) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)m.ntiles);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = variant == 2 ? kFlatTmaSmem : 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = use_pdl() ? 1 : 0;
+    if (variant == 1) return cudaLaunchKernelEx(&cfg, csr_flat_kernel<E, false, 6>, m, x, ea);
+    if (variant == 3) return cudaLaunchKernelEx(&cfg, csr_flat_kernel<E, false, 4>, m, x, ea);
+    if (variant == 4) return cudaLaunchKernelEx(&cfg, csr_flat_kernel<E, false, 8>, m, x, ea);
+    return cudaLaunchKernelEx(&cfg, csr_flat_kernel<E, true, 4>, m, x, ea);
   }
   if (g_sm_count == 0) {
     int dev = 0;
