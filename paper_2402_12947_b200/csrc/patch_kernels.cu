@@ -254,10 +254,8 @@ patch_kernel(const DevCsr a, const int32_t* __restrict__ pptr, const int32_t* __
         lrow[j] = (lane < pn && j <= lane) ? L[tri(i) + p0 + j] : 0.0;
       double xi = lane < pn ? s_x[i] : 0.0;
       // one reciprocal per lane, in parallel, instead of 32 serial divisions
-      double rd = 1.0;
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (j == lane && lane < pn) rd = 1.0 / lrow[j];
+      // one non-divergent reciprocal per lane instead of 32 serialised divisions
+      const double rd = 1.0 / (lane < pn ? L[tri(i) + i] : 1.0);
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         if (j < pn) {
@@ -299,10 +297,7 @@ patch_kernel(const DevCsr a, const int32_t* __restrict__ pptr, const int32_t* __
       for (int j = 0; j < 32; ++j)
         lcol[j] = (lane < pn && j < pn && j >= lane) ? L[tri(p0 + j) + p0 + lane] : 0.0;
       double yt = lane < pn ? s_x[p0 + lane] : 0.0;
-      double rd = 1.0;
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (j == lane && lane < pn) rd = 1.0 / lcol[j];
+      const double rd = 1.0 / (lane < pn ? L[tri(p0 + lane) + p0 + lane] : 1.0);
 #pragma unroll
       for (int j = 31; j >= 0; --j) {
         if (j < pn) {

@@ -107,7 +107,7 @@ constexpr int kRpCap = kRowsPerTile + 4;     // int64 (rows r0..r1 inclusive + a
 constexpr int kSlotBytes = kValCap * 8 + kColCap * 4 + kRpCap * 8;
 static_assert(kSlotBytes % 16 == 0, "slot must keep 16-byte alignment");
 constexpr int kSmemBytes = kStages * kSlotBytes + kTileNnz * 8;
-constexpr int kDefaultVariant = 1;
+constexpr int kDefaultVariant = 3;
 constexpr int kFlatMinBlocks = 6;   // <= 40 registers: 6 CTAs (48 warps) per SM
 
 template <Epi E>

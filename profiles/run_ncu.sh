@@ -17,3 +17,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
     -k 'regex:Epi\)4' -s 140 -c 2 -o $OUT/prof_k3_$TAG $CMD > $OUT/ncu_full_$TAG.log 2>&1
 echo "ncu done: $?"
+ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+    -k 'regex:patch_kernel' -s 8 -c 1 -o $OUT/prof_lc_$TAG $CMD > $OUT/ncu_lc_$TAG.log 2>&1
+echo "ncu lc done: $?"
