@@ -72,3 +72,15 @@ def test_workload_shapes():
     assert (configs.C1.grids[0] + 1) ** 2 == 16641
     assert (configs.C3.grids[0] + 1) ** 3 == 274625
     assert (2 * configs.C4.grids[0] + 1) ** 3 == 7189057
+
+
+@pytest.mark.parametrize("n", [2, 3, 5])
+def test_p2_tet_stencil_matches_assembly(n):
+    """C5's structured generator equals fem.assemble_poisson on the same grid."""
+    from paper_2402_12947_b200 import fem, stencil
+    m = generate_simplex_grid(3, n)
+    ref = fem.assemble_poisson(m, fem.build_dofmap(m, 2), None, dirichlet_all=True).a
+    a = stencil.p2_tet_laplacian(n)
+    assert np.array_equal(a.row_offsets, ref.row_offsets)
+    assert np.array_equal(a.col_indices, ref.col_indices)
+    assert np.max(np.abs(a.values - ref.values)) <= 1e-13 * np.max(np.abs(ref.values))
