@@ -67,10 +67,20 @@ static void free_all(std::vector<void*>& allocs)
   allocs.clear();
 }
 
-// Greedy tile partition: consecutive rows, <= kRowsPerTile rows, <= kTileNnz
-// nonzeros unless a single row is longer.
+// Greedy tile partition: consecutive rows, <= kRowsPerTile rows, <= cap
+// nonzeros unless a single row is longer.  Small operators (coarse levels)
+// get smaller tiles so every SM still has several independent CTAs.
+static int64_t tile_cap_for(int64_t nnz)
+{
+  const int64_t want = nnz / (148 * 8);  // ~8 CTAs per SM
+  int64_t cap = 256;
+  while (cap < want && cap < kTileNnz) cap *= 2;
+  return cap;
+}
+
 static std::vector<int32_t> make_tiles(int64_t nrows, const int64_t* rowptr)
 {
+  const int64_t cap = tile_cap_for(rowptr[nrows]);
   std::vector<int32_t> t;
   t.reserve((size_t)(nrows / 64 + 2));
   t.push_back(0);
@@ -79,7 +89,7 @@ static std::vector<int32_t> make_tiles(int64_t nrows, const int64_t* rowptr)
     const int64_t start = r;
     const int64_t base = rowptr[r];
     ++r;
-    while (r < nrows && r - start < kRowsPerTile && rowptr[r + 1] - base <= kTileNnz) ++r;
+    while (r < nrows && r - start < kRowsPerTile && rowptr[r + 1] - base <= cap) ++r;
     t.push_back((int32_t)r);
   }
   return t;
@@ -696,8 +706,9 @@ int smg_correction_create(const smg_operator* a, int64_t n_regions, const int64_
     if (nd <= 0) return fail("region " + std::to_string(r) + " is empty");
     max_dofs = std::max<int32_t>(max_dofs, (int32_t)nd);
     pptr[(size_t)r] = (int32_t)roff[r];
-    // 16-byte aligned, even-length slots so one bulk copy stages a factor
-    poff[(size_t)r + 1] = poff[(size_t)r] + ((nd * (nd + 1) / 2 + 1) & ~int64_t(1));
+    // slot = [packed L, even length][inverted 32x32 diagonal blocks]; 16-byte
+    // aligned and even-length so one bulk copy stages the whole slot
+    poff[(size_t)r + 1] = poff[(size_t)r] + patch_slot_doubles(nd);
     for (int64_t k = roff[r]; k < roff[r + 1]; ++k) {
       const int64_t g = dofs[k];
       if (g < 0 || g >= n)
@@ -712,14 +723,28 @@ int smg_correction_create(const smg_operator* a, int64_t n_regions, const int64_
     }
   }
   pptr[(size_t)n_regions] = (int32_t)m;
-  // pack lower triangles (row-major)
-  std::vector<double> packed((size_t)poff[(size_t)n_regions]);
+  // pack lower triangles (row-major) and invert each 32x32 diagonal block
+  // (row stride kDinvLd) so the panel triangle solves become small GEMVs
+  std::vector<double> packed((size_t)poff[(size_t)n_regions], 0.0);
   for (int64_t r = 0; r < n_regions; ++r) {
     const int64_t nd = roff[r + 1] - roff[r];
     const double* f = factors + foff[r];
-    double* dst = packed.data() + poff[(size_t)r];
+    double* base = packed.data() + poff[(size_t)r];
+    double* dst = base;
     for (int64_t i = 0; i < nd; ++i)
       for (int64_t j = 0; j <= i; ++j) *dst++ = f[i * nd + j];
+    double* dinv = base + ((nd * (nd + 1) / 2 + 1) & ~int64_t(1));
+    for (int64_t p0 = 0; p0 < nd; p0 += kPanel) {
+      const int64_t pn = std::min<int64_t>(kPanel, nd - p0);
+      double* D = dinv + (p0 / kPanel) * kDinvBlock;
+      for (int64_t j = 0; j < pn; ++j) {       // column j of the inverse
+        for (int64_t i = j; i < pn; ++i) {
+          double sacc = (i == j) ? 1.0 : 0.0;
+          for (int64_t k = j; k < i; ++k) sacc -= f[(p0 + i) * nd + (p0 + k)] * D[k * kDinvLd + j];
+          D[i * kDinvLd + j] = sacc / f[(p0 + i) * nd + (p0 + i)];
+        }
+      }
+    }
   }
   auto* cc = new smg_correction();
   Correction& c = cc->c;

@@ -16,8 +16,8 @@
 
 namespace smg {
 
-constexpr int kGemvThreads = 256;
-constexpr int kGemvRowsPerWarp = 2;
+constexpr int kGemvThreads = 128;                 // 4 rows (warps) per CTA
+constexpr int kGemvUnroll = 8;                    // independent 256 B loads in flight per warp
 
 __device__ __forceinline__ double warp_sum_d(double v)
 {
@@ -26,36 +26,39 @@ __device__ __forceinline__ double warp_sum_d(double v)
   return v;
 }
 
-// y = M x (add=false) or y += M x (add=true); M dense row-major n x n.
+// y = M x (kAdd=false) or y += M x (kAdd=true); M dense row-major n x n.
+// One warp per row, kGemvUnroll independent accumulators (fixed order: the
+// result is run-to-run deterministic).
 template <bool kAdd>
 __global__ void __launch_bounds__(kGemvThreads)
 dense_gemv_kernel(int64_t n, const double* __restrict__ m, const double* __restrict__ x,
                   double* __restrict__ y)
 {
   const int lane = threadIdx.x & 31;
-  const int64_t warp_global = ((int64_t)blockIdx.x * kGemvThreads + threadIdx.x) >> 5;
-  const int64_t r0 = warp_global * kGemvRowsPerWarp;
-  double acc[kGemvRowsPerWarp];
+  const int64_t row = (int64_t)blockIdx.x * (kGemvThreads / 32) + (threadIdx.x >> 5);
+  if (row >= n) return;
+  const double* __restrict__ mr = m + row * n;
+  double acc[kGemvUnroll];
 #pragma unroll
-  for (int r = 0; r < kGemvRowsPerWarp; ++r) acc[r] = 0.0;
-  for (int64_t j = lane; j < n; j += 32) {
-    const double xj = __ldg(x + j);
+  for (int u = 0; u < kGemvUnroll; ++u) acc[u] = 0.0;
+  int64_t j = lane;
+  for (; j + 32 * (kGemvUnroll - 1) < n; j += 32 * kGemvUnroll) {
+    double mv[kGemvUnroll];
 #pragma unroll
-    for (int r = 0; r < kGemvRowsPerWarp; ++r) {
-      const int64_t row = r0 + r;
-      if (row < n) acc[r] = fma(__ldcs(m + row * n + j), xj, acc[r]);
-    }
+    for (int u = 0; u < kGemvUnroll; ++u) mv[u] = __ldcs(mr + j + 32 * u);
+#pragma unroll
+    for (int u = 0; u < kGemvUnroll; ++u) acc[u] = fma(mv[u], __ldg(x + j + 32 * u), acc[u]);
   }
+  for (; j < n; j += 32) acc[0] = fma(__ldcs(mr + j), __ldg(x + j), acc[0]);
+  double s = 0.0;
 #pragma unroll
-  for (int r = 0; r < kGemvRowsPerWarp; ++r) {
-    const double s = warp_sum_d(acc[r]);
-    const int64_t row = r0 + r;
-    if (lane == 0 && row < n) {
-      if (kAdd)
-        y[row] += s;
-      else
-        y[row] = s;
-    }
+  for (int u = 0; u < kGemvUnroll; ++u) s += acc[u];
+  s = warp_sum_d(s);
+  if (lane == 0) {
+    if (kAdd)
+      y[row] += s;
+    else
+      y[row] = s;
   }
 }
 
@@ -63,8 +66,7 @@ static cudaError_t gemv(int64_t n, const double* m, const double* x, double* y, 
                         cudaStream_t s)
 {
   if (n == 0) return cudaSuccess;
-  const int64_t warps = (n + kGemvRowsPerWarp - 1) / kGemvRowsPerWarp;
-  const int64_t blocks = (warps * 32 + kGemvThreads - 1) / kGemvThreads;
+  const int64_t blocks = (n + (kGemvThreads / 32) - 1) / (kGemvThreads / 32);
   if (add)
     dense_gemv_kernel<true><<<(unsigned)blocks, kGemvThreads, 0, s>>>(n, m, x, y);
   else

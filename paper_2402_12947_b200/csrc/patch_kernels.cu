@@ -15,8 +15,10 @@
 //      segments and form exact products in shared memory -> each row is then
 //      summed sequentially in column order (bit-identical to scipy);
 //   3. forward substitution with L, back substitution with L^T, 32-row panels:
-//      off-panel updates are coalesced warp dot products, the panel triangle
-//      is solved by one warp from registers with shuffles;
+//      off-panel updates are coalesced warp dot products; each panel's
+//      triangle is applied as a 32-wide GEMV with its inverted diagonal block
+//      (computed once at upload), so the serial chain is n/32 panel steps
+//      instead of n dependent shuffle steps;
 //   4. u[B_d] += x (or out[B_d] = x for apply_local_correction).
 // Regions are DOF-disjoint but may be coupled through A: when
 // the upload-time check finds coupling, the residuals of ALL regions are
@@ -92,7 +94,7 @@ __host__ __device__ inline PatchSmem patch_smem_layout(int nmax)
   int64_t cap = (kSmemBudget - p.l_off) / 8;
   if (cap < 0) cap = 0;
   p.tri_cap = cap;
-  const int64_t need = (tri(nmax) + 1) & ~int64_t(1);
+  const int64_t need = patch_slot_doubles(nmax);
   cap &= ~int64_t(1);
   p.tri_cap = cap;
   p.bytes = p.l_off + 8 * (need < cap ? need : cap);
@@ -156,13 +158,13 @@ patch_kernel(const DevCsr a, const int32_t* __restrict__ pptr, const int32_t* __
   const int n = pptr[p + 1] - k0;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int64_t ntri = tri(n);
-  const bool staged = kMode != kResidualOnly && ((ntri + 1) & ~int64_t(1)) <= L_.tri_cap;
+  const int64_t nslot = patch_slot_doubles(n);
+  const bool staged = kMode != kResidualOnly && nslot <= L_.tri_cap;
   const double* __restrict__ Lg = lfac + foff[p];
   // factors are stored at 16-byte aligned offsets with even lengths, so one
   // bulk copy stages the whole factor while the residual is formed
   if (staged && threadIdx.x == 0)
-    factor_bulk_load(s_L, Lg, (uint32_t)(((ntri + 1) & ~int64_t(1)) * 8), &s_bar);
+    factor_bulk_load(s_L, Lg, (uint32_t)(nslot * 8), &s_bar);
 
   if (kMode != kSolveFromBuf) {
     // ---- residual rows: bounds, scan, streamed products, ordered sums
@@ -231,6 +233,7 @@ patch_kernel(const DevCsr a, const int32_t* __restrict__ pptr, const int32_t* __
   if (staged) factor_wait(&s_bar);
   __syncthreads();
   const double* L = staged ? s_L : Lg;
+  const double* Dinv = L + patch_tri_even(n);   // inverted diagonal blocks, row stride 33
 
   // ---- forward: L y = r (left-looking over 32-row panels)
   for (int p0 = 0; p0 < n; p0 += 32) {
@@ -247,24 +250,13 @@ patch_kernel(const DevCsr a, const int32_t* __restrict__ pptr, const int32_t* __
       __syncthreads();
     }
     if (warp == 0) {
-      double lrow[32];
-      const int i = p0 + lane;
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        lrow[j] = (lane < pn && j <= lane) ? L[tri(i) + p0 + j] : 0.0;
-      double xi = lane < pn ? s_x[i] : 0.0;
-      // one reciprocal per lane, in parallel, instead of 32 serial divisions
-      // one non-divergent reciprocal per lane instead of 32 serialised divisions
-      const double rd = 1.0 / (lane < pn ? L[tri(i) + i] : 1.0);
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        if (j < pn) {
-          if (lane == j) xi = xi * rd;
-          const double yj = __shfl_sync(0xffffffffu, xi, j);
-          if (lane > j) xi -= lrow[j] * yj;
-        }
-      }
-      if (lane < pn) s_x[i] = xi;
+      // x_P = inv(L_PP) r_P: a 32-wide GEMV with the precomputed inverse block
+      const double* D = Dinv + (p0 / kPanel) * kDinvBlock;
+      double acc = 0.0;
+      if (lane < pn)
+        for (int j = 0; j < pn; ++j) acc += D[lane * kDinvLd + j] * s_x[p0 + j];
+      __syncwarp();
+      if (lane < pn) s_x[p0 + lane] = acc;
     }
     __syncthreads();
   }
@@ -291,22 +283,13 @@ patch_kernel(const DevCsr a, const int32_t* __restrict__ pptr, const int32_t* __
       __syncthreads();
     }
     if (warp == 0) {
-      // lane t holds column t of the panel triangle: lcol[j] = L[p0+j][p0+t], j >= t
-      double lcol[32];
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        lcol[j] = (lane < pn && j < pn && j >= lane) ? L[tri(p0 + j) + p0 + lane] : 0.0;
-      double yt = lane < pn ? s_x[p0 + lane] : 0.0;
-      const double rd = 1.0 / (lane < pn ? L[tri(p0 + lane) + p0 + lane] : 1.0);
-#pragma unroll
-      for (int j = 31; j >= 0; --j) {
-        if (j < pn) {
-          if (lane == j) yt = yt * rd;
-          const double xj = __shfl_sync(0xffffffffu, yt, j);
-          if (lane < j) yt -= lcol[j] * xj;
-        }
-      }
-      if (lane < pn) s_x[p0 + lane] = yt;
+      // x_P = inv(L_PP)^T y_P
+      const double* D = Dinv + (p0 / kPanel) * kDinvBlock;
+      double acc = 0.0;
+      if (lane < pn)
+        for (int j = 0; j < pn; ++j) acc += D[j * kDinvLd + lane] * s_x[p0 + j];
+      __syncwarp();
+      if (lane < pn) s_x[p0 + lane] = acc;
     }
     __syncthreads();
   }

@@ -62,6 +62,19 @@ struct Correction {
   std::vector<void*> allocs;
 };
 
+// patch slot geometry: packed L (even length) + inverted 32x32 diagonal blocks
+constexpr int kPanel = 32;
+constexpr int kDinvLd = 33;                       // padded row stride (bank conflicts)
+constexpr int kDinvBlock = kPanel * kDinvLd;      // 1056 doubles (even)
+__host__ __device__ inline int64_t patch_tri_even(int64_t nd)
+{
+  return (nd * (nd + 1) / 2 + 1) & ~int64_t(1);
+}
+__host__ __device__ inline int64_t patch_slot_doubles(int64_t nd)
+{
+  return patch_tri_even(nd) + ((nd + kPanel - 1) / kPanel) * kDinvBlock;
+}
+
 enum SmootherKind : int { kChebyshev = 0, kJacobi = 1 };
 
 struct Smoother {
