@@ -188,6 +188,136 @@ def run_reference(args):
     return 0
 
 
+def make_c5_patches(n_rows: int, count: int = 1000, seed: int = 2402):
+    """C5 patches: sizes U[64, 512], disjoint random dof sets, SPD blocks
+    Q diag(logspace(0, -6)) Q^T (cond 1e6 exactly), Cholesky-factored (setup on
+    the GPU through torch; LAPACK-equivalent)."""
+    import torch
+    from paper_2402_12947_b200.smoothers import LocalCorrection
+    from paper_2402_12947_b200.sparse import DenseFactor
+    rng = np.random.default_rng(seed)
+    sizes = rng.integers(64, 513, size=count)
+    perm = rng.permutation(n_rows)
+    regions, start = [], 0
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    for nd in sizes:
+        idx = np.sort(perm[start:start + nd])
+        start += nd
+        q, _ = torch.linalg.qr(torch.randn(nd, nd, dtype=torch.float64, device="cuda", generator=g))
+        lam = torch.logspace(0, -6, int(nd), dtype=torch.float64, device="cuda")
+        blk = (q * lam) @ q.T
+        blk = 0.5 * (blk + blk.T)
+        c = torch.linalg.cholesky(blk).cpu().numpy()
+        regions.append((idx.astype(np.int64), DenseFactor("cholesky", (c, True), int(nd))))
+    return LocalCorrection(tuple(regions), n_rows)
+
+
+def run_c5(args):
+    """BASELINE configs[4]: fine-level SpMV / Jacobi / Chebyshev sweeps on the 3D P2
+    Laplacian at 2M / 8M / 16M DOFs and 1000 batched cond-1e6 patch solves."""
+    import torch
+    from paper_2402_12947_b200 import _lib, device as D, stencil
+    from paper_2402_12947_b200.mg import DeviceHierarchy  # noqa: F401
+    from oracle import oracle as O
+    torch.cuda.set_device(0)
+    lib = _lib.load()
+    peak, peak_src = _peaks()
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = max(20, min(args.steps, 200))
+    out = {"workload": "C5 micro-sweep (BASELINE configs[4])", "sizes": []}
+    grids = [int(g) for g in args.c5_grids.split(",")]
+    first_a = None
+    for g in grids:
+        t0 = time.perf_counter()
+        a = stencil.p2_tet_laplacian(g)
+        gen_s = time.perf_counter() - t0
+        op = D.device_operator(a)
+        n, z = op.nrows, op.nnz
+        x = torch.randn(n, dtype=torch.float64, device="cuda")
+        b = torch.randn(n, dtype=torch.float64, device="cuda")
+        y = torch.empty_like(x)
+        dbuf = torch.zeros_like(x)
+        res = {"grid": g, "dofs": n, "nnz": z, "nnz_per_row": z / n, "gen_s": gen_s}
+
+        def timeit(fn):
+            for _ in range(5):
+                fn()
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for _ in range(reps):
+                fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            return e0.elapsed_time(e1) / reps * 1e3  # us
+
+        us = timeit(lambda: _lib.check(lib.smg_spmv(op.handle, D.ptr(x), D.ptr(y), sh)))
+        byt = 12 * z + 4 * (n + 1) + 16 * n
+        res["spmv"] = {"us": us, "gbs": byt / us / 1e3, "frac": byt / us / 1e3 / peak, "bytes": byt}
+        us = timeit(lambda: _lib.check(lib.smg_smoother_step(op.handle, D.ptr(b), D.ptr(x), D.ptr(y),
+                                                             D.ptr(dbuf), 0, 1.5, 0.0, 0.0, sh)))
+        byt = 12 * z + 28 * n
+        res["jacobi_sweep"] = {"us": us, "sweeps_per_s": 1e6 / us, "gbs": byt / us / 1e3,
+                               "frac": byt / us / 1e3 / peak, "bytes": byt}
+        us = timeit(lambda: _lib.check(lib.smg_smoother_step(op.handle, D.ptr(b), D.ptr(x), D.ptr(y),
+                                                             D.ptr(dbuf), 2, 1.5, 0.3, 0.7, sh)))
+        byt = 12 * z + 44 * n
+        res["chebyshev_step"] = {"us": us, "sweeps_per_s": 1e6 / us, "gbs": byt / us / 1e3,
+                                 "frac": byt / us / 1e3 / peak, "bytes": byt}
+        # parity: bitwise vs the oracle on this matrix
+        xh = x.cpu().numpy()
+        _lib.check(lib.smg_spmv(op.handle, D.ptr(x), D.ptr(y), sh))
+        torch.cuda.synchronize()
+        res["spmv_bitwise_vs_oracle"] = bool(np.array_equal(y.cpu().numpy(), O.spmv(a, xh)))
+        if first_a is None:
+            t0 = time.perf_counter()
+            O.spmv(a, xh)
+            res["cpu_oracle_spmv_us"] = 1e6 * (time.perf_counter() - t0)
+            res["cpu_threads"] = O.num_threads()
+            first_a = (a, op)
+        out["sizes"].append(res)
+        del x, b, y, dbuf
+    # batched patch solves (1000 patches, 64..512 dofs, cond 1e6) on the first matrix
+    a, op = first_a
+    t0 = time.perf_counter()
+    lc = make_c5_patches(a.nrows)
+    patch_setup_s = time.perf_counter() - t0
+    dc = D.DeviceCorrection(op, lc)
+    r = torch.randn(a.nrows, dtype=torch.float64, device="cuda")
+    o = torch.empty_like(r)
+    us_lc = None
+    for _ in range(3):
+        _lib.check(lib.smg_apply_local_correction(dc.handle, D.ptr(r), D.ptr(o), sh))
+    torch.cuda.synchronize()
+    e0.record(stream)
+    nrep = 20
+    for _ in range(nrep):
+        _lib.check(lib.smg_apply_local_correction(dc.handle, D.ptr(r), D.ptr(o), sh))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    us_lc = e0.elapsed_time(e1) / nrep * 1e3
+    sizes = np.array([len(i) for i, _ in lc.regions])
+    fac_bytes = float(np.sum(8 * sizes * (sizes + 1) / 2))
+    lc_bytes = 2 * fac_bytes + 8 * 4 * sizes.sum()   # two triangular sweeps + gather/scatter
+    ref = O.apply_local_correction(lc, r.cpu().numpy())
+    rel = float(np.linalg.norm(o.cpu().numpy() - ref) / np.linalg.norm(ref))
+    t0 = time.perf_counter()
+    O.apply_local_correction(lc, r.cpu().numpy())
+    cpu_lc_s = time.perf_counter() - t0
+    out["patches"] = {"count": int(len(sizes)), "dofs_min": int(sizes.min()),
+                      "dofs_max": int(sizes.max()), "dofs_total": int(sizes.sum()),
+                      "factor_bytes": fac_bytes, "us": us_lc,
+                      "gbs": lc_bytes / us_lc / 1e3, "frac": lc_bytes / us_lc / 1e3 / peak,
+                      "rel_diff_vs_oracle": rel, "setup_s": patch_setup_s,
+                      "cpu_oracle_us": 1e6 * cpu_lc_s}
+    out["peak_gbs"] = peak
+    out["peak_source"] = peak_src
+    out["metric"] = "smoother sweeps/s and SpMV HBM GB/s (fp64), C5 micro-sweep"
+    print(json.dumps(out))
+    return 0
+
+
 def _config(wl, h):
     return {
         "workload": f"{wl.name}: BASELINE configs[1] (2D Poisson P2, 513x513 vertex grid, "
@@ -213,11 +343,15 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--c5-grids", default="63,100,126",
+                    help="C5 P2-tet grids (n cells per edge): 63/100/126 = 2M/8M/16M DOFs")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload == "C5":
+        return run_c5(args)
 
     import torch
     import torch.distributed as dist

@@ -348,7 +348,7 @@ static int enqueue_vcycle(Hierarchy& h, const double* b0, double* u0, cudaStream
       EpiArgs er;
       er.out = alt[l + 1];
       er.b_out = N.b;
-      er.diag = N.a->diag;
+      er.inv_diag = N.a->inv_diag;
       er.theta = N.cs.theta;
       er.d = N.cs.collapsed ? nullptr : N.d;
       SMG_CUDA(launch_csr_stream(L.p->t, L.r, Epi::kRestrictFirst, er, st));
@@ -511,14 +511,22 @@ int smg_operator_create(int64_t nrows, int64_t ncols, const int64_t* rowptr, con
   for (int64_t j = 0; j < nnz && o.all_finite; ++j)
     if (!std::isfinite(val[j])) o.all_finite = false;
   if (nrows == ncols && nd > 0) {
+    // inv_diag = 1.0 / diag: the same IEEE division numpy performs
+    // (smoothers.py:115), so the epilogue multiplies by identical values
+    std::vector<double> inv((size_t)nd);
+    for (int64_t i = 0; i < nd; ++i) inv[(size_t)i] = 1.0 / diag[(size_t)i];
     double* dd = nullptr;
+    double* di = nullptr;
     rc = dev_upload(o.allocs, o.device_bytes, diag.data(), diag.size(), &dd);
+    if (rc == SMG_OK) rc = dev_upload(o.allocs, o.device_bytes, inv.data(), inv.size(), &di);
     if (rc != SMG_OK) {
       free_all(o.allocs);
       delete op;
       return rc;
     }
     o.diag = dd;
+    o.inv_diag = di;
+    o.a.inv_diag = di;
   }
   if (with_transpose) {
     // CSR(A^T) with ascending source rows in each row (counting sort is stable)

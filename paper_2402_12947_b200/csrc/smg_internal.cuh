@@ -31,6 +31,7 @@ struct DevCsr {
   const double* val = nullptr;       // nnz
   const int32_t* tile_row = nullptr; // ntiles + 1 (row boundaries of tiles)
   const int64_t* tile_nz = nullptr;  // ntiles + 1 (rowptr at the tile boundaries)
+  const double* inv_diag = nullptr;  // 1.0 / a_ii (IEEE, as smoothers.py:115), square ops
   int32_t ntiles = 0;
 };
 
@@ -42,6 +43,7 @@ struct Operator {
   int64_t first_zero_diag = -1;   // -1: every row has a nonzero diagonal
   bool all_finite = true;          // every stored value is finite
   const double* diag = nullptr;    // explicit diagonal (0.0 where absent), square ops
+  const double* inv_diag = nullptr;  // 1.0 / diag, exactly as numpy forms inv_diag
   int64_t device_bytes = 0;
   std::vector<void*> allocs;
 };
@@ -110,7 +112,7 @@ struct EpiArgs {
   double* out = nullptr;   // y / r / u_out
   double* d = nullptr;
   double theta = 1.0, c1 = 0.0, c2 = 0.0;
-  const double* diag = nullptr;   // kRestrictFirst: coarse operator diagonal
+  const double* inv_diag = nullptr;  // kRestrictFirst: coarse operator 1/diagonal
   double* b_out = nullptr;        // kRestrictFirst: restricted right-hand side
 };
 

@@ -98,6 +98,7 @@ struct EpiTraits {
   static constexpr bool kD = (E == Epi::kChebNext);
   static constexpr bool kOut = (E == Epi::kAddTo);
   static constexpr bool kDiagVec = (E == Epi::kRestrictFirst);
+  static constexpr bool kInv = kDiag || kDiagVec;   // needs 1/a_ii
 };
 
 // ring-slot geometry (bytes are multiples of 16 as cp.async.bulk requires)
@@ -122,13 +123,13 @@ __device__ __forceinline__ void epilogue(const DevCsr& m, const EpiArgs& ea, int
     ea.out[row] = __dadd_rn(ov, sum);
   } else if constexpr (E == Epi::kRestrictFirst) {
     ea.b_out[row] = sum;
-    const double inv = __ddiv_rn(1.0, dg);
+    const double inv = dg;
     const double t = __dmul_rn(inv, __dsub_rn(sum, 0.0));
     const double d = __ddiv_rn(t, ea.theta);
     if (ea.d) ea.d[row] = d;
     ea.out[row] = __dadd_rn(0.0, d);
   } else {
-    const double inv = __ddiv_rn(1.0, dg);
+    const double inv = dg;  // 1.0 / a_ii, precomputed with the same IEEE division
     const double t = __dmul_rn(inv, __dsub_rn(bv, sum));
     if constexpr (E == Epi::kJacobi) {
       ea.out[row] = __dadd_rn(uv, __ddiv_rn(t, ea.theta));
@@ -216,8 +217,9 @@ csr_stream_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea
     const int64_t e1 = m.tile_nz[t + 1];
     double sum = 0.0;
     double dg = 0.0;
-    if constexpr (T::kDiagVec) {
-      if (has_row) dg = ea.diag[row];
+    if (has_row) {
+      if constexpr (T::kDiag) dg = m.inv_diag[row];
+      if constexpr (T::kDiagVec) dg = ea.inv_diag[row];
     }
     mbar_wait(&bars[s], parity);
     if (e1 - e0 <= kTileNnz) {
@@ -237,14 +239,7 @@ csr_stream_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea
       if (has_row) {
         const int a = (int)(srp[tid] - e0);
         const int bnd = (int)(srp[tid + 1] - e0);
-        int jd = -1;
-        for (int j = a; j < bnd; ++j) {
-          sum = __dadd_rn(sum, s_prod[j]);
-          if constexpr (T::kDiag) {
-            if (scol[j] == row) jd = j;
-          }
-        }
-        if constexpr (T::kDiag) dg = jd >= 0 ? sval[jd] : 0.0;
+        for (int j = a; j < bnd; ++j) sum = __dadd_rn(sum, s_prod[j]);
       }
     } else {
       // long tile (a row longer than one ring slot): chunked, global reads
@@ -253,7 +248,6 @@ csr_stream_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea
         lo = m.rowptr[row];
         hi = m.rowptr[row + 1];
       }
-      int64_t jd = -1;
       for (int64_t cs = e0; cs < e1; cs += kTileNnz) {
         const int64_t rem = e1 - cs;
         const int cnt = rem < (int64_t)kTileNnz ? (int)rem : kTileNnz;
@@ -263,16 +257,10 @@ csr_stream_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea
         if (has_row) {
           const int64_t a = lo > cs ? lo : cs;
           const int64_t bnd = hi < cs + cnt ? hi : cs + cnt;
-          for (int64_t j = a; j < bnd; ++j) {
-            sum = __dadd_rn(sum, s_prod[j - cs]);
-            if constexpr (T::kDiag) {
-              if (__ldg(m.col + j) == row) jd = j;
-            }
-          }
+          for (int64_t j = a; j < bnd; ++j) sum = __dadd_rn(sum, s_prod[j - cs]);
         }
         __syncthreads();
       }
-      if constexpr (T::kDiag) dg = jd >= 0 ? __ldg(m.val + jd) : 0.0;
     }
     if (has_row) epilogue<E>(m, ea, row, sum, dg, bv, uv, dv, ov);
     __syncthreads();  // slot s and s_prod are free again
@@ -303,7 +291,6 @@ csr_flat_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea)
   extern __shared__ __align__(128) unsigned char fsmem[];
   __shared__ uint64_t bar;
   __shared__ double s_prod_static[kTma ? 1 : kTileNnz];
-  __shared__ int32_t s_col_static[(kTma || !T::kDiag) ? 1 : kTileNnz];
   const int t = blockIdx.x;
   const int tid = threadIdx.x;
   // ---- operator data (never written by any kernel): safe before the
@@ -354,16 +341,15 @@ csr_flat_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea)
     if constexpr (T::kU) uv = ea.u_in[row];
     if constexpr (T::kD) dv = ea.d[row];
     if constexpr (T::kOut) ov = ea.out[row];
-    if constexpr (T::kDiagVec) dg = ea.diag[row];
+    if constexpr (T::kDiag) dg = m.inv_diag[row];
+    if constexpr (T::kDiagVec) dg = ea.inv_diag[row];
   }
   double* s_prod = kTma ? reinterpret_cast<double*>(fsmem + kSlotBytes) : s_prod_static;
   if (!longtile) {
-    const double* vals = nullptr;
-    const int32_t* cols;
     if constexpr (kTma) {
       mbar_wait(&bar, 0);
-      vals = reinterpret_cast<const double*>(fsmem) + (e0 & 1);
-      cols = reinterpret_cast<const int32_t*>(fsmem + kValCap * 8) + (e0 & 3);
+      const double* vals = reinterpret_cast<const double*>(fsmem) + (e0 & 1);
+      const int32_t* cols = reinterpret_cast<const int32_t*>(fsmem + kValCap * 8) + (e0 & 3);
       const int64_t* srp =
           reinterpret_cast<const int64_t*>(fsmem + kValCap * 8 + kColCap * 4) + (r0 & 1);
       if (has_row) {
@@ -379,31 +365,17 @@ csr_flat_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea)
 #pragma unroll
       for (int i = 0; i < kItems; ++i) {
         const int k = i * kThreads + tid;
-        if (k < cnt) {
-          s_prod[k] = __dmul_rn(v[i], __ldg(x + c[i]));
-          if constexpr (T::kDiag) s_col_static[k] = c[i];
-        }
+        if (k < cnt) s_prod[k] = __dmul_rn(v[i], __ldg(x + c[i]));
       }
-      cols = s_col_static;
     }
     __syncthreads();
     if (has_row) {
       const int a = (int)(lo - e0);
       const int bnd = (int)(hi - e0);
-      int jd = -1;
-      for (int j = a; j < bnd; ++j) {
-        sum = __dadd_rn(sum, s_prod[j]);
-        if constexpr (T::kDiag) {
-          if (cols[j] == row) jd = j;
-        }
-      }
-      if constexpr (T::kDiag) {
-        if (jd >= 0) dg = kTma ? vals[jd] : __ldg(m.val + e0 + jd);
-      }
+      for (int j = a; j < bnd; ++j) sum = __dadd_rn(sum, s_prod[j]);
     }
   } else {
     if constexpr (kTma) mbar_wait(&bar, 0);
-    int64_t jd = -1;
     for (int64_t cs = e0; cs < e1; cs += kTileNnz) {
       const int64_t rem = e1 - cs;
       const int cn = rem < (int64_t)kTileNnz ? (int)rem : kTileNnz;
@@ -413,18 +385,218 @@ csr_flat_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea)
       if (has_row) {
         const int64_t a = lo > cs ? lo : cs;
         const int64_t bnd = hi < cs + cn ? hi : cs + cn;
-        for (int64_t j = a; j < bnd; ++j) {
-          sum = __dadd_rn(sum, s_prod[j - cs]);
-          if constexpr (T::kDiag) {
-            if (__ldg(m.col + j) == row) jd = j;
-          }
-        }
+        for (int64_t j = a; j < bnd; ++j) sum = __dadd_rn(sum, s_prod[j - cs]);
       }
       __syncthreads();
     }
-    if constexpr (T::kDiag) dg = jd >= 0 ? __ldg(m.val + jd) : 0.0;
   }
   if (has_row) epilogue<E>(m, ea, row, sum, dg, bv, uv, dv, ov);
+}
+
+// ---------------------------------------------------------------------------
+// Variant 5: persistent CTAs over CONTIGUOUS tile ranges with a TMA ring that
+// carries everything a tile needs -- values, column indices, row offsets AND
+// the per-row epilogue vectors (b, u, d, 1/a_ii, out) -- so each tile costs
+// the consumers one barrier wait, the x gathers (L1/L2: neighbouring tiles
+// share x) and the sums.  The CTA's tile descriptors are staged in shared
+// memory up front, so the producer never waits on a dependent global load.
+// Operator data of the first kPStages tiles is requested before the
+// programmatic-dependency wait; vectors (produced by earlier kernels) after.
+constexpr int kPStages = 2;
+constexpr int kPCtas = 2;
+constexpr int kVecCap = kRowsPerTile + 2;               // doubles per vector slot
+constexpr int kPVal = 0;
+constexpr int kPCol = kPVal + kValCap * 8;
+constexpr int kPRp = kPCol + kColCap * 4;
+constexpr int kPVec = kPRp + kRpCap * 8;
+constexpr int kPSlot = kPVec + 4 * kVecCap * 8;          // 4 vector slots
+constexpr int kPMaxTiles = 512;                          // descriptors staged per pass
+static_assert(kPSlot % 16 == 0, "slot alignment");
+constexpr int kPSmem = kPStages * kPSlot + kTileNnz * 8 + kPMaxTiles * 12 + 16;
+
+template <Epi E>
+struct PVecs {
+  using T = EpiTraits<E>;
+  // which vectors ride in the ring, in slot order
+  static constexpr int kN = (T::kB ? 1 : 0) + (T::kU ? 1 : 0) + (T::kD ? 1 : 0) + (T::kOut ? 1 : 0) +
+                            (T::kInv ? 1 : 0);
+  __device__ static int fill(const DevCsr& m, const EpiArgs& ea, const double** v)
+  {
+    int k = 0;
+    if constexpr (T::kB) v[k++] = ea.b;
+    if constexpr (T::kU) v[k++] = ea.u_in;
+    if constexpr (T::kD) v[k++] = ea.d;
+    if constexpr (T::kOut) v[k++] = ea.out;
+    if constexpr (T::kDiag) v[k++] = m.inv_diag;
+    if constexpr (T::kDiagVec) v[k++] = ea.inv_diag;
+    return k;
+  }
+};
+
+__device__ __forceinline__ uint32_t tile_op_bytes(int32_t r0, int32_t r1, int64_t e0, int64_t e1)
+{
+  if (e1 - e0 > kTileNnz) return 0;
+  const int64_t va = e0 & ~int64_t(1), vb = (e1 + 1) & ~int64_t(1);
+  const int64_t ca = e0 & ~int64_t(3), cb = (e1 + 3) & ~int64_t(3);
+  const int64_t ra = r0 & ~1, rb = (int64_t(r1) + 2) & ~int64_t(1);
+  return (uint32_t)((vb - va) * 8 + (cb - ca) * 4 + (rb - ra) * 8);
+}
+
+__device__ __forceinline__ uint32_t tile_vec_bytes(int32_t r0, int32_t r1, int nvec)
+{
+  const int32_t ra = r0 & ~1, rb = r1 & ~1;
+  return rb > ra ? (uint32_t)((rb - ra) * 8 * nvec) : 0u;
+}
+
+template <Epi E>
+__global__ void __launch_bounds__(kThreads, kPCtas)
+csr_pipe_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea)
+{
+  using T = EpiTraits<E>;
+  using V = PVecs<E>;
+  extern __shared__ __align__(128) unsigned char psm[];
+  __shared__ uint64_t bars[kPStages];
+  double* s_prod = reinterpret_cast<double*>(psm + kPStages * kPSlot);
+  int32_t* s_trow = reinterpret_cast<int32_t*>(psm + kPStages * kPSlot + kTileNnz * 8);
+  int64_t* s_tnz = reinterpret_cast<int64_t*>(psm + kPStages * kPSlot + kTileNnz * 8 + kPMaxTiles * 4 + 8);
+  const int tid = threadIdx.x;
+  const int G = gridDim.x;
+  const int tb_all = (int)(((int64_t)m.ntiles * blockIdx.x) / G);
+  const int te_all = (int)(((int64_t)m.ntiles * (blockIdx.x + 1)) / G);
+  const double* vecs[5];
+  V::fill(m, ea, vecs);
+
+  if (tid == 0) {
+    for (int s = 0; s < kPStages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  int it = 0;  // global tile counter (ring position)
+  bool waited = false;
+  for (int tb = tb_all; tb < te_all; tb += kPMaxTiles) {
+    const int te = min(te_all, tb + kPMaxTiles);
+    const int nt = te - tb;
+    __syncthreads();
+    for (int i = tid; i <= nt; i += kThreads) {
+      s_trow[i] = m.tile_row[tb + i];
+      s_tnz[i] = m.tile_nz[tb + i];
+    }
+    __syncthreads();
+    auto issue_op = [&](int i, int s) {
+      const int32_t r0 = s_trow[i], r1 = s_trow[i + 1];
+      const int64_t e0 = s_tnz[i], e1 = s_tnz[i + 1];
+      unsigned char* slot = psm + s * kPSlot;
+      const uint32_t bo = tile_op_bytes(r0, r1, e0, e1);
+      const uint32_t bvv = tile_vec_bytes(r0, r1, V::kN);
+      mbar_arrive_expect_tx(&bars[s], bo + bvv);
+      if (bo) {
+        const int64_t va = e0 & ~int64_t(1), vb = (e1 + 1) & ~int64_t(1);
+        const int64_t ca = e0 & ~int64_t(3), cb = (e1 + 3) & ~int64_t(3);
+        const int64_t ra = r0 & ~1, rb = (int64_t(r1) + 2) & ~int64_t(1);
+        if (vb > va) bulk_g2s(slot + kPVal, m.val + va, (uint32_t)((vb - va) * 8), &bars[s]);
+        if (cb > ca) bulk_g2s(slot + kPCol, m.col + ca, (uint32_t)((cb - ca) * 4), &bars[s]);
+        bulk_g2s(slot + kPRp, m.rowptr + ra, (uint32_t)((rb - ra) * 8), &bars[s]);
+      }
+    };
+    auto issue_vec = [&](int i, int s) {
+      const int32_t r0 = s_trow[i], r1 = s_trow[i + 1];
+      const int32_t ra = r0 & ~1, rb = r1 & ~1;
+      if (rb <= ra) return;
+      unsigned char* slot = psm + s * kPSlot;
+      for (int k = 0; k < V::kN; ++k)
+        bulk_g2s(slot + kPVec + k * kVecCap * 8, vecs[k] + ra, (uint32_t)((rb - ra) * 8), &bars[s]);
+    };
+    if (tid == 0) {
+      for (int j = 0; j < kPStages && j < nt; ++j) issue_op(j, (it + j) % kPStages);
+    }
+    if (!waited) {
+      pdl_wait();
+      pdl_trigger();
+      waited = true;
+    }
+    if (tid == 0) {
+      for (int j = 0; j < kPStages && j < nt; ++j) issue_vec(j, (it + j) % kPStages);
+    }
+    for (int i = 0; i < nt; ++i, ++it) {
+      const int s = it % kPStages;
+      const uint32_t parity = (uint32_t)((it / kPStages) & 1);
+      unsigned char* slot = psm + s * kPSlot;
+      const int32_t r0 = s_trow[i], r1 = s_trow[i + 1];
+      const int64_t e0 = s_tnz[i], e1 = s_tnz[i + 1];
+      const int32_t row = r0 + tid;
+      const bool has_row = row < r1;
+      const int32_t ra = r0 & ~1, rbv = r1 & ~1;
+      double sum = 0.0;
+      mbar_wait(&bars[s], parity);
+      // epilogue operands: from the ring, or (one odd trailing row) from global
+      double ev[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+      if (has_row) {
+        if (row < rbv) {
+          const double* vs = reinterpret_cast<const double*>(slot + kPVec) + (row - ra);
+#pragma unroll
+          for (int k = 0; k < V::kN; ++k) ev[k] = vs[k * kVecCap];
+        } else {
+#pragma unroll
+          for (int k = 0; k < V::kN; ++k) ev[k] = vecs[k][row];
+        }
+      }
+      if (e1 - e0 <= kTileNnz) {
+        const double* sval = reinterpret_cast<const double*>(slot + kPVal) + (e0 & 1);
+        const int32_t* scol = reinterpret_cast<const int32_t*>(slot + kPCol) + (e0 & 3);
+        const int64_t* srp = reinterpret_cast<const int64_t*>(slot + kPRp) + (r0 & 1);
+        const int cnt = (int)(e1 - e0);
+#pragma unroll
+        for (int q = 0; q < kItems; ++q) {
+          const int k = q * kThreads + tid;
+          if (k < cnt) s_prod[k] = __dmul_rn(sval[k], __ldg(x + scol[k]));
+        }
+        __syncthreads();
+        if (has_row) {
+          const int a = (int)(srp[tid] - e0);
+          const int bnd = (int)(srp[tid + 1] - e0);
+          for (int j = a; j < bnd; ++j) sum = __dadd_rn(sum, s_prod[j]);
+        }
+      } else {
+        int64_t lo = 0, hi = 0;
+        if (has_row) {
+          lo = m.rowptr[row];
+          hi = m.rowptr[row + 1];
+        }
+        for (int64_t cs = e0; cs < e1; cs += kTileNnz) {
+          const int64_t rem = e1 - cs;
+          const int cn = rem < (int64_t)kTileNnz ? (int)rem : kTileNnz;
+          for (int k = tid; k < cn; k += kThreads)
+            s_prod[k] = __dmul_rn(__ldg(m.val + cs + k), __ldg(x + __ldg(m.col + cs + k)));
+          __syncthreads();
+          if (has_row) {
+            const int64_t a = lo > cs ? lo : cs;
+            const int64_t bnd = hi < cs + cn ? hi : cs + cn;
+            for (int64_t j = a; j < bnd; ++j) sum = __dadd_rn(sum, s_prod[j - cs]);
+          }
+          __syncthreads();
+        }
+      }
+      if (has_row) {
+        int k = 0;
+        double bv = 0.0, uv = 0.0, dv = 0.0, ov = 0.0, dg = 0.0;
+        if constexpr (T::kB) bv = ev[k++];
+        if constexpr (T::kU) uv = ev[k++];
+        if constexpr (T::kD) dv = ev[k++];
+        if constexpr (T::kOut) ov = ev[k++];
+        if constexpr (T::kInv) dg = ev[k++];
+        epilogue<E>(m, ea, row, sum, dg, bv, uv, dv, ov);
+      }
+      __syncthreads();  // slot s and s_prod are free again
+      if (tid == 0 && i + kPStages < nt) {
+        fence_proxy_async();
+        issue_op(i + kPStages, s);
+        issue_vec(i + kPStages, s);
+      }
+    }
+  }
+  if (!waited) {
+    pdl_wait();
+    pdl_trigger();
+  }
 }
 
 static int g_sm_count = 0;
@@ -466,6 +638,34 @@ static cudaError_t launch_t(const DevCsr& m, const double* x, const EpiArgs& ea,
     configured = true;
   }
   const int variant = spmv_variant();
+  if (variant == 5) {
+    static bool configured5 = false;
+    if (!configured5) {
+      cudaError_t e = cudaFuncSetAttribute(csr_pipe_kernel<E>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmem);
+      if (e != cudaSuccess) return e;
+      configured5 = true;
+    }
+    if (g_sm_count == 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
+      if (g_sm_count <= 0) g_sm_count = 148;
+    }
+    int grid = g_sm_count * kPCtas;
+    if (grid > m.ntiles) grid = m.ntiles;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kPSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = use_pdl() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, csr_pipe_kernel<E>, m, x, ea);
+  }
   if (variant >= 1) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)m.ntiles);

@@ -1,4 +1,4 @@
-"""BASELINE-size parity: C1 (16,641 DOFs) and C2 (1,050,625 DOFs) hierarchies
+"""BASELINE-size parity: C1 (16,641 DOFs), C2 (1,050,625) and C3 (274,625) hierarchies
 built by this repo's setup, GPU path vs the CPU oracle on identical inputs,
 plus size-independent properties of the V-cycle.
 
@@ -17,7 +17,7 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
-@pytest.fixture(scope="module", params=["C1", "C2"])
+@pytest.fixture(scope="module", params=["C1", "C2", "C3"])
 def case(request):
     from paper_2402_12947_b200 import configs
     h, b, u0 = configs.build(configs.WORKLOADS[request.param])
