@@ -115,6 +115,23 @@ def _dist():
     return ws, rank, local
 
 
+def max_over_ranks(value: float, device: str = "cuda") -> float:
+    """Replica timing aggregation for N > 1: every rank's elapsed time, max-reduced
+    (the slowest replica bounds the whole job).  Single-process: identity."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], device=device, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def whole_job_rate(units_per_rank: int, elapsed_max_s: float, world: int) -> float:
+    """`value` = units all ranks processed / the max-over-ranks time (weak scaling)."""
+    return world * units_per_rank / elapsed_max_s
+
+
 def _cheb_steps(cfg):
     """(theta, [(c1, c2), ...]) exactly as smoothers.py:109-135 computes them."""
     lam_max, frac = cfg.chebyshev_parameters()
@@ -395,13 +412,9 @@ def main():
     if ws > 1:
         dist.barrier()
     clocks = sampler.stop()
-    ms = e0.elapsed_time(e1)
-    if ws > 1:
-        tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
+    ms = max_over_ranks(e0.elapsed_time(e1))
     ms_per_step = ms / args.steps
-    value = ws * args.steps / (ms / 1e3)
+    value = whole_job_rate(args.steps, ms / 1e3, ws)
 
     # ---- dominant kernel: fine-level Chebyshev step (K3), CUDA events on its stream
     lv = h.levels[0]
@@ -473,12 +486,8 @@ def main():
     for _ in range(e2e_steps):
         dh.vcycle(bnp, unp)
     e2e_s = time.perf_counter() - t0
-    e2e_val = e2e_s
-    if ws > 1:
-        tt = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_val = float(tt.item())
-    e2e = {"value": ws * e2e_steps / e2e_val, "unit": UNIT,
+    e2e_val = max_over_ranks(e2e_s)
+    e2e = {"value": whole_job_rate(e2e_steps, e2e_val, ws), "unit": UNIT,
            "h2d_bytes_per_step": 2 * 8 * n0, "d2h_bytes_per_step": 8 * n0,
            "steps": e2e_steps, "path": "smg_vcycle_host (pinned numpy b, u)"}
 
