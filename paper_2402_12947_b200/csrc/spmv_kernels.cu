@@ -93,7 +93,7 @@ __device__ __forceinline__ void pdl_trigger()
 template <Epi E>
 struct EpiTraits {
   static constexpr bool kDiag = (E == Epi::kJacobi || E == Epi::kChebFirst || E == Epi::kChebNext);
-  static constexpr bool kB = (E != Epi::kSpmv && E != Epi::kAddTo);
+  static constexpr bool kB = (E != Epi::kSpmv && E != Epi::kAddTo && E != Epi::kRestrictFirst);
   static constexpr bool kU = (E == Epi::kJacobi || E == Epi::kChebFirst || E == Epi::kChebNext);
   static constexpr bool kD = (E == Epi::kChebNext);
   static constexpr bool kOut = (E == Epi::kAddTo);
