@@ -82,7 +82,8 @@ SMG_API int smg_prolong_add(const smg_operator *p, const double *u_coarse, doubl
                     void *stream);
 
 /* Chebyshev / damped-Jacobi smoother in place on u (smoothers.py:99-136;
- * bitwise).  work: 2*n device doubles, or NULL for a library allocation. */
+ * bitwise).  work: 2*((n+1)/2)*2 device doubles (two 16-byte aligned halves),
+ * or NULL for a library allocation. */
 SMG_API int smg_chebyshev_smooth(const smg_operator *a, const double *b, double *u, int sweeps,
                          double lambda_max, double lambda_min_fraction, double *work,
                          void *stream);

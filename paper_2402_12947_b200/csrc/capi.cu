@@ -664,10 +664,11 @@ static int smooth_standalone(const Operator& o, const double* b, double* u, cons
   std::vector<void*> tmp;
   int64_t bytes = 0;
   double* w = work;
-  if (!w && n > 0) SMG_TRY(dev_alloc(tmp, bytes, (size_t)(2 * n), &w));
+  const int64_t n_even = (n + 1) & ~int64_t(1);   // keep d 16-byte aligned
+  if (!w && n > 0) SMG_TRY(dev_alloc(tmp, bytes, (size_t)(2 * n_even), &w));
   double* cur = u;
   double* alt = w;
-  double* d = w ? w + n : nullptr;
+  double* d = w ? w + n_even : nullptr;
   int64_t launches = 0;
   int rc = SMG_OK;
   const bool active = c && c->n_regions > 0;

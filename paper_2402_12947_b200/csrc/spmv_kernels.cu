@@ -283,9 +283,14 @@ csr_stream_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea
 // values) as early as possible so a tile costs ~3 memory latencies.
 constexpr int kFlatTmaSmem = kSlotBytes + kTileNnz * 8;
 
-template <Epi E, bool kTma, int kMinB>
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes)
+{
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+template <Epi E, bool kTma, int kMinB, bool kPf = false>
 __global__ void __launch_bounds__(kThreads, kMinB)
-csr_flat_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea)
+csr_flat_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, int pf_dist = 0)
 {
   using T = EpiTraits<E>;
   extern __shared__ __align__(128) unsigned char fsmem[];
@@ -327,6 +332,22 @@ csr_flat_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea)
       if (!longtile && k < cnt) {
         c[i] = __ldg(m.col + e0 + k);
         v[i] = __ldg(m.val + e0 + k);
+      }
+    }
+  }
+  if constexpr (kPf) {
+    // pull the tile that will start one resident-wave later into L2 (bulk
+    // prefetch: no registers, no shared memory), so its CTA's loads hit L2
+    if (tid == 0) {
+      const int tp = t + pf_dist;
+      if (tp < m.ntiles) {
+        const int64_t p0 = m.tile_nz[tp], p1 = m.tile_nz[tp + 1];
+        if (p1 - p0 <= kTileNnz && p1 > p0) {
+          const int64_t va = p0 & ~int64_t(1), vb = (p1 + 1) & ~int64_t(1);
+          const int64_t ca = p0 & ~int64_t(3), cb = (p1 + 3) & ~int64_t(3);
+          prefetch_l2(m.val + va, (uint32_t)((vb - va) * 8));
+          prefetch_l2(m.col + ca, (uint32_t)((cb - ca) * 4));
+        }
       }
     }
   }
@@ -465,6 +486,8 @@ csr_pipe_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea)
   const int te_all = (int)(((int64_t)m.ntiles * (blockIdx.x + 1)) / G);
   const double* vecs[5];
   V::fill(m, ea, vecs);
+  bool vec_bulk = true;  // bulk copies need 16-byte aligned vector bases
+  for (int k = 0; k < V::kN; ++k) vec_bulk &= ((reinterpret_cast<uintptr_t>(vecs[k]) & 15) == 0);
 
   if (tid == 0) {
     for (int s = 0; s < kPStages; ++s) mbar_init(&bars[s], 1);
@@ -486,7 +509,7 @@ csr_pipe_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea)
       const int64_t e0 = s_tnz[i], e1 = s_tnz[i + 1];
       unsigned char* slot = psm + s * kPSlot;
       const uint32_t bo = tile_op_bytes(r0, r1, e0, e1);
-      const uint32_t bvv = tile_vec_bytes(r0, r1, V::kN);
+      const uint32_t bvv = vec_bulk ? tile_vec_bytes(r0, r1, V::kN) : 0u;
       mbar_arrive_expect_tx(&bars[s], bo + bvv);
       if (bo) {
         const int64_t va = e0 & ~int64_t(1), vb = (e1 + 1) & ~int64_t(1);
@@ -500,7 +523,7 @@ csr_pipe_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea)
     auto issue_vec = [&](int i, int s) {
       const int32_t r0 = s_trow[i], r1 = s_trow[i + 1];
       const int32_t ra = r0 & ~1, rb = r1 & ~1;
-      if (rb <= ra) return;
+      if (rb <= ra || !vec_bulk) return;
       unsigned char* slot = psm + s * kPSlot;
       for (int k = 0; k < V::kN; ++k)
         bulk_g2s(slot + kPVec + k * kVecCap * 8, vecs[k] + ra, (uint32_t)((rb - ra) * 8), &bars[s]);
@@ -524,7 +547,7 @@ csr_pipe_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea)
       const int64_t e0 = s_tnz[i], e1 = s_tnz[i + 1];
       const int32_t row = r0 + tid;
       const bool has_row = row < r1;
-      const int32_t ra = r0 & ~1, rbv = r1 & ~1;
+      const int32_t ra = r0 & ~1, rbv = vec_bulk ? (r1 & ~1) : r0;
       double sum = 0.0;
       mbar_wait(&bars[s], parity);
       // epilogue operands: from the ring, or (one odd trailing row) from global
@@ -677,10 +700,20 @@ static cudaError_t launch_t(const DevCsr& m, const double* x, const EpiArgs& ea,
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = use_pdl() ? 1 : 0;
-    if (variant == 1) return cudaLaunchKernelEx(&cfg, csr_flat_kernel<E, false, 6>, m, x, ea);
-    if (variant == 3) return cudaLaunchKernelEx(&cfg, csr_flat_kernel<E, false, 4>, m, x, ea);
-    if (variant == 4) return cudaLaunchKernelEx(&cfg, csr_flat_kernel<E, false, 8>, m, x, ea);
-    return cudaLaunchKernelEx(&cfg, csr_flat_kernel<E, true, 4>, m, x, ea);
+    if (variant == 1) return cudaLaunchKernelEx(&cfg, csr_flat_kernel<E, false, 6>, m, x, ea, 0);
+    if (variant == 3) return cudaLaunchKernelEx(&cfg, csr_flat_kernel<E, false, 4>, m, x, ea, 0);
+    if (variant == 4) return cudaLaunchKernelEx(&cfg, csr_flat_kernel<E, false, 8>, m, x, ea, 0);
+    if (variant == 10 || variant == 11) {
+      if (g_sm_count == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
+        if (g_sm_count <= 0) g_sm_count = 148;
+      }
+      const int dist = g_sm_count * 4 * (variant == 11 ? 2 : 1);
+      return cudaLaunchKernelEx(&cfg, csr_flat_kernel<E, false, 4, true>, m, x, ea, dist);
+    }
+    return cudaLaunchKernelEx(&cfg, csr_flat_kernel<E, true, 4>, m, x, ea, 0);
   }
   if (g_sm_count == 0) {
     int dev = 0;
