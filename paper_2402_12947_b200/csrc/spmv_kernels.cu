@@ -108,7 +108,7 @@ constexpr int kRpCap = kRowsPerTile + 4;     // int64 (rows r0..r1 inclusive + a
 constexpr int kSlotBytes = kValCap * 8 + kColCap * 4 + kRpCap * 8;
 static_assert(kSlotBytes % 16 == 0, "slot must keep 16-byte alignment");
 constexpr int kSmemBytes = kStages * kSlotBytes + kTileNnz * 8;
-constexpr int kDefaultVariant = 3;
+constexpr int kDefaultVariant = 10;
 constexpr int kFlatMinBlocks = 6;   // <= 40 registers: 6 CTAs (48 warps) per SM
 
 template <Epi E>
@@ -288,7 +288,7 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes)
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-template <Epi E, bool kTma, int kMinB, bool kPf = false>
+template <Epi E, bool kTma, int kMinB, bool kPf = false, bool kPfVec = false>
 __global__ void __launch_bounds__(kThreads, kMinB)
 csr_flat_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, int pf_dist = 0)
 {
@@ -354,6 +354,27 @@ csr_flat_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, 
   // ---- vectors produced by earlier kernels: after the dependency wait
   pdl_wait();
   pdl_trigger();
+  if constexpr (kPfVec) {
+    // the same future tile's per-row epilogue vectors (contiguous rows)
+    if (tid == 0) {
+      const int tp = t + pf_dist;
+      if (tp < m.ntiles) {
+        const int32_t ra = m.tile_row[tp] & ~1, rb = m.tile_row[tp + 1] & ~1;
+        if (rb > ra) {
+          const uint32_t nb = (uint32_t)(rb - ra) * 8;
+          auto pf = [&](const double* v) {
+            if ((reinterpret_cast<uintptr_t>(v) & 15) == 0) prefetch_l2(v + ra, nb);
+          };
+          if constexpr (T::kB) pf(ea.b);
+          if constexpr (T::kU) pf(ea.u_in);
+          if constexpr (T::kD) pf(ea.d);
+          if constexpr (T::kOut) pf(ea.out);
+          if constexpr (T::kDiag) pf(m.inv_diag);
+          if constexpr (T::kDiagVec) pf(ea.inv_diag);
+        }
+      }
+    }
+  }
   double bv = 0.0, uv = 0.0, dv = 0.0, ov = 0.0;
   double sum = 0.0;
   double dg = 0.0;
@@ -703,7 +724,7 @@ static cudaError_t launch_t(const DevCsr& m, const double* x, const EpiArgs& ea,
     if (variant == 1) return cudaLaunchKernelEx(&cfg, csr_flat_kernel<E, false, 6>, m, x, ea, 0);
     if (variant == 3) return cudaLaunchKernelEx(&cfg, csr_flat_kernel<E, false, 4>, m, x, ea, 0);
     if (variant == 4) return cudaLaunchKernelEx(&cfg, csr_flat_kernel<E, false, 8>, m, x, ea, 0);
-    if (variant == 10 || variant == 11) {
+    if (variant == 10 || variant == 11 || variant == 12) {
       if (g_sm_count == 0) {
         int dev = 0;
         cudaGetDevice(&dev);
@@ -711,6 +732,8 @@ static cudaError_t launch_t(const DevCsr& m, const double* x, const EpiArgs& ea,
         if (g_sm_count <= 0) g_sm_count = 148;
       }
       const int dist = g_sm_count * 4 * (variant == 11 ? 2 : 1);
+      if (variant == 12)
+        return cudaLaunchKernelEx(&cfg, csr_flat_kernel<E, false, 4, true, true>, m, x, ea, dist);
       return cudaLaunchKernelEx(&cfg, csr_flat_kernel<E, false, 4, true>, m, x, ea, dist);
     }
     return cudaLaunchKernelEx(&cfg, csr_flat_kernel<E, true, 4>, m, x, ea, 0);

@@ -1,9 +1,7 @@
 #!/bin/bash
 mkdir -p gpurun_out
-SMG_SPMV_VARIANT=5 timeout 900 python -m pytest tests -x -q -m gpu -k "sparse or sweep or vcycle or iteration or fusion or edge" > gpurun_out/pytest_v5.log 2>&1
-echo "v5 pytest rc=$?" >> gpurun_out/rc.txt
-SMG_SPMV_VARIANT=10 timeout 900 python -m pytest tests -x -q -m gpu -k "sparse or sweep or vcycle" > gpurun_out/pytest_v10.log 2>&1
-echo "v10 pytest rc=$?" >> gpurun_out/rc.txt
-for v in 3 10 11 5; do
+SMG_SPMV_VARIANT=12 timeout 900 python -m pytest tests -x -q -m gpu -k "sparse or sweep or vcycle" > gpurun_out/pytest_v12.log 2>&1
+echo "v12 pytest rc=$?" >> gpurun_out/rc.txt
+for v in 10 12; do
   SMG_SPMV_VARIANT=$v timeout 600 python bench.py --steps 1000 --warmup 10 --no-cpu-baseline > gpurun_out/bench_ab_v$v.json 2> gpurun_out/bench_ab_v$v.err
 done
