@@ -43,6 +43,17 @@ METRIC = "V-cycles/sec & smoother sweeps/sec (fp64) at 1 B200; SpMV HBM GB/s vs 
 UNIT = "V-cycles/s"
 
 
+def _ncu_traffic():
+    """dram read+write bytes per launch of the dominant kernel from the committed
+    ncu --set full capture (profiles/ncu_dominant_kernel.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_dominant_kernel.json")) as f:
+            j = json.load(f)
+        return int(j["dram_read_bytes"]) + int(j["dram_write_bytes"]), j.get("source")
+    except Exception:
+        return None, None
+
+
 def _peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -500,6 +511,7 @@ def main():
                "sample": f"{n_done} oracle V-cycles of {args.workload} in {el:.1f} s "
                          f"(sparse rows on {cores} OpenMP threads, numpy elementwise 1 thread)"}
 
+    traffic, traffic_src = _ncu_traffic()
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
@@ -508,8 +520,9 @@ def main():
             "data": "synthetic (seeded BASELINE C2 construction; random-N(0,1) RHS)",
             "config": _config(wl, h),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
-                         "kernel": "csr_stream_kernel<ChebNext> on the fine level",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "traffic_source": traffic_src,
+                         "kernel": "csr_flat_kernel<ChebNext> (fine-level Chebyshev step)",
                          "bytes_per_launch": bytes_per, "us_per_launch": 1e3 * k_ms,
                          "peak_source": peak_src, "nnz": z, "rows": nn,
                          "nnz_per_row": z / nn},
