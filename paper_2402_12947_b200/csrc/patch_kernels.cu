@@ -80,7 +80,10 @@ enum PatchMode : int { kAddResidualSolve = 0, kSolveFromBuf = 1, kResidualOnly =
 // shared-memory carve-up for a region of at most nmax dofs
 struct PatchSmem {
   int64_t x_off, lo_off, off_off, prod_off, l_off, tri_cap, bytes;
+  int64_t stage;   // > 0: streaming ring of 2 stages of `stage` doubles at l_off
 };
+
+constexpr int kChunkRows = 8;   // factor rows per streamed chunk (divides the 32-row panel)
 
 __host__ __device__ inline PatchSmem patch_smem_layout(int nmax)
 {
@@ -93,11 +96,17 @@ __host__ __device__ inline PatchSmem patch_smem_layout(int nmax)
   p.l_off = p.prod_off + 8 * kProdCap;
   int64_t cap = (kSmemBudget - p.l_off) / 8;
   if (cap < 0) cap = 0;
-  p.tri_cap = cap;
-  const int64_t need = patch_slot_doubles(nmax);
   cap &= ~int64_t(1);
-  p.tri_cap = cap;
-  p.bytes = p.l_off + 8 * (need < cap ? need : cap);
+  const int64_t need = patch_slot_doubles(nmax);
+  p.stage = 0;
+  if (need <= cap) {  // every region's slot (factor + inverted blocks) fits: stage it whole
+    p.tri_cap = need;
+    p.bytes = p.l_off + 8 * need;
+  } else {            // stream factor rows through a 2-stage ring (smaller regions still staged)
+    p.stage = ((int64_t)kChunkRows * (nmax + 2) + 1) & ~int64_t(1);
+    p.tri_cap = 2 * p.stage;
+    p.bytes = p.l_off + 8 * p.tri_cap;
+  }
   return p;
 }
 
@@ -135,6 +144,157 @@ __device__ int block_scan(const int32_t* len, int32_t* off, int n, int* s_carry)
   return total;
 }
 
+
+// ---------------------------------------------------------------------------
+// Streaming triangular solves for regions whose factor does not fit in shared
+// memory (C5: 64..512-dof patches).  Row chunks of kChunkRows factor rows --
+// contiguous in the packed row-major layout -- flow HBM -> smem through a
+// 2-stage bulk-copy ring.  Forward: left-looking (chunk rows against the
+// solved prefix), then the panel's inverted diagonal block.  Backward:
+// right-looking from the last panel (inverted block first, then the panel's
+// rows update the unsolved prefix), so both passes stream the same row chunks.
+struct ChunkInfo {
+  int i0, rows, panel;
+};
+
+__device__ __forceinline__ ChunkInfo chunk_of(int seq, int n)
+{
+  const int nb = (n + kPanel - 1) / kPanel;
+  const int cpp = kPanel / kChunkRows;
+  const int pn_last = n - (nb - 1) * kPanel;
+  const int k_last = (pn_last + kChunkRows - 1) / kChunkRows;
+  const int C = (nb - 1) * cpp + k_last;
+  int panel, j;
+  if (seq < C) {  // forward: ascending
+    panel = seq / cpp;
+    if (panel > nb - 1) panel = nb - 1;
+    j = seq - panel * cpp;
+  } else {        // backward: panels descending
+    const int t = seq - C;
+    if (t < k_last) {
+      panel = nb - 1;
+      j = t;
+    } else {
+      const int t2 = t - k_last;
+      panel = nb - 2 - t2 / cpp;
+      j = t2 % cpp;
+    }
+  }
+  ChunkInfo c;
+  c.panel = panel;
+  c.i0 = panel * kPanel + j * kChunkRows;
+  c.rows = min(kChunkRows, n - c.i0);
+  return c;
+}
+
+__device__ __forceinline__ int n_chunks(int n)
+{
+  const int nb = (n + kPanel - 1) / kPanel;
+  const int pn_last = n - (nb - 1) * kPanel;
+  return (nb - 1) * (kPanel / kChunkRows) + (pn_last + kChunkRows - 1) / kChunkRows;
+}
+
+__device__ __forceinline__ void ring_issue(const double* Lg, double* ring, int64_t stage, int n,
+                                           int seq, uint64_t* bars)
+{
+  const ChunkInfo c = chunk_of(seq, n);
+  const int64_t a = tri(c.i0) & ~int64_t(1);
+  const int64_t b = (tri(c.i0 + c.rows) + 1) & ~int64_t(1);
+  const int s = seq & 1;
+  uint64_t* bar = &bars[s];
+  const uint32_t bytes = (uint32_t)((b - a) * 8);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(psmem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(psmem_u32(ring + s * stage)),
+      "l"(Lg + a), "r"(bytes), "r"(psmem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void ring_wait(uint64_t* bar, uint32_t parity)
+{
+  asm volatile(
+      "{\n.reg .pred p;\nRW_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra RW_%=;\n}\n" ::"r"(psmem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_t stage, int n,
+                             double* s_x, double (*s_red)[32], uint64_t* bars)
+{
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const double* Dinv = Lg + patch_tri_even(n);
+  const int C = n_chunks(n);
+  const int total = 2 * C;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(psmem_u32(&bars[s])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int q = 0; q < 2 && q < total; ++q) ring_issue(Lg, ring, stage, n, q, bars);
+  }
+  __syncthreads();
+  for (int seq = 0; seq < total; ++seq) {
+    const ChunkInfo c = chunk_of(seq, n);
+    const int p0 = c.panel * kPanel;
+    const int pn = min(kPanel, n - p0);
+    const bool fwd = seq < C;
+    if (!fwd && c.i0 == p0) {
+      // backward: the panel's own block first, x_P = inv(L_PP)^T y_P
+      if (warp == 0) {
+        const double* D = Dinv + c.panel * kDinvBlock;
+        double acc = 0.0;
+        if (lane < pn)
+          for (int j = 0; j < pn; ++j) acc += D[j * kDinvLd + lane] * s_x[p0 + j];
+        __syncwarp();
+        if (lane < pn) s_x[p0 + lane] = acc;
+      }
+      __syncthreads();
+    }
+    ring_wait(&bars[seq & 1], (uint32_t)((seq >> 1) & 1));
+    const double* rows = ring + (seq & 1) * stage + (tri(c.i0) & 1) - tri(c.i0);  // rows[tri(i)+j]
+    if (fwd) {
+      // x_i -= L[i, 0:p0] . x[0:p0] for the chunk's rows (one warp per row)
+      if (warp < c.rows && p0 > 0) {
+        const int i = c.i0 + warp;
+        const double* Li = rows + tri(i);
+        double acc = 0.0;
+        for (int j = lane; j < p0; j += 32) acc += Li[j] * s_x[j];
+        acc = warp_sum(acc);
+        if (lane == 0) s_x[i] -= acc;
+      }
+    } else if (p0 > 0) {
+      // y[c] -= sum_{i in chunk} L[i][c] x_i  for c < p0 (thread per column)
+      for (int col = threadIdx.x; col < p0; col += kSolveThreads) {
+        double acc = 0.0;
+        for (int r = 0; r < c.rows; ++r) acc += rows[tri(c.i0 + r) + col] * s_x[c.i0 + r];
+        s_x[col] -= acc;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && seq + 2 < total) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      ring_issue(Lg, ring, stage, n, seq + 2, bars);
+    }
+    if (fwd && c.i0 + c.rows == p0 + pn) {
+      // forward: panel complete, x_P = inv(L_PP) r_P
+      if (warp == 0) {
+        const double* D = Dinv + c.panel * kDinvBlock;
+        double acc = 0.0;
+        if (lane < pn)
+          for (int j = 0; j < pn; ++j) acc += D[lane * kDinvLd + j] * s_x[p0 + j];
+        __syncwarp();
+        if (lane < pn) s_x[p0 + lane] = acc;
+      }
+      __syncthreads();
+    }
+  }
+}
+
 template <int kMode>
 __global__ void __launch_bounds__(kSolveThreads)
 patch_kernel(const DevCsr a, const int32_t* __restrict__ pptr, const int32_t* __restrict__ dofs,
@@ -146,6 +306,7 @@ patch_kernel(const DevCsr a, const int32_t* __restrict__ pptr, const int32_t* __
   __shared__ double s_red[kSolveWarps][32];
   __shared__ int s_carry;
   __shared__ uint64_t s_bar;
+  __shared__ uint64_t s_ring_bar[2];
   const PatchSmem L_ = patch_smem_layout(nmax);
   double* s_x = reinterpret_cast<double*>(psm + L_.x_off);
   int64_t* s_lo = reinterpret_cast<int64_t*>(psm + L_.lo_off);
@@ -235,6 +396,10 @@ patch_kernel(const DevCsr a, const int32_t* __restrict__ pptr, const int32_t* __
   const double* L = staged ? s_L : Lg;
   const double* Dinv = L + patch_tri_even(n);   // inverted diagonal blocks, row stride 33
 
+  if (!staged && L_.stage > 0) {
+    stream_solve(Lg, s_L, L_.stage, n, s_x, s_red, s_ring_bar);
+  } else {
+
   // ---- forward: L y = r (left-looking over 32-row panels)
   for (int p0 = 0; p0 < n; p0 += 32) {
     const int pn = min(32, n - p0);
@@ -293,6 +458,8 @@ patch_kernel(const DevCsr a, const int32_t* __restrict__ pptr, const int32_t* __
     }
     __syncthreads();
   }
+
+  }  // generic (staged / global) path
 
   for (int i = threadIdx.x; i < n; i += kSolveThreads) {
     const int32_t g = dofs[k0 + i];
