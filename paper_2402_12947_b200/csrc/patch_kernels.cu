@@ -28,6 +28,8 @@
 // bitwise: LAPACK's blocked order is not reproducible.
 #include "smg_internal.cuh"
 
+#include <cstdlib>
+
 namespace smg {
 
 __device__ __forceinline__ uint32_t psmem_u32(const void* p)
@@ -496,6 +498,16 @@ cudaError_t launch_patch_residual(const DevCsr& a, const Correction& c, const do
   return cudaGetLastError();
 }
 
+static size_t smem_pad()
+{
+  static long pad = -1;
+  if (pad < 0) {
+    const char* v = getenv("SMG_PATCH_SMEM_PAD");
+    pad = v ? atol(v) : 0;
+  }
+  return (size_t)pad;
+}
+
 // u_add != nullptr -> u += x ; else out_scatter[dofs] = x.  fused: residual in-kernel.
 cudaError_t launch_patch_solve(const Correction& c, const double* b, const double* u_res,
                                double* u_add, double* out_scatter, bool fused, cudaStream_t s)
@@ -504,11 +516,12 @@ cudaError_t launch_patch_solve(const Correction& c, const double* b, const doubl
   const PatchSmem L = patch_smem_layout(c.max_dofs);
   double* tgt = u_add ? u_add : out_scatter;
   const int add = u_add ? 1 : 0;
+  const size_t smem = (size_t)L.bytes + smem_pad();
   if (fused)
-    patch_kernel<kAddResidualSolve><<<c.n_regions, kSolveThreads, (size_t)L.bytes, s>>>(
+    patch_kernel<kAddResidualSolve><<<c.n_regions, kSolveThreads, smem, s>>>(
         c.op->a, c.pptr, c.dofs, c.foff, c.lfac, b, u_res, c.rbuf, tgt, add, c.max_dofs);
   else
-    patch_kernel<kSolveFromBuf><<<c.n_regions, kSolveThreads, (size_t)L.bytes, s>>>(
+    patch_kernel<kSolveFromBuf><<<c.n_regions, kSolveThreads, smem, s>>>(
         c.op->a, c.pptr, c.dofs, c.foff, c.lfac, b, u_res, c.rbuf, tgt, add, c.max_dofs);
   return cudaGetLastError();
 }
@@ -516,11 +529,12 @@ cudaError_t launch_patch_solve(const Correction& c, const double* b, const doubl
 cudaError_t configure_patch_solve_smem(const Correction& c)
 {
   const PatchSmem L = patch_smem_layout(c.max_dofs);
+  const int bytes = (int)(L.bytes + smem_pad());
   cudaError_t e = cudaFuncSetAttribute(patch_kernel<kAddResidualSolve>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(patch_kernel<kSolveFromBuf>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(patch_kernel<kResidualOnly>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.l_off);
