@@ -232,7 +232,8 @@ def make_c5_patches(n_rows: int, count: int = 1000, seed: int = 2402):
         idx = np.sort(perm[start:start + nd])
         start += nd
         q, _ = torch.linalg.qr(torch.randn(nd, nd, dtype=torch.float64, device="cuda", generator=g))
-        lam = torch.logspace(0, -6, int(nd), dtype=torch.float64, device="cuda")
+        lam = torch.logspace(0, -float(os.environ.get("SMG_C5_COND_DECADES", "6")), int(nd),
+                             dtype=torch.float64, device="cuda")
         blk = (q * lam) @ q.T
         blk = 0.5 * (blk + blk.T)
         c = torch.linalg.cholesky(blk).cpu().numpy()

@@ -79,6 +79,12 @@ constexpr int64_t kSmemBudget = 220 * 1024;    // dynamic smem per CTA (of 227 K
 
 enum PatchMode : int { kAddResidualSolve = 0, kSolveFromBuf = 1, kResidualOnly = 2 };
 
+static bool nostream_env()
+{
+  const char* v = getenv("SMG_PATCH_NOSTREAM");
+  return v && v[0] == '1';
+}
+
 // shared-memory carve-up for a region of at most nmax dofs
 struct PatchSmem {
   int64_t x_off, lo_off, off_off, prod_off, l_off, tri_cap, bytes;
@@ -87,7 +93,7 @@ struct PatchSmem {
 
 constexpr int kChunkRows = 8;   // factor rows per streamed chunk (divides the 32-row panel)
 
-__host__ __device__ inline PatchSmem patch_smem_layout(int nmax)
+__host__ __device__ inline PatchSmem patch_smem_layout(int nmax, bool allow_stream = true)
 {
   PatchSmem p;
   const int64_t n2 = (nmax + 2) & ~int64_t(1);
@@ -101,7 +107,7 @@ __host__ __device__ inline PatchSmem patch_smem_layout(int nmax)
   cap &= ~int64_t(1);
   const int64_t need = patch_slot_doubles(nmax);
   p.stage = 0;
-  if (need <= cap) {  // every region's slot (factor + inverted blocks) fits: stage it whole
+  if (need <= cap || !allow_stream) {  // every region's slot (factor + inverted blocks) fits: stage it whole
     p.tri_cap = need;
     p.bytes = p.l_off + 8 * need;
   } else {            // stream factor rows through a 2-stage ring (smaller regions still staged)
@@ -302,14 +308,14 @@ __global__ void __launch_bounds__(kSolveThreads)
 patch_kernel(const DevCsr a, const int32_t* __restrict__ pptr, const int32_t* __restrict__ dofs,
              const int64_t* __restrict__ foff, const double* __restrict__ lfac,
              const double* __restrict__ b, const double* u_res, double* rbuf, double* target,
-             int scatter_add, int nmax)
+             int scatter_add, int nmax, int allow_stream)
 {
   extern __shared__ __align__(16) unsigned char psm[];
   __shared__ double s_red[kSolveWarps][32];
   __shared__ int s_carry;
   __shared__ uint64_t s_bar;
   __shared__ uint64_t s_ring_bar[2];
-  const PatchSmem L_ = patch_smem_layout(nmax);
+  const PatchSmem L_ = patch_smem_layout(nmax, allow_stream != 0);
   double* s_x = reinterpret_cast<double*>(psm + L_.x_off);
   int64_t* s_lo = reinterpret_cast<int64_t*>(psm + L_.lo_off);
   int32_t* s_off = reinterpret_cast<int32_t*>(psm + L_.off_off);
@@ -328,6 +334,8 @@ patch_kernel(const DevCsr a, const int32_t* __restrict__ pptr, const int32_t* __
   // bulk copy stages the whole factor while the residual is formed
   if (staged && threadIdx.x == 0)
     factor_bulk_load(s_L, Lg, (uint32_t)(nslot * 8), &s_bar);
+  // every thread may only wait on the barrier after thread 0 has initialised it
+  __syncthreads();
 
   if (kMode != kSolveFromBuf) {
     // ---- residual rows: bounds, scan, streamed products, ordered sums
@@ -494,7 +502,7 @@ cudaError_t launch_patch_residual(const DevCsr& a, const Correction& c, const do
   if (c.n_regions == 0) return cudaSuccess;
   const PatchSmem L = patch_smem_layout(c.max_dofs);
   patch_kernel<kResidualOnly><<<c.n_regions, kSolveThreads, (size_t)L.l_off, s>>>(
-      a, c.pptr, c.dofs, c.foff, c.lfac, b, u, c.rbuf, nullptr, 0, c.max_dofs);
+      a, c.pptr, c.dofs, c.foff, c.lfac, b, u, c.rbuf, nullptr, 0, c.max_dofs, 1);
   return cudaGetLastError();
 }
 
@@ -513,22 +521,23 @@ cudaError_t launch_patch_solve(const Correction& c, const double* b, const doubl
                                double* u_add, double* out_scatter, bool fused, cudaStream_t s)
 {
   if (c.n_regions == 0) return cudaSuccess;
-  const PatchSmem L = patch_smem_layout(c.max_dofs);
+  const int st = nostream_env() ? 0 : 1;
+  const PatchSmem L = patch_smem_layout(c.max_dofs, st != 0);
   double* tgt = u_add ? u_add : out_scatter;
   const int add = u_add ? 1 : 0;
   const size_t smem = (size_t)L.bytes + smem_pad();
   if (fused)
     patch_kernel<kAddResidualSolve><<<c.n_regions, kSolveThreads, smem, s>>>(
-        c.op->a, c.pptr, c.dofs, c.foff, c.lfac, b, u_res, c.rbuf, tgt, add, c.max_dofs);
+        c.op->a, c.pptr, c.dofs, c.foff, c.lfac, b, u_res, c.rbuf, tgt, add, c.max_dofs, st);
   else
     patch_kernel<kSolveFromBuf><<<c.n_regions, kSolveThreads, smem, s>>>(
-        c.op->a, c.pptr, c.dofs, c.foff, c.lfac, b, u_res, c.rbuf, tgt, add, c.max_dofs);
+        c.op->a, c.pptr, c.dofs, c.foff, c.lfac, b, u_res, c.rbuf, tgt, add, c.max_dofs, st);
   return cudaGetLastError();
 }
 
 cudaError_t configure_patch_solve_smem(const Correction& c)
 {
-  const PatchSmem L = patch_smem_layout(c.max_dofs);
+  const PatchSmem L = patch_smem_layout(c.max_dofs, !nostream_env());
   const int bytes = (int)(L.bytes + smem_pad());
   cudaError_t e = cudaFuncSetAttribute(patch_kernel<kAddResidualSolve>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);

@@ -16,7 +16,13 @@ perm = rng.permutation(n)
 regs, st = [], 0
 for nd in sizes:
     idx = np.sort(perm[st:st + nd]); st += nd
-    m = rng.standard_normal((nd, nd)); a = m @ m.T + nd * np.eye(nd)
+    dec = float(os.environ.get("COND_DECADES", "0"))
+    if dec > 0:
+        q, _ = np.linalg.qr(rng.standard_normal((nd, nd)))
+        a = (q * np.logspace(0, -dec, nd)) @ q.T
+        a = 0.5 * (a + a.T)
+    else:
+        m = rng.standard_normal((nd, nd)); a = m @ m.T + nd * np.eye(nd)
     c = sl.cholesky(a, lower=True)
     regs.append((idx, DenseFactor("cholesky", (c, True), nd)))
 lc = LocalCorrection(tuple(regs), n)
