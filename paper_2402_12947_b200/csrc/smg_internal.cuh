@@ -21,8 +21,6 @@ constexpr int kThreads = 256;        // one row per thread at most
 constexpr int kRowsPerTile = kThreads;
 constexpr int kTileNnz = 2048;       // products staged per pass (16 KB smem)
 constexpr int kItems = kTileNnz / kThreads;
-constexpr int kStages = 3;           // TMA ring depth (tiles in flight per CTA)
-constexpr int kCtasPerSm = 2;        // persistent grid: 2 CTAs per SM
 
 struct DevCsr {
   int64_t nrows = 0, ncols = 0, nnz = 0;

@@ -44,8 +44,8 @@ def test_sass_is_sm100a_and_parity_kernels_have_no_fma():
             funcs[current].append(line)
     # Epi 0 = spmv, 1 = residual, 5 = add-to (prolong): pure multiply/add
     for epi in ("0", "1", "5"):
-        name = [f for f in funcs if f.startswith(f"_ZN3smg17csr_stream_kernelILNS_3EpiE{epi}E")]
-        assert name, f"csr_stream_kernel<{epi}> missing"
+        name = [f for f in funcs if f.startswith(f"_ZN3smg15csr_tile_kernelILNS_3EpiE{epi}E")]
+        assert name, f"csr_tile_kernel<{epi}> missing"
         body = "\n".join(funcs[name[0]])
-        assert "DFMA" not in body, f"csr_stream_kernel<{epi}> contains DFMA"
+        assert "DFMA" not in body, f"csr_tile_kernel<{epi}> contains DFMA"
         assert "DMUL" in body and "DADD" in body
