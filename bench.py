@@ -206,7 +206,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
         "steps": steps, "warmup": warm, "ms_per_step": 1e3 * el / steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded BASELINE C2 construction)",
+        "data": f"synthetic (seeded BASELINE {args.workload} construction)",
         "config": _config(wl, h),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": O.num_threads(), "kind": "port",
                          "sample": sample},
@@ -347,11 +347,14 @@ def run_c5(args):
     return 0
 
 
+def configs_mod():
+    from paper_2402_12947_b200 import configs
+    return configs
+
+
 def _config(wl, h):
     return {
-        "workload": f"{wl.name}: BASELINE configs[1] (2D Poisson P2, 513x513 vertex grid, "
-                    "jitter 0.2h, 20 collapsed-node clusters, 2-layer patches, Chebyshev "
-                    "degree 3, random N(0,1) RHS, 5-level non-nested Galerkin hierarchy)",
+        "workload": f"{wl.name}: " + configs_mod().DESCRIPTIONS.get(wl.name.split("-")[0], ""),
         "levels_dofs": [lv.a.nrows for lv in h.levels],
         "levels_nnz": [lv.a.nnz for lv in h.levels],
         "patches": [0 if lv.local_correction is None else len(lv.local_correction.regions)
@@ -518,7 +521,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded BASELINE C2 construction; random-N(0,1) RHS)",
+            "data": f"synthetic (seeded BASELINE {args.workload} construction)",
             "config": _config(wl, h),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,

@@ -77,6 +77,19 @@ C4 = Workload("C4-3d-p2-cheb2", 3, 2, (96, 48, 24, 12), 0.15, "flatten", 50, 1, 
               "random", 1)
 WORKLOADS = {"C1": C1, "C2": C2, "C3": C3, "C4": C4}
 
+DESCRIPTIONS = {
+    "C1": "BASELINE configs[0] (2D Poisson P1, 129x129 vertex grid, jitter 0.2h, one cluster of "
+          "3 nodes moved within 1e-3h of a neighbour, f=1, damped Jacobi omega=2/3 x2, "
+          "4-level non-nested Galerkin hierarchy)",
+    "C2": "BASELINE configs[1] (2D Poisson P2, 513x513 vertex grid, jitter 0.2h, 20 "
+          "collapsed-node clusters, 2-layer patches, Chebyshev degree 3, random N(0,1) RHS, "
+          "5-level non-nested Galerkin hierarchy)",
+    "C3": "BASELINE configs[2] (3D Poisson P1, 65^3 vertex grid, jitter 0.15h, 8 flattened "
+          "tets, damped Jacobi omega=2/3 x2, 4-level non-nested Galerkin hierarchy)",
+    "C4": "BASELINE configs[3] (3D Poisson P2, 97^3 vertex grid (7.2M DOFs), jitter 0.15h, 50 "
+          "flattened-tet patches, Chebyshev degree 2, random N(0,1) RHS, 4 levels)",
+}
+
 
 def _interior_mask(mesh: SimplexMesh) -> np.ndarray:
     return ~mesh.boundary_vertex_mask()

@@ -27,8 +27,8 @@ import numpy as np
 
 from . import _lib
 from . import device as _dev
-from .sparse import (CsrMatrix, DenseFactor, NotPositiveDefiniteError, dense_factor,
-                     estimate_lambda_max)
+from .sparse import (DEVICE_LANCZOS_MIN_ROWS, CsrMatrix, DenseFactor, NotPositiveDefiniteError,
+                     dense_factor, estimate_lambda_max, estimate_lambda_max_device)
 
 
 class ZeroDiagonalError(ValueError):
@@ -233,6 +233,8 @@ def jacobi_lambda_max(a, tol: float = 1e-8) -> float:
     if len(zero):
         raise ZeroDiagonalError(int(zero[0]))
     scale = 1.0 / np.sqrt(np.abs(diag))
+    if a.nrows >= DEVICE_LANCZOS_MIN_ROWS and _dev.torch().cuda.is_available():
+        return estimate_lambda_max_device(a, scale, tol)
     s = a.to_scipy()
     return estimate_lambda_max(lambda x: scale * (s @ (scale * x)), a.nrows, tol)
 
