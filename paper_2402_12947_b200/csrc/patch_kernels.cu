@@ -91,7 +91,8 @@ struct PatchSmem {
   int64_t stage;   // > 0: streaming ring of 2 stages of `stage` doubles at l_off
 };
 
-constexpr int kChunkRows = 8;   // factor rows per streamed chunk (divides the 32-row panel)
+constexpr int kChunkRows = 4;   // factor rows per streamed chunk (divides the 32-row panel)
+constexpr int kRingStages = 4;  // chunks in flight per CTA
 
 __host__ __device__ inline PatchSmem patch_smem_layout(int nmax, bool allow_stream = true)
 {
@@ -112,7 +113,7 @@ __host__ __device__ inline PatchSmem patch_smem_layout(int nmax, bool allow_stre
     p.bytes = p.l_off + 8 * need;
   } else {            // stream factor rows through a 2-stage ring (smaller regions still staged)
     p.stage = ((int64_t)kChunkRows * (nmax + 2) + 1) & ~int64_t(1);
-    p.tri_cap = 2 * p.stage;
+    p.tri_cap = kRingStages * p.stage;
     p.bytes = p.l_off + 8 * p.tri_cap;
   }
   return p;
@@ -157,7 +158,7 @@ __device__ int block_scan(const int32_t* len, int32_t* off, int n, int* s_carry)
 // Streaming triangular solves for regions whose factor does not fit in shared
 // memory (C5: 64..512-dof patches).  Row chunks of kChunkRows factor rows --
 // contiguous in the packed row-major layout -- flow HBM -> smem through a
-// 2-stage bulk-copy ring.  Forward: left-looking (chunk rows against the
+// kRingStages-deep bulk-copy ring.  Forward: left-looking (chunk rows against the
 // solved prefix), then the panel's inverted diagonal block.  Backward:
 // right-looking from the last panel (inverted block first, then the panel's
 // rows update the unsolved prefix), so both passes stream the same row chunks.
@@ -208,7 +209,7 @@ __device__ __forceinline__ void ring_issue(const double* Lg, double* ring, int64
   const ChunkInfo c = chunk_of(seq, n);
   const int64_t a = tri(c.i0) & ~int64_t(1);
   const int64_t b = (tri(c.i0 + c.rows) + 1) & ~int64_t(1);
-  const int s = seq & 1;
+  const int s = seq % kRingStages;
   uint64_t* bar = &bars[s];
   const uint32_t bytes = (uint32_t)((b - a) * 8);
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(psmem_u32(bar)),
@@ -240,10 +241,10 @@ __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_
   const int C = n_chunks(n);
   const int total = 2 * C;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s)
+    for (int s = 0; s < kRingStages; ++s)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(psmem_u32(&bars[s])) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int q = 0; q < 2 && q < total; ++q) ring_issue(Lg, ring, stage, n, q, bars);
+    for (int q = 0; q < kRingStages && q < total; ++q) ring_issue(Lg, ring, stage, n, q, bars);
   }
   __syncthreads();
   for (int seq = 0; seq < total; ++seq) {
@@ -263,8 +264,8 @@ __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_
       }
       __syncthreads();
     }
-    ring_wait(&bars[seq & 1], (uint32_t)((seq >> 1) & 1));
-    const double* rows = ring + (seq & 1) * stage + (tri(c.i0) & 1) - tri(c.i0);  // rows[tri(i)+j]
+    ring_wait(&bars[seq % kRingStages], (uint32_t)((seq / kRingStages) & 1));
+    const double* rows = ring + (seq % kRingStages) * stage + (tri(c.i0) & 1) - tri(c.i0);
     if (fwd) {
       // x_i -= L[i, 0:p0] . x[0:p0] for the chunk's rows (one warp per row)
       if (warp < c.rows && p0 > 0) {
@@ -284,9 +285,9 @@ __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_
       }
     }
     __syncthreads();
-    if (threadIdx.x == 0 && seq + 2 < total) {
+    if (threadIdx.x == 0 && seq + kRingStages < total) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      ring_issue(Lg, ring, stage, n, seq + 2, bars);
+      ring_issue(Lg, ring, stage, n, seq + kRingStages, bars);
     }
     if (fwd && c.i0 + c.rows == p0 + pn) {
       // forward: panel complete, x_P = inv(L_PP) r_P
@@ -314,7 +315,7 @@ patch_kernel(const DevCsr a, const int32_t* __restrict__ pptr, const int32_t* __
   __shared__ double s_red[kSolveWarps][32];
   __shared__ int s_carry;
   __shared__ uint64_t s_bar;
-  __shared__ uint64_t s_ring_bar[2];
+  __shared__ uint64_t s_ring_bar[kRingStages];
   const PatchSmem L_ = patch_smem_layout(nmax, allow_stream != 0);
   double* s_x = reinterpret_cast<double*>(psm + L_.x_off);
   int64_t* s_lo = reinterpret_cast<int64_t*>(psm + L_.lo_off);
