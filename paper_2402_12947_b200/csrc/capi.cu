@@ -95,6 +95,12 @@ static std::vector<int32_t> make_tiles(int64_t nrows, const int64_t* rowptr)
   return t;
 }
 
+static bool stream_env()
+{
+  const char* v = getenv("SMG_EVICT_FIRST");
+  return !(v && v[0] == '0');
+}
+
 static int build_devcsr(std::vector<void*>& allocs, int64_t& bytes, int64_t nrows, int64_t ncols,
                         const int64_t* rowptr, const int64_t* col64, const double* val,
                         DevCsr* out)
@@ -115,6 +121,7 @@ static int build_devcsr(std::vector<void*>& allocs, int64_t& bytes, int64_t nrow
   d.ncols = ncols;
   d.nnz = nnz;
   d.ntiles = (int32_t)(tiles.size() - 1);
+  d.streaming = stream_env() && nnz * 12 > kStreamBytes;
   int64_t* rp = nullptr;
   int32_t* c = nullptr;
   double* v = nullptr;

@@ -21,6 +21,7 @@ constexpr int kThreads = 256;        // one row per thread at most
 constexpr int kRowsPerTile = kThreads;
 constexpr int kTileNnz = 2048;       // products staged per pass (16 KB smem)
 constexpr int kItems = kTileNnz / kThreads;
+constexpr int64_t kStreamBytes = 64ll << 20;   // operators above this are streamed evict-first
 
 struct DevCsr {
   int64_t nrows = 0, ncols = 0, nnz = 0;
@@ -31,6 +32,7 @@ struct DevCsr {
   const int64_t* tile_nz = nullptr;  // ntiles + 1 (rowptr at the tile boundaries)
   const double* inv_diag = nullptr;  // 1.0 / a_ii (IEEE, as smoothers.py:115), square ops
   int32_t ntiles = 0;
+  bool streaming = false;            // val+col exceed kStreamBytes: evict-first reads
 };
 
 // Host-side owner of one operator's device arrays.

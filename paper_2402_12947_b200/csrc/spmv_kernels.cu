@@ -26,6 +26,10 @@
 //     division (__ddiv_rn) for /theta; 1/a_ii is a precomputed vector formed
 //     with the same IEEE division numpy uses (smoothers.py:115).
 //
+// L2 residency: operators too large to stay in L2 (DevCsr::streaming, set at
+// upload) are read with evict-first priority, so the coarse levels -- visited
+// twice per V-cycle -- stay L2-resident across the fine-level sweeps.
+//
 // Latency hiding (the kernel is latency-, not instruction-bound):
 //   * operator data (tile bounds, row offsets, values, columns) is requested
 //     before griddepcontrol.wait; kernels are launched with programmatic
@@ -47,9 +51,18 @@ __device__ __forceinline__ void pdl_trigger()
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes)
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes, bool evict_first)
 {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+  if (evict_first) {
+    asm volatile(
+        "{\n.reg .b64 pol;\n"
+        "createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+        "cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, pol;\n}\n" ::"l"(p),
+        "r"(bytes)
+        : "memory");
+  } else {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+  }
 }
 
 template <Epi E>
@@ -128,8 +141,13 @@ csr_tile_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, 
     c[i] = 0;
     v[i] = 0.0;
     if (!longtile && k < cnt) {
-      c[i] = __ldg(m.col + e0 + k);
-      v[i] = __ldg(m.val + e0 + k);
+      if (m.streaming) {  // operator larger than L2 share: don't evict the small levels
+        c[i] = __ldcs(m.col + e0 + k);
+        v[i] = __ldcs(m.val + e0 + k);
+      } else {
+        c[i] = __ldg(m.col + e0 + k);
+        v[i] = __ldg(m.val + e0 + k);
+      }
     }
   }
   if constexpr (kPf) {
@@ -142,8 +160,8 @@ csr_tile_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, 
         if (p1 - p0 <= kTileNnz && p1 > p0) {
           const int64_t va = p0 & ~int64_t(1), vb = (p1 + 1) & ~int64_t(1);
           const int64_t ca = p0 & ~int64_t(3), cb = (p1 + 3) & ~int64_t(3);
-          prefetch_l2(m.val + va, (uint32_t)((vb - va) * 8));
-          prefetch_l2(m.col + ca, (uint32_t)((cb - ca) * 4));
+          prefetch_l2(m.val + va, (uint32_t)((vb - va) * 8), m.streaming);
+          prefetch_l2(m.col + ca, (uint32_t)((cb - ca) * 4), m.streaming);
         }
       }
     }
