@@ -232,8 +232,14 @@ __device__ __forceinline__ void ring_wait(uint64_t* bar, uint32_t parity)
       : "memory");
 }
 
+// cooperative, coalesced copy of one inverted diagonal block into shared memory
+__device__ __forceinline__ void load_dinv(const double* __restrict__ src, double* dst)
+{
+  for (int i = threadIdx.x; i < kDinvBlock; i += kSolveThreads) dst[i] = __ldg(src + i);
+}
+
 __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_t stage, int n,
-                             double* s_x, double (*s_red)[32], uint64_t* bars)
+                             double* s_x, double* s_dinv, uint64_t* bars)
 {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -254,8 +260,10 @@ __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_
     const bool fwd = seq < C;
     if (!fwd && c.i0 == p0) {
       // backward: the panel's own block first, x_P = inv(L_PP)^T y_P
+      load_dinv(Dinv + c.panel * kDinvBlock, s_dinv);
+      __syncthreads();
       if (warp == 0) {
-        const double* D = Dinv + c.panel * kDinvBlock;
+        const double* D = s_dinv;
         double acc = 0.0;
         if (lane < pn)
           for (int j = 0; j < pn; ++j) acc += D[j * kDinvLd + lane] * s_x[p0 + j];
@@ -291,8 +299,10 @@ __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_
     }
     if (fwd && c.i0 + c.rows == p0 + pn) {
       // forward: panel complete, x_P = inv(L_PP) r_P
+      load_dinv(Dinv + c.panel * kDinvBlock, s_dinv);
+      __syncthreads();
       if (warp == 0) {
-        const double* D = Dinv + c.panel * kDinvBlock;
+        const double* D = s_dinv;
         double acc = 0.0;
         if (lane < pn)
           for (int j = 0; j < pn; ++j) acc += D[lane * kDinvLd + j] * s_x[p0 + j];
@@ -408,7 +418,7 @@ patch_kernel(const DevCsr a, const int32_t* __restrict__ pptr, const int32_t* __
   const double* Dinv = L + patch_tri_even(n);   // inverted diagonal blocks, row stride 33
 
   if (!staged && L_.stage > 0) {
-    stream_solve(Lg, s_L, L_.stage, n, s_x, s_red, s_ring_bar);
+    stream_solve(Lg, s_L, L_.stage, n, s_x, s_prod, s_ring_bar);
   } else {
 
   // ---- forward: L y = r (left-looking over 32-row panels)
