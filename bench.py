@@ -464,6 +464,34 @@ def main():
     achieved = bytes_per / (k_ms / 1e3) / 1e9
     sweeps_per_s = 1e3 / k_ms
 
+    # ---- per-level sweep rates (same step kind on every non-coarse level; levels
+    # below the fine one are L2-resident: their GB/s is algorithmic bytes / time)
+    per_level = []
+    for li in range(len(dh.ops) - 1):
+        opl = dh.ops[li]
+        zl, nl = opl.nnz, opl.nrows
+        xa = torch.randn(nl, dtype=torch.float64, device="cuda")
+        xb = torch.empty_like(xa)
+        dl = torch.zeros_like(xa)
+        bl = torch.randn(nl, dtype=torch.float64, device="cuda")
+        bpl = 12 * zl + (44 if steps else 28) * nl
+        for _ in range(5):
+            _lib.check(lib.smg_smoother_step(opl.handle, D.ptr(bl), D.ptr(xa), D.ptr(xb), D.ptr(dl),
+                                             step_kind, theta, c1, c2, sh))
+            xa, xb = xb, xa
+        torch.cuda.synchronize()
+        k0.record(stream)
+        for _ in range(100):
+            _lib.check(lib.smg_smoother_step(opl.handle, D.ptr(bl), D.ptr(xa), D.ptr(xb), D.ptr(dl),
+                                             step_kind, theta, c1, c2, sh))
+            xa, xb = xb, xa
+        k1.record(stream)
+        torch.cuda.synchronize()
+        us = k0.elapsed_time(k1) / 100 * 1e3
+        per_level.append({"level": li, "rows": nl, "nnz": zl, "us": round(us, 2),
+                          "gbs": round(bpl / us / 1e3, 1), "frac": round(bpl / us / 1e3 / _peaks()[0], 3)})
+        del xa, xb, dl, bl
+
     # ---- local-correction share: same hierarchy with the corrections removed,
     # both timed as graph replays (LC share = (T_with - T_without) / T_with)
     lc_share = None
@@ -531,6 +559,7 @@ def main():
                          "peak_source": peak_src, "nnz": z, "rows": nn,
                          "nnz_per_row": z / nn},
             "sweeps_per_s": sweeps_per_s,
+            "per_level_sweep": per_level,
             "lc_share": lc_share,
             "lc_us_per_vcycle": lc_us,
             "e2e": e2e,

@@ -102,7 +102,8 @@ __host__ __device__ inline PatchSmem patch_smem_layout(int nmax, bool allow_stre
   p.lo_off = p.x_off + 8 * n2;                   // int64[n2]
   p.off_off = p.lo_off + 8 * n2;                 // int32[n2 + 2]
   p.prod_off = p.off_off + ((4 * (n2 + 2) + 15) & ~int64_t(15));  // double[kProdCap]
-  p.l_off = p.prod_off + 8 * kProdCap;
+  // the product buffer doubles as the streamed path's inverted-block double buffer
+  p.l_off = p.prod_off + 8 * (kProdCap > 2 * kDinvBlock ? kProdCap : 2 * kDinvBlock);
   int64_t cap = (kSmemBudget - p.l_off) / 8;
   if (cap < 0) cap = 0;
   cap &= ~int64_t(1);
@@ -232,46 +233,75 @@ __device__ __forceinline__ void ring_wait(uint64_t* bar, uint32_t parity)
       : "memory");
 }
 
-// cooperative, coalesced copy of one inverted diagonal block into shared memory
-__device__ __forceinline__ void load_dinv(const double* __restrict__ src, double* dst)
+// Inverted diagonal blocks are consumed in a fixed order -- forward panels
+// 0..nb-1, then backward panels nb-1..0 -- and prefetched two uses ahead into
+// a double buffer by bulk copy (each block is 1056 contiguous doubles).
+__device__ __forceinline__ int dinv_panel(int q, int nb) { return q < nb ? q : 2 * nb - 1 - q; }
+
+__device__ __forceinline__ void dinv_issue(const double* Dinv, double* s_dinv, int q, int nb,
+                                           uint64_t* dbars)
 {
-  for (int i = threadIdx.x; i < kDinvBlock; i += kSolveThreads) dst[i] = __ldg(src + i);
+  const int slot = q & 1;
+  uint64_t* bar = &dbars[slot];
+  const uint32_t bytes = kDinvBlock * 8;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(psmem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(psmem_u32(s_dinv + slot * kDinvBlock)),
+      "l"(Dinv + (int64_t)dinv_panel(q, nb) * kDinvBlock), "r"(bytes), "r"(psmem_u32(bar))
+      : "memory");
 }
 
 __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_t stage, int n,
-                             double* s_x, double* s_dinv, uint64_t* bars)
+                             double* s_x, double* s_dinv, uint64_t* bars, uint64_t* dbars)
 {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const double* Dinv = Lg + patch_tri_even(n);
+  const int nb = (n + kPanel - 1) / kPanel;
   const int C = n_chunks(n);
   const int total = 2 * C;
+  int dq = 0;  // next inverted block to consume
   if (threadIdx.x == 0) {
     for (int s = 0; s < kRingStages; ++s)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(psmem_u32(&bars[s])) : "memory");
+    for (int s = 0; s < 2; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(psmem_u32(&dbars[s])) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int q = 0; q < kRingStages && q < total; ++q) ring_issue(Lg, ring, stage, n, q, bars);
+    for (int q = 0; q < 2 && q < 2 * nb; ++q) dinv_issue(Dinv, s_dinv, q, nb, dbars);
   }
   __syncthreads();
+  // consume block dq: wait, x_P = inv(L_PP) r_P (forward) or inv(L_PP)^T y_P (backward)
+  auto panel_solve = [&](int p0, int pn, bool transposed) {
+    ring_wait(&dbars[dq & 1], (uint32_t)((dq >> 1) & 1));
+    if (warp == 0) {
+      const double* D = s_dinv + (dq & 1) * kDinvBlock;
+      double acc = 0.0;
+      if (lane < pn) {
+        if (transposed)
+          for (int j = 0; j < pn; ++j) acc += D[j * kDinvLd + lane] * s_x[p0 + j];
+        else
+          for (int j = 0; j < pn; ++j) acc += D[lane * kDinvLd + j] * s_x[p0 + j];
+      }
+      __syncwarp();
+      if (lane < pn) s_x[p0 + lane] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && dq + 2 < 2 * nb) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      dinv_issue(Dinv, s_dinv, dq + 2, nb, dbars);
+    }
+    ++dq;
+  };
   for (int seq = 0; seq < total; ++seq) {
     const ChunkInfo c = chunk_of(seq, n);
     const int p0 = c.panel * kPanel;
     const int pn = min(kPanel, n - p0);
     const bool fwd = seq < C;
-    if (!fwd && c.i0 == p0) {
-      // backward: the panel's own block first, x_P = inv(L_PP)^T y_P
-      load_dinv(Dinv + c.panel * kDinvBlock, s_dinv);
-      __syncthreads();
-      if (warp == 0) {
-        const double* D = s_dinv;
-        double acc = 0.0;
-        if (lane < pn)
-          for (int j = 0; j < pn; ++j) acc += D[j * kDinvLd + lane] * s_x[p0 + j];
-        __syncwarp();
-        if (lane < pn) s_x[p0 + lane] = acc;
-      }
-      __syncthreads();
-    }
+    if (!fwd && c.i0 == p0) panel_solve(p0, pn, true);   // backward: own block first
     ring_wait(&bars[seq % kRingStages], (uint32_t)((seq / kRingStages) & 1));
     const double* rows = ring + (seq % kRingStages) * stage + (tri(c.i0) & 1) - tri(c.i0);
     if (fwd) {
@@ -297,20 +327,7 @@ __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       ring_issue(Lg, ring, stage, n, seq + kRingStages, bars);
     }
-    if (fwd && c.i0 + c.rows == p0 + pn) {
-      // forward: panel complete, x_P = inv(L_PP) r_P
-      load_dinv(Dinv + c.panel * kDinvBlock, s_dinv);
-      __syncthreads();
-      if (warp == 0) {
-        const double* D = s_dinv;
-        double acc = 0.0;
-        if (lane < pn)
-          for (int j = 0; j < pn; ++j) acc += D[lane * kDinvLd + j] * s_x[p0 + j];
-        __syncwarp();
-        if (lane < pn) s_x[p0 + lane] = acc;
-      }
-      __syncthreads();
-    }
+    if (fwd && c.i0 + c.rows == p0 + pn) panel_solve(p0, pn, false);  // forward: panel done
   }
 }
 
@@ -326,6 +343,7 @@ patch_kernel(const DevCsr a, const int32_t* __restrict__ pptr, const int32_t* __
   __shared__ int s_carry;
   __shared__ uint64_t s_bar;
   __shared__ uint64_t s_ring_bar[kRingStages];
+  __shared__ uint64_t s_dinv_bar[2];
   const PatchSmem L_ = patch_smem_layout(nmax, allow_stream != 0);
   double* s_x = reinterpret_cast<double*>(psm + L_.x_off);
   int64_t* s_lo = reinterpret_cast<int64_t*>(psm + L_.lo_off);
@@ -418,7 +436,7 @@ patch_kernel(const DevCsr a, const int32_t* __restrict__ pptr, const int32_t* __
   const double* Dinv = L + patch_tri_even(n);   // inverted diagonal blocks, row stride 33
 
   if (!staged && L_.stage > 0) {
-    stream_solve(Lg, s_L, L_.stage, n, s_x, s_prod, s_ring_bar);
+    stream_solve(Lg, s_L, L_.stage, n, s_x, s_prod, s_ring_bar, s_dinv_bar);
   } else {
 
   // ---- forward: L y = r (left-looking over 32-row panels)
