@@ -72,7 +72,13 @@ static void free_all(std::vector<void*>& allocs)
 // get smaller tiles so every SM still has several independent CTAs.
 static int64_t tile_cap_for(int64_t nnz)
 {
-  const int64_t want = nnz / (148 * 8);  // ~8 CTAs per SM
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    const char* v = getenv("SMG_TILES_PER_SM");
+    per_sm = v ? atoi(v) : 8;
+    if (per_sm <= 0) per_sm = 8;
+  }
+  const int64_t want = nnz / (148 * per_sm);  // ~per_sm tiles per SM
   int64_t cap = 256;
   while (cap < want && cap < kTileNnz) cap *= 2;
   return cap;
