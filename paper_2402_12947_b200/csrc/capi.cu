@@ -70,24 +70,17 @@ static void free_all(std::vector<void*>& allocs)
 // Greedy tile partition: consecutive rows, <= kRowsPerTile rows, <= cap
 // nonzeros unless a single row is longer.  Small operators (coarse levels)
 // get smaller tiles so every SM still has several independent CTAs.
-static bool async_tiles_env()
-{
-  const char* v = getenv("SMG_ASYNC_TILES");
-  return v && v[0] == '1';
-}
-
 static int64_t tile_cap_for(int64_t nnz)
 {
   static int per_sm = -1;
   if (per_sm < 0) {
     const char* v = getenv("SMG_TILES_PER_SM");
-    per_sm = v ? atoi(v) : 8;
-    if (per_sm <= 0) per_sm = 8;
+    per_sm = v ? atoi(v) : 4;
+    if (per_sm <= 0) per_sm = 4;
   }
   const int64_t want = nnz / (148 * per_sm);  // ~per_sm tiles per SM
   int64_t cap = 256;
-  const int64_t maxcap = async_tiles_env() ? kAsyncTileNnz : kTileNnz;
-  while (cap < want && cap < maxcap) cap *= 2;
+  while (cap < want && cap < kTileNnz) cap *= 2;
   return cap;
 }
 
@@ -127,7 +120,6 @@ static int build_devcsr(std::vector<void*>& allocs, int64_t& bytes, int64_t nrow
   std::vector<int64_t> rpp((size_t)nrows + 3, nnz);
   std::memcpy(rpp.data(), rowptr, sizeof(int64_t) * (size_t)(nrows + 1));
   std::vector<int32_t> tiles = make_tiles(nrows, rowptr);
-  const int64_t tcap = tile_cap_for(nnz);
   std::vector<int64_t> tnz(tiles.size());
   for (size_t i = 0; i < tiles.size(); ++i) tnz[i] = rowptr[tiles[i]];
   DevCsr d;
@@ -136,7 +128,6 @@ static int build_devcsr(std::vector<void*>& allocs, int64_t& bytes, int64_t nrow
   d.nnz = nnz;
   d.ntiles = (int32_t)(tiles.size() - 1);
   d.streaming = stream_env() && nnz * 12 > kStreamBytes;
-  d.tile_cap = (int32_t)tcap;
   int64_t* rp = nullptr;
   int32_t* c = nullptr;
   double* v = nullptr;

@@ -21,7 +21,6 @@ constexpr int kThreads = 256;        // one row per thread at most
 constexpr int kRowsPerTile = kThreads;
 constexpr int kTileNnz = 2048;       // products staged per pass (16 KB smem)
 constexpr int kItems = kTileNnz / kThreads;
-constexpr int kAsyncTileNnz = 4096;  // cp.async tile variant: (val, col) staged in 48 KB smem
 constexpr int64_t kStreamBytes = 64ll << 20;   // operators above this are streamed evict-first
 
 struct DevCsr {
@@ -33,7 +32,6 @@ struct DevCsr {
   const int64_t* tile_nz = nullptr;  // ntiles + 1 (rowptr at the tile boundaries)
   const double* inv_diag = nullptr;  // 1.0 / a_ii (IEEE, as smoothers.py:115), square ops
   int32_t ntiles = 0;
-  int32_t tile_cap = kTileNnz;       // nonzeros per tile the partition was built for
   bool streaming = false;            // val+col exceed kStreamBytes: evict-first reads
 };
 

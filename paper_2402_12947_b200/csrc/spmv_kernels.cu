@@ -210,114 +210,6 @@ csr_tile_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, 
   if (has_row) epilogue<E>(ea, row, sum, inv, bv, uv, dv, ov);
 }
 
-// ---------------------------------------------------------------------------
-// Variant with cp.async (LDGSTS) staging: the tile's values and columns go
-// straight to shared memory without occupying registers, so a CTA can keep a
-// 4096-nonzero tile in flight (2x the register-staged kernel) at 4 CTAs/SM.
-// Products overwrite the staged values in place.  Selected per operator by
-// the tile capacity its partition was built for (SMG_ASYNC_TILES=1).
-__device__ __forceinline__ void cp_async8(void* dst, const void* src)
-{
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
-               "l"(src)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async4(void* dst, const void* src)
-{
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
-               "l"(src)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all()
-{
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-}
-
-constexpr int kAsyncSmem = kAsyncTileNnz * 12;
-
-template <Epi E, bool kPf>
-__global__ void __launch_bounds__(kThreads, 4)
-csr_tile_async_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, int pf_dist)
-{
-  using T = EpiTraits<E>;
-  extern __shared__ __align__(16) unsigned char asm_[];
-  double* s_val = reinterpret_cast<double*>(asm_);
-  int32_t* s_col = reinterpret_cast<int32_t*>(asm_ + kAsyncTileNnz * 8);
-  const int t = blockIdx.x;
-  const int tid = threadIdx.x;
-  const int32_t r0 = m.tile_row[t];
-  const int32_t r1 = m.tile_row[t + 1];
-  const int64_t e0 = m.tile_nz[t];
-  const int64_t e1 = m.tile_nz[t + 1];
-  const bool longtile = e1 - e0 > kAsyncTileNnz;
-  const int cnt = (int)(e1 - e0);
-  const int32_t row = r0 + tid;
-  const bool has_row = row < r1;
-  int64_t lo = 0, hi = 0;
-  if (has_row) {
-    lo = m.rowptr[row];
-    hi = m.rowptr[row + 1];
-  }
-  if (!longtile) {
-    for (int k = tid; k < cnt; k += kThreads) {
-      cp_async8(s_val + k, m.val + e0 + k);
-      cp_async4(s_col + k, m.col + e0 + k);
-    }
-  }
-  if constexpr (kPf) {
-    if (tid == 0) {
-      const int tp = t + pf_dist;
-      if (tp < m.ntiles) {
-        const int64_t p0 = m.tile_nz[tp], p1 = m.tile_nz[tp + 1];
-        if (p1 - p0 <= kAsyncTileNnz && p1 > p0) {
-          const int64_t va = p0 & ~int64_t(1), vb = (p1 + 1) & ~int64_t(1);
-          const int64_t ca = p0 & ~int64_t(3), cb = (p1 + 3) & ~int64_t(3);
-          prefetch_l2(m.val + va, (uint32_t)((vb - va) * 8), m.streaming);
-          prefetch_l2(m.col + ca, (uint32_t)((cb - ca) * 4), m.streaming);
-        }
-      }
-    }
-  }
-  pdl_wait();
-  pdl_trigger();
-  double bv = 0.0, uv = 0.0, dv = 0.0, ov = 0.0, inv = 0.0;
-  if (has_row) {
-    if constexpr (T::kB) bv = ea.b[row];
-    if constexpr (T::kU) uv = ea.u_in[row];
-    if constexpr (T::kD) dv = ea.d[row];
-    if constexpr (T::kOut) ov = ea.out[row];
-    if constexpr (T::kDiag) inv = m.inv_diag[row];
-    if constexpr (T::kDiagVec) inv = ea.inv_diag[row];
-  }
-  double sum = 0.0;
-  if (!longtile) {
-    cp_async_wait_all();
-    __syncthreads();
-    for (int k = tid; k < cnt; k += kThreads) s_val[k] = __dmul_rn(s_val[k], __ldg(x + s_col[k]));
-    __syncthreads();
-    if (has_row) {
-      const int a = (int)(lo - e0);
-      const int bnd = (int)(hi - e0);
-      for (int j = a; j < bnd; ++j) sum = __dadd_rn(sum, s_val[j]);
-    }
-  } else {
-    for (int64_t cs = e0; cs < e1; cs += kAsyncTileNnz) {
-      const int64_t rem = e1 - cs;
-      const int cn = rem < (int64_t)kAsyncTileNnz ? (int)rem : kAsyncTileNnz;
-      for (int k = tid; k < cn; k += kThreads)
-        s_val[k] = __dmul_rn(__ldg(m.val + cs + k), __ldg(x + __ldg(m.col + cs + k)));
-      __syncthreads();
-      if (has_row) {
-        const int64_t a = lo > cs ? lo : cs;
-        const int64_t bnd = hi < cs + cn ? hi : cs + cn;
-        for (int64_t j = a; j < bnd; ++j) sum = __dadd_rn(sum, s_val[j - cs]);
-      }
-      __syncthreads();
-    }
-  }
-  if (has_row) epilogue<E>(ea, row, sum, inv, bv, uv, dv, ov);
-}
-
 static int g_sm_count = 0;
 static int g_prefetch = -1;
 static int g_pdl = -1;
@@ -352,22 +244,6 @@ static cudaError_t launch_t(const DevCsr& m, const double* x, const EpiArgs& ea,
   cfg.attrs = attr;
   cfg.numAttrs = env_flag(g_pdl, "SMG_PDL", 1) ? 1 : 0;
   const int dist = g_sm_count * kMinBlocks;  // one resident wave ahead
-  if (m.tile_cap > kTileNnz) {
-    static bool configured = false;
-    if (!configured) {
-      cudaError_t e = cudaFuncSetAttribute(csr_tile_async_kernel<E, true>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, kAsyncSmem);
-      if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(csr_tile_async_kernel<E, false>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kAsyncSmem);
-      if (e != cudaSuccess) return e;
-      configured = true;
-    }
-    cfg.dynamicSmemBytes = kAsyncSmem;
-    if (env_flag(g_prefetch, "SMG_L2_PREFETCH", 1))
-      return cudaLaunchKernelEx(&cfg, csr_tile_async_kernel<E, true>, m, x, ea, dist);
-    return cudaLaunchKernelEx(&cfg, csr_tile_async_kernel<E, false>, m, x, ea, dist);
-  }
   if (env_flag(g_prefetch, "SMG_L2_PREFETCH", 1))
     return cudaLaunchKernelEx(&cfg, csr_tile_kernel<E, true>, m, x, ea, dist);
   return cudaLaunchKernelEx(&cfg, csr_tile_kernel<E, false>, m, x, ea, dist);
