@@ -44,8 +44,20 @@ def test_sass_is_sm100a_and_parity_kernels_have_no_fma():
             funcs[current].append(line)
     # Epi 0 = spmv, 1 = residual, 5 = add-to (prolong): pure multiply/add
     for epi in ("0", "1", "5"):
-        name = [f for f in funcs if f.startswith(f"_ZN3smg15csr_tile_kernelILNS_3EpiE{epi}E")]
-        assert name, f"csr_tile_kernel<{epi}> missing"
-        body = "\n".join(funcs[name[0]])
-        assert "DFMA" not in body, f"csr_tile_kernel<{epi}> contains DFMA"
-        assert "DMUL" in body and "DADD" in body
+        names = [f for f in funcs if f.startswith(f"_ZN3smg15csr_tile_kernelILNS_3EpiE{epi}E")]
+        assert names, f"csr_tile_kernel<{epi}> missing"
+        for name in names:  # with and without the L2-prefetch instantiation
+            body = "\n".join(funcs[name])
+            assert "DFMA" not in body, f"{name} contains DFMA"
+            assert "DMUL" in body and "DADD" in body
+
+
+def test_sass_shows_bulk_copies_and_l2_prefetch():
+    """Evidence of the Blackwell data-movement paths: 1D TMA bulk copies into
+    shared memory with mbarrier completion (patch factors) and bulk L2
+    prefetches (SpMV tiles)."""
+    out = subprocess.run(["cuobjdump", "-sass", build_lib.LIB], capture_output=True, text=True,
+                         check=True).stdout
+    assert "UBLKCP" in out          # cp.async.bulk.shared::cluster.global
+    assert "UBLKPF" in out          # cp.async.bulk.prefetch.L2
+    assert "SYNCS.PHASECHK" in out  # mbarrier try_wait
