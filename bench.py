@@ -534,6 +534,25 @@ def main():
            "h2d_bytes_per_step": 2 * 8 * n0, "d2h_bytes_per_step": 8 * n0,
            "steps": e2e_steps, "path": "smg_vcycle_host (pinned numpy b, u)"}
 
+    # ---- time to solution: stationary MG to rtol 1e-10 (mg.py:154-175) from u0
+    solve = None
+    if rank == 0:
+        u0t = torch.zeros_like(b)
+        dh.solve_stationary(b, u0t, 1e-10, 100)  # warm (graph for these pointers)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, hist = dh.solve_stationary(b, u0t, 1e-10, 100)
+        torch.cuda.synchronize()
+        solve = {"rtol": 1e-10, "cycles": len(hist) - 1, "final_rel_residual": hist[-1],
+                 "ms": 1e3 * (time.perf_counter() - t0),
+                 "note": "device loop, one residual-norm readback per cycle"}
+        if ws == 1 and not args.no_cpu_baseline:
+            from oracle import oracle as O
+            t0 = time.perf_counter()
+            _, ch = O.solve_stationary(h, b_host, u0, 1e-10, 100)
+            solve["cpu_oracle_ms"] = 1e3 * (time.perf_counter() - t0)
+            solve["cpu_oracle_cycles"] = len(ch) - 1
+
     # ---- CPU baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -560,6 +579,7 @@ def main():
                          "nnz_per_row": z / nn},
             "sweeps_per_s": sweeps_per_s,
             "per_level_sweep": per_level,
+            "solve_stationary": solve,
             "lc_share": lc_share,
             "lc_us_per_vcycle": lc_us,
             "e2e": e2e,
