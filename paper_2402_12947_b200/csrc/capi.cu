@@ -775,35 +775,57 @@ int smg_correction_create(const smg_operator* a, int64_t n_regions, const int64_
   c.m = m;
   c.max_dofs = max_dofs;
   c.op = &o;
-  // coupling through A between different regions
-  c.coupled = false;
-  {
-    std::vector<int64_t> hrp((size_t)n + 1);
-    std::vector<int32_t> hcol((size_t)o.a.nnz);
-    cudaMemcpy(hrp.data(), o.a.rowptr, sizeof(int64_t) * (size_t)(n + 1), cudaMemcpyDeviceToHost);
-    cudaMemcpy(hcol.data(), o.a.col, sizeof(int32_t) * (size_t)o.a.nnz, cudaMemcpyDeviceToHost);
-    for (int64_t k = 0; k < m && !c.coupled; ++k) {
-      const int32_t g = dof32[(size_t)k];
-      for (int64_t j = hrp[(size_t)g]; j < hrp[(size_t)g + 1]; ++j) {
-        const int32_t own = owner[(size_t)hcol[(size_t)j]];
-        if (own >= 0 && own != owner[(size_t)g]) {
-          c.coupled = true;
-          break;
-        }
-      }
-    }
-  }
   int32_t* dp = nullptr;
   int32_t* dd = nullptr;
   int64_t* df = nullptr;
   double* dl = nullptr;
   int rc = SMG_OK;
+  c.coupled = false;
   if (n_regions > 0) {
     rc = dev_upload(c.allocs, c.device_bytes, pptr.data(), pptr.size(), &dp);
     if (rc == SMG_OK) rc = dev_upload(c.allocs, c.device_bytes, dof32.data(), dof32.size(), &dd);
     if (rc == SMG_OK) rc = dev_upload(c.allocs, c.device_bytes, poff.data(), poff.size(), &df);
     if (rc == SMG_OK) rc = dev_upload(c.allocs, c.device_bytes, packed.data(), packed.size(), &dl);
     if (rc == SMG_OK) rc = dev_alloc(c.allocs, c.device_bytes, (size_t)m, &c.rbuf);
+    // gathered copy of the patch rows of A (residuals read it coalesced)
+    int64_t* dlen = nullptr;
+    int64_t* dprow = nullptr;
+    int32_t* dpcol = nullptr;
+    double* dpval = nullptr;
+    std::vector<int64_t> prow((size_t)m + 1, 0);
+    if (rc == SMG_OK) rc = dev_alloc(c.allocs, c.device_bytes, (size_t)m, &dlen);
+    if (rc == SMG_OK) rc = check_cuda(launch_patch_row_len(o.a, dd, m, dlen), "patch row lengths");
+    if (rc == SMG_OK)
+      rc = check_cuda(cudaMemcpy(prow.data() + 1, dlen, sizeof(int64_t) * (size_t)m,
+                                 cudaMemcpyDeviceToHost), "patch row lengths D2H");
+    if (rc == SMG_OK) {
+      for (int64_t k = 0; k < m; ++k) prow[(size_t)k + 1] += prow[(size_t)k];
+      rc = dev_upload(c.allocs, c.device_bytes, prow.data(), prow.size(), &dprow);
+    }
+    const int64_t pn = prow[(size_t)m];
+    if (rc == SMG_OK) rc = dev_alloc(c.allocs, c.device_bytes, (size_t)pn + 1, &dpcol);
+    if (rc == SMG_OK) rc = dev_alloc(c.allocs, c.device_bytes, (size_t)pn + 1, &dpval);
+    if (rc == SMG_OK)
+      rc = check_cuda(launch_patch_row_gather(o.a, dd, m, dprow, dpcol, dpval), "patch row gather");
+    // coupling through A between different regions
+    if (rc == SMG_OK) {
+      std::vector<int32_t> hcol((size_t)pn);
+      rc = check_cuda(cudaMemcpy(hcol.data(), dpcol, sizeof(int32_t) * (size_t)pn,
+                                 cudaMemcpyDeviceToHost), "patch columns D2H");
+      for (int64_t k = 0; rc == SMG_OK && k < m && !c.coupled; ++k) {
+        const int32_t own_row = owner[(size_t)dof32[(size_t)k]];
+        for (int64_t j = prow[(size_t)k]; j < prow[(size_t)k + 1]; ++j) {
+          const int32_t own = owner[(size_t)hcol[(size_t)j]];
+          if (own >= 0 && own != own_row) {
+            c.coupled = true;
+            break;
+          }
+        }
+      }
+    }
+    c.prow = dprow;
+    c.pcol = dpcol;
+    c.pval = dpval;
     if (rc == SMG_OK) {
       c.pptr = dp;
       c.dofs = dd;

@@ -333,7 +333,9 @@ __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_
 
 template <int kMode>
 __global__ void __launch_bounds__(kSolveThreads)
-patch_kernel(const DevCsr a, const int32_t* __restrict__ pptr, const int32_t* __restrict__ dofs,
+patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
+             const double* __restrict__ pval, const int32_t* __restrict__ pptr,
+             const int32_t* __restrict__ dofs,
              const int64_t* __restrict__ foff, const double* __restrict__ lfac,
              const double* __restrict__ b, const double* u_res, double* rbuf, double* target,
              int scatter_add, int nmax, int allow_stream)
@@ -367,49 +369,34 @@ patch_kernel(const DevCsr a, const int32_t* __restrict__ pptr, const int32_t* __
   __syncthreads();
 
   if (kMode != kSolveFromBuf) {
-    // ---- residual rows: bounds, scan, streamed products, ordered sums
-    int32_t* s_len = reinterpret_cast<int32_t*>(s_prod);  // temporary
-    for (int i = threadIdx.x; i < n; i += kSolveThreads) {
-      const int32_t g = dofs[k0 + i];
-      const int64_t lo = a.rowptr[g];
-      s_lo[i] = lo;
-      s_len[i] = (int32_t)(a.rowptr[g + 1] - lo);
-      s_x[i] = 0.0;
+    // ---- residual rows from the region's gathered row copy (prow/pcol/pval,
+    //      built at upload): coalesced streamed products, then ordered sums
+    const int64_t base = prow[k0];
+    const int total = (int)(prow[k0 + n] - base);
+    for (int i = threadIdx.x; i <= n; i += kSolveThreads) {
+      s_off[i] = (int)(prow[k0 + i] - base);
+      if (i < n) s_x[i] = 0.0;
     }
     __syncthreads();
-    const int total = block_scan(s_len, s_off, n, &s_carry);
     for (int c0 = 0; c0 < total; c0 += kProdCap) {
       const int cnt = min(kProdCap, total - c0);
-      // batched: locate all of this thread's elements, then issue every load
-      int64_t jj[kProdItems];
-#pragma unroll
-      for (int it = 0; it < kProdItems; ++it) {
-        const int e = it * kSolveThreads + threadIdx.x;
-        jj[it] = -1;
-        if (e < cnt) {
-          const int eg = c0 + e;
-          int lo = 0, hi = n;  // last row r with s_off[r] <= eg
-          while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (s_off[mid] <= eg) lo = mid; else hi = mid;
-          }
-          jj[it] = s_lo[lo] + (eg - s_off[lo]);
-        }
-      }
       int32_t cc[kProdItems];
       double vv[kProdItems];
 #pragma unroll
       for (int it = 0; it < kProdItems; ++it) {
+        const int e = it * kSolveThreads + threadIdx.x;
         cc[it] = 0;
         vv[it] = 0.0;
-        if (jj[it] >= 0) {
-          cc[it] = __ldg(a.col + jj[it]);
-          vv[it] = __ldg(a.val + jj[it]);
+        if (e < cnt) {
+          cc[it] = __ldg(pcol + base + c0 + e);
+          vv[it] = __ldg(pval + base + c0 + e);
         }
       }
 #pragma unroll
-      for (int it = 0; it < kProdItems; ++it)
-        if (jj[it] >= 0) s_prod[it * kSolveThreads + threadIdx.x] = __dmul_rn(vv[it], u_res[cc[it]]);
+      for (int it = 0; it < kProdItems; ++it) {
+        const int e = it * kSolveThreads + threadIdx.x;
+        if (e < cnt) s_prod[e] = __dmul_rn(vv[it], u_res[cc[it]]);
+      }
       __syncthreads();
       for (int i = threadIdx.x; i < n; i += kSolveThreads) {
         const int a0 = max(s_off[i], c0), a1 = min(s_off[i + 1], c0 + cnt);
@@ -509,6 +496,43 @@ patch_kernel(const DevCsr a, const int32_t* __restrict__ pptr, const int32_t* __
   }
 }
 
+// upload-time helpers: bounds of the patch rows, then their (col, val) copy
+__global__ void patch_row_len_kernel(const DevCsr a, const int32_t* __restrict__ dofs, int64_t m,
+                                     int64_t* __restrict__ len)
+{
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < m) len[k] = a.rowptr[dofs[k] + 1] - a.rowptr[dofs[k]];
+}
+
+__global__ void patch_row_gather_kernel(const DevCsr a, const int32_t* __restrict__ dofs, int64_t m,
+                                        const int64_t* __restrict__ prow, int32_t* __restrict__ pcol,
+                                        double* __restrict__ pval)
+{
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const int64_t lo = a.rowptr[dofs[k]], hi = a.rowptr[dofs[k] + 1];
+  int64_t o = prow[k];
+  for (int64_t j = lo; j < hi; ++j, ++o) {
+    pcol[o] = a.col[j];
+    pval[o] = a.val[j];
+  }
+}
+
+cudaError_t launch_patch_row_len(const DevCsr& a, const int32_t* dofs, int64_t m, int64_t* len)
+{
+  if (m == 0) return cudaSuccess;
+  patch_row_len_kernel<<<(unsigned)((m + 127) / 128), 128>>>(a, dofs, m, len);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_patch_row_gather(const DevCsr& a, const int32_t* dofs, int64_t m,
+                                    const int64_t* prow, int32_t* pcol, double* pval)
+{
+  if (m == 0) return cudaSuccess;
+  patch_row_gather_kernel<<<(unsigned)((m + 127) / 128), 128>>>(a, dofs, m, prow, pcol, pval);
+  return cudaGetLastError();
+}
+
 __global__ void gather_kernel(const int32_t* __restrict__ idx, int64_t m,
                               const double* __restrict__ src, double* __restrict__ dst)
 {
@@ -531,7 +555,7 @@ cudaError_t launch_patch_residual(const DevCsr& a, const Correction& c, const do
   if (c.n_regions == 0) return cudaSuccess;
   const PatchSmem L = patch_smem_layout(c.max_dofs);
   patch_kernel<kResidualOnly><<<c.n_regions, kSolveThreads, (size_t)L.l_off, s>>>(
-      a, c.pptr, c.dofs, c.foff, c.lfac, b, u, c.rbuf, nullptr, 0, c.max_dofs, 1);
+      c.prow, c.pcol, c.pval, c.pptr, c.dofs, c.foff, c.lfac, b, u, c.rbuf, nullptr, 0, c.max_dofs, 1);
   return cudaGetLastError();
 }
 
@@ -557,10 +581,12 @@ cudaError_t launch_patch_solve(const Correction& c, const double* b, const doubl
   const size_t smem = (size_t)L.bytes + smem_pad();
   if (fused)
     patch_kernel<kAddResidualSolve><<<c.n_regions, kSolveThreads, smem, s>>>(
-        c.op->a, c.pptr, c.dofs, c.foff, c.lfac, b, u_res, c.rbuf, tgt, add, c.max_dofs, st);
+        c.prow, c.pcol, c.pval, c.pptr, c.dofs, c.foff, c.lfac, b, u_res, c.rbuf, tgt, add,
+        c.max_dofs, st);
   else
     patch_kernel<kSolveFromBuf><<<c.n_regions, kSolveThreads, smem, s>>>(
-        c.op->a, c.pptr, c.dofs, c.foff, c.lfac, b, u_res, c.rbuf, tgt, add, c.max_dofs, st);
+        c.prow, c.pcol, c.pval, c.pptr, c.dofs, c.foff, c.lfac, b, u_res, c.rbuf, tgt, add,
+        c.max_dofs, st);
   return cudaGetLastError();
 }
 

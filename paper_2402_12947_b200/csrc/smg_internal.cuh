@@ -58,6 +58,9 @@ struct Correction {
   const int64_t* foff = nullptr;   // n_regions + 1, offsets into packed factors
   const double* lfac = nullptr;    // packed lower factors, row-major
   double* rbuf = nullptr;          // m scratch (patch residual / correction)
+  const int64_t* prow = nullptr;   // m + 1: offsets of the patch rows' gathered copy
+  const int32_t* pcol = nullptr;   // gathered columns of the patch rows of A
+  const double* pval = nullptr;    // gathered values of the patch rows of A
   bool coupled = true;             // some A[B_d, B_d'] != 0 (d != d')
   const Operator* op = nullptr;
   int64_t device_bytes = 0;
@@ -127,6 +130,9 @@ cudaError_t launch_gather(const int32_t* idx, int64_t m, const double* src, doub
 cudaError_t launch_patch_solve(const Correction& c, const double* b, const double* u_res,
                                double* u_add, double* out_scatter, bool fused, cudaStream_t s);
 cudaError_t configure_patch_solve_smem(const Correction& c);
+cudaError_t launch_patch_row_len(const DevCsr& a, const int32_t* dofs, int64_t m, int64_t* len);
+cudaError_t launch_patch_row_gather(const DevCsr& a, const int32_t* dofs, int64_t m,
+                                    const int64_t* prow, int32_t* pcol, double* pval);
 
 // dense / reduction kernels (dense_kernels.cu)
 cudaError_t launch_dense_gemv(int64_t n, const double* m, const double* x, double* y,
