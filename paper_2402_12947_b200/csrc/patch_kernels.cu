@@ -32,6 +32,15 @@
 
 namespace smg {
 
+// programmatic dependent launch (no-ops without the launch attribute): wait
+// for the producer of u / b / rbuf, then let the next kernel's CTAs start
+// their own static prologue on the SMs this kernel leaves idle.
+__device__ __forceinline__ void patch_pdl_wait()
+{
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ uint32_t psmem_u32(const void* p)
 {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -370,18 +379,18 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
 
   if (kMode != kSolveFromBuf) {
     // ---- residual rows from the region's gathered row copy (prow/pcol/pval,
-    //      built at upload): coalesced streamed products, then ordered sums
+    //      built at upload): coalesced streamed products, then ordered sums.
+    //      The copy is static, so its first chunk is requested before the
+    //      programmatic-dependency wait; u and b are read after it.
     const int64_t base = prow[k0];
     const int total = (int)(prow[k0 + n] - base);
     for (int i = threadIdx.x; i <= n; i += kSolveThreads) {
       s_off[i] = (int)(prow[k0 + i] - base);
       if (i < n) s_x[i] = 0.0;
     }
-    __syncthreads();
-    for (int c0 = 0; c0 < total; c0 += kProdCap) {
-      const int cnt = min(kProdCap, total - c0);
-      int32_t cc[kProdItems];
-      double vv[kProdItems];
+    int32_t cc[kProdItems];
+    double vv[kProdItems];
+    auto load_chunk = [&](int c0, int cnt) {
 #pragma unroll
       for (int it = 0; it < kProdItems; ++it) {
         const int e = it * kSolveThreads + threadIdx.x;
@@ -392,6 +401,13 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
           vv[it] = __ldg(pval + base + c0 + e);
         }
       }
+    };
+    load_chunk(0, min(kProdCap, total));
+    patch_pdl_wait();
+    __syncthreads();
+    for (int c0 = 0; c0 < total; c0 += kProdCap) {
+      const int cnt = min(kProdCap, total - c0);
+      if (c0 > 0) load_chunk(c0, cnt);
 #pragma unroll
       for (int it = 0; it < kProdItems; ++it) {
         const int e = it * kSolveThreads + threadIdx.x;
@@ -415,6 +431,7 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
     }
     if (kMode == kResidualOnly) return;
   } else {
+    patch_pdl_wait();
     for (int i = threadIdx.x; i < n; i += kSolveThreads) s_x[i] = rbuf[k0 + i];
   }
   if (staged) factor_wait(&s_bar);
@@ -548,15 +565,33 @@ cudaError_t launch_gather(const int32_t* idx, int64_t m, const double* src, doub
   return cudaGetLastError();
 }
 
+template <int kMode>
+static cudaError_t launch_patch(const Correction& c, size_t smem, const double* b,
+                                const double* u_res, double* tgt, int add, int allow_stream,
+                                cudaStream_t s)
+{
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)c.n_regions);
+  cfg.blockDim = dim3(kSolveThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, patch_kernel<kMode>, c.prow, c.pcol, c.pval, c.pptr, c.dofs,
+                            c.foff, c.lfac, b, u_res, c.rbuf, tgt, add, c.max_dofs, allow_stream);
+}
+
 // residual-only pass (coupled regions): rbuf[k] = (b - A u)[dofs[k]]
 cudaError_t launch_patch_residual(const DevCsr& a, const Correction& c, const double* b,
                                   const double* u, cudaStream_t s)
 {
+  (void)a;
   if (c.n_regions == 0) return cudaSuccess;
   const PatchSmem L = patch_smem_layout(c.max_dofs);
-  patch_kernel<kResidualOnly><<<c.n_regions, kSolveThreads, (size_t)L.l_off, s>>>(
-      c.prow, c.pcol, c.pval, c.pptr, c.dofs, c.foff, c.lfac, b, u, c.rbuf, nullptr, 0, c.max_dofs, 1);
-  return cudaGetLastError();
+  return launch_patch<kResidualOnly>(c, (size_t)L.l_off, b, u, nullptr, 0, 1, s);
 }
 
 static size_t smem_pad()
@@ -579,15 +614,8 @@ cudaError_t launch_patch_solve(const Correction& c, const double* b, const doubl
   double* tgt = u_add ? u_add : out_scatter;
   const int add = u_add ? 1 : 0;
   const size_t smem = (size_t)L.bytes + smem_pad();
-  if (fused)
-    patch_kernel<kAddResidualSolve><<<c.n_regions, kSolveThreads, smem, s>>>(
-        c.prow, c.pcol, c.pval, c.pptr, c.dofs, c.foff, c.lfac, b, u_res, c.rbuf, tgt, add,
-        c.max_dofs, st);
-  else
-    patch_kernel<kSolveFromBuf><<<c.n_regions, kSolveThreads, smem, s>>>(
-        c.prow, c.pcol, c.pval, c.pptr, c.dofs, c.foff, c.lfac, b, u_res, c.rbuf, tgt, add,
-        c.max_dofs, st);
-  return cudaGetLastError();
+  if (fused) return launch_patch<kAddResidualSolve>(c, smem, b, u_res, tgt, add, st, s);
+  return launch_patch<kSolveFromBuf>(c, smem, b, u_res, tgt, add, st, s);
 }
 
 cudaError_t configure_patch_solve_smem(const Correction& c)
