@@ -129,41 +129,6 @@ __host__ __device__ inline PatchSmem patch_smem_layout(int nmax, bool allow_stre
   return p;
 }
 
-// exclusive scan of len[0..n) into off[0..n], returns the total (block-wide)
-__device__ int block_scan(const int32_t* len, int32_t* off, int n, int* s_carry)
-{
-  __shared__ int s_warp[kSolveWarps];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) *s_carry = 0;
-  __syncthreads();
-  for (int base = 0; base < n; base += kSolveThreads) {
-    const int i = base + threadIdx.x;
-    const int v = i < n ? len[i] : 0;
-    int incl = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (lane == 31) s_warp[warp] = incl;
-    __syncthreads();
-    int wpre = 0;
-    for (int w = 0; w < warp; ++w) wpre += s_warp[w];
-    int tot = 0;
-    for (int w = 0; w < kSolveWarps; ++w) tot += s_warp[w];
-    const int carry = *s_carry;
-    if (i < n) off[i] = carry + wpre + incl - v;
-    __syncthreads();
-    if (threadIdx.x == 0) *s_carry = carry + tot;
-    __syncthreads();
-  }
-  const int total = *s_carry;
-  if (threadIdx.x == 0) off[n] = total;
-  __syncthreads();
-  return total;
-}
-
-
 // ---------------------------------------------------------------------------
 // Streaming triangular solves for regions whose factor does not fit in shared
 // memory (C5: 64..512-dof patches).  Row chunks of kChunkRows factor rows --
@@ -351,13 +316,11 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
 {
   extern __shared__ __align__(16) unsigned char psm[];
   __shared__ double s_red[kSolveWarps][32];
-  __shared__ int s_carry;
   __shared__ uint64_t s_bar;
   __shared__ uint64_t s_ring_bar[kRingStages];
   __shared__ uint64_t s_dinv_bar[2];
   const PatchSmem L_ = patch_smem_layout(nmax, allow_stream != 0);
   double* s_x = reinterpret_cast<double*>(psm + L_.x_off);
-  int64_t* s_lo = reinterpret_cast<int64_t*>(psm + L_.lo_off);
   int32_t* s_off = reinterpret_cast<int32_t*>(psm + L_.off_off);
   double* s_prod = reinterpret_cast<double*>(psm + L_.prod_off);
   double* s_L = reinterpret_cast<double*>(psm + L_.l_off);
