@@ -144,9 +144,14 @@ SMG_API int smg_hierarchy_set_graphs(smg_hierarchy *h, int enable);
  *   SMG_OPT_GRAPHS          1 = capture V-cycles as CUDA graphs (default 1)
  *   SMG_OPT_FUSE_ZERO_GUESS 1 = fuse each coarse level's restriction with its
  *                           first smoother sweep from the zero initial guess
- *                           (mg.py:143; bit-identical, default 1) */
+ *                           (mg.py:143; bit-identical, default 1)
+ *   SMG_OPT_LC_OVERLAP      1 = run each local correction concurrently with the
+ *                           patch-independent (interior) rows of the adjacent
+ *                           smoother sweep; the halo rows follow (bit-identical,
+ *                           default 1) */
 #define SMG_OPT_GRAPHS 0
 #define SMG_OPT_FUSE_ZERO_GUESS 1
+#define SMG_OPT_LC_OVERLAP 2
 SMG_API int smg_hierarchy_set_option(smg_hierarchy *h, int option, int value);
 /* kernels one V-cycle launches (for launch accounting) */
 SMG_API int smg_hierarchy_launches_per_vcycle(const smg_hierarchy *h, int64_t *launches);

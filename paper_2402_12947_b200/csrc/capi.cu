@@ -304,6 +304,9 @@ struct Hierarchy {
   int64_t bytes = 0;
   bool use_graphs = true;
   bool fuse_zero_guess = true;
+  bool lc_overlap = true;
+  cudaStream_t side = nullptr;       // local corrections overlapping interior sweeps
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   std::map<std::pair<const void*, void*>, cudaGraphExec_t> graphs;
   cudaStream_t capture_stream = nullptr;
   int64_t launches = 0;
@@ -315,18 +318,98 @@ struct Hierarchy {
   {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     if (capture_stream) cudaStreamDestroy(capture_stream);
+    if (side) cudaStreamDestroy(side);
+    if (fork_ev) cudaEventDestroy(fork_ev);
+    if (join_ev) cudaEventDestroy(join_ev);
     dots.release();
     free_all(allocs);
   }
 };
 
-static int enqueue_smooth(HLevel& L, const double* b, double** cur, double** alt, cudaStream_t st,
-                          int64_t* launches, bool first_done = false)
+// One combined smoothing step (smoothers.py:240-269: LC, k global sweeps, LC).
+// With a halo split the first local correction runs on a side stream
+// concurrently with the interior rows of sweep 1 (rows with no column in any
+// patch, so they neither read nor write what the correction changes); the halo
+// rows of sweep 1 follow once both finished.  Symmetrically the last sweep's
+// halo rows run first, then the second correction overlaps its interior rows.
+// Every row is computed by exactly the arithmetic of the unsplit sweep, so the
+// result is bit-identical.
+static int enqueue_smooth(Hierarchy& h, HLevel& L, const double* b, double** cur, double** alt,
+                          cudaStream_t st, int64_t* launches, bool first_done = false)
 {
   const bool active = L.lc && L.lc->n_regions > 0;
-  if (active) SMG_TRY(enqueue_local_correct(*L.lc, b, *cur, st, launches));
-  SMG_TRY(enqueue_global_smooth(*L.a, b, cur, alt, L.d, L.sweeps, L.cs, st, launches, first_done));
-  if (active) SMG_TRY(enqueue_local_correct(*L.lc, b, *cur, st, launches));
+  if (!active || first_done || !h.lc_overlap || !L.lc->has_halo) {
+    if (active) SMG_TRY(enqueue_local_correct(*L.lc, b, *cur, st, launches));
+    SMG_TRY(enqueue_global_smooth(*L.a, b, cur, alt, L.d, L.sweeps, L.cs, st, launches,
+                                  first_done));
+    if (active) SMG_TRY(enqueue_local_correct(*L.lc, b, *cur, st, launches));
+    return SMG_OK;
+  }
+  const Correction& lc = *L.lc;
+  if (!h.side) {
+    SMG_CUDA(cudaStreamCreateWithFlags(&h.side, cudaStreamNonBlocking));
+    SMG_CUDA(cudaEventCreateWithFlags(&h.fork_ev, cudaEventDisableTiming));
+    SMG_CUDA(cudaEventCreateWithFlags(&h.join_ev, cudaEventDisableTiming));
+  }
+  struct Step {
+    Epi e;
+    double c1, c2;
+  };
+  std::vector<Step> steps;
+  if (L.cs.collapsed) {
+    for (int k = 0; k < L.sweeps; ++k) steps.push_back({Epi::kJacobi, 0.0, 0.0});
+  } else {
+    steps.push_back({Epi::kChebFirst, 0.0, 0.0});
+    for (const auto& c : L.cs.steps) steps.push_back({Epi::kChebNext, c.first, c.second});
+  }
+  enum Part { kAll, kInterior, kHalo };
+  auto sweep = [&](const Step& s, Part part) -> int {
+    EpiArgs ea;
+    ea.b = b;
+    ea.theta = L.cs.theta;
+    ea.d = L.d;
+    ea.u_in = *cur;
+    ea.out = *alt;
+    ea.c1 = s.c1;
+    ea.c2 = s.c2;
+    if (part == kInterior) ea.skip_rows = lc.halo_mask;
+    SMG_CUDA(launch_csr_stream(part == kHalo ? lc.halo : L.a->a, *cur, s.e, ea, st));
+    ++*launches;
+    return SMG_OK;
+  };
+  auto fork = [&]() -> int {
+    SMG_CUDA(cudaEventRecord(h.fork_ev, st));
+    SMG_CUDA(cudaStreamWaitEvent(h.side, h.fork_ev, 0));
+    return SMG_OK;
+  };
+  auto join = [&]() -> int {
+    SMG_CUDA(cudaEventRecord(h.join_ev, h.side));
+    SMG_CUDA(cudaStreamWaitEvent(st, h.join_ev, 0));
+    return SMG_OK;
+  };
+  const size_t k = steps.size();
+  // LC1 (in place on cur) || interior rows of sweep 1; then its halo rows
+  SMG_TRY(fork());
+  SMG_TRY(enqueue_local_correct(lc, b, *cur, h.side, launches));
+  SMG_TRY(sweep(steps[0], kInterior));
+  SMG_TRY(join());
+  SMG_TRY(sweep(steps[0], kHalo));
+  std::swap(*cur, *alt);
+  for (size_t i = 1; i + 1 < k; ++i) {
+    SMG_TRY(sweep(steps[i], kAll));
+    std::swap(*cur, *alt);
+  }
+  if (k >= 2) {
+    // halo rows of the last sweep, then LC2 on them || the interior rows
+    SMG_TRY(sweep(steps[k - 1], kHalo));
+    SMG_TRY(fork());
+    SMG_TRY(enqueue_local_correct(lc, b, *alt, h.side, launches));
+    SMG_TRY(sweep(steps[k - 1], kInterior));
+    SMG_TRY(join());
+    std::swap(*cur, *alt);
+  } else {
+    SMG_TRY(enqueue_local_correct(lc, b, *cur, st, launches));
+  }
   return SMG_OK;
 }
 
@@ -348,7 +431,7 @@ static int enqueue_vcycle(Hierarchy& h, const double* b0, double* u0, cudaStream
   std::vector<char> first_done(nl, 0);
   for (int l = 0; l < nl - 1; ++l) {
     HLevel& L = h.lv[l];
-    SMG_TRY(enqueue_smooth(L, bl[l], &cur[l], &alt[l], st, launches, first_done[l] != 0));
+    SMG_TRY(enqueue_smooth(h, L, bl[l], &cur[l], &alt[l], st, launches, first_done[l] != 0));
     EpiArgs ea;
     ea.b = bl[l];
     ea.out = L.r;
@@ -396,7 +479,7 @@ static int enqueue_vcycle(Hierarchy& h, const double* b0, double* u0, cudaStream
     ea.out = cur[l];
     SMG_CUDA(launch_csr_stream(L.p->a, cur[l + 1], Epi::kAddTo, ea, st));
     ++*launches;
-    SMG_TRY(enqueue_smooth(L, bl[l], &cur[l], &alt[l], st, launches));
+    SMG_TRY(enqueue_smooth(h, L, bl[l], &cur[l], &alt[l], st, launches));
   }
   if (cur[0] != u0) {
     SMG_CUDA(cudaMemcpyAsync(u0, cur[0], sizeof(double) * (size_t)h.lv[0].n,
@@ -706,6 +789,87 @@ int smg_chebyshev_smooth(const smg_operator* a, const double* b, double* u, int 
                            work, as_stream(stream));
 }
 
+// Interior/halo split of A around the patches (for overlapping the local
+// corrections with smoother sweeps).  Halo rows: every row with a column in a
+// patch, every patch row and every column of a patch row (the correction reads
+// u there).  Only worth it while the halo is a minority of the rows.
+static int build_halo(const Operator& o, const std::vector<int32_t>& dof32,
+                      const std::vector<int32_t>& patch_cols, Correction& c)
+{
+  const int64_t n = o.a.nrows;
+  const char* env = getenv("SMG_LC_SPLIT");
+  if ((env && env[0] == '0') || n == 0 || dof32.empty() || !o.a.inv_diag) return SMG_OK;
+  std::vector<void*> tmp;
+  int64_t tmp_bytes = 0;
+  std::vector<uint8_t> inb((size_t)n, 0);
+  for (int32_t g : dof32) inb[(size_t)g] = 1;
+  uint8_t* d_inb = nullptr;
+  uint8_t* d_mask = nullptr;
+  int rc = dev_upload(tmp, tmp_bytes, inb.data(), inb.size(), &d_inb);
+  if (rc == SMG_OK) rc = dev_alloc(tmp, tmp_bytes, (size_t)n, &d_mask);
+  if (rc == SMG_OK) rc = check_cuda(launch_mark_halo(o.a, d_inb, d_mask), "halo mark");
+  std::vector<uint8_t> mask((size_t)n, 0);
+  if (rc == SMG_OK)
+    rc = check_cuda(cudaMemcpy(mask.data(), d_mask, (size_t)n, cudaMemcpyDeviceToHost), "halo D2H");
+  free_all(tmp);
+  SMG_TRY(rc);
+  for (int32_t g : dof32) mask[(size_t)g] = 1;
+  for (int32_t j : patch_cols) mask[(size_t)j] = 1;
+  std::vector<int32_t> rows;
+  for (int64_t i = 0; i < n; ++i)
+    if (mask[(size_t)i]) rows.push_back((int32_t)i);
+  const int64_t nh = (int64_t)rows.size();
+  if (nh == 0 || 2 * nh > n) return SMG_OK;
+  uint8_t* mk = nullptr;
+  int32_t* drows = nullptr;
+  int64_t* dlen = nullptr;
+  SMG_TRY(dev_upload(c.allocs, c.device_bytes, mask.data(), mask.size(), &mk));
+  SMG_TRY(dev_upload(c.allocs, c.device_bytes, rows.data(), rows.size(), &drows));
+  SMG_TRY(dev_alloc(tmp, tmp_bytes, (size_t)nh, &dlen));
+  std::vector<int64_t> hrow((size_t)nh + 3, 0);
+  rc = check_cuda(launch_patch_row_len(o.a, drows, nh, dlen), "halo row lengths");
+  if (rc == SMG_OK)
+    rc = check_cuda(cudaMemcpy(hrow.data() + 1, dlen, sizeof(int64_t) * (size_t)nh,
+                               cudaMemcpyDeviceToHost), "halo row lengths D2H");
+  free_all(tmp);
+  SMG_TRY(rc);
+  for (int64_t k = 0; k < nh; ++k) hrow[(size_t)k + 1] += hrow[(size_t)k];
+  const int64_t hn = hrow[(size_t)nh];
+  hrow[(size_t)nh + 1] = hrow[(size_t)nh + 2] = hn;
+  std::vector<int32_t> tiles = make_tiles(nh, hrow.data());
+  std::vector<int64_t> tnz(tiles.size());
+  for (size_t i = 0; i < tiles.size(); ++i) tnz[i] = hrow[(size_t)tiles[i]];
+  int64_t* drp = nullptr;
+  int32_t* dcol = nullptr;
+  double* dval = nullptr;
+  int32_t* dtr = nullptr;
+  int64_t* dtz = nullptr;
+  SMG_TRY(dev_upload(c.allocs, c.device_bytes, hrow.data(), hrow.size(), &drp));
+  SMG_TRY(dev_alloc(c.allocs, c.device_bytes, (size_t)hn + 4, &dcol));  // prefetch padding
+  SMG_TRY(dev_alloc(c.allocs, c.device_bytes, (size_t)hn + 2, &dval));
+  SMG_TRY(dev_upload(c.allocs, c.device_bytes, tiles.data(), tiles.size(), &dtr));
+  SMG_TRY(dev_upload(c.allocs, c.device_bytes, tnz.data(), tnz.size(), &dtz));
+  SMG_TRY(check_cuda(launch_patch_row_gather(o.a, drows, nh, drp, dcol, dval), "halo gather"));
+  SMG_CUDA(cudaDeviceSynchronize());
+  DevCsr hm;
+  hm.nrows = nh;
+  hm.ncols = o.a.ncols;
+  hm.nnz = hn;
+  hm.rowptr = drp;
+  hm.col = dcol;
+  hm.val = dval;
+  hm.tile_row = dtr;
+  hm.tile_nz = dtz;
+  hm.inv_diag = o.a.inv_diag;   // indexed by operator row (row_map)
+  hm.row_map = drows;
+  hm.ntiles = (int32_t)(tiles.size() - 1);
+  hm.streaming = o.a.streaming;
+  c.halo = hm;
+  c.halo_mask = mk;
+  c.has_halo = true;
+  return SMG_OK;
+}
+
 int smg_correction_create(const smg_operator* a, int64_t n_regions, const int64_t* roff,
                           const int64_t* dofs, const int64_t* foff, const double* factors,
                           smg_correction** out)
@@ -808,8 +972,9 @@ int smg_correction_create(const smg_operator* a, int64_t n_regions, const int64_
     if (rc == SMG_OK)
       rc = check_cuda(launch_patch_row_gather(o.a, dd, m, dprow, dpcol, dpval), "patch row gather");
     // coupling through A between different regions
+    std::vector<int32_t> hcol;
     if (rc == SMG_OK) {
-      std::vector<int32_t> hcol((size_t)pn);
+      hcol.resize((size_t)pn);
       rc = check_cuda(cudaMemcpy(hcol.data(), dpcol, sizeof(int32_t) * (size_t)pn,
                                  cudaMemcpyDeviceToHost), "patch columns D2H");
       for (int64_t k = 0; rc == SMG_OK && k < m && !c.coupled; ++k) {
@@ -826,6 +991,7 @@ int smg_correction_create(const smg_operator* a, int64_t n_regions, const int64_
     c.prow = dprow;
     c.pcol = dpcol;
     c.pval = dpval;
+    if (rc == SMG_OK) rc = build_halo(o, dof32, hcol, c);
     if (rc == SMG_OK) {
       c.pptr = dp;
       c.dofs = dd;
@@ -988,6 +1154,8 @@ int smg_hierarchy_set_option(smg_hierarchy* h, int option, int value)
     H.use_graphs = value != 0;
   else if (option == SMG_OPT_FUSE_ZERO_GUESS)
     H.fuse_zero_guess = value != 0;
+  else if (option == SMG_OPT_LC_OVERLAP)
+    H.lc_overlap = value != 0;
   else
     return fail("unknown hierarchy option");
   for (auto& kv : H.graphs) cudaGraphExecDestroy(kv.second);

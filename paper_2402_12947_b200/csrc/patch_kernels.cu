@@ -513,6 +513,25 @@ cudaError_t launch_patch_row_gather(const DevCsr& a, const int32_t* dofs, int64_
   return cudaGetLastError();
 }
 
+// mask[i] = 1 iff row i of A has a column inside some patch (the rows whose
+// value depends on a local correction of u)
+__global__ void mark_halo_kernel(const DevCsr a, const uint8_t* __restrict__ in_patch,
+                                 uint8_t* __restrict__ mask)
+{
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.nrows) return;
+  uint8_t h = 0;
+  for (int64_t j = a.rowptr[i]; j < a.rowptr[i + 1] && !h; ++j) h = in_patch[a.col[j]];
+  mask[i] = h;
+}
+
+cudaError_t launch_mark_halo(const DevCsr& a, const uint8_t* in_patch, uint8_t* mask)
+{
+  if (a.nrows == 0) return cudaSuccess;
+  mark_halo_kernel<<<(unsigned)((a.nrows + 255) / 256), 256>>>(a, in_patch, mask);
+  return cudaGetLastError();
+}
+
 __global__ void gather_kernel(const int32_t* __restrict__ idx, int64_t m,
                               const double* __restrict__ src, double* __restrict__ dst)
 {

@@ -31,6 +31,7 @@ struct DevCsr {
   const int32_t* tile_row = nullptr; // ntiles + 1 (row boundaries of tiles)
   const int64_t* tile_nz = nullptr;  // ntiles + 1 (rowptr at the tile boundaries)
   const double* inv_diag = nullptr;  // 1.0 / a_ii (IEEE, as smoothers.py:115), square ops
+  const int32_t* row_map = nullptr;  // gathered row subsets: local row -> operator row
   int32_t ntiles = 0;
   bool streaming = false;            // val+col exceed kStreamBytes: evict-first reads
 };
@@ -61,6 +62,12 @@ struct Correction {
   const int64_t* prow = nullptr;   // m + 1: offsets of the patch rows' gathered copy
   const int32_t* pcol = nullptr;   // gathered columns of the patch rows of A
   const double* pval = nullptr;    // gathered values of the patch rows of A
+  // interior/halo split of A around the patches: halo rows are those whose
+  // stencil touches a patch dof (they depend on the correction); `halo` holds
+  // their gathered rows (with row_map), `halo_mask` flags them per row
+  bool has_halo = false;
+  DevCsr halo;
+  const uint8_t* halo_mask = nullptr;
   bool coupled = true;             // some A[B_d, B_d'] != 0 (d != d')
   const Operator* op = nullptr;
   int64_t device_bytes = 0;
@@ -117,6 +124,7 @@ struct EpiArgs {
   double theta = 1.0, c1 = 0.0, c2 = 0.0;
   const double* inv_diag = nullptr;  // kRestrictFirst: coarse operator 1/diagonal
   double* b_out = nullptr;        // kRestrictFirst: restricted right-hand side
+  const uint8_t* skip_rows = nullptr;  // interior pass: rows flagged here are not written
 };
 
 cudaError_t launch_csr_stream(const DevCsr& m, const double* x, Epi epi, const EpiArgs& ea,
@@ -133,6 +141,7 @@ cudaError_t configure_patch_solve_smem(const Correction& c);
 cudaError_t launch_patch_row_len(const DevCsr& a, const int32_t* dofs, int64_t m, int64_t* len);
 cudaError_t launch_patch_row_gather(const DevCsr& a, const int32_t* dofs, int64_t m,
                                     const int64_t* prow, int32_t* pcol, double* pval);
+cudaError_t launch_mark_halo(const DevCsr& a, const uint8_t* in_patch, uint8_t* mask);
 
 // dense / reduction kernels (dense_kernels.cu)
 cudaError_t launch_dense_gemv(int64_t n, const double* m, const double* x, double* y,

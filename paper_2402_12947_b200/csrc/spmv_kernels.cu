@@ -169,14 +169,18 @@ csr_tile_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, 
   // ---- vectors produced by earlier kernels: after the dependency wait
   pdl_wait();
   pdl_trigger();
+  // gathered row subsets (halo pass) address vectors through row_map; the
+  // interior pass skips the rows a concurrent local correction may change
+  const int32_t grow = (has_row && m.row_map) ? m.row_map[row] : row;
+  const bool write = has_row && !(ea.skip_rows && ea.skip_rows[grow]);
   double bv = 0.0, uv = 0.0, dv = 0.0, ov = 0.0, inv = 0.0;
-  if (has_row) {
-    if constexpr (T::kB) bv = ea.b[row];
-    if constexpr (T::kU) uv = ea.u_in[row];
-    if constexpr (T::kD) dv = ea.d[row];
-    if constexpr (T::kOut) ov = ea.out[row];
-    if constexpr (T::kDiag) inv = m.inv_diag[row];
-    if constexpr (T::kDiagVec) inv = ea.inv_diag[row];
+  if (write) {
+    if constexpr (T::kB) bv = ea.b[grow];
+    if constexpr (T::kU) uv = ea.u_in[grow];
+    if constexpr (T::kD) dv = ea.d[grow];
+    if constexpr (T::kOut) ov = ea.out[grow];
+    if constexpr (T::kDiag) inv = m.inv_diag[grow];
+    if constexpr (T::kDiagVec) inv = ea.inv_diag[grow];
   }
   double sum = 0.0;
   if (!longtile) {
@@ -207,7 +211,7 @@ csr_tile_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, 
       __syncthreads();
     }
   }
-  if (has_row) epilogue<E>(ea, row, sum, inv, bv, uv, dv, ov);
+  if (write) epilogue<E>(ea, grow, sum, inv, bv, uv, dv, ov);
 }
 
 static int g_sm_count = 0;

@@ -1,4 +1,5 @@
 #!/bin/bash
+# HISTORICAL: the SMG_SPMV_VARIANT kernels were removed after these A/Bs.
 mkdir -p gpurun_out
 SMG_SPMV_VARIANT=12 timeout 900 python -m pytest tests -x -q -m gpu -k "sparse or sweep or vcycle" > gpurun_out/pytest_v12.log 2>&1
 echo "v12 pytest rc=$?" >> gpurun_out/rc.txt

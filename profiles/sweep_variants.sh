@@ -1,4 +1,5 @@
 #!/bin/bash
+# HISTORICAL: the SMG_SPMV_VARIANT kernels were removed after these A/Bs.
 # A/B the SpMV kernel variants (SMG_SPMV_VARIANT) and PDL (SMG_PDL) on the C2 bench.
 mkdir -p gpurun_out
 for cfg in "1 1" "3 1" "4 1" "2 1" "1 0"; do

@@ -150,6 +150,30 @@ def test_zero_guess_fusion_is_bitwise(P, fx):
     assert np.array_equal(res[0], res[1])
 
 
+@pytest.mark.parametrize("graphs", [True, False])
+def test_lc_overlap_is_bitwise(P, fx, graphs):
+    """Local corrections running concurrently with the interior rows of the
+    adjacent sweep (halo rows after) give the sequential result bit for bit."""
+    import torch
+    from paper_2402_12947_b200.mg import DeviceHierarchy
+    name, z, h = fx
+    b = torch.from_numpy(z["g/b"]).cuda()
+    res, launches = [], []
+    for overlap in (1, 0):
+        dh = DeviceHierarchy(h.levels, h.coarse_factor, use_graphs=graphs)
+        dh.set_option(2, overlap)
+        u = torch.from_numpy(z["g/u_rand"]).cuda()
+        dh.vcycle(b, u)
+        dh.vcycle(b, u)
+        res.append(u.cpu().numpy())
+        launches.append(dh.launches_per_vcycle())
+    assert np.array_equal(res[0], res[1])
+    has_lc = any(lv.local_correction is not None and lv.local_correction.regions
+                 for lv in h.levels)
+    if has_lc:  # the fixtures' halos are a few % of the rows: the split is active
+        assert launches[0] > launches[1]
+
+
 def test_iteration_counts(P, fx):
     name, z, h = fx
     b = z["g/b"]
