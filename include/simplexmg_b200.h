@@ -148,7 +148,8 @@ SMG_API int smg_hierarchy_set_graphs(smg_hierarchy *h, int enable);
  *   SMG_OPT_LC_OVERLAP      1 = run each local correction concurrently with the
  *                           patch-independent (interior) rows of the adjacent
  *                           smoother sweep; the halo rows follow (bit-identical,
- *                           default 1) */
+ *                           default 0: the extra halo launch and the fork/join
+ *                           cost more than the overlap saves on C1-C3) */
 #define SMG_OPT_GRAPHS 0
 #define SMG_OPT_FUSE_ZERO_GUESS 1
 #define SMG_OPT_LC_OVERLAP 2
@@ -160,6 +161,12 @@ SMG_API int smg_hierarchy_launches_per_vcycle(const smg_hierarchy *h, int64_t *l
 SMG_API int smg_vcycle(smg_hierarchy *h, const double *b, double *u, void *stream);
 /* same with HOST b/u: H2D copies, V-cycle, D2H of u (the e2e path)                */
 SMG_API int smg_vcycle_host(smg_hierarchy *h, const double *b_host, double *u_host, void *stream);
+/* count independent HOST (b[i], u[i]) pairs, one V-cycle each (u[i] in place),
+ * pipelined: the copies of neighbouring pairs overlap each V-cycle.  Pinned
+ * host memory gives the overlap; pageable memory is correct but serial.
+ * Returns after the last u[i] is written back.                                   */
+SMG_API int smg_vcycle_host_many(smg_hierarchy *h, int64_t count, const double *const *b_host,
+                                 double *const *u_host, void *stream);
 /* stationary MG (mg.py:154-175): u holds u0 on entry and the result on exit.
  * history: capacity max_cycles + 1 host doubles; *n_history entries written.  */
 SMG_API int smg_solve_stationary(smg_hierarchy *h, const double *b, double *u, double rtol,

@@ -60,6 +60,7 @@ PROTOTYPES = {
     "smg_hierarchy_launches_per_vcycle": (ctypes.c_int, [_vp, _i64p]),
     "smg_vcycle": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "smg_vcycle_host": (ctypes.c_int, [_vp, _f64p, _f64p, _vp]),
+    "smg_vcycle_host_many": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp]),
     "smg_solve_stationary": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_double, ctypes.c_int,
                                             _f64p, _intp, _vp]),
     "smg_cg": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int, ctypes.c_double, ctypes.c_int,

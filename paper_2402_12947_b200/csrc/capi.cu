@@ -304,7 +304,7 @@ struct Hierarchy {
   int64_t bytes = 0;
   bool use_graphs = true;
   bool fuse_zero_guess = true;
-  bool lc_overlap = true;
+  bool lc_overlap = false;  // measured slower: opt-in
   cudaStream_t side = nullptr;       // local corrections overlapping interior sweeps
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   std::map<std::pair<const void*, void*>, cudaGraphExec_t> graphs;
@@ -312,6 +312,10 @@ struct Hierarchy {
   int64_t launches = 0;
   double* stage_b = nullptr;  // device copies for the host-buffer path
   double* stage_u = nullptr;
+  double* stage_b2 = nullptr;  // second staging slot (pipelined host path)
+  double* stage_u2 = nullptr;
+  cudaStream_t copy_in = nullptr, copy_out = nullptr;
+  cudaEvent_t pipe_ev[6] = {};
   DotScratch dots;
 
   ~Hierarchy()
@@ -321,6 +325,10 @@ struct Hierarchy {
     if (side) cudaStreamDestroy(side);
     if (fork_ev) cudaEventDestroy(fork_ev);
     if (join_ev) cudaEventDestroy(join_ev);
+    if (copy_in) cudaStreamDestroy(copy_in);
+    if (copy_out) cudaStreamDestroy(copy_out);
+    for (cudaEvent_t e : pipe_ev)
+      if (e) cudaEventDestroy(e);
     dots.release();
     free_all(allocs);
   }
@@ -950,6 +958,16 @@ int smg_correction_create(const smg_operator* a, int64_t n_regions, const int64_
     if (rc == SMG_OK) rc = dev_upload(c.allocs, c.device_bytes, dof32.data(), dof32.size(), &dd);
     if (rc == SMG_OK) rc = dev_upload(c.allocs, c.device_bytes, poff.data(), poff.size(), &df);
     if (rc == SMG_OK) rc = dev_upload(c.allocs, c.device_bytes, packed.data(), packed.size(), &dl);
+    if (rc == SMG_OK) {
+      std::vector<int32_t> ord((size_t)n_regions);
+      for (int64_t r = 0; r < n_regions; ++r) ord[(size_t)r] = (int32_t)r;
+      std::stable_sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) {
+        return roff[x + 1] - roff[x] > roff[y + 1] - roff[y];
+      });
+      int32_t* dord = nullptr;
+      rc = dev_upload(c.allocs, c.device_bytes, ord.data(), ord.size(), &dord);
+      c.order = dord;
+    }
     if (rc == SMG_OK) rc = dev_alloc(c.allocs, c.device_bytes, (size_t)m, &c.rbuf);
     // gathered copy of the patch rows of A (residuals read it coalesced)
     int64_t* dlen = nullptr;
@@ -1186,6 +1204,52 @@ int smg_vcycle_host(smg_hierarchy* h, const double* b_host, double* u_host, void
   SMG_CUDA(cudaMemcpyAsync(H.stage_u, u_host, bytes, cudaMemcpyHostToDevice, st));
   SMG_TRY(run_vcycle(H, H.stage_b, H.stage_u, st));
   SMG_CUDA(cudaMemcpyAsync(u_host, H.stage_u, bytes, cudaMemcpyDeviceToHost, st));
+  SMG_CUDA(cudaStreamSynchronize(st));
+  return SMG_OK;
+}
+
+// Independent (b, u) pairs in host memory, one V-cycle each, pipelined: the
+// H2D copies of pair i+1 (copy-in stream) and the D2H copy of pair i-1
+// (copy-out stream) overlap the V-cycle of pair i (two staging slots).
+int smg_vcycle_host_many(smg_hierarchy* h, int64_t count, const double* const* b_host,
+                         double* const* u_host, void* stream)
+{
+  if (!h) return fail("hierarchy is NULL");
+  if (count < 0) return fail("negative count");
+  if (count > 0 && (!b_host || !u_host)) return fail("NULL host pointer arrays");
+  Hierarchy& H = h->h;
+  cudaStream_t st = as_stream(stream);
+  if (!H.stage_b2) {
+    SMG_TRY(dev_alloc(H.allocs, H.bytes, (size_t)H.lv[0].n, &H.stage_b2));
+    SMG_TRY(dev_alloc(H.allocs, H.bytes, (size_t)H.lv[0].n, &H.stage_u2));
+    SMG_CUDA(cudaStreamCreateWithFlags(&H.copy_in, cudaStreamNonBlocking));
+    SMG_CUDA(cudaStreamCreateWithFlags(&H.copy_out, cudaStreamNonBlocking));
+    for (cudaEvent_t& e : H.pipe_ev) SMG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  double* sb[2] = {H.stage_b, H.stage_b2};
+  double* su[2] = {H.stage_u, H.stage_u2};
+  cudaEvent_t* in_done = H.pipe_ev;       // per slot: H2D finished
+  cudaEvent_t* out_done = H.pipe_ev + 2;  // per slot: D2H finished (slot free)
+  cudaEvent_t start = H.pipe_ev[4];
+  const size_t bytes = sizeof(double) * (size_t)H.lv[0].n;
+  // the copies must follow whatever the caller queued on its stream
+  SMG_CUDA(cudaEventRecord(start, st));
+  SMG_CUDA(cudaStreamWaitEvent(H.copy_in, start, 0));
+  SMG_CUDA(cudaStreamWaitEvent(H.copy_out, start, 0));
+  for (int64_t i = 0; i < count; ++i) {
+    const int s = (int)(i & 1);
+    if (i >= 2) SMG_CUDA(cudaStreamWaitEvent(H.copy_in, out_done[s], 0));
+    SMG_CUDA(cudaMemcpyAsync(sb[s], b_host[i], bytes, cudaMemcpyHostToDevice, H.copy_in));
+    SMG_CUDA(cudaMemcpyAsync(su[s], u_host[i], bytes, cudaMemcpyHostToDevice, H.copy_in));
+    SMG_CUDA(cudaEventRecord(in_done[s], H.copy_in));
+    SMG_CUDA(cudaStreamWaitEvent(st, in_done[s], 0));
+    SMG_TRY(run_vcycle(H, sb[s], su[s], st));
+    SMG_CUDA(cudaEventRecord(H.pipe_ev[5], st));
+    SMG_CUDA(cudaStreamWaitEvent(H.copy_out, H.pipe_ev[5], 0));
+    SMG_CUDA(cudaMemcpyAsync(u_host[i], su[s], bytes, cudaMemcpyDeviceToHost, H.copy_out));
+    SMG_CUDA(cudaEventRecord(out_done[s], H.copy_out));
+  }
+  SMG_CUDA(cudaStreamSynchronize(H.copy_out));
   SMG_CUDA(cudaStreamSynchronize(st));
   return SMG_OK;
 }

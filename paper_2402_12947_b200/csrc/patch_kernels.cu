@@ -87,6 +87,14 @@ constexpr int kProdItems = kProdCap / kSolveThreads;
 constexpr int64_t kSmemBudget = 220 * 1024;    // dynamic smem per CTA (of 227 KB)
 
 enum PatchMode : int { kAddResidualSolve = 0, kSolveFromBuf = 1, kResidualOnly = 2 };
+constexpr int kFlagStream = 1;      // factors larger than shared memory stream through a ring
+constexpr int kFlagL2Prefetch = 2;  // ... after an L2 prefetch of the whole factor
+
+static int patch_env(const char* name, int dflt)
+{
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
 
 static bool nostream_env()
 {
@@ -312,20 +320,23 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
              const int32_t* __restrict__ dofs,
              const int64_t* __restrict__ foff, const double* __restrict__ lfac,
              const double* __restrict__ b, const double* u_res, double* rbuf, double* target,
-             int scatter_add, int nmax, int allow_stream)
+             int scatter_add, int nmax, int flags, const int32_t* __restrict__ order)
 {
+  const bool allow_stream = (flags & kFlagStream) != 0;
   extern __shared__ __align__(16) unsigned char psm[];
   __shared__ double s_red[kSolveWarps][32];
   __shared__ uint64_t s_bar;
   __shared__ uint64_t s_ring_bar[kRingStages];
   __shared__ uint64_t s_dinv_bar[2];
-  const PatchSmem L_ = patch_smem_layout(nmax, allow_stream != 0);
+  const PatchSmem L_ = patch_smem_layout(nmax, allow_stream);
   double* s_x = reinterpret_cast<double*>(psm + L_.x_off);
   int32_t* s_off = reinterpret_cast<int32_t*>(psm + L_.off_off);
   double* s_prod = reinterpret_cast<double*>(psm + L_.prod_off);
   double* s_L = reinterpret_cast<double*>(psm + L_.l_off);
 
-  const int p = blockIdx.x;
+  // regions run largest first (order, built at upload) so the long solves
+  // start in the first wave and the short ones fill in behind them
+  const int p = order ? order[blockIdx.x] : (int)blockIdx.x;
   const int32_t k0 = pptr[p];
   const int n = pptr[p + 1] - k0;
   const int lane = threadIdx.x & 31;
@@ -337,6 +348,21 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   // bulk copy stages the whole factor while the residual is formed
   if (staged && threadIdx.x == 0)
     factor_bulk_load(s_L, Lg, (uint32_t)(nslot * 8), &s_bar);
+  // a factor streamed through the ring: pull all of it towards L2 now, so the
+  // ring's dependent copies hit L2 instead of paying HBM latency one chunk at
+  // a time (the slot is contiguous, 16-byte aligned, even length)
+  if (!staged && kMode != kResidualOnly && L_.stage > 0 && (flags & kFlagL2Prefetch) &&
+      warp == 0) {
+    const int64_t total = nslot * 8;
+    constexpr int64_t kPiece = 32 * 1024;
+    for (int64_t off = (int64_t)lane * kPiece; off < total; off += 32 * kPiece) {
+      const int64_t len = total - off < kPiece ? total - off : kPiece;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                       reinterpret_cast<const char*>(Lg) + off),
+                   "r"((uint32_t)len)
+                   : "memory");
+    }
+  }
   // every thread may only wait on the barrier after thread 0 has initialised it
   __syncthreads();
 
@@ -562,8 +588,12 @@ static cudaError_t launch_patch(const Correction& c, size_t smem, const double* 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  static const int l2pf = patch_env("SMG_PATCH_L2PF", 1);
+  static const int lpt = patch_env("SMG_PATCH_LPT", 1);
+  const int flags = (allow_stream ? kFlagStream : 0) | (l2pf ? kFlagL2Prefetch : 0);
   return cudaLaunchKernelEx(&cfg, patch_kernel<kMode>, c.prow, c.pcol, c.pval, c.pptr, c.dofs,
-                            c.foff, c.lfac, b, u_res, c.rbuf, tgt, add, c.max_dofs, allow_stream);
+                            c.foff, c.lfac, b, u_res, c.rbuf, tgt, add, c.max_dofs, flags,
+                            lpt ? c.order : (const int32_t*)nullptr);
 }
 
 // residual-only pass (coupled regions): rbuf[k] = (b - A u)[dofs[k]]

@@ -56,6 +56,7 @@ struct Correction {
   int32_t max_dofs = 0;
   const int32_t* pptr = nullptr;   // n_regions + 1
   const int32_t* dofs = nullptr;   // m (global dof of each patch slot)
+  const int32_t* order = nullptr;  // n_regions: launch order, largest region first
   const int64_t* foff = nullptr;   // n_regions + 1, offsets into packed factors
   const double* lfac = nullptr;    // packed lower factors, row-major
   double* rbuf = nullptr;          // m scratch (patch residual / correction)

@@ -247,7 +247,12 @@ static cudaError_t launch_t(const DevCsr& m, const double* x, const EpiArgs& ea,
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = env_flag(g_pdl, "SMG_PDL", 1) ? 1 : 0;
-  const int dist = g_sm_count * kMinBlocks;  // one resident wave ahead
+  static const int waves = [] {
+    const char* v = getenv("SMG_PF_WAVES");
+    const int w = v ? atoi(v) : 1;
+    return w > 0 ? w : 1;
+  }();
+  const int dist = g_sm_count * kMinBlocks * waves;  // resident waves ahead (default one)
   if (env_flag(g_prefetch, "SMG_L2_PREFETCH", 1))
     return cudaLaunchKernelEx(&cfg, csr_tile_kernel<E, true>, m, x, ea, dist);
   return cudaLaunchKernelEx(&cfg, csr_tile_kernel<E, false>, m, x, ea, dist);

@@ -211,6 +211,26 @@ class DeviceHierarchy:
                                        u.ctypes.data_as(_f64p), _dev.stream_handle()))
         return u
 
+    def vcycles_host(self, bs, us):
+        """One V-cycle on each independent host pair (bs[i], us[i]), us[i] in
+        place, with the host<->device copies of neighbouring pairs overlapping
+        each V-cycle (smg_vcycle_host_many; pinned arrays give the overlap)."""
+        n0 = self.n[0]
+        if len(bs) != len(us):
+            raise ValueError("dimension mismatch: bs and us differ in length")
+        for b, u in zip(bs, us):
+            for name, a in (("b", b), ("u", u)):
+                if not (isinstance(a, np.ndarray) and a.dtype == np.float64
+                        and a.flags.c_contiguous and a.shape == (n0,)):
+                    raise ValueError(f"{name} must be a contiguous float64 array of "
+                                     f"{n0} dofs (dimension mismatch)")
+        cnt = len(bs)
+        bp = (ctypes.c_void_p * max(cnt, 1))(*[b.ctypes.data for b in bs])
+        up = (ctypes.c_void_p * max(cnt, 1))(*[u.ctypes.data for u in us])
+        _lib.check(_lib.load().smg_vcycle_host_many(self.handle, cnt, bp, up,
+                                                    _dev.stream_handle()))
+        return us
+
     def solve_stationary(self, b, u0, rtol: float = 1e-10, max_cycles: int = 100):
         n0 = self.n[0]
         t = _dev.torch()

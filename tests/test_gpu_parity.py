@@ -174,6 +174,29 @@ def test_lc_overlap_is_bitwise(P, fx, graphs):
         assert launches[0] > launches[1]
 
 
+def test_pipelined_host_vcycles_match_single_calls(P, fx):
+    """smg_vcycle_host_many (copies overlapping V-cycles, two staging slots)
+    gives every pair exactly the single-call result."""
+    import torch
+    from paper_2402_12947_b200.mg import DeviceHierarchy
+    name, z, h = fx
+    n = h.levels[0].a.nrows
+    dh = DeviceHierarchy(h.levels, h.coarse_factor)
+    rng = np.random.default_rng(11)
+    bs = [torch.from_numpy(rng.standard_normal(n)).pin_memory().numpy() for _ in range(5)]
+    us = [torch.from_numpy(rng.standard_normal(n)).pin_memory().numpy() for _ in range(5)]
+    expect = []
+    for b, u in zip(bs, us):
+        ud = torch.from_numpy(u.copy()).cuda()
+        dh.vcycle(torch.from_numpy(b).cuda(), ud)
+        expect.append(ud.cpu().numpy())
+    dh.vcycles_host(bs, us)
+    for u, e in zip(us, expect):
+        assert np.array_equal(u, e)
+    with pytest.raises(ValueError, match="dimension mismatch"):
+        dh.vcycles_host(bs[:2], us[:1])
+
+
 def test_iteration_counts(P, fx):
     name, z, h = fx
     b = z["g/b"]
