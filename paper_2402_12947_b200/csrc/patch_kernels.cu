@@ -90,6 +90,21 @@ enum PatchMode : int { kAddResidualSolve = 0, kSolveFromBuf = 1, kResidualOnly =
 constexpr int kFlagStream = 1;      // factors larger than shared memory stream through a ring
 constexpr int kFlagL2Prefetch = 2;  // ... after an L2 prefetch of the whole factor
 
+// Phase timestamps (SM clock) of the first 256 CTAs, compiled in only for the
+// tools/trace_patch.py build (-DSMG_PATCH_TRACE); no cost otherwise.
+#ifdef SMG_PATCH_TRACE
+__device__ unsigned long long g_patch_trace[256][8];
+#define PTRACE(k)                                                  \
+  do {                                                             \
+    if (threadIdx.x == 0 && blockIdx.x < 256)                      \
+      g_patch_trace[blockIdx.x][k] = (unsigned long long)clock64(); \
+  } while (0)
+#else
+#define PTRACE(k) \
+  do {            \
+  } while (0)
+#endif
+
 static int patch_env(const char* name, int dflt)
 {
   const char* v = getenv(name);
@@ -323,6 +338,7 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
              int scatter_add, int nmax, int flags, const int32_t* __restrict__ order)
 {
   const bool allow_stream = (flags & kFlagStream) != 0;
+  PTRACE(0);
   extern __shared__ __align__(16) unsigned char psm[];
   __shared__ double s_red[kSolveWarps][32];
   __shared__ uint64_t s_bar;
@@ -393,6 +409,7 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
     };
     load_chunk(0, min(kProdCap, total));
     patch_pdl_wait();
+    PTRACE(1);
     __syncthreads();
     for (int c0 = 0; c0 < total; c0 += kProdCap) {
       const int cnt = min(kProdCap, total - c0);
@@ -418,6 +435,7 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
       else
         s_x[i] = r;
     }
+    PTRACE(2);
     if (kMode == kResidualOnly) return;
   } else {
     patch_pdl_wait();
@@ -425,6 +443,7 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   }
   if (staged) factor_wait(&s_bar);
   __syncthreads();
+  PTRACE(3);
   const double* L = staged ? s_L : Lg;
   const double* Dinv = L + patch_tri_even(n);   // inverted diagonal blocks, row stride 33
 
@@ -458,6 +477,7 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
     __syncthreads();
   }
 
+  PTRACE(4);
   // ---- backward: L^T x = y (panels from the bottom)
   const int last = ((n - 1) / 32) * 32;
   for (int p0 = last; p0 >= 0; p0 -= 32) {
@@ -492,6 +512,7 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   }
 
   }  // generic (staged / global) path
+  PTRACE(5);
 
   for (int i = threadIdx.x; i < n; i += kSolveThreads) {
     const int32_t g = dofs[k0 + i];
@@ -500,6 +521,7 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
     else
       target[g] = s_x[i];
   }
+  PTRACE(6);
 }
 
 // upload-time helpers: bounds of the patch rows, then their (col, val) copy
@@ -588,7 +610,7 @@ static cudaError_t launch_patch(const Correction& c, size_t smem, const double* 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  static const int l2pf = patch_env("SMG_PATCH_L2PF", 1);
+  static const int l2pf = patch_env("SMG_PATCH_L2PF", 0);  // measured slower on C5 (222 vs 240 us)
   static const int lpt = patch_env("SMG_PATCH_LPT", 1);
   const int flags = (allow_stream ? kFlagStream : 0) | (l2pf ? kFlagL2Prefetch : 0);
   return cudaLaunchKernelEx(&cfg, patch_kernel<kMode>, c.prow, c.pcol, c.pval, c.pptr, c.dofs,
@@ -646,3 +668,10 @@ cudaError_t configure_patch_solve_smem(const Correction& c)
 }
 
 }  // namespace smg
+
+#ifdef SMG_PATCH_TRACE
+extern "C" __attribute__((visibility("default"))) int smg_debug_patch_trace(unsigned long long* out)
+{
+  return (int)cudaMemcpyFromSymbol(out, smg::g_patch_trace, sizeof(smg::g_patch_trace));
+}
+#endif
