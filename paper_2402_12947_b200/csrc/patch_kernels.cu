@@ -82,6 +82,37 @@ __host__ __device__ __forceinline__ int64_t tri(int64_t i) { return i * (i + 1) 
 
 constexpr int kSolveThreads = 256;
 constexpr int kSolveWarps = kSolveThreads / 32;
+static_assert(kSolveWarps * 4 == 32, "panel_gemv splits a 32-wide panel over the warps");
+
+// x[0:pn] <- D x (or D^T x) for one inverted 32x32 diagonal block D (row
+// stride kDinvLd; zero-padded).  All threads: warp w forms the partial sums
+// over columns [4w, 4w+4), then one thread per row adds the eight partials --
+// dependency depth 4 + 8 instead of a 32-step chain in one warp.  Called with
+// x ready (after a barrier); returns after a barrier.
+__device__ __forceinline__ void panel_gemv(const double* D, double* x, int pn, bool transposed,
+                                           double (*red)[32])
+{
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  double acc = 0.0;
+  if (lane < pn) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = warp * 4 + q;
+      if (j < pn) acc += (transposed ? D[j * kDinvLd + lane] : D[lane * kDinvLd + j]) * x[j];
+    }
+  }
+  red[warp][lane] = acc;
+  __syncthreads();
+  if (threadIdx.x < pn) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < kSolveWarps; ++w) t += red[w][threadIdx.x];
+    x[threadIdx.x] = t;
+  }
+  __syncthreads();
+}
+
 constexpr int kProdCap = 2048;                 // residual products staged per pass
 constexpr int kProdItems = kProdCap / kSolveThreads;
 constexpr int64_t kSmemBudget = 220 * 1024;    // dynamic smem per CTA (of 227 KB)
@@ -111,6 +142,7 @@ static int patch_env(const char* name, int dflt)
   return v ? atoi(v) : dflt;
 }
 
+
 static bool nostream_env()
 {
   const char* v = getenv("SMG_PATCH_NOSTREAM");
@@ -120,13 +152,14 @@ static bool nostream_env()
 // shared-memory carve-up for a region of at most nmax dofs
 struct PatchSmem {
   int64_t x_off, lo_off, off_off, prod_off, l_off, tri_cap, bytes;
-  int64_t stage;   // > 0: streaming ring of 2 stages of `stage` doubles at l_off
+  int64_t stage;   // > 0: streaming ring of tri_cap doubles at l_off (stage = longest chunk)
 };
 
 constexpr int kChunkRows = 8;   // factor rows per streamed chunk (divides the 32-row panel)
-constexpr int kRingStages = 2;  // chunks in flight per CTA (4 x 4-row chunks measured slower)
+constexpr int kRingStages = 2;  // default ring capacity, in longest chunks
 
-__host__ __device__ inline PatchSmem patch_smem_layout(int nmax, bool allow_stream = true)
+__host__ __device__ inline PatchSmem patch_smem_layout(int nmax, bool allow_stream = true,
+                                                       int ring_chunks = kRingStages)
 {
   PatchSmem p;
   const int64_t n2 = (nmax + 2) & ~int64_t(1);
@@ -144,19 +177,29 @@ __host__ __device__ inline PatchSmem patch_smem_layout(int nmax, bool allow_stre
   if (need <= cap || !allow_stream) {  // every region's slot (factor + inverted blocks) fits: stage it whole
     p.tri_cap = need;
     p.bytes = p.l_off + 8 * need;
-  } else {            // stream factor rows through a 2-stage ring (smaller regions still staged)
+  } else {            // stream factor rows through a ring (smaller regions still staged)
     p.stage = ((int64_t)kChunkRows * (nmax + 2) + 1) & ~int64_t(1);
-    p.tri_cap = kRingStages * p.stage;
+    p.tri_cap = (ring_chunks > 1 ? ring_chunks : 2) * p.stage;
     p.bytes = p.l_off + 8 * p.tri_cap;
   }
   return p;
+}
+
+// ring capacity of the streamed solves, in longest chunks (SMG_PATCH_RING)
+static int ring_chunks()
+{
+  static const int r = [] {
+    const int v = patch_env("SMG_PATCH_RING", kRingStages);
+    return v < 2 ? 2 : (v > 24 ? 24 : v);
+  }();
+  return r;
 }
 
 // ---------------------------------------------------------------------------
 // Streaming triangular solves for regions whose factor does not fit in shared
 // memory (C5: 64..512-dof patches).  Row chunks of kChunkRows factor rows --
 // contiguous in the packed row-major layout -- flow HBM -> smem through a
-// kRingStages-deep bulk-copy ring.  Forward: left-looking (chunk rows against the
+// bulk-copy byte ring (ring_fill).  Forward: left-looking (chunk rows against the
 // solved prefix), then the panel's inverted diagonal block.  Backward:
 // right-looking from the last panel (inverted block first, then the panel's
 // rows update the unsolved prefix), so both passes stream the same row chunks.
@@ -201,23 +244,63 @@ __device__ __forceinline__ int n_chunks(int n)
   return (nb - 1) * (kPanel / kChunkRows) + (pn_last + kChunkRows - 1) / kChunkRows;
 }
 
-__device__ __forceinline__ void ring_issue(const double* Lg, double* ring, int64_t stage, int n,
-                                           int seq, uint64_t* bars)
+// Factor rows stream through a byte ring: chunks have the size of their rows
+// (short near the top of L, long near the bottom), are packed contiguously and
+// wrap to the ring start when they do not fit before its end.  Thread 0 keeps
+// as many chunks in flight as fit (at most kRingSlots), so the bytes in flight
+// per CTA track the ring size rather than the longest chunk.
+constexpr int kRingSlots = 16;
+
+struct RingProducer {  // thread 0's private state
+  int next = 0;        // next chunk to issue
+  int consumed = 0;    // chunks fully consumed (their ring space is free)
+  int64_t head = 0;    // ring offset (doubles) where the next chunk would go
+};
+
+__device__ __forceinline__ void chunk_range(int seq, int n, int64_t* a, int64_t* b)
 {
   const ChunkInfo c = chunk_of(seq, n);
-  const int64_t a = tri(c.i0) & ~int64_t(1);
-  const int64_t b = (tri(c.i0 + c.rows) + 1) & ~int64_t(1);
-  const int s = seq % kRingStages;
-  uint64_t* bar = &bars[s];
-  const uint32_t bytes = (uint32_t)((b - a) * 8);
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(psmem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(psmem_u32(ring + s * stage)),
-      "l"(Lg + a), "r"(bytes), "r"(psmem_u32(bar))
-      : "memory");
+  *a = tri(c.i0) & ~int64_t(1);
+  *b = (tri(c.i0 + c.rows) + 1) & ~int64_t(1);
+}
+
+__device__ __forceinline__ void ring_fill(RingProducer& rp, const double* Lg, double* ring,
+                                          int64_t cap, int n, int total, uint64_t* bars,
+                                          int32_t* coff)
+{
+  while (rp.next < total && rp.next - rp.consumed < kRingSlots) {
+    int64_t a, b;
+    chunk_range(rp.next, n, &a, &b);
+    const int64_t size = b - a;
+    int64_t pos;
+    if (rp.next == rp.consumed) {  // ring empty
+      pos = 0;
+    } else {
+      const int64_t tail = coff[rp.consumed % kRingSlots];
+      if (tail < rp.head) {        // occupied [tail, head)
+        if (rp.head + size <= cap) pos = rp.head;
+        else if (size <= tail) pos = 0;
+        else break;
+      } else {                     // occupied [tail, cap) + [0, head)
+        if (rp.head + size <= tail) pos = rp.head;
+        else break;
+      }
+    }
+    const int slot = rp.next % kRingSlots;
+    coff[slot] = (int32_t)pos;
+    uint64_t* bar = &bars[slot];
+    const uint32_t bytes = (uint32_t)(size * 8);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(psmem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(psmem_u32(ring + pos)),
+        "l"(Lg + a), "r"(bytes), "r"(psmem_u32(bar))
+        : "memory");
+    rp.head = pos + size;
+    ++rp.next;
+  }
 }
 
 __device__ __forceinline__ void ring_wait(uint64_t* bar, uint32_t parity)
@@ -251,8 +334,9 @@ __device__ __forceinline__ void dinv_issue(const double* Dinv, double* s_dinv, i
       : "memory");
 }
 
-__device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_t stage, int n,
-                             double* s_x, double* s_dinv, uint64_t* bars, uint64_t* dbars)
+__device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_t cap, int n,
+                             double* s_x, double* s_dinv, uint64_t* bars, int32_t* coff,
+                             uint64_t* dbars, double (*red)[32])
 {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -261,32 +345,21 @@ __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_
   const int C = n_chunks(n);
   const int total = 2 * C;
   int dq = 0;  // next inverted block to consume
+  RingProducer rp;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kRingStages; ++s)
+    for (int s = 0; s < kRingSlots; ++s)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(psmem_u32(&bars[s])) : "memory");
     for (int s = 0; s < 2; ++s)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(psmem_u32(&dbars[s])) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int q = 0; q < kRingStages && q < total; ++q) ring_issue(Lg, ring, stage, n, q, bars);
+    ring_fill(rp, Lg, ring, cap, n, total, bars, coff);
     for (int q = 0; q < 2 && q < 2 * nb; ++q) dinv_issue(Dinv, s_dinv, q, nb, dbars);
   }
   __syncthreads();
   // consume block dq: wait, x_P = inv(L_PP) r_P (forward) or inv(L_PP)^T y_P (backward)
   auto panel_solve = [&](int p0, int pn, bool transposed) {
     ring_wait(&dbars[dq & 1], (uint32_t)((dq >> 1) & 1));
-    if (warp == 0) {
-      const double* D = s_dinv + (dq & 1) * kDinvBlock;
-      double acc = 0.0;
-      if (lane < pn) {
-        if (transposed)
-          for (int j = 0; j < pn; ++j) acc += D[j * kDinvLd + lane] * s_x[p0 + j];
-        else
-          for (int j = 0; j < pn; ++j) acc += D[lane * kDinvLd + j] * s_x[p0 + j];
-      }
-      __syncwarp();
-      if (lane < pn) s_x[p0 + lane] = acc;
-    }
-    __syncthreads();
+    panel_gemv(s_dinv + (dq & 1) * kDinvBlock, s_x + p0, pn, transposed, red);
     if (threadIdx.x == 0 && dq + 2 < 2 * nb) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       dinv_issue(Dinv, s_dinv, dq + 2, nb, dbars);
@@ -298,9 +371,10 @@ __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_
     const int p0 = c.panel * kPanel;
     const int pn = min(kPanel, n - p0);
     const bool fwd = seq < C;
+    if (seq == C) PTRACE(4);
     if (!fwd && c.i0 == p0) panel_solve(p0, pn, true);   // backward: own block first
-    ring_wait(&bars[seq % kRingStages], (uint32_t)((seq / kRingStages) & 1));
-    const double* rows = ring + (seq % kRingStages) * stage + (tri(c.i0) & 1) - tri(c.i0);
+    ring_wait(&bars[seq % kRingSlots], (uint32_t)((seq / kRingSlots) & 1));
+    const double* rows = ring + coff[seq % kRingSlots] + (tri(c.i0) & 1) - tri(c.i0);
     if (fwd) {
       // x_i -= L[i, 0:p0] . x[0:p0] for the chunk's rows (one warp per row)
       if (warp < c.rows && p0 > 0) {
@@ -320,9 +394,10 @@ __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_
       }
     }
     __syncthreads();
-    if (threadIdx.x == 0 && seq + kRingStages < total) {
+    if (threadIdx.x == 0) {  // chunk seq's space is free: refill the ring
+      rp.consumed = seq + 1;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      ring_issue(Lg, ring, stage, n, seq + kRingStages, bars);
+      ring_fill(rp, Lg, ring, cap, n, total, bars, coff);
     }
     if (fwd && c.i0 + c.rows == p0 + pn) panel_solve(p0, pn, false);  // forward: panel done
   }
@@ -342,9 +417,10 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   extern __shared__ __align__(16) unsigned char psm[];
   __shared__ double s_red[kSolveWarps][32];
   __shared__ uint64_t s_bar;
-  __shared__ uint64_t s_ring_bar[kRingStages];
+  __shared__ uint64_t s_ring_bar[kRingSlots];
+  __shared__ int32_t s_ring_off[kRingSlots];
   __shared__ uint64_t s_dinv_bar[2];
-  const PatchSmem L_ = patch_smem_layout(nmax, allow_stream);
+  const PatchSmem L_ = patch_smem_layout(nmax, allow_stream, flags >> 8);
   double* s_x = reinterpret_cast<double*>(psm + L_.x_off);
   int32_t* s_off = reinterpret_cast<int32_t*>(psm + L_.off_off);
   double* s_prod = reinterpret_cast<double*>(psm + L_.prod_off);
@@ -360,6 +436,17 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   const int64_t nslot = patch_slot_doubles(n);
   const bool staged = kMode != kResidualOnly && nslot <= L_.tri_cap;
   const double* __restrict__ Lg = lfac + foff[p];
+  // this thread's own patch dof (rows < kSolveThreads): b and the scatter
+  // target there are fetched right after the dependency wait, off the
+  // residual's and the scatter's critical paths
+  const int32_t g_own = threadIdx.x < n ? dofs[k0 + threadIdx.x] : 0;
+  double b_own = 0.0, t_own = 0.0;
+  auto fetch_own = [&]() {
+    if (threadIdx.x < n) {
+      if (kMode != kSolveFromBuf) b_own = b[g_own];
+      if (kMode != kResidualOnly && scatter_add) t_own = target[g_own];
+    }
+  };
   // factors are stored at 16-byte aligned offsets with even lengths, so one
   // bulk copy stages the whole factor while the residual is formed
   if (staged && threadIdx.x == 0)
@@ -409,6 +496,7 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
     };
     load_chunk(0, min(kProdCap, total));
     patch_pdl_wait();
+    fetch_own();
     PTRACE(1);
     __syncthreads();
     for (int c0 = 0; c0 < total; c0 += kProdCap) {
@@ -429,7 +517,7 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
       __syncthreads();
     }
     for (int i = threadIdx.x; i < n; i += kSolveThreads) {
-      const double r = __dsub_rn(b[dofs[k0 + i]], s_x[i]);
+      const double r = __dsub_rn(i == (int)threadIdx.x ? b_own : b[dofs[k0 + i]], s_x[i]);
       if (kMode == kResidualOnly)
         rbuf[k0 + i] = r;
       else
@@ -439,7 +527,10 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
     if (kMode == kResidualOnly) return;
   } else {
     patch_pdl_wait();
+    fetch_own();
+    PTRACE(1);
     for (int i = threadIdx.x; i < n; i += kSolveThreads) s_x[i] = rbuf[k0 + i];
+    PTRACE(2);
   }
   if (staged) factor_wait(&s_bar);
   __syncthreads();
@@ -448,33 +539,29 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   const double* Dinv = L + patch_tri_even(n);   // inverted diagonal blocks, row stride 33
 
   if (!staged && L_.stage > 0) {
-    stream_solve(Lg, s_L, L_.stage, n, s_x, s_prod, s_ring_bar, s_dinv_bar);
+    stream_solve(Lg, s_L, L_.tri_cap, n, s_x, s_prod, s_ring_bar, s_ring_off, s_dinv_bar, s_red);
   } else {
 
   // ---- forward: L y = r (left-looking over 32-row panels)
   for (int p0 = 0; p0 < n; p0 += 32) {
     const int pn = min(32, n - p0);
     if (p0 > 0) {
-      for (int ii = warp; ii < pn; ii += kSolveWarps) {
-        const int i = p0 + ii;
-        const double* Li = L + tri(i);
-        double acc = 0.0;
-        for (int j = lane; j < p0; j += 32) acc += Li[j] * s_x[j];
-        acc = warp_sum(acc);
-        if (lane == 0) s_x[i] -= acc;
+      // x_i -= L[i, 0:p0] . x[0:p0] for the panel's rows: 8 lanes per row,
+      // all 32 rows at once
+      const int r = threadIdx.x >> 3, sub = threadIdx.x & 7;
+      double acc = 0.0;
+      if (r < pn) {
+        const double* Li = L + tri(p0 + r);
+        for (int j = sub; j < p0; j += 8) acc += Li[j] * s_x[j];
       }
+      acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      if (r < pn && sub == 0) s_x[p0 + r] -= acc;
       __syncthreads();
     }
-    if (warp == 0) {
-      // x_P = inv(L_PP) r_P: a 32-wide GEMV with the precomputed inverse block
-      const double* D = Dinv + (p0 / kPanel) * kDinvBlock;
-      double acc = 0.0;
-      if (lane < pn)
-        for (int j = 0; j < pn; ++j) acc += D[lane * kDinvLd + j] * s_x[p0 + j];
-      __syncwarp();
-      if (lane < pn) s_x[p0 + lane] = acc;
-    }
-    __syncthreads();
+    // x_P = inv(L_PP) r_P with the precomputed inverse block
+    panel_gemv(Dinv + (p0 / kPanel) * kDinvBlock, s_x + p0, pn, false, s_red);
   }
 
   PTRACE(4);
@@ -499,25 +586,18 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
       }
       __syncthreads();
     }
-    if (warp == 0) {
-      // x_P = inv(L_PP)^T y_P
-      const double* D = Dinv + (p0 / kPanel) * kDinvBlock;
-      double acc = 0.0;
-      if (lane < pn)
-        for (int j = 0; j < pn; ++j) acc += D[j * kDinvLd + lane] * s_x[p0 + j];
-      __syncwarp();
-      if (lane < pn) s_x[p0 + lane] = acc;
-    }
-    __syncthreads();
+    // x_P = inv(L_PP)^T y_P
+    panel_gemv(Dinv + (p0 / kPanel) * kDinvBlock, s_x + p0, pn, true, s_red);
   }
 
   }  // generic (staged / global) path
   PTRACE(5);
 
   for (int i = threadIdx.x; i < n; i += kSolveThreads) {
-    const int32_t g = dofs[k0 + i];
+    const bool own = i == (int)threadIdx.x;
+    const int32_t g = own ? g_own : dofs[k0 + i];
     if (scatter_add)
-      target[g] = __dadd_rn(target[g], s_x[i]);
+      target[g] = __dadd_rn(own ? t_own : target[g], s_x[i]);
     else
       target[g] = s_x[i];
   }
@@ -611,8 +691,9 @@ static cudaError_t launch_patch(const Correction& c, size_t smem, const double* 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   static const int l2pf = patch_env("SMG_PATCH_L2PF", 0);  // measured slower on C5 (222 vs 240 us)
+  const int ring = ring_chunks();
   static const int lpt = patch_env("SMG_PATCH_LPT", 1);
-  const int flags = (allow_stream ? kFlagStream : 0) | (l2pf ? kFlagL2Prefetch : 0);
+  const int flags = (allow_stream ? kFlagStream : 0) | (l2pf ? kFlagL2Prefetch : 0) | (ring << 8);
   return cudaLaunchKernelEx(&cfg, patch_kernel<kMode>, c.prow, c.pcol, c.pval, c.pptr, c.dofs,
                             c.foff, c.lfac, b, u_res, c.rbuf, tgt, add, c.max_dofs, flags,
                             lpt ? c.order : (const int32_t*)nullptr);
@@ -644,7 +725,7 @@ cudaError_t launch_patch_solve(const Correction& c, const double* b, const doubl
 {
   if (c.n_regions == 0) return cudaSuccess;
   const int st = nostream_env() ? 0 : 1;
-  const PatchSmem L = patch_smem_layout(c.max_dofs, st != 0);
+  const PatchSmem L = patch_smem_layout(c.max_dofs, st != 0, ring_chunks());
   double* tgt = u_add ? u_add : out_scatter;
   const int add = u_add ? 1 : 0;
   const size_t smem = (size_t)L.bytes + smem_pad();
@@ -654,7 +735,7 @@ cudaError_t launch_patch_solve(const Correction& c, const double* b, const doubl
 
 cudaError_t configure_patch_solve_smem(const Correction& c)
 {
-  const PatchSmem L = patch_smem_layout(c.max_dofs, !nostream_env());
+  const PatchSmem L = patch_smem_layout(c.max_dofs, !nostream_env(), ring_chunks());
   const int bytes = (int)(L.bytes + smem_pad());
   cudaError_t e = cudaFuncSetAttribute(patch_kernel<kAddResidualSolve>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);

@@ -43,7 +43,7 @@ def load_trace_lib():
     return lib
 
 
-def trace(lib, lc_host, a_host, label):
+def trace(lib, lc_host, a_host, label, apply=False):
     import torch
     from paper_2402_12947_b200 import device as D, _lib
     op = D.device_operator(a_host)
@@ -52,7 +52,11 @@ def trace(lib, lc_host, a_host, label):
     b = torch.randn(n, dtype=torch.float64, device="cuda")
     u = torch.randn(n, dtype=torch.float64, device="cuda")
     for _ in range(5):
-        _lib.check(lib.smg_local_correct(dc.handle, D.ptr(b), D.ptr(u), D.stream_handle()))
+        if apply:  # r -> S_c r (the C5 micro-benchmark's call)
+            _lib.check(lib.smg_apply_local_correction(dc.handle, D.ptr(b), D.ptr(u),
+                                                      D.stream_handle()))
+        else:
+            _lib.check(lib.smg_local_correct(dc.handle, D.ptr(b), D.ptr(u), D.stream_handle()))
     torch.cuda.synchronize()
     buf = np.zeros((256, 8), dtype=np.uint64)
     assert lib.smg_debug_patch_trace(buf.ctypes.data) == 0
@@ -75,7 +79,8 @@ def run(names):
             from paper_2402_12947_b200 import stencil
             a = stencil.p2_tet_laplacian(63)
             lc = bench.make_c5_patches(a.nrows)
-            out.append(trace(lib, lc, a, "c5 grid 63"))
+            out.append(trace(lib, lc, a, "c5 grid 63 (apply; phase 3->4 forward, 4->5 backward)",
+                             apply=True))
         else:
             from tests.golden import fixtures
             z, h = fixtures.load(name)
