@@ -152,14 +152,16 @@ static bool nostream_env()
 // shared-memory carve-up for a region of at most nmax dofs
 struct PatchSmem {
   int64_t x_off, lo_off, off_off, prod_off, l_off, tri_cap, bytes;
-  int64_t stage;   // > 0: streaming ring of tri_cap doubles at l_off (stage = longest chunk)
+  int64_t stage;   // > 0: streaming ring of kRingStages stages of `stage` doubles at l_off
 };
 
 constexpr int kChunkRows = 8;   // factor rows per streamed chunk (divides the 32-row panel)
-constexpr int kRingStages = 2;  // default ring capacity, in longest chunks
+// chunks in flight per CTA; measured best on C5: 2 x 8 rows (227 us) beat
+// 4 x 4 rows and a variable-size byte ring holding 2-4 longest chunks
+// (282-475 us: fewer CTAs per SM or more per-chunk overhead)
+constexpr int kRingStages = 2;
 
-__host__ __device__ inline PatchSmem patch_smem_layout(int nmax, bool allow_stream = true,
-                                                       int ring_chunks = kRingStages)
+__host__ __device__ inline PatchSmem patch_smem_layout(int nmax, bool allow_stream = true)
 {
   PatchSmem p;
   const int64_t n2 = (nmax + 2) & ~int64_t(1);
@@ -179,27 +181,17 @@ __host__ __device__ inline PatchSmem patch_smem_layout(int nmax, bool allow_stre
     p.bytes = p.l_off + 8 * need;
   } else {            // stream factor rows through a ring (smaller regions still staged)
     p.stage = ((int64_t)kChunkRows * (nmax + 2) + 1) & ~int64_t(1);
-    p.tri_cap = (ring_chunks > 1 ? ring_chunks : 2) * p.stage;
+    p.tri_cap = kRingStages * p.stage;
     p.bytes = p.l_off + 8 * p.tri_cap;
   }
   return p;
-}
-
-// ring capacity of the streamed solves, in longest chunks (SMG_PATCH_RING)
-static int ring_chunks()
-{
-  static const int r = [] {
-    const int v = patch_env("SMG_PATCH_RING", kRingStages);
-    return v < 2 ? 2 : (v > 24 ? 24 : v);
-  }();
-  return r;
 }
 
 // ---------------------------------------------------------------------------
 // Streaming triangular solves for regions whose factor does not fit in shared
 // memory (C5: 64..512-dof patches).  Row chunks of kChunkRows factor rows --
 // contiguous in the packed row-major layout -- flow HBM -> smem through a
-// bulk-copy byte ring (ring_fill).  Forward: left-looking (chunk rows against the
+// kRingStages-deep bulk-copy ring.  Forward: left-looking (chunk rows against the
 // solved prefix), then the panel's inverted diagonal block.  Backward:
 // right-looking from the last panel (inverted block first, then the panel's
 // rows update the unsolved prefix), so both passes stream the same row chunks.
@@ -244,63 +236,24 @@ __device__ __forceinline__ int n_chunks(int n)
   return (nb - 1) * (kPanel / kChunkRows) + (pn_last + kChunkRows - 1) / kChunkRows;
 }
 
-// Factor rows stream through a byte ring: chunks have the size of their rows
-// (short near the top of L, long near the bottom), are packed contiguously and
-// wrap to the ring start when they do not fit before its end.  Thread 0 keeps
-// as many chunks in flight as fit (at most kRingSlots), so the bytes in flight
-// per CTA track the ring size rather than the longest chunk.
-constexpr int kRingSlots = 16;
-
-struct RingProducer {  // thread 0's private state
-  int next = 0;        // next chunk to issue
-  int consumed = 0;    // chunks fully consumed (their ring space is free)
-  int64_t head = 0;    // ring offset (doubles) where the next chunk would go
-};
-
-__device__ __forceinline__ void chunk_range(int seq, int n, int64_t* a, int64_t* b)
+// chunk seq -> ring stage seq % kRingStages (one mbarrier per stage)
+__device__ __forceinline__ void ring_issue(const double* Lg, double* ring, int64_t stage, int n,
+                                           int seq, uint64_t* bars)
 {
   const ChunkInfo c = chunk_of(seq, n);
-  *a = tri(c.i0) & ~int64_t(1);
-  *b = (tri(c.i0 + c.rows) + 1) & ~int64_t(1);
-}
-
-__device__ __forceinline__ void ring_fill(RingProducer& rp, const double* Lg, double* ring,
-                                          int64_t cap, int n, int total, uint64_t* bars,
-                                          int32_t* coff)
-{
-  while (rp.next < total && rp.next - rp.consumed < kRingSlots) {
-    int64_t a, b;
-    chunk_range(rp.next, n, &a, &b);
-    const int64_t size = b - a;
-    int64_t pos;
-    if (rp.next == rp.consumed) {  // ring empty
-      pos = 0;
-    } else {
-      const int64_t tail = coff[rp.consumed % kRingSlots];
-      if (tail < rp.head) {        // occupied [tail, head)
-        if (rp.head + size <= cap) pos = rp.head;
-        else if (size <= tail) pos = 0;
-        else break;
-      } else {                     // occupied [tail, cap) + [0, head)
-        if (rp.head + size <= tail) pos = rp.head;
-        else break;
-      }
-    }
-    const int slot = rp.next % kRingSlots;
-    coff[slot] = (int32_t)pos;
-    uint64_t* bar = &bars[slot];
-    const uint32_t bytes = (uint32_t)(size * 8);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(psmem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-            "r"(psmem_u32(ring + pos)),
-        "l"(Lg + a), "r"(bytes), "r"(psmem_u32(bar))
-        : "memory");
-    rp.head = pos + size;
-    ++rp.next;
-  }
+  const int64_t a = tri(c.i0) & ~int64_t(1);
+  const int64_t b = (tri(c.i0 + c.rows) + 1) & ~int64_t(1);
+  const int s = seq % kRingStages;
+  uint64_t* bar = &bars[s];
+  const uint32_t bytes = (uint32_t)((b - a) * 8);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(psmem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(psmem_u32(ring + s * stage)),
+      "l"(Lg + a), "r"(bytes), "r"(psmem_u32(bar))
+      : "memory");
 }
 
 __device__ __forceinline__ void ring_wait(uint64_t* bar, uint32_t parity)
@@ -334,9 +287,9 @@ __device__ __forceinline__ void dinv_issue(const double* Dinv, double* s_dinv, i
       : "memory");
 }
 
-__device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_t cap, int n,
-                             double* s_x, double* s_dinv, uint64_t* bars, int32_t* coff,
-                             uint64_t* dbars, double (*red)[32])
+__device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_t stage, int n,
+                             double* s_x, double* s_dinv, uint64_t* bars, uint64_t* dbars,
+                             double (*red)[32])
 {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -345,14 +298,13 @@ __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_
   const int C = n_chunks(n);
   const int total = 2 * C;
   int dq = 0;  // next inverted block to consume
-  RingProducer rp;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kRingSlots; ++s)
+    for (int s = 0; s < kRingStages; ++s)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(psmem_u32(&bars[s])) : "memory");
     for (int s = 0; s < 2; ++s)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(psmem_u32(&dbars[s])) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    ring_fill(rp, Lg, ring, cap, n, total, bars, coff);
+    for (int q = 0; q < kRingStages && q < total; ++q) ring_issue(Lg, ring, stage, n, q, bars);
     for (int q = 0; q < 2 && q < 2 * nb; ++q) dinv_issue(Dinv, s_dinv, q, nb, dbars);
   }
   __syncthreads();
@@ -373,8 +325,8 @@ __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_
     const bool fwd = seq < C;
     if (seq == C) PTRACE(4);
     if (!fwd && c.i0 == p0) panel_solve(p0, pn, true);   // backward: own block first
-    ring_wait(&bars[seq % kRingSlots], (uint32_t)((seq / kRingSlots) & 1));
-    const double* rows = ring + coff[seq % kRingSlots] + (tri(c.i0) & 1) - tri(c.i0);
+    ring_wait(&bars[seq % kRingStages], (uint32_t)((seq / kRingStages) & 1));
+    const double* rows = ring + (seq % kRingStages) * stage + (tri(c.i0) & 1) - tri(c.i0);
     if (fwd) {
       // x_i -= L[i, 0:p0] . x[0:p0] for the chunk's rows (one warp per row)
       if (warp < c.rows && p0 > 0) {
@@ -394,10 +346,9 @@ __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_
       }
     }
     __syncthreads();
-    if (threadIdx.x == 0) {  // chunk seq's space is free: refill the ring
-      rp.consumed = seq + 1;
+    if (threadIdx.x == 0 && seq + kRingStages < total) {  // stage free: next chunk into it
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      ring_fill(rp, Lg, ring, cap, n, total, bars, coff);
+      ring_issue(Lg, ring, stage, n, seq + kRingStages, bars);
     }
     if (fwd && c.i0 + c.rows == p0 + pn) panel_solve(p0, pn, false);  // forward: panel done
   }
@@ -417,10 +368,9 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   extern __shared__ __align__(16) unsigned char psm[];
   __shared__ double s_red[kSolveWarps][32];
   __shared__ uint64_t s_bar;
-  __shared__ uint64_t s_ring_bar[kRingSlots];
-  __shared__ int32_t s_ring_off[kRingSlots];
+  __shared__ uint64_t s_ring_bar[kRingStages];
   __shared__ uint64_t s_dinv_bar[2];
-  const PatchSmem L_ = patch_smem_layout(nmax, allow_stream, flags >> 8);
+  const PatchSmem L_ = patch_smem_layout(nmax, allow_stream);
   double* s_x = reinterpret_cast<double*>(psm + L_.x_off);
   int32_t* s_off = reinterpret_cast<int32_t*>(psm + L_.off_off);
   double* s_prod = reinterpret_cast<double*>(psm + L_.prod_off);
@@ -539,7 +489,7 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   const double* Dinv = L + patch_tri_even(n);   // inverted diagonal blocks, row stride 33
 
   if (!staged && L_.stage > 0) {
-    stream_solve(Lg, s_L, L_.tri_cap, n, s_x, s_prod, s_ring_bar, s_ring_off, s_dinv_bar, s_red);
+    stream_solve(Lg, s_L, L_.stage, n, s_x, s_prod, s_ring_bar, s_dinv_bar, s_red);
   } else {
 
   // ---- forward: L y = r (left-looking over 32-row panels)
@@ -691,9 +641,8 @@ static cudaError_t launch_patch(const Correction& c, size_t smem, const double* 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   static const int l2pf = patch_env("SMG_PATCH_L2PF", 0);  // measured slower on C5 (222 vs 240 us)
-  const int ring = ring_chunks();
   static const int lpt = patch_env("SMG_PATCH_LPT", 1);
-  const int flags = (allow_stream ? kFlagStream : 0) | (l2pf ? kFlagL2Prefetch : 0) | (ring << 8);
+  const int flags = (allow_stream ? kFlagStream : 0) | (l2pf ? kFlagL2Prefetch : 0);
   return cudaLaunchKernelEx(&cfg, patch_kernel<kMode>, c.prow, c.pcol, c.pval, c.pptr, c.dofs,
                             c.foff, c.lfac, b, u_res, c.rbuf, tgt, add, c.max_dofs, flags,
                             lpt ? c.order : (const int32_t*)nullptr);
@@ -725,7 +674,7 @@ cudaError_t launch_patch_solve(const Correction& c, const double* b, const doubl
 {
   if (c.n_regions == 0) return cudaSuccess;
   const int st = nostream_env() ? 0 : 1;
-  const PatchSmem L = patch_smem_layout(c.max_dofs, st != 0, ring_chunks());
+  const PatchSmem L = patch_smem_layout(c.max_dofs, st != 0);
   double* tgt = u_add ? u_add : out_scatter;
   const int add = u_add ? 1 : 0;
   const size_t smem = (size_t)L.bytes + smem_pad();
@@ -735,7 +684,7 @@ cudaError_t launch_patch_solve(const Correction& c, const double* b, const doubl
 
 cudaError_t configure_patch_solve_smem(const Correction& c)
 {
-  const PatchSmem L = patch_smem_layout(c.max_dofs, !nostream_env(), ring_chunks());
+  const PatchSmem L = patch_smem_layout(c.max_dofs, !nostream_env());
   const int bytes = (int)(L.bytes + smem_pad());
   cudaError_t e = cudaFuncSetAttribute(patch_kernel<kAddResidualSolve>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
