@@ -95,7 +95,9 @@ def load(build_if_missing: bool = True):
     global _lib
     if _lib is not None:
         return _lib
-    path = build_lib.LIB
+    # SMG_LIB: an alternative in-tree build of the same C-ABI (compile-time
+    # A/B variants, tools/build_variant.py); default: the product library
+    path = os.environ.get("SMG_LIB", build_lib.LIB)
     if not os.path.exists(path):
         if not build_if_missing:
             raise RuntimeError(f"{path} is missing: run `python -m paper_2402_12947_b200.build_lib`")

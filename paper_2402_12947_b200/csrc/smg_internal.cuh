@@ -19,7 +19,10 @@ namespace smg {
 // csr_matvec uses -- so results are bit-identical to the reference.
 constexpr int kThreads = 256;        // one row per thread at most
 constexpr int kRowsPerTile = kThreads;
-constexpr int kTileNnz = 2048;       // products staged per pass (16 KB smem)
+#ifndef SMG_TILE_NNZ
+#define SMG_TILE_NNZ 2048
+#endif
+constexpr int kTileNnz = SMG_TILE_NNZ;  // products staged per pass (16 KB smem)
 constexpr int kItems = kTileNnz / kThreads;
 constexpr int64_t kStreamBytes = 64ll << 20;   // operators above this are streamed evict-first
 

@@ -109,7 +109,10 @@ __device__ __forceinline__ void epilogue(const EpiArgs& ea, int32_t row, double 
 
 // 64 registers, 4 CTAs (32 warps) per SM: measured faster than 40 registers /
 // 6 CTAs with spills (profiles/r01/bench_variant_v*.json).
-constexpr int kMinBlocks = 4;
+#ifndef SMG_SPMV_MIN_BLOCKS
+#define SMG_SPMV_MIN_BLOCKS 4
+#endif
+constexpr int kMinBlocks = SMG_SPMV_MIN_BLOCKS;
 
 template <Epi E, bool kPf>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)

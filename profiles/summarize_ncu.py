@@ -2,7 +2,9 @@
 """Summarise ncu reports / launch lists into markdown (run here, no GPU needed).
 
     python profiles/summarize_ncu.py gpurun_out/prof_k3_TAG.ncu-rep [...]
-    python profiles/summarize_ncu.py --launches gpurun_out/launches_TAG.csv --per-cycle 38
+    python profiles/summarize_ncu.py --launches gpurun_out/launches_TAG.csv --per-cycle 38 \
+        [--cycle-index 0] [--sequence]
+(launch lists from profiles/run_ncu.sh hold exactly one V-cycle: --cycle-index 0)
 """
 
 import csv
@@ -44,16 +46,17 @@ def report(path):
         print()
 
 
-def launches(path, per_cycle, cycle_index=3):
+def launches(path, per_cycle, cycle_index=3, sequence=False):
     rows = list(csv.reader(open(path)))
     h = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     hdr = rows[h]
     ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
-    data = [(r[ki], float(r[vi].replace(",", ""))) for r in rows[h + 1:] if len(r) > vi]
+    gi = hdr.index("Grid Size")
+    data = [(r[ki], float(r[vi].replace(",", "")), r[gi]) for r in rows[h + 1:] if len(r) > vi]
     cyc = data[cycle_index * per_cycle:(cycle_index + 1) * per_cycle]
     tot = sum(d[1] for d in cyc)
     agg = defaultdict(lambda: [0.0, 0])
-    for name, ns in cyc:
+    for name, ns, _ in cyc:
         key = name.split("(")[0][:70]
         agg[key][0] += ns
         agg[key][1] += 1
@@ -64,13 +67,20 @@ def launches(path, per_cycle, cycle_index=3):
     for k, (ns, c) in sorted(agg.items(), key=lambda kv: -kv[1][0]):
         print(f"| `{k}` | {c} | {ns / 1e3:.1f} | {100 * ns / tot:.1f}% |")
     print()
+    if sequence:
+        print("| # | kernel | grid | us |")
+        print("|---|---|---|---|")
+        for i, (name, ns, grid) in enumerate(cyc):
+            print(f"| {i} | `{name.split('(')[0][:60]}` | {grid} | {ns / 1e3:.1f} |")
+        print()
 
 
 if __name__ == "__main__":
     args = sys.argv[1:]
     if args and args[0] == "--launches":
         per = int(args[args.index("--per-cycle") + 1]) if "--per-cycle" in args else 38
-        launches(args[1], per)
+        ci = int(args[args.index("--cycle-index") + 1]) if "--cycle-index" in args else 3
+        launches(args[1], per, ci, "--sequence" in args)
     else:
         for p in args:
             report(p)
