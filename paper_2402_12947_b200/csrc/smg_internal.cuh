@@ -28,12 +28,14 @@ constexpr int64_t kStreamBytes = 64ll << 20;   // operators above this are strea
 
 struct DevCsr {
   int64_t nrows = 0, ncols = 0, nnz = 0;
-  const int64_t* rowptr = nullptr;   // nrows + 1
+  const int64_t* rowptr = nullptr;   // nrows + 1 (setup kernels)
+  const int32_t* rowrel = nullptr;   // nrows: rowptr[row] - tile_nz[tile of row] (hot path)
   const int32_t* col = nullptr;      // nnz
   const double* val = nullptr;       // nnz
   const int32_t* tile_row = nullptr; // ntiles + 1 (row boundaries of tiles)
   const int64_t* tile_nz = nullptr;  // ntiles + 1 (rowptr at the tile boundaries)
-  const double* inv_diag = nullptr;  // 1.0 / a_ii (IEEE, as smoothers.py:115), square ops
+  const double* inv_diag = nullptr;  // 1.0 / a_ii (IEEE, as smoothers.py:115), square ops;
+                                     // read only for gathered row subsets (row_map)
   const int32_t* row_map = nullptr;  // gathered row subsets: local row -> operator row
   int32_t ntiles = 0;
   bool streaming = false;            // val+col exceed kStreamBytes: evict-first reads
