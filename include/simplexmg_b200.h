@@ -128,7 +128,8 @@ SMG_API int smg_combined_smooth(const smg_operator *a, const double *b, double *
  * into l; created with_transpose; ignored on the coarsest level), optional
  * correction[l] and smoother parameters.  The coarsest level is solved with
  * the dense operator coarse_inverse = A_L^{-1} (n_coarse x n_coarse row-major,
- * e.g. LAPACK dpotri on the reference's coarse_factor, mg.py:123);
+ * e.g. LAPACK dpotri on the reference's coarse_factor, mg.py:123; symmetric:
+ * only its lower triangle is read and kept on the device, in 64 x 64 tiles);
  * coarse_refine != 0 adds one refinement step with a[n_levels-1].
  * The hierarchy borrows (does not own) the operators and corrections. */
 SMG_API int smg_hierarchy_create(int n_levels, const smg_operator *const *a,

@@ -101,18 +101,6 @@ static std::vector<int32_t> make_tiles(int64_t nrows, const int64_t* rowptr)
   return t;
 }
 
-// row starts relative to their tile's first nonzero: the hot kernels read
-// 4 bytes per row instead of two 8-byte row offsets
-static std::vector<int32_t> tile_relative_rows(int64_t nrows, const int64_t* rowptr,
-                                               const std::vector<int32_t>& tiles)
-{
-  std::vector<int32_t> rel((size_t)nrows + 1, 0);
-  for (size_t t = 0; t + 1 < tiles.size(); ++t)
-    for (int32_t r = tiles[t]; r < tiles[t + 1]; ++r)
-      rel[(size_t)r] = (int32_t)(rowptr[r] - rowptr[tiles[t]]);
-  return rel;
-}
-
 static bool stream_env()
 {
   const char* v = getenv("SMG_EVICT_FIRST");
@@ -134,7 +122,6 @@ static int build_devcsr(std::vector<void*>& allocs, int64_t& bytes, int64_t nrow
   std::vector<int32_t> tiles = make_tiles(nrows, rowptr);
   std::vector<int64_t> tnz(tiles.size());
   for (size_t i = 0; i < tiles.size(); ++i) tnz[i] = rowptr[tiles[i]];
-  std::vector<int32_t> rel = tile_relative_rows(nrows, rowptr, tiles);
   DevCsr d;
   d.nrows = nrows;
   d.ncols = ncols;
@@ -151,9 +138,6 @@ static int build_devcsr(std::vector<void*>& allocs, int64_t& bytes, int64_t nrow
   SMG_TRY(dev_upload(allocs, bytes, valp.data(), valp.size(), &v));
   SMG_TRY(dev_upload(allocs, bytes, tiles.data(), tiles.size(), &tr));
   SMG_TRY(dev_upload(allocs, bytes, tnz.data(), tnz.size(), &tz));
-  int32_t* rr = nullptr;
-  SMG_TRY(dev_upload(allocs, bytes, rel.data(), rel.size(), &rr));
-  d.rowrel = rr;
   d.rowptr = rp;
   d.col = c;
   d.val = v;
@@ -312,7 +296,7 @@ struct HLevel {
 struct Hierarchy {
   std::vector<HLevel> lv;
   int64_t n_coarse = 0;
-  double* coarse_inv = nullptr;
+  SymTiles coarse;                    // A_L^{-1}, lower-triangle tiles
   int coarse_refine = 0;
   double* coarse_r = nullptr;
   double* coarse_x = nullptr;
@@ -486,15 +470,15 @@ static int enqueue_vcycle(Hierarchy& h, const double* b0, double* u0, cudaStream
   // coarse solve
   {
     HLevel& C = h.lv[nl - 1];
-    SMG_CUDA(launch_dense_gemv(h.n_coarse, h.coarse_inv, bl[nl - 1], cur[nl - 1], st));
-    ++*launches;
+    SMG_CUDA(launch_sym_apply(h.coarse, bl[nl - 1], cur[nl - 1], false, st));
+    *launches += 2;
     if (h.coarse_refine) {
       EpiArgs ea;
       ea.b = bl[nl - 1];
       ea.out = h.coarse_r;
       SMG_CUDA(launch_csr_stream(C.a->a, cur[nl - 1], Epi::kResidual, ea, st));
-      SMG_CUDA(launch_dense_gemv_add(h.n_coarse, h.coarse_inv, h.coarse_r, cur[nl - 1], st));
-      *launches += 2;
+      SMG_CUDA(launch_sym_apply(h.coarse, h.coarse_r, cur[nl - 1], true, st));
+      *launches += 3;
     }
   }
   for (int l = nl - 2; l >= 0; --l) {
@@ -863,7 +847,6 @@ static int build_halo(const Operator& o, const std::vector<int32_t>& dof32,
   std::vector<int32_t> tiles = make_tiles(nh, hrow.data());
   std::vector<int64_t> tnz(tiles.size());
   for (size_t i = 0; i < tiles.size(); ++i) tnz[i] = hrow[(size_t)tiles[i]];
-  std::vector<int32_t> rel = tile_relative_rows(nh, hrow.data(), tiles);
   int64_t* drp = nullptr;
   int32_t* dcol = nullptr;
   double* dval = nullptr;
@@ -874,8 +857,6 @@ static int build_halo(const Operator& o, const std::vector<int32_t>& dof32,
   SMG_TRY(dev_alloc(c.allocs, c.device_bytes, (size_t)hn + 2, &dval));
   SMG_TRY(dev_upload(c.allocs, c.device_bytes, tiles.data(), tiles.size(), &dtr));
   SMG_TRY(dev_upload(c.allocs, c.device_bytes, tnz.data(), tnz.size(), &dtz));
-  int32_t* drel = nullptr;
-  SMG_TRY(dev_upload(c.allocs, c.device_bytes, rel.data(), rel.size(), &drel));
   SMG_TRY(check_cuda(launch_patch_row_gather(o.a, drows, nh, drp, dcol, dval), "halo gather"));
   SMG_CUDA(cudaDeviceSynchronize());
   DevCsr hm;
@@ -883,7 +864,6 @@ static int build_halo(const Operator& o, const std::vector<int32_t>& dof32,
   hm.ncols = o.a.ncols;
   hm.nnz = hn;
   hm.rowptr = drp;
-  hm.rowrel = drel;
   hm.col = dcol;
   hm.val = dval;
   hm.tile_row = dtr;
@@ -1099,6 +1079,44 @@ int smg_combined_smooth(const smg_operator* a, const double* b, double* u, const
                            as_stream(stream));
 }
 
+// A_L^{-1} (dense, row-major, symmetric) -> lower-triangle 64 x 64 tiles
+static int upload_sym_tiles(std::vector<void*>& allocs, int64_t& bytes, int64_t n,
+                            const double* dense, SymTiles* out)
+{
+  SymTiles m;
+  m.n = n;
+  m.nb = (int)((n + kSymTile - 1) / kSymTile);
+  const int64_t ntiles = (int64_t)m.nb * (m.nb + 1) / 2;
+  std::vector<double> t((size_t)(ntiles * kSymTile * kSymTile), 0.0);
+  std::vector<int32_t> ti((size_t)ntiles);
+  int64_t k = 0;
+  for (int I = 0; I < m.nb; ++I)
+    for (int J = 0; J <= I; ++J, ++k) {
+      ti[(size_t)k] = I;
+      double* dst = t.data() + k * kSymTile * kSymTile;
+      for (int r = 0; r < kSymTile; ++r) {
+        const int64_t gi = (int64_t)I * kSymTile + r;
+        if (gi >= n) break;
+        for (int c = 0; c < kSymTile; ++c) {
+          const int64_t gj = (int64_t)J * kSymTile + c;
+          if (gj >= n) break;
+          dst[r * kSymTile + c] = dense[gi * n + gj];
+        }
+      }
+    }
+  double* dt = nullptr;
+  int32_t* dti = nullptr;
+  double* dp = nullptr;
+  SMG_TRY(dev_upload(allocs, bytes, t.data(), t.size(), &dt));
+  SMG_TRY(dev_upload(allocs, bytes, ti.data(), ti.size(), &dti));
+  SMG_TRY(dev_alloc(allocs, bytes, (size_t)m.nb * m.nb * kSymTile, &dp));
+  m.tiles = dt;
+  m.tile_i = dti;
+  m.partial = dp;
+  *out = m;
+  return SMG_OK;
+}
+
 int smg_hierarchy_create(int n_levels, const smg_operator* const* a, const smg_operator* const* p,
                          const smg_correction* const* corrections, const int* kinds,
                          const int* sweeps, const double* lambda_max, const double* frac,
@@ -1159,8 +1177,7 @@ int smg_hierarchy_create(int n_levels, const smg_operator* const* a, const smg_o
       if (rc == SMG_OK) rc = dev_alloc(h.allocs, h.bytes, n, &L.r);
     }
   }
-  if (rc == SMG_OK)
-    rc = dev_upload(h.allocs, h.bytes, coarse_inverse, (size_t)(n_coarse * n_coarse), &h.coarse_inv);
+  if (rc == SMG_OK) rc = upload_sym_tiles(h.allocs, h.bytes, n_coarse, coarse_inverse, &h.coarse);
   h.n_coarse = n_coarse;
   h.coarse_refine = coarse_refine;
   if (rc == SMG_OK && coarse_refine) rc = dev_alloc(h.allocs, h.bytes, (size_t)n_coarse, &h.coarse_r);

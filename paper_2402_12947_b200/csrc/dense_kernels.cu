@@ -3,10 +3,11 @@
 // Coarse solve (mg.py:145, Hierarchy.coarse_factor from mg.py:123): the
 // reference runs LAPACK dpotrs on the dense Cholesky factor of A_L.  Two
 // dependent triangular sweeps over an n_L^2 factor are latency-bound on a GPU
-// (n_L sequential steps), so the library applies the precomputed dense
-// operator A_L^{-1} = (L L^T)^{-1} as one HBM-streaming GEMV across every SM,
-// optionally followed by one refinement step x += A_L^{-1}(b - A_L x) (the
-// residual uses the sparse coarse operator).  Parity is tolerance-based, like
+// (n_L sequential steps), so the library applies the precomputed symmetric
+// operator A_L^{-1} = (L L^T)^{-1} as an HBM-streaming symmetric matrix-vector
+// product over its lower triangle (every tile read once, used for A x and
+// A^T x), optionally followed by one refinement step x += A_L^{-1}(b - A_L x)
+// (the residual uses the sparse coarse operator).  Parity is tolerance-based, like
 // every dense solve on this path.
 //
 // Reductions (solve_stationary norms mg.py:164,174; CG dots sparse.py:184-208):
@@ -16,9 +17,6 @@
 
 namespace smg {
 
-constexpr int kGemvThreads = 128;                 // 4 rows (warps) per CTA
-constexpr int kGemvUnroll = 8;                    // independent 256 B loads in flight per warp
-
 __device__ __forceinline__ double warp_sum_d(double v)
 {
 #pragma unroll
@@ -26,64 +24,96 @@ __device__ __forceinline__ double warp_sum_d(double v)
   return v;
 }
 
-// y = M x (kAdd=false) or y += M x (kAdd=true); M dense row-major n x n.
-// One warp per row, kGemvUnroll independent accumulators (fixed order: the
-// result is run-to-run deterministic).
+// ---------------------------------------------------------------------------
+// Symmetric coarse operator applied from its lower triangle only (half the
+// bytes of the dense GEMV): A_L^{-1} is stored as 64 x 64 tiles (I, J), J <= I,
+// row-major inside a tile, zero-padded, tile (I, J) at index I(I+1)/2 + J.
+// Kernel 1, one CTA per tile: partial[I][J] = A_IJ x_J and, off the diagonal,
+// partial[J][I] = A_IJ^T x_I.  Kernel 2: y_i = sum_J partial[I][J][i] in
+// ascending J.  Every sum has a fixed order: run-to-run deterministic.
+constexpr int kSymThreads = 256;
+constexpr int kSymRowsPerThread = kSymTile * kSymTile / kSymThreads;   // 16
+
+__global__ void __launch_bounds__(kSymThreads)
+sym_tile_kernel(int nb, const int32_t* __restrict__ tile_i, const double* __restrict__ tiles,
+                const double* __restrict__ x, int64_t n, double* __restrict__ partial)
+{
+  __shared__ double s_xi[kSymTile], s_xj[kSymTile];
+  __shared__ double s_row[kSymTile][2];
+  __shared__ double s_col[kSymThreads / kSymTile][kSymTile];
+  const int t = blockIdx.x;
+  const int I = tile_i[t];
+  const int J = t - I * (I + 1) / 2;
+  const int tid = threadIdx.x;
+  const int c = tid & (kSymTile - 1);      // column inside the tile
+  const int g = tid / kSymTile;            // rows g, g + 4, g + 8, ...
+  const double* __restrict__ a = tiles + (int64_t)t * kSymTile * kSymTile;
+  double v[kSymRowsPerThread];
+#pragma unroll
+  for (int i = 0; i < kSymRowsPerThread; ++i) v[i] = __ldcs(a + (g + 4 * i) * kSymTile + c);
+  if (tid < kSymTile) {
+    const int64_t gi = (int64_t)I * kSymTile + tid, gj = (int64_t)J * kSymTile + tid;
+    s_xi[tid] = gi < n ? x[gi] : 0.0;
+    s_xj[tid] = gj < n ? x[gj] : 0.0;
+  }
+  __syncthreads();
+  const int lane = tid & 31, warp = tid >> 5;
+  // rows: each warp covers 32 of the 64 columns of its 16 rows
+  const double xc = s_xj[c];
+#pragma unroll
+  for (int i = 0; i < kSymRowsPerThread; ++i) {
+    double p = v[i] * xc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+    if (lane == 0) s_row[g + 4 * i][warp & 1] = p;
+  }
+  // columns (off-diagonal tiles): this thread's 16 rows, then the 4 row groups
+  if (I != J) {
+    double q = 0.0;
+#pragma unroll
+    for (int i = 0; i < kSymRowsPerThread; ++i) q += v[i] * s_xi[g + 4 * i];
+    s_col[g][c] = q;
+  }
+  __syncthreads();
+  double* out = partial + ((int64_t)I * nb + J) * kSymTile;
+  if (tid < kSymTile) out[tid] = s_row[tid][0] + s_row[tid][1];
+  if (I != J && tid < kSymTile) {
+    double q = 0.0;
+#pragma unroll
+    for (int gg = 0; gg < kSymThreads / kSymTile; ++gg) q += s_col[gg][tid];
+    partial[((int64_t)J * nb + I) * kSymTile + tid] = q;
+  }
+}
+
 template <bool kAdd>
-__global__ void __launch_bounds__(kGemvThreads)
-dense_gemv_kernel(int64_t n, const double* __restrict__ m, const double* __restrict__ x,
-                  double* __restrict__ y)
+__global__ void sym_reduce_kernel(int nb, int64_t n, const double* __restrict__ partial,
+                                  double* __restrict__ y)
 {
-  const int lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * (kGemvThreads / 32) + (threadIdx.x >> 5);
-  if (row >= n) return;
-  const double* __restrict__ mr = m + row * n;
-  double acc[kGemvUnroll];
-#pragma unroll
-  for (int u = 0; u < kGemvUnroll; ++u) acc[u] = 0.0;
-  int64_t j = lane;
-  for (; j + 32 * (kGemvUnroll - 1) < n; j += 32 * kGemvUnroll) {
-    double mv[kGemvUnroll];
-#pragma unroll
-    for (int u = 0; u < kGemvUnroll; ++u) mv[u] = __ldcs(mr + j + 32 * u);
-#pragma unroll
-    for (int u = 0; u < kGemvUnroll; ++u) acc[u] = fma(mv[u], __ldg(x + j + 32 * u), acc[u]);
-  }
-  for (; j < n; j += 32) acc[0] = fma(__ldcs(mr + j), __ldg(x + j), acc[0]);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t I = i / kSymTile, r = i % kSymTile;
+  const double* p = partial + I * nb * kSymTile + r;
   double s = 0.0;
-#pragma unroll
-  for (int u = 0; u < kGemvUnroll; ++u) s += acc[u];
-  s = warp_sum_d(s);
-  if (lane == 0) {
-    if (kAdd)
-      y[row] += s;
-    else
-      y[row] = s;
-  }
-}
-
-static cudaError_t gemv(int64_t n, const double* m, const double* x, double* y, bool add,
-                        cudaStream_t s)
-{
-  if (n == 0) return cudaSuccess;
-  const int64_t blocks = (n + (kGemvThreads / 32) - 1) / (kGemvThreads / 32);
-  if (add)
-    dense_gemv_kernel<true><<<(unsigned)blocks, kGemvThreads, 0, s>>>(n, m, x, y);
+  for (int J = 0; J < nb; ++J) s += p[(int64_t)J * kSymTile];
+  if (kAdd)
+    y[i] += s;
   else
-    dense_gemv_kernel<false><<<(unsigned)blocks, kGemvThreads, 0, s>>>(n, m, x, y);
+    y[i] = s;
+}
+
+cudaError_t launch_sym_apply(const SymTiles& m, const double* x, double* y, bool add,
+                             cudaStream_t s)
+{
+  if (m.n == 0) return cudaSuccess;
+  const int64_t ntiles = (int64_t)m.nb * (m.nb + 1) / 2;
+  sym_tile_kernel<<<(unsigned)ntiles, kSymThreads, 0, s>>>(m.nb, m.tile_i, m.tiles, x, m.n,
+                                                            m.partial);
+  const unsigned blocks = (unsigned)((m.n + 255) / 256);
+  if (add)
+    sym_reduce_kernel<true><<<blocks, 256, 0, s>>>(m.nb, m.n, m.partial, y);
+  else
+    sym_reduce_kernel<false><<<blocks, 256, 0, s>>>(m.nb, m.n, m.partial, y);
   return cudaGetLastError();
-}
-
-cudaError_t launch_dense_gemv(int64_t n, const double* m, const double* x, double* y,
-                              cudaStream_t s)
-{
-  return gemv(n, m, x, y, false, s);
-}
-
-cudaError_t launch_dense_gemv_add(int64_t n, const double* m, const double* x, double* y,
-                                  cudaStream_t s)
-{
-  return gemv(n, m, x, y, true, s);
 }
 
 // ---------------------------------------------------------------------------

@@ -28,14 +28,12 @@ constexpr int64_t kStreamBytes = 64ll << 20;   // operators above this are strea
 
 struct DevCsr {
   int64_t nrows = 0, ncols = 0, nnz = 0;
-  const int64_t* rowptr = nullptr;   // nrows + 1 (setup kernels)
-  const int32_t* rowrel = nullptr;   // nrows: rowptr[row] - tile_nz[tile of row] (hot path)
+  const int64_t* rowptr = nullptr;   // nrows + 1
   const int32_t* col = nullptr;      // nnz
   const double* val = nullptr;       // nnz
   const int32_t* tile_row = nullptr; // ntiles + 1 (row boundaries of tiles)
   const int64_t* tile_nz = nullptr;  // ntiles + 1 (rowptr at the tile boundaries)
-  const double* inv_diag = nullptr;  // 1.0 / a_ii (IEEE, as smoothers.py:115), square ops;
-                                     // read only for gathered row subsets (row_map)
+  const double* inv_diag = nullptr;  // 1.0 / a_ii (IEEE, as smoothers.py:115), square ops
   const int32_t* row_map = nullptr;  // gathered row subsets: local row -> operator row
   int32_t ntiles = 0;
   bool streaming = false;            // val+col exceed kStreamBytes: evict-first reads
@@ -149,11 +147,19 @@ cudaError_t launch_patch_row_gather(const DevCsr& a, const int32_t* dofs, int64_
                                     const int64_t* prow, int32_t* pcol, double* pval);
 cudaError_t launch_mark_halo(const DevCsr& a, const uint8_t* in_patch, uint8_t* mask);
 
+// symmetric coarse operator, lower-triangle 64 x 64 tiles (dense_kernels.cu)
+constexpr int kSymTile = 64;
+struct SymTiles {
+  int64_t n = 0;
+  int nb = 0;                        // tiles per dimension
+  const double* tiles = nullptr;     // nb(nb+1)/2 tiles of kSymTile^2 doubles
+  const int32_t* tile_i = nullptr;   // block row of each tile
+  double* partial = nullptr;         // nb * nb * kSymTile scratch
+};
+cudaError_t launch_sym_apply(const SymTiles& m, const double* x, double* y, bool add,
+                             cudaStream_t s);
+
 // dense / reduction kernels (dense_kernels.cu)
-cudaError_t launch_dense_gemv(int64_t n, const double* m, const double* x, double* y,
-                              cudaStream_t s);
-cudaError_t launch_dense_gemv_add(int64_t n, const double* m, const double* x, double* y,
-                                  cudaStream_t s);
 cudaError_t launch_dot(int64_t n, const double* a, const double* b, double* partials,
                        unsigned int* counter, double* result, cudaStream_t s);
 cudaError_t launch_axpby(int64_t n, double alpha, const double* x, double beta, double* y,

@@ -120,12 +120,6 @@ csr_tile_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, 
 {
   using T = EpiTraits<E>;
   __shared__ double s_prod[kTileNnz];
-  // diagonal-scaled epilogues take a_ii from the row itself (1/a_ii formed
-  // with the same IEEE division numpy uses, smoothers.py:115) instead of
-  // streaming an inverse-diagonal vector: the thread that stages a_ii's
-  // product also records it
-  __shared__ int32_t s_lo[T::kDiag ? kThreads + 1 : 1];
-  __shared__ double s_diag[T::kDiag ? kThreads : 1];
   const int t = blockIdx.x;
   const int tid = threadIdx.x;
   // ---- operator data (never written by any kernel): before the dependency wait
@@ -137,17 +131,10 @@ csr_tile_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, 
   const int cnt = (int)(e1 - e0);
   const int32_t row = r0 + tid;
   const bool has_row = row < r1;
-  int rel0 = 0, rel1 = 0;   // the row's nonzeros, relative to the tile's first
+  int64_t lo = 0, hi = 0;
   if (has_row) {
-    rel0 = m.rowrel[row];
-    rel1 = row + 1 < r1 ? m.rowrel[row + 1] : cnt;
-  }
-  const int64_t lo = e0 + rel0, hi = e0 + rel1;
-  const bool row_diag = T::kDiag && m.row_map == nullptr;  // uniform
-  if (row_diag) {
-    if (has_row) s_lo[tid] = rel0;
-    if (tid == 0) s_lo[r1 - r0] = cnt;
-    s_diag[tid] = 0.0;
+    lo = m.rowptr[row];
+    hi = m.rowptr[row + 1];
   }
   int32_t c[kItems];
   double v[kItems];
@@ -195,25 +182,15 @@ csr_tile_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, 
     if constexpr (T::kU) uv = ea.u_in[grow];
     if constexpr (T::kD) dv = ea.d[grow];
     if constexpr (T::kOut) ov = ea.out[grow];
-    if constexpr (T::kDiag) {
-      if (!row_diag) inv = m.inv_diag[grow];
-    }
+    if constexpr (T::kDiag) inv = m.inv_diag[grow];
     if constexpr (T::kDiagVec) inv = ea.inv_diag[grow];
   }
-  if (row_diag) __syncthreads();   // s_lo, s_diag initialised
   double sum = 0.0;
   if (!longtile) {
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
       const int k = i * kThreads + tid;
-      if (k < cnt) {
-        s_prod[k] = __dmul_rn(v[i], __ldg(x + c[i]));
-        if (row_diag) {
-          const int rr = c[i] - r0;
-          if ((unsigned)rr < (unsigned)(r1 - r0) && k >= s_lo[rr] && k < s_lo[rr + 1])
-            s_diag[rr] = v[i];
-        }
-      }
+      if (k < cnt) s_prod[k] = __dmul_rn(v[i], __ldg(x + c[i]));
     }
     __syncthreads();
     if (has_row) {
@@ -226,12 +203,8 @@ csr_tile_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, 
     for (int64_t cs = e0; cs < e1; cs += kTileNnz) {
       const int64_t rem = e1 - cs;
       const int cn = rem < (int64_t)kTileNnz ? (int)rem : kTileNnz;
-      for (int k = tid; k < cn; k += kThreads) {
-        const int32_t col = __ldg(m.col + cs + k);
-        const double val = __ldg(m.val + cs + k);
-        s_prod[k] = __dmul_rn(val, __ldg(x + col));
-        if (row_diag && col == r0) s_diag[0] = val;   // a long tile holds one row
-      }
+      for (int k = tid; k < cn; k += kThreads)
+        s_prod[k] = __dmul_rn(__ldg(m.val + cs + k), __ldg(x + __ldg(m.col + cs + k)));
       __syncthreads();
       if (has_row) {
         const int64_t a = lo > cs ? lo : cs;
@@ -241,7 +214,6 @@ csr_tile_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, 
       __syncthreads();
     }
   }
-  if (row_diag && write) inv = __ddiv_rn(1.0, s_diag[tid]);
   if (write) epilogue<E>(ea, grow, sum, inv, bv, uv, dv, ov);
 }
 
