@@ -70,23 +70,40 @@ static void free_all(std::vector<void*>& allocs)
 // Greedy tile partition: consecutive rows, <= kRowsPerTile rows, <= cap
 // nonzeros unless a single row is longer.  Small operators (coarse levels)
 // get smaller tiles so every SM still has several independent CTAs.
-static int64_t tile_cap_for(int64_t nnz)
+// operators whose rows average >= SMG_MC_MIN_ROW nonzeros (default 24) get
+// multi-chunk tiles (csr_tile_kernel<.., kMulti>)
+static bool long_rows(int64_t nnz, int64_t nrows)
 {
-  static int per_sm = -1;
+  static int mc_row = -1;
+  if (mc_row < 0) {
+    const char* v = getenv("SMG_MC_MIN_ROW");
+    mc_row = v ? atoi(v) : 24;
+    if (mc_row < 0) mc_row = 0;
+  }
+  return mc_row > 0 && nrows > 0 && nnz >= (int64_t)mc_row * nrows;
+}
+
+static int64_t tile_cap_for(int64_t nnz, int64_t nrows)
+{
+  static int per_sm = -1, mc_chunks = -1;
   if (per_sm < 0) {
     const char* v = getenv("SMG_TILES_PER_SM");
     per_sm = v ? atoi(v) : 4;
     if (per_sm <= 0) per_sm = 4;
+    v = getenv("SMG_MC_CHUNKS");
+    mc_chunks = v ? atoi(v) : kMaxTileChunks;
+    if (mc_chunks < 1 || mc_chunks > kMaxTileChunks) mc_chunks = kMaxTileChunks;
   }
+  const int64_t max_cap = long_rows(nnz, nrows) ? (int64_t)kTileNnz * mc_chunks : kTileNnz;
   const int64_t want = nnz / (148 * per_sm);  // ~per_sm tiles per SM
   int64_t cap = 256;
-  while (cap < want && cap < kTileNnz) cap *= 2;
+  while (cap < want && cap < max_cap) cap *= 2;
   return cap;
 }
 
 static std::vector<int32_t> make_tiles(int64_t nrows, const int64_t* rowptr)
 {
-  const int64_t cap = tile_cap_for(rowptr[nrows]);
+  const int64_t cap = tile_cap_for(rowptr[nrows], nrows);
   std::vector<int32_t> t;
   t.reserve((size_t)(nrows / 64 + 2));
   t.push_back(0);
@@ -128,6 +145,7 @@ static int build_devcsr(std::vector<void*>& allocs, int64_t& bytes, int64_t nrow
   d.nnz = nnz;
   d.ntiles = (int32_t)(tiles.size() - 1);
   d.streaming = stream_env() && nnz * 12 > kStreamBytes;
+  d.multichunk = long_rows(nnz, nrows);
   int64_t* rp = nullptr;
   int32_t* c = nullptr;
   double* v = nullptr;
@@ -872,6 +890,7 @@ static int build_halo(const Operator& o, const std::vector<int32_t>& dof32,
   hm.row_map = drows;
   hm.ntiles = (int32_t)(tiles.size() - 1);
   hm.streaming = o.a.streaming;
+  hm.multichunk = long_rows(hn, nh);
   c.halo = hm;
   c.halo_mask = mk;
   c.has_halo = true;

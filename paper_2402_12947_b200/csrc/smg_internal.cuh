@@ -24,6 +24,10 @@ constexpr int kRowsPerTile = kThreads;
 #endif
 constexpr int kTileNnz = SMG_TILE_NNZ;  // products staged per pass (16 KB smem)
 constexpr int kItems = kTileNnz / kThreads;
+// operators with long rows get tiles of up to kMaxTileChunks chunks of
+// kTileNnz nonzeros (<= kRowsPerTile rows): more rows sum in parallel per CTA
+// and each chunk's loads overlap the previous chunk's sums
+constexpr int kMaxTileChunks = 4;
 constexpr int64_t kStreamBytes = 64ll << 20;   // operators above this are streamed evict-first
 
 struct DevCsr {
@@ -37,6 +41,7 @@ struct DevCsr {
   const int32_t* row_map = nullptr;  // gathered row subsets: local row -> operator row
   int32_t ntiles = 0;
   bool streaming = false;            // val+col exceed kStreamBytes: evict-first reads
+  bool multichunk = false;           // long rows: tiles of up to kMaxTileChunks chunks
 };
 
 // Host-side owner of one operator's device arrays.

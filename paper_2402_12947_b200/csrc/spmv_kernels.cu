@@ -114,12 +114,16 @@ __device__ __forceinline__ void epilogue(const EpiArgs& ea, int32_t row, double 
 #endif
 constexpr int kMinBlocks = SMG_SPMV_MIN_BLOCKS;
 
-template <Epi E, bool kPf>
+template <Epi E, bool kPf, bool kMulti>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
 csr_tile_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, int pf_dist)
 {
   using T = EpiTraits<E>;
-  __shared__ double s_prod[kTileNnz];
+  // kMulti (operators with long rows, multi-chunk tiles): two chunk buffers,
+  // chunk q's products are summed while chunk q+1's values and columns are
+  // already in flight.  Otherwise one buffer (only a single row longer than a
+  // chunk makes a tile span several chunks).
+  __shared__ double s_prod[kMulti ? 2 * kTileNnz : kTileNnz];
   const int t = blockIdx.x;
   const int tid = threadIdx.x;
   // ---- operator data (never written by any kernel): before the dependency wait
@@ -127,8 +131,8 @@ csr_tile_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, 
   const int32_t r1 = m.tile_row[t + 1];
   const int64_t e0 = m.tile_nz[t];
   const int64_t e1 = m.tile_nz[t + 1];
-  const bool longtile = e1 - e0 > kTileNnz;
   const int cnt = (int)(e1 - e0);
+  const int nq = (cnt + kTileNnz - 1) / kTileNnz;   // chunks of this tile
   const int32_t row = r0 + tid;
   const bool has_row = row < r1;
   int64_t lo = 0, hi = 0;
@@ -138,21 +142,24 @@ csr_tile_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, 
   }
   int32_t c[kItems];
   double v[kItems];
+  auto load_chunk = [&](int q0) {
 #pragma unroll
-  for (int i = 0; i < kItems; ++i) {
-    const int k = i * kThreads + tid;
-    c[i] = 0;
-    v[i] = 0.0;
-    if (!longtile && k < cnt) {
-      if (m.streaming) {  // operator larger than L2 share: don't evict the small levels
-        c[i] = __ldcs(m.col + e0 + k);
-        v[i] = __ldcs(m.val + e0 + k);
-      } else {
-        c[i] = __ldg(m.col + e0 + k);
-        v[i] = __ldg(m.val + e0 + k);
+    for (int i = 0; i < kItems; ++i) {
+      const int k = q0 + i * kThreads + tid;
+      c[i] = 0;
+      v[i] = 0.0;
+      if (k < cnt && k < q0 + kTileNnz) {
+        if (m.streaming) {  // operator larger than L2 share: don't evict the small levels
+          c[i] = __ldcs(m.col + e0 + k);
+          v[i] = __ldcs(m.val + e0 + k);
+        } else {
+          c[i] = __ldg(m.col + e0 + k);
+          v[i] = __ldg(m.val + e0 + k);
+        }
       }
     }
-  }
+  };
+  load_chunk(0);
   if constexpr (kPf) {
     // pull the tile that starts one resident wave later into L2 (bulk
     // prefetch: no registers, no shared memory), so its CTA's loads hit L2
@@ -160,7 +167,7 @@ csr_tile_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, 
       const int tp = t + pf_dist;
       if (tp < m.ntiles) {
         const int64_t p0 = m.tile_nz[tp], p1 = m.tile_nz[tp + 1];
-        if (p1 - p0 <= kTileNnz && p1 > p0) {
+        if (p1 - p0 <= kTileNnz * kMaxTileChunks && p1 > p0) {
           const int64_t va = p0 & ~int64_t(1), vb = (p1 + 1) & ~int64_t(1);
           const int64_t ca = p0 & ~int64_t(3), cb = (p1 + 3) & ~int64_t(3);
           prefetch_l2(m.val + va, (uint32_t)((vb - va) * 8), m.streaming);
@@ -185,34 +192,24 @@ csr_tile_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, 
     if constexpr (T::kDiag) inv = m.inv_diag[grow];
     if constexpr (T::kDiagVec) inv = ea.inv_diag[grow];
   }
+  const int a = (int)(lo - e0), bnd = (int)(hi - e0);   // this row's tile-relative range
   double sum = 0.0;
-  if (!longtile) {
+  for (int q = 0; q < nq; ++q) {
+    const int q0 = q * kTileNnz;
+    const int qn = min(kTileNnz, cnt - q0);
+    double* buf = s_prod + (kMulti ? (q & 1) * kTileNnz : 0);
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
       const int k = i * kThreads + tid;
-      if (k < cnt) s_prod[k] = __dmul_rn(v[i], __ldg(x + c[i]));
+      if (k < qn) buf[k] = __dmul_rn(v[i], __ldg(x + c[i]));
     }
+    if (q + 1 < nq) load_chunk(q0 + kTileNnz);   // in flight during this chunk's sums
     __syncthreads();
     if (has_row) {
-      const int a = (int)(lo - e0);
-      const int bnd = (int)(hi - e0);
-      for (int j = a; j < bnd; ++j) sum = __dadd_rn(sum, s_prod[j]);
+      const int j0 = max(a, q0), j1 = min(bnd, q0 + qn);
+      for (int j = j0; j < j1; ++j) sum = __dadd_rn(sum, buf[j - q0]);
     }
-  } else {
-    // a row longer than one tile: stream it in kTileNnz chunks, keeping the sum
-    for (int64_t cs = e0; cs < e1; cs += kTileNnz) {
-      const int64_t rem = e1 - cs;
-      const int cn = rem < (int64_t)kTileNnz ? (int)rem : kTileNnz;
-      for (int k = tid; k < cn; k += kThreads)
-        s_prod[k] = __dmul_rn(__ldg(m.val + cs + k), __ldg(x + __ldg(m.col + cs + k)));
-      __syncthreads();
-      if (has_row) {
-        const int64_t a = lo > cs ? lo : cs;
-        const int64_t bnd = hi < cs + cn ? hi : cs + cn;
-        for (int64_t j = a; j < bnd; ++j) sum = __dadd_rn(sum, s_prod[j - cs]);
-      }
-      __syncthreads();
-    }
+    if (!kMulti && q + 1 < nq) __syncthreads();   // single buffer: sums done before reuse
   }
   if (write) epilogue<E>(ea, grow, sum, inv, bv, uv, dv, ov);
 }
@@ -256,9 +253,12 @@ static cudaError_t launch_t(const DevCsr& m, const double* x, const EpiArgs& ea,
     return w > 0 ? w : 1;
   }();
   const int dist = g_sm_count * kMinBlocks * waves;  // resident waves ahead (default one)
-  if (env_flag(g_prefetch, "SMG_L2_PREFETCH", 1))
-    return cudaLaunchKernelEx(&cfg, csr_tile_kernel<E, true>, m, x, ea, dist);
-  return cudaLaunchKernelEx(&cfg, csr_tile_kernel<E, false>, m, x, ea, dist);
+  const bool pf = env_flag(g_prefetch, "SMG_L2_PREFETCH", 1);
+  if (m.multichunk)
+    return pf ? cudaLaunchKernelEx(&cfg, csr_tile_kernel<E, true, true>, m, x, ea, dist)
+              : cudaLaunchKernelEx(&cfg, csr_tile_kernel<E, false, true>, m, x, ea, dist);
+  return pf ? cudaLaunchKernelEx(&cfg, csr_tile_kernel<E, true, false>, m, x, ea, dist)
+            : cudaLaunchKernelEx(&cfg, csr_tile_kernel<E, false, false>, m, x, ea, dist);
 }
 
 cudaError_t launch_csr_stream(const DevCsr& m, const double* x, Epi epi, const EpiArgs& ea,
