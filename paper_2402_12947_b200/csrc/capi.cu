@@ -70,17 +70,24 @@ static void free_all(std::vector<void*>& allocs)
 // Greedy tile partition: consecutive rows, <= kRowsPerTile rows, <= cap
 // nonzeros unless a single row is longer.  Small operators (coarse levels)
 // get smaller tiles so every SM still has several independent CTAs.
-// operators whose rows average >= SMG_MC_MIN_ROW nonzeros (default 24) get
-// multi-chunk tiles (csr_tile_kernel<.., kMulti>)
+// Multi-chunk tiles (csr_tile_kernel<.., kMulti>) for operators whose rows
+// average >= SMG_MC_MIN_ROW nonzeros (default 24) -- except operators streamed
+// from HBM with rows averaging >= SMG_MC_MAX_STREAM_ROW (default 36), where the
+// per-chunk serialisation cost more than it saved (profiles/r01/ab_multichunk:
+// C5 and C4's fine level gain 4-10 %, C2 level 1 and C4 levels 1-2 lose).
 static bool long_rows(int64_t nnz, int64_t nrows)
 {
-  static int mc_row = -1;
+  static int mc_row = -1, mc_stream_max = -1;
   if (mc_row < 0) {
     const char* v = getenv("SMG_MC_MIN_ROW");
     mc_row = v ? atoi(v) : 24;
     if (mc_row < 0) mc_row = 0;
+    v = getenv("SMG_MC_MAX_STREAM_ROW");
+    mc_stream_max = v ? atoi(v) : 36;
   }
-  return mc_row > 0 && nrows > 0 && nnz >= (int64_t)mc_row * nrows;
+  if (mc_row == 0 || nrows == 0 || nnz < (int64_t)mc_row * nrows) return false;
+  const bool streamed = nnz * 12 > kStreamBytes;
+  return !streamed || mc_stream_max <= 0 || nnz < (int64_t)mc_stream_max * nrows;
 }
 
 static int64_t tile_cap_for(int64_t nnz, int64_t nrows)

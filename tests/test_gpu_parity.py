@@ -76,6 +76,22 @@ def test_per_sweep_bitwise(P, fx):
         assert np.array_equal(u, z[f"g/cheb{k}"]), f"{name}: sweep {k}"
 
 
+def test_every_level_sweep_and_spmv_bitwise(P, fx):
+    """Coarse Galerkin levels have long rows (multi-chunk tiles when they
+    average >= 24 nonzeros per row): their SpMV and sweeps are bitwise too."""
+    from oracle import oracle as O
+    name, z, h = fx
+    rng = np.random.default_rng(8)
+    for l, lv in enumerate(h.levels[:-1]):
+        n = lv.a.nrows
+        x, b = rng.standard_normal(n), rng.standard_normal(n)
+        assert np.array_equal(P.spmv(lv.a, x), O.spmv(lv.a, x)), f"{name} level {l}"
+        u = x.copy()
+        P.chebyshev_smooth(lv.a, b, u, lv.smoother.sweeps, lv.smoother)
+        assert np.array_equal(u, O.global_smooth(lv.a, b, x.copy(), lv.smoother)), \
+            f"{name} level {l} sweeps"
+
+
 def test_sandwich_and_local_correction(P, fx):
     name, z, h = fx
     lv = h.levels[0]
@@ -294,3 +310,34 @@ def test_edge_cases(P):
     u1 = z["g/u_rand"].copy()
     P.combined_smooth(lv.a, z["g/b"], u1, None, lv.smoother)
     assert np.array_equal(u1, z["g/cheb3"])
+
+
+def test_long_row_operators_multichunk(P):
+    """Operators averaging >= 24 nonzeros per row use multi-chunk tiles
+    (double-buffered chunks); a single row longer than a whole tile spans
+    many chunks.  SpMV and smoother sweeps stay bit-identical."""
+    from paper_2402_12947_b200.sparse import CsrMatrix
+    from oracle import oracle as O
+    n, w = 12000, 40
+    rng = np.random.default_rng(3)
+    r, c = [], []
+    for k in range(-w, w + 1):
+        i = np.arange(max(0, -k), min(n, n - k))
+        r.append(i)
+        c.append(i + k)
+    r.append(np.zeros(n, dtype=np.int64))          # row 0: dense, 12000 nonzeros
+    c.append(np.arange(n))
+    rr, cc = np.concatenate(r), np.concatenate(c)
+    key = np.unique(rr * n + cc)
+    rr, cc = key // n, key % n
+    vals = rng.uniform(-1, 1, len(rr))
+    vals[rr == cc] = 4.0 * w + 1.0
+    a = CsrMatrix.from_coo(n, n, rr, cc, vals)
+    assert a.nnz >= 24 * n
+    x = rng.standard_normal(n)
+    assert np.array_equal(P.spmv(a, x), O.spmv(a, x))
+    b = rng.standard_normal(n)
+    cfg = P.SmootherConfig("chebyshev", 3, lambda_max=2.0)
+    u = x.copy()
+    P.chebyshev_smooth(a, b, u, 3, cfg)
+    assert np.array_equal(u, O.global_smooth(a, b, x.copy(), cfg))
