@@ -256,6 +256,16 @@ __device__ __forceinline__ void ring_issue(const double* Lg, double* ring, int64
       : "memory");
 }
 
+// L2 prefetch of chunk seq (ahead of its bulk copy into the ring)
+__device__ __forceinline__ void chunk_prefetch_l2(const double* Lg, int n, int seq)
+{
+  const ChunkInfo c = chunk_of(seq, n);
+  const int64_t a = tri(c.i0) & ~int64_t(1);
+  const int64_t b = (tri(c.i0 + c.rows) + 1) & ~int64_t(1);
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Lg + a), "r"((uint32_t)((b - a) * 8))
+               : "memory");
+}
+
 __device__ __forceinline__ void ring_wait(uint64_t* bar, uint32_t parity)
 {
   asm volatile(
@@ -289,7 +299,7 @@ __device__ __forceinline__ void dinv_issue(const double* Dinv, double* s_dinv, i
 
 __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_t stage, int n,
                              double* s_x, double* s_dinv, uint64_t* bars, uint64_t* dbars,
-                             double (*red)[32])
+                             double (*red)[32], int pf_chunks)
 {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -305,6 +315,8 @@ __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(psmem_u32(&dbars[s])) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int q = 0; q < kRingStages && q < total; ++q) ring_issue(Lg, ring, stage, n, q, bars);
+    for (int q = kRingStages; q < kRingStages + pf_chunks && q < total; ++q)
+      chunk_prefetch_l2(Lg, n, q);
     for (int q = 0; q < 2 && q < 2 * nb; ++q) dinv_issue(Dinv, s_dinv, q, nb, dbars);
   }
   __syncthreads();
@@ -349,6 +361,10 @@ __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_
     if (threadIdx.x == 0 && seq + kRingStages < total) {  // stage free: next chunk into it
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       ring_issue(Lg, ring, stage, n, seq + kRingStages, bars);
+      // keep pf_chunks further chunks on their way into L2 (a small window:
+      // prefetching whole factors at once thrashed L2)
+      if (pf_chunks > 0 && seq + kRingStages + pf_chunks < total)
+        chunk_prefetch_l2(Lg, n, seq + kRingStages + pf_chunks);
     }
     if (fwd && c.i0 + c.rows == p0 + pn) panel_solve(p0, pn, false);  // forward: panel done
   }
@@ -489,7 +505,7 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   const double* Dinv = L + patch_tri_even(n);   // inverted diagonal blocks, row stride 33
 
   if (!staged && L_.stage > 0) {
-    stream_solve(Lg, s_L, L_.stage, n, s_x, s_prod, s_ring_bar, s_dinv_bar, s_red);
+    stream_solve(Lg, s_L, L_.stage, n, s_x, s_prod, s_ring_bar, s_dinv_bar, s_red, flags >> 8);
   } else {
 
   // ---- forward: L y = r (left-looking over 32-row panels)
@@ -642,7 +658,9 @@ static cudaError_t launch_patch(const Correction& c, size_t smem, const double* 
   cfg.numAttrs = 1;
   static const int l2pf = patch_env("SMG_PATCH_L2PF", 0);  // measured slower on C5 (222 vs 240 us)
   static const int lpt = patch_env("SMG_PATCH_LPT", 1);
-  const int flags = (allow_stream ? kFlagStream : 0) | (l2pf ? kFlagL2Prefetch : 0);
+  static const int pf_chunks = patch_env("SMG_PATCH_PF_CHUNKS", 3);
+  const int flags =
+      (allow_stream ? kFlagStream : 0) | (l2pf ? kFlagL2Prefetch : 0) | (pf_chunks << 8);
   return cudaLaunchKernelEx(&cfg, patch_kernel<kMode>, c.prow, c.pcol, c.pval, c.pptr, c.dofs,
                             c.foff, c.lfac, b, u_res, c.rbuf, tgt, add, c.max_dofs, flags,
                             lpt ? c.order : (const int32_t*)nullptr);
