@@ -157,8 +157,9 @@ struct PatchSmem {
 
 constexpr int kChunkRows = 8;   // factor rows per streamed chunk (divides the 32-row panel)
 // chunks in flight per CTA; measured best on C5: 2 x 8 rows (227 us) beat
-// 4 x 4 rows and a variable-size byte ring holding 2-4 longest chunks
-// (282-475 us: fewer CTAs per SM or more per-chunk overhead)
+// 4 x 4 rows, a variable-size byte ring holding 2-4 longest chunks (282-475
+// us) and an L2 prefetch window 2-6 chunks ahead (265 vs 247 us): the
+// streamed solve is bound by its per-chunk arithmetic, not by copy latency
 constexpr int kRingStages = 2;
 
 __host__ __device__ inline PatchSmem patch_smem_layout(int nmax, bool allow_stream = true)
@@ -256,16 +257,6 @@ __device__ __forceinline__ void ring_issue(const double* Lg, double* ring, int64
       : "memory");
 }
 
-// L2 prefetch of chunk seq (ahead of its bulk copy into the ring)
-__device__ __forceinline__ void chunk_prefetch_l2(const double* Lg, int n, int seq)
-{
-  const ChunkInfo c = chunk_of(seq, n);
-  const int64_t a = tri(c.i0) & ~int64_t(1);
-  const int64_t b = (tri(c.i0 + c.rows) + 1) & ~int64_t(1);
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Lg + a), "r"((uint32_t)((b - a) * 8))
-               : "memory");
-}
-
 __device__ __forceinline__ void ring_wait(uint64_t* bar, uint32_t parity)
 {
   asm volatile(
@@ -299,7 +290,7 @@ __device__ __forceinline__ void dinv_issue(const double* Dinv, double* s_dinv, i
 
 __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_t stage, int n,
                              double* s_x, double* s_dinv, uint64_t* bars, uint64_t* dbars,
-                             double (*red)[32], int pf_chunks)
+                             double (*red)[32])
 {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -315,8 +306,6 @@ __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(psmem_u32(&dbars[s])) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int q = 0; q < kRingStages && q < total; ++q) ring_issue(Lg, ring, stage, n, q, bars);
-    for (int q = kRingStages; q < kRingStages + pf_chunks && q < total; ++q)
-      chunk_prefetch_l2(Lg, n, q);
     for (int q = 0; q < 2 && q < 2 * nb; ++q) dinv_issue(Dinv, s_dinv, q, nb, dbars);
   }
   __syncthreads();
@@ -344,27 +333,40 @@ __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_
       if (warp < c.rows && p0 > 0) {
         const int i = c.i0 + warp;
         const double* Li = rows + tri(i);
-        double acc = 0.0;
-        for (int j = lane; j < p0; j += 32) acc += Li[j] * s_x[j];
-        acc = warp_sum(acc);
+        // four independent partial sums: the loads of the next products do not
+        // wait on the previous multiply-add
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int j = lane;
+        for (; j + 96 < p0; j += 128) {
+          a0 += Li[j] * s_x[j];
+          a1 += Li[j + 32] * s_x[j + 32];
+          a2 += Li[j + 64] * s_x[j + 64];
+          a3 += Li[j + 96] * s_x[j + 96];
+        }
+        for (; j < p0; j += 32) a0 += Li[j] * s_x[j];
+        const double acc = warp_sum((a0 + a1) + (a2 + a3));
         if (lane == 0) s_x[i] -= acc;
       }
     } else if (p0 > 0) {
       // y[c] -= sum_{i in chunk} L[i][c] x_i  for c < p0 (thread per column)
       for (int col = threadIdx.x; col < p0; col += kSolveThreads) {
-        double acc = 0.0;
-        for (int r = 0; r < c.rows; ++r) acc += rows[tri(c.i0 + r) + col] * s_x[c.i0 + r];
-        s_x[col] -= acc;
+        double a0 = 0.0, a1 = 0.0;
+        const double* rc = rows + tri(c.i0) + col;   // row c.i0 + r starts tri(c.i0 + r)
+        int r = 0;
+        for (; r + 1 < c.rows; r += 2) {
+          a0 += rc[0] * s_x[c.i0 + r];
+          rc += c.i0 + r + 1;
+          a1 += rc[0] * s_x[c.i0 + r + 1];
+          rc += c.i0 + r + 2;
+        }
+        if (r < c.rows) a0 += rc[0] * s_x[c.i0 + r];
+        s_x[col] -= a0 + a1;
       }
     }
     __syncthreads();
     if (threadIdx.x == 0 && seq + kRingStages < total) {  // stage free: next chunk into it
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       ring_issue(Lg, ring, stage, n, seq + kRingStages, bars);
-      // keep pf_chunks further chunks on their way into L2 (a small window:
-      // prefetching whole factors at once thrashed L2)
-      if (pf_chunks > 0 && seq + kRingStages + pf_chunks < total)
-        chunk_prefetch_l2(Lg, n, seq + kRingStages + pf_chunks);
     }
     if (fwd && c.i0 + c.rows == p0 + pn) panel_solve(p0, pn, false);  // forward: panel done
   }
@@ -505,7 +507,7 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   const double* Dinv = L + patch_tri_even(n);   // inverted diagonal blocks, row stride 33
 
   if (!staged && L_.stage > 0) {
-    stream_solve(Lg, s_L, L_.stage, n, s_x, s_prod, s_ring_bar, s_dinv_bar, s_red, flags >> 8);
+    stream_solve(Lg, s_L, L_.stage, n, s_x, s_prod, s_ring_bar, s_dinv_bar, s_red);
   } else {
 
   // ---- forward: L y = r (left-looking over 32-row panels)
@@ -518,7 +520,14 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
       double acc = 0.0;
       if (r < pn) {
         const double* Li = L + tri(p0 + r);
-        for (int j = sub; j < p0; j += 8) acc += Li[j] * s_x[j];
+        double a1 = 0.0;
+        int j = sub;
+        for (; j + 8 < p0; j += 16) {
+          acc += Li[j] * s_x[j];
+          a1 += Li[j + 8] * s_x[j + 8];
+        }
+        if (j < p0) acc += Li[j] * s_x[j];
+        acc += a1;
       }
       acc += __shfl_xor_sync(0xffffffffu, acc, 4);
       acc += __shfl_xor_sync(0xffffffffu, acc, 2);
@@ -658,9 +667,7 @@ static cudaError_t launch_patch(const Correction& c, size_t smem, const double* 
   cfg.numAttrs = 1;
   static const int l2pf = patch_env("SMG_PATCH_L2PF", 0);  // measured slower on C5 (222 vs 240 us)
   static const int lpt = patch_env("SMG_PATCH_LPT", 1);
-  static const int pf_chunks = patch_env("SMG_PATCH_PF_CHUNKS", 3);
-  const int flags =
-      (allow_stream ? kFlagStream : 0) | (l2pf ? kFlagL2Prefetch : 0) | (pf_chunks << 8);
+  const int flags = (allow_stream ? kFlagStream : 0) | (l2pf ? kFlagL2Prefetch : 0);
   return cudaLaunchKernelEx(&cfg, patch_kernel<kMode>, c.prow, c.pcol, c.pval, c.pptr, c.dofs,
                             c.foff, c.lfac, b, u_res, c.rbuf, tgt, add, c.max_dofs, flags,
                             lpt ? c.order : (const int32_t*)nullptr);
