@@ -52,6 +52,7 @@ extern "C" {
 typedef struct smg_operator smg_operator;
 typedef struct smg_correction smg_correction;
 typedef struct smg_hierarchy smg_hierarchy;
+typedef struct smg_csr smg_csr;           /* device-resident CSR product result */
 
 SMG_API int smg_abi_version(void);
 SMG_API const char *smg_last_error(void);
@@ -80,6 +81,25 @@ SMG_API int smg_spmv_transpose(const smg_operator *p, const double *r, double *y
 /* u_fine += P u_coarse          (transfer.py:165-172 prolong_add, mg.py:149)     */
 SMG_API int smg_prolong_add(const smg_operator *p, const double *u_coarse, double *u_fine,
                     void *stream);
+
+/* ---- setup: Galerkin coarse operator (sparse.py:147-154 triple_product, via
+ * transfer.py:153-155 coarsen_system, mg.py:100) -------------------------------
+ * *out = P^T (A P) on the device, bit-identical to scipy's `ps.T @ (a @ ps)`:
+ * both products accumulate in csr_matmat's order (each output entry sums its
+ * products in ascending order of the inner index, no FMA), entries whose sum
+ * is exactly 0 are dropped as csr_matmat drops them, rows are canonical
+ * (columns ascending).  p must have been created with_transpose.              */
+SMG_API int smg_galerkin(const smg_operator *a, const smg_operator *p, smg_csr **out,
+                         void *stream);
+/* *out = X Y (scipy csr_matmat order, as above; the building block of
+ * smg_galerkin, exposed for testing and other Galerkin-type products)          */
+SMG_API int smg_matmul(const smg_operator *x, const smg_operator *y, smg_csr **out,
+                       void *stream);
+SMG_API int smg_csr_info(const smg_csr *c, int64_t *nrows, int64_t *ncols, int64_t *nnz);
+/* copy to host CSR arrays (nrows + 1, nnz, nnz; int64 columns as sparse.py:63-65) */
+SMG_API int smg_csr_to_host(const smg_csr *c, int64_t *row_offsets, int64_t *col_indices,
+                            double *values);
+SMG_API int smg_csr_destroy(smg_csr *c);
 
 /* Chebyshev / damped-Jacobi smoother in place on u (smoothers.py:99-136;
  * bitwise).  work: 2*((n+1)/2)*2 device doubles (two 16-byte aligned halves),

@@ -67,6 +67,8 @@ def lib():
         L.oracle_csrT_matvec.argtypes = [ctypes.c_int64, _i64p, _i64p, _f64p, _f64p, _f64p]
         L.oracle_chol_solve.argtypes = [ctypes.c_int64, _f64p, _f64p]
         L.oracle_patch_solves.argtypes = [ctypes.c_int64, _i64p, _i64p, _f64p, _f64p]
+        L.oracle_spgemm.argtypes = [ctypes.c_int64, ctypes.c_int64, _i64p, _i64p, _f64p,
+                                    _i64p, _i64p, _f64p, _i64p, _i64p, _f64p]
         L.oracle_dot.argtypes = [ctypes.c_int64, _f64p, _f64p]
         L.oracle_dot.restype = ctypes.c_double
         L.oracle_num_threads.restype = ctypes.c_int
@@ -176,6 +178,45 @@ def spmv_transpose(p, r: np.ndarray) -> np.ndarray:
 
 def diagonal(a) -> np.ndarray:
     return _csr(a).diagonal()
+
+
+def _spgemm_arrays(nrows, ncols, xptr, xcol, xval, yptr, ycol, yval):
+    ptr = np.zeros(nrows + 1, dtype=np.int64)
+    args = [_p(np.ascontiguousarray(t, dtype=dt), tp)
+            for t, dt, tp in ((xptr, np.int64, _i64p), (xcol, np.int64, _i64p),
+                              (xval, np.float64, _f64p), (yptr, np.int64, _i64p),
+                              (ycol, np.int64, _i64p), (yval, np.float64, _f64p))]
+    keep = [np.ascontiguousarray(t) for t in (xptr, xcol, xval, yptr, ycol, yval)]  # noqa: F841
+    lib().oracle_spgemm(nrows, ncols, *args, _p(ptr, _i64p), None, None)
+    col = np.empty(int(ptr[-1]), dtype=np.int64)
+    val = np.empty(int(ptr[-1]), dtype=np.float64)
+    lib().oracle_spgemm(nrows, ncols, *args, _p(ptr, _i64p), _p(col, _i64p), _p(val, _f64p))
+    return ptr, col, val
+
+
+def spgemm(x, y):
+    """``x @ y`` for CSR x, y (scipy csr_matmat order, explicit zeros dropped,
+    columns sorted); returns (row_offsets, col_indices, values)."""
+    a, b = _csr(x), _csr(y)
+    if a.ncols != b.nrows:
+        raise ValueError(f"dimension mismatch: {a.nrows}x{a.ncols} @ {b.nrows}x{b.ncols}")
+    return _spgemm_arrays(a.nrows, b.ncols, a.ptr, a.col, a.val, b.ptr, b.col, b.val)
+
+
+def galerkin(p, a):
+    """Galerkin coarse operator ``p.T @ (a @ p)`` (sparse.py:147-154) as CSR arrays.
+
+    scipy forms ``a @ p`` with csr_matmat, then ``p.T @ M`` as a CSC product
+    whose column c accumulates ``M[i,c] * P[i,k]`` over fine rows i ascending;
+    the same sums arise from CSR(P^T) @ M with CSR(P^T) listing fine rows
+    ascending (multiplication commutes; the addition order is identical)."""
+    pc, ac = _csr(p), _csr(a)
+    if ac.ncols != pc.nrows or ac.nrows != pc.nrows:
+        raise ValueError(f"dimension mismatch: a is {ac.nrows}x{ac.ncols}, p is {pc.nrows}x{pc.ncols}")
+    mptr, mcol, mval = _spgemm_arrays(ac.nrows, pc.ncols, ac.ptr, ac.col, ac.val,
+                                      pc.ptr, pc.col, pc.val)
+    tptr, tcol, tval = pc.transpose()
+    return _spgemm_arrays(pc.ncols, pc.ncols, tptr, tcol, tval, mptr, mcol, mval)
 
 
 # --------------------------------------------------------------------------

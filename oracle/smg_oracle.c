@@ -19,6 +19,12 @@
  *                       (P.to_scipy().T @ r): y[c] += P[i,c] r[i] for fine
  *                       rows i in ascending order.  Restated over an explicit
  *                       CSR(P^T) whose rows list fine indices ascending.
+ *   oracle_spgemm       scipy sparsetools csr_matmat (SMMP), reached from the
+ *                       Galerkin product sparse.py:147-154 (ps.T @ (a @ ps),
+ *                       via transfer.py:153-155 coarsen_system, mg.py:100):
+ *                       row i of C = X Y accumulates sums[k] += X_ij * Y_jk
+ *                       over X's row in stored (ascending column) order,
+ *                       starting from 0.0, and keeps only sums != 0.
  *   oracle_chol_solve   LAPACK dpotrs via scipy.linalg.cho_solve
  *                       (sparse.py:225-231): forward substitution with L,
  *                       back substitution with L^T.  Sequential order differs
@@ -30,6 +36,7 @@
  * never changes a result bit.
  */
 #include <stdint.h>
+#include <stdlib.h>
 #include <math.h>
 #include <omp.h>
 
@@ -120,4 +127,66 @@ double oracle_dot(int64_t n, const double *a, const double *b)
     double s = 0.0;
     for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
     return s;
+}
+
+/* C = X Y (scipy csr_matmat order, see the header).  The output rows are
+ * canonical (columns ascending), as CsrMatrix.from_scipy leaves them
+ * (sparse.py:93-99: sort_indices; sorting does not touch values).
+ * Pass 1 (cptr != NULL, ccol == NULL): cptr[0..nrows] = row offsets of the
+ * kept entries.  Pass 2 (ccol, cval != NULL): fill them. */
+static int cmp_i64(const void *a, const void *b)
+{
+    int64_t x = *(const int64_t *)a, y = *(const int64_t *)b;
+    return (x > y) - (x < y);
+}
+
+void oracle_spgemm(int64_t nrows, int64_t ncols, const int64_t *xptr, const int64_t *xcol,
+                   const double *xval, const int64_t *yptr, const int64_t *ycol,
+                   const double *yval, int64_t *cptr, int64_t *ccol, double *cval)
+{
+    #pragma omp parallel
+    {
+        double *sums = (double *)calloc((size_t)ncols, sizeof(double));
+        int64_t *mark = (int64_t *)malloc((size_t)ncols * sizeof(int64_t));
+        int64_t *keys = (int64_t *)malloc((size_t)ncols * sizeof(int64_t));
+        for (int64_t k = 0; k < ncols; ++k) mark[k] = -1;
+        #pragma omp for schedule(dynamic, 256)
+        for (int64_t i = 0; i < nrows; ++i) {
+            int64_t nk = 0;
+            for (int64_t jj = xptr[i]; jj < xptr[i + 1]; ++jj) {
+                const int64_t j = xcol[jj];
+                const double v = xval[jj];
+                for (int64_t kk = yptr[j]; kk < yptr[j + 1]; ++kk) {
+                    const int64_t k = ycol[kk];
+                    if (mark[k] != i) {
+                        mark[k] = i;
+                        keys[nk++] = k;
+                    }
+                    sums[k] += v * yval[kk];
+                }
+            }
+            qsort(keys, (size_t)nk, sizeof(int64_t), cmp_i64);
+            int64_t kept = 0;
+            int64_t out = ccol ? cptr[i] : 0;
+            for (int64_t t = 0; t < nk; ++t) {
+                const int64_t k = keys[t];
+                if (sums[k] != 0) {
+                    if (ccol) {
+                        ccol[out + kept] = k;
+                        cval[out + kept] = sums[k];
+                    }
+                    ++kept;
+                }
+                sums[k] = 0.0;
+            }
+            if (!ccol) cptr[i + 1] = kept;
+        }
+        free(sums);
+        free(mark);
+        free(keys);
+    }
+    if (!ccol) {
+        cptr[0] = 0;
+        for (int64_t i = 0; i < nrows; ++i) cptr[i + 1] += cptr[i];
+    }
 }

@@ -66,6 +66,11 @@ PROTOTYPES = {
     "smg_cg": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int, ctypes.c_double, ctypes.c_int,
                               _f64p, _intp, _i64p, _f64p, _vp]),
     "smg_dot": (ctypes.c_int, [_i64, _vp, _vp, _f64p, _vp]),
+    "smg_galerkin": (ctypes.c_int, [_vp, _vp, _pp, _vp]),
+    "smg_matmul": (ctypes.c_int, [_vp, _vp, _pp, _vp]),
+    "smg_csr_info": (ctypes.c_int, [_vp, _i64p, _i64p, _i64p]),
+    "smg_csr_to_host": (ctypes.c_int, [_vp, _i64p, _i64p, _f64p]),
+    "smg_csr_destroy": (ctypes.c_int, [_vp]),
 }
 
 _lib = None

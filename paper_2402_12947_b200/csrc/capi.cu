@@ -575,6 +575,10 @@ struct smg_correction {
 struct smg_hierarchy {
   Hierarchy h;
 };
+struct smg_csr {
+  DevCsrOwned m;
+  ~smg_csr() { m.release(); }
+};
 
 static cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
@@ -730,6 +734,89 @@ int smg_spmv_transpose(const smg_operator* p, const double* r, double* y, void* 
   EpiArgs ea;
   ea.out = y;
   SMG_CUDA(launch_csr_stream(p->o.t, r, Epi::kSpmv, ea, as_stream(stream)));
+  return SMG_OK;
+}
+
+static int spgemm_checked(const DevCsr& x, const DevCsr& y, DevCsrOwned* out, cudaStream_t st)
+{
+  const cudaError_t e = spgemm_device(x, y, out, st);
+  if (e != cudaSuccess) {
+    out->release();
+    return check_cuda(e, "spgemm_device");
+  }
+  return SMG_OK;
+}
+
+int smg_matmul(const smg_operator* x, const smg_operator* y, smg_csr** out, void* stream)
+{
+  if (!out) return fail("out is NULL");
+  *out = nullptr;
+  if (!x || !y) return fail("operator is NULL");
+  if (x->o.a.ncols != y->o.a.nrows) {
+    set_error("dimension mismatch: " + std::to_string(x->o.a.nrows) + "x" +
+              std::to_string(x->o.a.ncols) + " @ " + std::to_string(y->o.a.nrows) + "x" +
+              std::to_string(y->o.a.ncols));
+    return SMG_ERR_DIMENSION;
+  }
+  auto c = std::make_unique<smg_csr>();
+  SMG_TRY(spgemm_checked(x->o.a, y->o.a, &c->m, as_stream(stream)));
+  *out = c.release();
+  return SMG_OK;
+}
+
+int smg_galerkin(const smg_operator* a, const smg_operator* p, smg_csr** out, void* stream)
+{
+  if (!out) return fail("out is NULL");
+  *out = nullptr;
+  if (!a || !p) return fail("operator is NULL");
+  if (a->o.a.ncols != p->o.a.nrows || a->o.a.nrows != p->o.a.nrows) {
+    set_error("dimension mismatch: a is " + std::to_string(a->o.a.nrows) + "x" +
+              std::to_string(a->o.a.ncols) + ", p is " + std::to_string(p->o.a.nrows) + "x" +
+              std::to_string(p->o.a.ncols));
+    return SMG_ERR_DIMENSION;
+  }
+  if (!p->o.has_t) return fail("prolongation was created without its transpose");
+  const cudaStream_t st = as_stream(stream);
+  DevCsrOwned m;  // A P
+  SMG_TRY(spgemm_checked(a->o.a, p->o.a, &m, st));
+  auto c = std::make_unique<smg_csr>();
+  const int rc = spgemm_checked(p->o.t, m.view(), &c->m, st);  // CSR(P^T) (A P)
+  m.release();
+  SMG_TRY(rc);
+  *out = c.release();
+  return SMG_OK;
+}
+
+int smg_csr_info(const smg_csr* c, int64_t* nrows, int64_t* ncols, int64_t* nnz)
+{
+  if (!c) return fail("matrix is NULL");
+  if (nrows) *nrows = c->m.nrows;
+  if (ncols) *ncols = c->m.ncols;
+  if (nnz) *nnz = c->m.nnz;
+  return SMG_OK;
+}
+
+int smg_csr_to_host(const smg_csr* c, int64_t* row_offsets, int64_t* col_indices, double* values)
+{
+  if (!c) return fail("matrix is NULL");
+  const DevCsrOwned& m = c->m;
+  if (row_offsets)
+    SMG_CUDA(cudaMemcpy(row_offsets, m.rowptr, (size_t)(m.nrows + 1) * sizeof(int64_t),
+                        cudaMemcpyDeviceToHost));
+  if (col_indices && m.nnz > 0) {
+    std::vector<int32_t> tmp((size_t)m.nnz);
+    SMG_CUDA(cudaMemcpy(tmp.data(), m.col, (size_t)m.nnz * sizeof(int32_t),
+                        cudaMemcpyDeviceToHost));
+    for (int64_t k = 0; k < m.nnz; ++k) col_indices[k] = tmp[(size_t)k];
+  }
+  if (values && m.nnz > 0)
+    SMG_CUDA(cudaMemcpy(values, m.val, (size_t)m.nnz * sizeof(double), cudaMemcpyDeviceToHost));
+  return SMG_OK;
+}
+
+int smg_csr_destroy(smg_csr* c)
+{
+  delete c;
   return SMG_OK;
 }
 

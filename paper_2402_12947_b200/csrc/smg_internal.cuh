@@ -164,6 +164,18 @@ struct SymTiles {
 cudaError_t launch_sym_apply(const SymTiles& m, const double* x, double* y, bool add,
                              cudaStream_t s);
 
+// sparse matrix product C = X Y in scipy csr_matmat's order, bit-identical
+// (galerkin_kernels.cu; the Galerkin operator P^T (A P), sparse.py:147-154)
+struct DevCsrOwned {
+  int64_t nrows = 0, ncols = 0, nnz = 0;
+  int64_t* rowptr = nullptr;
+  int32_t* col = nullptr;
+  double* val = nullptr;
+  void release();
+  DevCsr view() const;
+};
+cudaError_t spgemm_device(const DevCsr& X, const DevCsr& Y, DevCsrOwned* out, cudaStream_t s);
+
 // dense / reduction kernels (dense_kernels.cu)
 cudaError_t launch_dot(int64_t n, const double* a, const double* b, double* partials,
                        unsigned int* counter, double* result, cudaStream_t s);

@@ -159,5 +159,38 @@ def device_correction(a, correction) -> DeviceCorrection:
     return _cached(_corr_cache, correction, lambda: DeviceCorrection(op, correction))
 
 
+def _csr_result_to_host(lib, h):
+    """Copy an smg_csr result to host arrays and free it."""
+    try:
+        nr, nc, nnz = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(lib.smg_csr_info(h, ctypes.byref(nr), ctypes.byref(nc), ctypes.byref(nnz)))
+        ptr_ = np.empty(nr.value + 1, dtype=np.int64)
+        col = np.empty(nnz.value, dtype=np.int64)
+        val = np.empty(nnz.value, dtype=np.float64)
+        _lib.check(lib.smg_csr_to_host(h, _i64(ptr_), _i64(col), _f64(val)))
+        return nr.value, nc.value, ptr_, col, val
+    finally:
+        lib.smg_csr_destroy(h)
+
+
+def galerkin(a, p):
+    """``P^T (A P)`` on the device (smg_galerkin): (nrows, ncols, ptr, col, val)."""
+    lib = _lib.load()
+    oa = device_operator(a)
+    op = device_operator(p, with_transpose=True)
+    h = ctypes.c_void_p()
+    _lib.check(lib.smg_galerkin(oa.handle, op.handle, ctypes.byref(h), stream_handle()))
+    return _csr_result_to_host(lib, h)
+
+
+def matmul(x, y):
+    """``X Y`` on the device (smg_matmul): (nrows, ncols, ptr, col, val)."""
+    lib = _lib.load()
+    ox, oy = device_operator(x), device_operator(y)
+    h = ctypes.c_void_p()
+    _lib.check(lib.smg_matmul(ox.handle, oy.handle, ctypes.byref(h), stream_handle()))
+    return _csr_result_to_host(lib, h)
+
+
 def ptr(t) -> int:
     return int(t.data_ptr())

@@ -328,8 +328,14 @@ def as_preconditioner(h) -> Callable:
 def build_hierarchy(meshes: Sequence, smoother: SmootherConfig, use_local_correction: bool,
                     quality_threshold: float = 0.1, element_degree: int = 1,
                     source=None, region_layers: int = 1,
-                    lambda_tol: float = 1e-8, coarse_refine: bool = False) -> Hierarchy:
-    """Poisson with homogeneous Dirichlet on every box face; fine to coarse meshes."""
+                    lambda_tol: float = 1e-8, coarse_refine: bool = False,
+                    device_setup: Optional[bool] = None) -> Hierarchy:
+    """Poisson with homogeneous Dirichlet on every box face; fine to coarse meshes.
+
+    ``device_setup``: Galerkin products on the GPU (``smg_galerkin``, bit-identical
+    to the reference's scipy product); default: whenever a CUDA device exists.
+    Host-only setup (no GPU, e.g. the CPU test suite) uses the reference's own
+    scipy product."""
     from .fem import assemble_poisson, build_dofmap
     from .mesh import identify_regions
     from .smoothers import (adjusted_lambda_max, build_local_correction, dofs_for_regions,
@@ -337,28 +343,52 @@ def build_hierarchy(meshes: Sequence, smoother: SmootherConfig, use_local_correc
     from .transfer import build_prolongation, coarsen_system
     if len(meshes) < 2:
         raise ValueError(f"a hierarchy needs at least 2 meshes, got {len(meshes)}")
+    if device_setup is None:
+        from .device import torch
+        device_setup = bool(torch().cuda.is_available())
+    import time
+    times = {"dofmap_s": 0.0, "assembly_s": 0.0, "prolongation_s": 0.0, "galerkin_s": 0.0,
+             "regions_s": 0.0, "local_factor_s": 0.0, "lambda_s": 0.0, "coarse_factor_s": 0.0}
+    t = time.perf_counter()
     dofmaps = [build_dofmap(m, element_degree) for m in meshes]
+    times["dofmap_s"] += time.perf_counter() - t
+    t = time.perf_counter()
     system = assemble_poisson(meshes[0], dofmaps[0], source)
+    times["assembly_s"] += time.perf_counter() - t
     operators = [system.a]
     prolongations = []
     for l in range(len(meshes) - 1):
+        t = time.perf_counter()
         p = build_prolongation(dofmaps[l], meshes[l + 1], dofmaps[l + 1])
         prolongations.append(Prolongation(p, l, l + 1))
-        operators.append(coarsen_system(operators[l], p))
+        times["prolongation_s"] += time.perf_counter() - t
+        t = time.perf_counter()
+        operators.append(coarsen_system(operators[l], p, device=device_setup))
+        times["galerkin_s"] += time.perf_counter() - t
     levels = []
     for l, (mesh, dofmap, a) in enumerate(zip(meshes, dofmaps, operators)):
+        t = time.perf_counter()
         regions = identify_regions(mesh, quality_threshold, layers=region_layers)
         dof_sets = dofs_for_regions(dofmap, mesh, regions)
+        times["regions_s"] += time.perf_counter() - t
         correction = None
         if use_local_correction and dof_sets:
+            t = time.perf_counter()
             correction = build_local_correction(a, dof_sets)
+            times["local_factor_s"] += time.perf_counter() - t
         lam = lam_adj = None
         cfg = smoother
         if smoother.kind == "chebyshev":
+            t = time.perf_counter()
             lam = jacobi_lambda_max(a, lambda_tol)
             lam_adj = adjusted_lambda_max(a, dof_sets, lambda_tol) if dof_sets else lam
             cfg = replace(smoother, lambda_max=lam_adj if smoother.adjusted else lam)
+            times["lambda_s"] += time.perf_counter() - t
         prol = prolongations[l] if l < len(prolongations) else None
         levels.append(Level(l, mesh, dofmap, a, prol, cfg, regions, correction, None, lam, lam_adj))
+    t = time.perf_counter()
     coarse = dense_factor(operators[-1].to_dense())
-    return Hierarchy(levels, coarse, system, coarse_refine)
+    times["coarse_factor_s"] += time.perf_counter() - t
+    h = Hierarchy(levels, coarse, system, coarse_refine)
+    h.setup_times = dict(times, galerkin_device=bool(device_setup))
+    return h

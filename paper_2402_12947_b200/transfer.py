@@ -17,7 +17,7 @@ import scipy.sparse as sp
 
 from .fem import DofMap, basis_values
 from .mesh import SimplexMesh
-from .sparse import CsrMatrix, triple_product
+from .sparse import CsrMatrix, host_triple_product, triple_product
 
 
 class PointLocationError(RuntimeError):
@@ -135,6 +135,9 @@ def build_prolongation(fine: DofMap, coarse_mesh: SimplexMesh, coarse: DofMap,
     return CsrMatrix.from_scipy(m)
 
 
-def coarsen_system(a_fine, p) -> CsrMatrix:
-    """Galerkin coarse operator (transfer.py:153-155)."""
-    return triple_product(getattr(p, "matrix", p), a_fine)
+def coarsen_system(a_fine, p, device: bool = True) -> CsrMatrix:
+    """Galerkin coarse operator (transfer.py:153-155): on the GPU by default
+    (``smg_galerkin``, bit-identical); ``device=False`` is the host-only setup
+    path (the reference's scipy product)."""
+    m = getattr(p, "matrix", p)
+    return triple_product(m, a_fine) if device else host_triple_product(m, a_fine)

@@ -142,3 +142,55 @@ def test_oracle_edge_cases():
     z = CsrMatrix.from_dense(np.diag([1.0, 0.0, 2.0]) + np.eye(3, k=1))
     with pytest.raises(O.ZeroDiagonalError):
         O.chebyshev_smooth(z, np.ones(3), np.zeros(3), 1, SmootherConfig("chebyshev", 1, 1.0))
+
+
+# ---------------------------------------------------------------------------
+# Galerkin coarse operators (sparse.py:147-154 triple_product)
+
+def _csr_equal(ptr, col, val, m) -> bool:
+    return (np.array_equal(ptr, m.row_offsets) and np.array_equal(col, m.col_indices)
+            and np.array_equal(val, m.values))
+
+
+def test_galerkin_bitwise_vs_reference_coarse_operators(fx):
+    """The reference built every A_{l+1} as triple_product(P_l, A_l): the
+    oracle reproduces pattern, column order and every value bit for bit."""
+    name, z, h = fx
+    for l in range(len(h.levels) - 1):
+        lv = h.levels[l]
+        ptr, col, val = O.galerkin(lv.prolongation.matrix, lv.a)
+        assert _csr_equal(ptr, col, val, h.levels[l + 1].a), f"{name} level {l + 1}"
+
+
+def random_int_csr(rng, nrows, ncols, density, values=(-2.0, -1.0, 1.0, 2.0), empty_rows=()):
+    """Small-integer CSR: exact cancellations (zero sums) happen often."""
+    import scipy.sparse as sp
+    from paper_2402_12947_b200.sparse import CsrMatrix
+    m = sp.random(nrows, ncols, density=density, format="csr", random_state=rng,
+                  data_rvs=lambda k: rng.choice(values, size=k))
+    m = m.tolil()
+    for r in empty_rows:
+        m.rows[r] = []
+        m.data[r] = []
+    return CsrMatrix.from_scipy(m.tocsr())
+
+
+def test_spgemm_matches_scipy_with_cancellations():
+    """oracle.spgemm is scipy's csr_matmat: zero sums dropped, sums in order."""
+    rng = np.random.default_rng(5)
+    for (n, k, m, d) in [(40, 30, 50, 0.2), (7, 300, 9, 0.5), (60, 60, 60, 0.05)]:
+        x = random_int_csr(rng, n, k, d, empty_rows=(0, n // 2))
+        y = random_int_csr(rng, k, m, d)
+        ref = (x.to_scipy() @ y.to_scipy()).tocsr()
+        ref.sort_indices()
+        ptr, col, val = O.spgemm(x, y)
+        assert np.array_equal(ptr, ref.indptr) and np.array_equal(col, ref.indices)
+        assert np.array_equal(val, ref.data)
+        assert np.all(val != 0.0)
+    # irrational values: the per-entry sum order matters and is scipy's
+    xf = random_int_csr(rng, 50, 80, 0.3, values=tuple(rng.standard_normal(16)))
+    yf = random_int_csr(rng, 80, 40, 0.3, values=tuple(rng.standard_normal(16)))
+    ref = (xf.to_scipy() @ yf.to_scipy()).tocsr()
+    ref.sort_indices()
+    ptr, col, val = O.spgemm(xf, yf)
+    assert np.array_equal(val, ref.data) and np.array_equal(col, ref.indices)
