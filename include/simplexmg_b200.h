@@ -42,6 +42,7 @@ extern "C" {
 #define SMG_ERR_ZERO_DIAGONAL 4  /* ZeroDiagonalError(row) (smoothers.py:112-114)     */
 #define SMG_ERR_INDEFINITE 5     /* IndefiniteOperatorError (sparse.py:199-200)       */
 #define SMG_ERR_UNSUPPORTED 6    /* NotImplementedError (e.g. SGS smoother)           */
+#define SMG_ERR_POINT_LOCATION 7 /* PointLocationError (transfer.py:21-33)            */
 
 /* smoother kinds (smoothers.py:33-59).  SMG_SMOOTHER_CHEBYSHEV with
  * lambda_min_fraction == 1 is the reference's damped-Jacobi branch
@@ -100,6 +101,28 @@ SMG_API int smg_csr_info(const smg_csr *c, int64_t *nrows, int64_t *ncols, int64
 SMG_API int smg_csr_to_host(const smg_csr *c, int64_t *row_offsets, int64_t *col_indices,
                             double *values);
 SMG_API int smg_csr_destroy(smg_csr *c);
+
+/* ---- setup: interpolation prolongation (transfer.py:117-150 build_prolongation
+ * with CellLocator.locate, transfer.py:36-91) ---------------------------------
+ * Row i of *out holds the coarse Lagrange basis (degree 1 or 2, dim 2 or 3)
+ * evaluated at fine point i inside the lowest-index coarse cell whose
+ * barycentric coordinates are all >= -tol (candidates: the cells listed for the
+ * point's bin, ascending; if none hits, every cell), clamped to [0, 1] and
+ * renormalised; entries with |value| <= drop_tol are dropped.  Host inputs:
+ * points (n_points x dim), the coarse cells' first vertices v0 (n_cells x dim)
+ * and inverse Jacobians inv_jac (n_cells x dim x dim, np.linalg.inv of the
+ * edge matrices as transfer.py:46-48 forms them), cell_nodes (n_cells x
+ * nodes per cell), and the bin index: nb bins per dimension over
+ * [lo, hi] with scale = nb / span, bin_ptr (nb^dim + 1) / bin_cells.  Bitwise
+ * equal to the reference's P.  A point outside every cell returns
+ * SMG_ERR_POINT_LOCATION with *failed_point = the lowest such index.          */
+SMG_API int smg_prolongation_build(int dim, int degree, int64_t n_points, const double *points,
+                                   int64_t n_cells, const double *v0, const double *inv_jac,
+                                   const int64_t *cell_nodes, int64_t n_coarse_nodes, int nb,
+                                   const double *lo, const double *hi, const double *scale,
+                                   const int64_t *bin_ptr, const int64_t *bin_cells, double tol,
+                                   double drop_tol, smg_csr **out, int64_t *failed_point,
+                                   void *stream);
 
 /* Chebyshev / damped-Jacobi smoother in place on u (smoothers.py:99-136;
  * bitwise).  work: 2*((n+1)/2)*2 device doubles (two 16-byte aligned halves),

@@ -787,6 +787,79 @@ int smg_galerkin(const smg_operator* a, const smg_operator* p, smg_csr** out, vo
   return SMG_OK;
 }
 
+int smg_prolongation_build(int dim, int degree, int64_t n_points, const double* points,
+                           int64_t n_cells, const double* v0, const double* inv_jac,
+                           const int64_t* cell_nodes, int64_t n_coarse_nodes, int nb,
+                           const double* lo, const double* hi, const double* scale,
+                           const int64_t* bin_ptr, const int64_t* bin_cells, double tol,
+                           double drop_tol, smg_csr** out, int64_t* failed_point, void* stream)
+{
+  if (!out) return fail("out is NULL");
+  *out = nullptr;
+  if (failed_point) *failed_point = -1;
+  if (dim != 2 && dim != 3) return fail("dim must be 2 or 3");
+  if (degree != 1 && degree != 2) return fail("element degree must be 1 or 2");
+  if (n_points < 0 || n_cells <= 0 || nb <= 0 || n_coarse_nodes <= 0)
+    return fail("empty coarse mesh or negative sizes");
+  if (n_points >= INT32_MAX || n_coarse_nodes >= INT32_MAX)
+    return fail("dimensions exceed int32 indexing");
+  if ((n_points > 0 && !points) || !v0 || !inv_jac || !cell_nodes || !lo || !hi || !scale ||
+      !bin_ptr || !bin_cells)
+    return fail("NULL input array");
+  const int npc = degree == 1 ? dim + 1 : (dim + 1) * (dim + 2) / 2;
+  int64_t nbins = 1;
+  for (int d = 0; d < dim; ++d) nbins *= nb;
+  const int64_t nbc = bin_ptr[nbins];
+  for (int64_t k = 0; k < n_cells * npc; ++k)
+    if (cell_nodes[k] < 0 || cell_nodes[k] >= n_coarse_nodes) return fail("cell node out of range");
+  for (int64_t k = 0; k < nbc; ++k)
+    if (bin_cells[k] < 0 || bin_cells[k] >= n_cells) return fail("bin cell out of range");
+  std::vector<void*> tmp;
+  int64_t bytes = 0;
+  LocateArgs a;
+  a.n_points = n_points;
+  a.n_cells = n_cells;
+  a.n_coarse = n_coarse_nodes;
+  a.nb = nb;
+  for (int d = 0; d < dim; ++d) {
+    a.lo[d] = lo[d];
+    a.hi[d] = hi[d];
+    a.scale[d] = scale[d];
+  }
+  a.tol = tol;
+  a.drop_tol = drop_tol;
+  double *dp = nullptr, *dv0 = nullptr, *dinv = nullptr;
+  int64_t *dcn = nullptr, *dbp = nullptr, *dbc = nullptr;
+  int rc = dev_upload(tmp, bytes, points, (size_t)(n_points * dim), &dp);
+  if (rc == SMG_OK) rc = dev_upload(tmp, bytes, v0, (size_t)(n_cells * dim), &dv0);
+  if (rc == SMG_OK) rc = dev_upload(tmp, bytes, inv_jac, (size_t)(n_cells * dim * dim), &dinv);
+  if (rc == SMG_OK) rc = dev_upload(tmp, bytes, cell_nodes, (size_t)(n_cells * npc), &dcn);
+  if (rc == SMG_OK) rc = dev_upload(tmp, bytes, bin_ptr, (size_t)(nbins + 1), &dbp);
+  if (rc == SMG_OK) rc = dev_upload(tmp, bytes, bin_cells, (size_t)std::max<int64_t>(nbc, 1), &dbc);
+  if (rc != SMG_OK) {
+    free_all(tmp);
+    return rc;
+  }
+  a.points = dp;
+  a.v0 = dv0;
+  a.inv_jac = dinv;
+  a.cell_nodes = dcn;
+  a.bin_ptr = dbp;
+  a.bin_cells = dbc;
+  auto c = std::make_unique<smg_csr>();
+  int64_t bad = -1;
+  const cudaError_t e = prolongation_device(a, dim, degree, &c->m, &bad, as_stream(stream));
+  free_all(tmp);
+  if (e != cudaSuccess) return check_cuda(e, "prolongation_device");
+  if (bad >= 0) {
+    if (failed_point) *failed_point = bad;
+    set_error("point " + std::to_string(bad) + " lies outside the coarse mesh");
+    return SMG_ERR_POINT_LOCATION;
+  }
+  *out = c.release();
+  return SMG_OK;
+}
+
 int smg_csr_info(const smg_csr* c, int64_t* nrows, int64_t* ncols, int64_t* nnz)
 {
   if (!c) return fail("matrix is NULL");

@@ -176,6 +176,24 @@ struct DevCsrOwned {
 };
 cudaError_t spgemm_device(const DevCsr& X, const DevCsr& Y, DevCsrOwned* out, cudaStream_t s);
 
+// prolongation rows by point location (transfer_kernels.cu; transfer.py:73-150)
+struct LocateArgs {
+  int64_t n_points = 0;
+  const double* points = nullptr;      // n_points x dim fine DOF coordinates
+  int64_t n_cells = 0;
+  const double* v0 = nullptr;          // n_cells x dim first vertex of each coarse cell
+  const double* inv_jac = nullptr;     // n_cells x dim x dim (np.linalg.inv of the edge matrix)
+  const int64_t* cell_nodes = nullptr; // n_cells x nodes-per-cell coarse DOFs
+  int64_t n_coarse = 0;
+  int nb = 1;                          // bins per dimension
+  double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0}, scale[3] = {0, 0, 0};
+  const int64_t* bin_ptr = nullptr;    // nb^dim + 1
+  const int64_t* bin_cells = nullptr;  // ascending cell ids per bin
+  double tol = 1e-10, drop_tol = 1e-14;
+};
+cudaError_t prolongation_device(const LocateArgs& a, int dim, int degree, DevCsrOwned* out,
+                                int64_t* failed_point, cudaStream_t s);
+
 // dense / reduction kernels (dense_kernels.cu)
 cudaError_t launch_dot(int64_t n, const double* a, const double* b, double* partials,
                        unsigned int* counter, double* result, cudaStream_t s);

@@ -332,8 +332,9 @@ def build_hierarchy(meshes: Sequence, smoother: SmootherConfig, use_local_correc
                     device_setup: Optional[bool] = None) -> Hierarchy:
     """Poisson with homogeneous Dirichlet on every box face; fine to coarse meshes.
 
-    ``device_setup``: Galerkin products on the GPU (``smg_galerkin``, bit-identical
-    to the reference's scipy product); default: whenever a CUDA device exists.
+    ``device_setup``: prolongations (point location, ``smg_prolongation_build``)
+    and Galerkin products (``smg_galerkin``) on the GPU, both bit-identical to
+    the reference's; default: whenever a CUDA device exists.
     Host-only setup (no GPU, e.g. the CPU test suite) uses the reference's own
     scipy product."""
     from .fem import assemble_poisson, build_dofmap
@@ -359,7 +360,7 @@ def build_hierarchy(meshes: Sequence, smoother: SmootherConfig, use_local_correc
     prolongations = []
     for l in range(len(meshes) - 1):
         t = time.perf_counter()
-        p = build_prolongation(dofmaps[l], meshes[l + 1], dofmaps[l + 1])
+        p = build_prolongation(dofmaps[l], meshes[l + 1], dofmaps[l + 1], device=device_setup)
         prolongations.append(Prolongation(p, l, l + 1))
         times["prolongation_s"] += time.perf_counter() - t
         t = time.perf_counter()

@@ -118,11 +118,18 @@ class CellLocator:
 
 
 def build_prolongation(fine: DofMap, coarse_mesh: SimplexMesh, coarse: DofMap,
-                       drop_tol: float = 1e-14) -> CsrMatrix:
-    """Row i holds the coarse basis values at fine dof i (transfer.py:117-150)."""
+                       drop_tol: float = 1e-14, device: bool = False) -> CsrMatrix:
+    """Row i holds the coarse basis values at fine dof i (transfer.py:117-150).
+
+    ``device=True``: point location and basis evaluation run on the GPU
+    (``smg_prolongation_build``, one thread per fine DOF; bit-identical); the
+    bin index and the inverse Jacobians are formed here exactly as the
+    reference forms them.  ``device=False``: the vectorised host restatement."""
     if fine.element_degree != coarse.element_degree:
         raise ValueError("fine and coarse dof maps must have equal element degree")
     loc = CellLocator(coarse_mesh)
+    if device:
+        return _build_prolongation_device(fine, coarse_mesh, coarse, loc, drop_tol)
     cells, bary = loc.locate(fine.node_coords)
     point = bary[:, 1:]
     lam = np.column_stack([1.0 - point.sum(axis=1), point])
@@ -133,6 +140,42 @@ def build_prolongation(fine: DofMap, coarse_mesh: SimplexMesh, coarse: DofMap,
     m = sp.coo_matrix((values[keep], (rows, nodes[keep])),
                       shape=(fine.n_nodes, coarse.n_nodes)).tocsr()
     return CsrMatrix.from_scipy(m)
+
+
+def _build_prolongation_device(fine, coarse_mesh, coarse, loc, drop_tol) -> CsrMatrix:
+    import ctypes
+    from . import _lib
+    from . import device as _dev
+    _dev.require_cuda()
+    lib = _lib.load()
+    dim = coarse_mesh.dim
+    i64p = ctypes.POINTER(ctypes.c_int64)
+    f64p = ctypes.POINTER(ctypes.c_double)
+
+    def f64(a):
+        return np.ascontiguousarray(a, dtype=np.float64)
+
+    def i64(a):
+        return np.ascontiguousarray(a, dtype=np.int64)
+
+    pts, v0, inv = f64(fine.node_coords), f64(loc._v0), f64(loc._inv_jac)
+    nodes = i64(coarse.cell_nodes)
+    lo, hi, scale = f64(loc._lo), f64(loc._hi), f64(loc._scale)
+    bptr, bcells = i64(loc._bin_ptr), i64(loc._bin_cells)
+    out = ctypes.c_void_p()
+    bad = ctypes.c_int64(-1)
+    rc = lib.smg_prolongation_build(
+        dim, int(coarse.element_degree), len(pts), pts.ctypes.data_as(f64p), len(v0),
+        v0.ctypes.data_as(f64p), inv.ctypes.data_as(f64p), nodes.ctypes.data_as(i64p),
+        int(coarse.n_nodes), int(loc._nb), lo.ctypes.data_as(f64p), hi.ctypes.data_as(f64p),
+        scale.ctypes.data_as(f64p), bptr.ctypes.data_as(i64p), bcells.ctypes.data_as(i64p),
+        float(loc.tol), float(drop_tol), ctypes.byref(out), ctypes.byref(bad),
+        _dev.stream_handle())
+    if rc == _lib.SMG_ERR_POINT_LOCATION:
+        raise PointLocationError(pts[bad.value], dof_index=int(bad.value))
+    _lib.check(rc)
+    nr, nc, ptr, col, val = _dev._csr_result_to_host(lib, out)
+    return CsrMatrix(nr, nc, ptr, col, val)
 
 
 def coarsen_system(a_fine, p, device: bool = True) -> CsrMatrix:
