@@ -43,6 +43,7 @@ extern "C" {
 #define SMG_ERR_INDEFINITE 5     /* IndefiniteOperatorError (sparse.py:199-200)       */
 #define SMG_ERR_UNSUPPORTED 6    /* NotImplementedError (e.g. SGS smoother)           */
 #define SMG_ERR_POINT_LOCATION 7 /* PointLocationError (transfer.py:21-33)            */
+#define SMG_ERR_NOT_SPD 8        /* NotPositiveDefiniteError (sparse.py:234-254)      */
 
 /* smoother kinds (smoothers.py:33-59).  SMG_SMOOTHER_CHEBYSHEV with
  * lambda_min_fraction == 1 is the reference's damped-Jacobi branch
@@ -156,6 +157,19 @@ SMG_API int smg_correction_create(const smg_operator *a, int64_t n_regions,
 SMG_API int smg_correction_destroy(smg_correction *c);
 SMG_API int smg_correction_info(const smg_correction *c, int64_t *n_regions, int64_t *covered_dofs,
                         int *coupled, int64_t *device_bytes);
+/* Factor every region's principal submatrix on the device (setup;
+ * smoothers.py:176-200 build_local_correction -> sparse.py:234-254
+ * dense_factor(lu_fallback=False) -> scipy cho_factor(lower=True)): one CTA per
+ * region gathers A[B_d, B_d] and runs a blocked Cholesky.  factors (host, size
+ * sum n_d^2, region order, row-major) receives cho_factor's `c` layout: L in
+ * the lower triangle, A in the strict upper triangle.  Errors, first failing
+ * region in order: SMG_ERR_INVALID "… expects a symmetric matrix" when
+ * max|a - a^T| > 1e-10 max|a| (sparse.py:245-247), SMG_ERR_NOT_SPD with
+ * *failed_region / *failed_minor (dpotrf info) when a pivot is not positive.
+ * Region dofs must be sorted, unique, disjoint and in range.                  */
+SMG_API int smg_patch_factor(const smg_operator *a, int64_t n_regions,
+                             const int64_t *region_offsets, const int64_t *dofs, double *factors,
+                             int64_t *failed_region, int64_t *failed_minor, void *stream);
 /* out = S_c r, zero outside the regions (smoothers.py:203-211)                    */
 SMG_API int smg_apply_local_correction(const smg_correction *c, const double *r, double *out,
                                void *stream);

@@ -29,6 +29,7 @@ SMG_ERR_ZERO_DIAGONAL = 4
 SMG_ERR_INDEFINITE = 5
 SMG_ERR_UNSUPPORTED = 6
 SMG_ERR_POINT_LOCATION = 7
+SMG_ERR_NOT_SPD = 8
 
 # name -> (restype, argtypes); mirrors include/simplexmg_b200.h
 PROTOTYPES = {
@@ -72,6 +73,7 @@ PROTOTYPES = {
     "smg_csr_info": (ctypes.c_int, [_vp, _i64p, _i64p, _i64p]),
     "smg_csr_to_host": (ctypes.c_int, [_vp, _i64p, _i64p, _f64p]),
     "smg_csr_destroy": (ctypes.c_int, [_vp]),
+    "smg_patch_factor": (ctypes.c_int, [_vp, _i64, _i64p, _i64p, _f64p, _i64p, _i64p, _vp]),
     "smg_prolongation_build": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _i64, _f64p, _i64, _f64p,
                                               _f64p, _i64p, _i64, ctypes.c_int, _f64p, _f64p,
                                               _f64p, _i64p, _i64p, ctypes.c_double,

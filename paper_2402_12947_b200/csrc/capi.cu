@@ -1064,6 +1064,90 @@ static int build_halo(const Operator& o, const std::vector<int32_t>& dof32,
   return SMG_OK;
 }
 
+int smg_patch_factor(const smg_operator* a, int64_t n_regions, const int64_t* roff,
+                     const int64_t* dofs, double* factors, int64_t* failed_region,
+                     int64_t* failed_minor, void* stream)
+{
+  if (failed_region) *failed_region = -1;
+  if (failed_minor) *failed_minor = 0;
+  if (!a) return fail("operator is NULL");
+  const Operator& o = a->o;
+  const int64_t n = o.a.nrows;
+  if (o.a.nrows != o.a.ncols) return fail("local corrections need a square operator");
+  if (n_regions < 0) return fail("negative region count");
+  if (n_regions == 0) return SMG_OK;
+  if (!roff || !dofs || !factors) return fail("NULL region arrays");
+  std::vector<uint8_t> seen((size_t)n, 0);
+  const int64_t m = roff[n_regions];
+  std::vector<int32_t> pptr((size_t)n_regions + 1), dof32((size_t)m);
+  std::vector<int64_t> foff((size_t)n_regions + 1, 0);
+  for (int64_t r = 0; r < n_regions; ++r) {
+    const int64_t nd = roff[r + 1] - roff[r];
+    if (nd <= 0) return fail("region " + std::to_string(r) + " is empty");
+    pptr[(size_t)r] = (int32_t)roff[r];
+    foff[(size_t)r + 1] = foff[(size_t)r] + nd * nd;
+    for (int64_t k = roff[r]; k < roff[r + 1]; ++k) {
+      const int64_t g = dofs[k];
+      if (g < 0 || g >= n)
+        return fail("region " + std::to_string(r) + " has dof indices outside 0.." +
+                    std::to_string(n - 1));
+      if (k > roff[r] && g <= dofs[k - 1])
+        return fail("region " + std::to_string(r) + " dofs must be sorted and unique");
+      if (seen[(size_t)g]) return fail("region " + std::to_string(r) + " overlaps a previous region's dofs");
+      seen[(size_t)g] = 1;
+      dof32[(size_t)k] = (int32_t)g;
+    }
+  }
+  pptr[(size_t)n_regions] = (int32_t)m;
+  std::vector<void*> tmp;
+  int64_t bytes = 0;
+  int32_t *dp = nullptr, *dd = nullptr;
+  int64_t *df = nullptr, *dst = nullptr;
+  double *dw = nullptr, *dsym = nullptr;
+  const cudaStream_t st = as_stream(stream);
+  int rc = dev_upload(tmp, bytes, pptr.data(), pptr.size(), &dp);
+  if (rc == SMG_OK) rc = dev_upload(tmp, bytes, dof32.data(), dof32.size(), &dd);
+  if (rc == SMG_OK) rc = dev_upload(tmp, bytes, foff.data(), foff.size(), &df);
+  if (rc == SMG_OK) rc = dev_alloc(tmp, bytes, (size_t)foff.back(), &dw);
+  if (rc == SMG_OK) rc = dev_alloc(tmp, bytes, (size_t)n_regions, &dst);
+  if (rc == SMG_OK) rc = dev_alloc(tmp, bytes, (size_t)n_regions * 2, &dsym);
+  if (rc == SMG_OK)
+    rc = check_cuda(cudaMemsetAsync(dst, 0, sizeof(int64_t) * (size_t)n_regions, st), "memset");
+  if (rc == SMG_OK)
+    rc = check_cuda(launch_patch_factor(o.a, n_regions, dp, dd, df, dw, dst, dsym, st),
+                    "patch_factor_kernel");
+  std::vector<int64_t> status((size_t)n_regions);
+  std::vector<double> sym((size_t)n_regions * 2);
+  if (rc == SMG_OK) rc = check_cuda(cudaStreamSynchronize(st), "patch factor");
+  if (rc == SMG_OK)
+    rc = check_cuda(cudaMemcpy(status.data(), dst, sizeof(int64_t) * status.size(),
+                               cudaMemcpyDeviceToHost), "status D2H");
+  if (rc == SMG_OK)
+    rc = check_cuda(cudaMemcpy(sym.data(), dsym, sizeof(double) * sym.size(),
+                               cudaMemcpyDeviceToHost), "sym D2H");
+  if (rc == SMG_OK)
+    rc = check_cuda(cudaMemcpy(factors, dw, sizeof(double) * (size_t)foff.back(),
+                               cudaMemcpyDeviceToHost), "factors D2H");
+  free_all(tmp);
+  SMG_TRY(rc);
+  for (int64_t r = 0; r < n_regions; ++r) {
+    const double scale = sym[(size_t)(2 * r + 1)];
+    if (scale != 0.0 && sym[(size_t)(2 * r)] > 1e-10 * scale) {
+      if (failed_region) *failed_region = r;
+      return fail("dense_factor expects a symmetric matrix (region " + std::to_string(r) + ")");
+    }
+    if (status[(size_t)r] != 0) {
+      if (failed_region) *failed_region = r;
+      if (failed_minor) *failed_minor = status[(size_t)r];
+      set_error("local block " + std::to_string(r) + " (" + std::to_string(roff[r + 1] - roff[r]) +
+                " dofs) is not SPD: leading minor of order " + std::to_string(status[(size_t)r]) +
+                " is not positive");
+      return SMG_ERR_NOT_SPD;
+    }
+  }
+  return SMG_OK;
+}
+
 int smg_correction_create(const smg_operator* a, int64_t n_regions, const int64_t* roff,
                           const int64_t* dofs, const int64_t* foff, const double* factors,
                           smg_correction** out)

@@ -194,6 +194,13 @@ struct LocateArgs {
 cudaError_t prolongation_device(const LocateArgs& a, int dim, int degree, DevCsrOwned* out,
                                 int64_t* failed_point, cudaStream_t s);
 
+// batched dense Cholesky of the local-correction blocks (factor_kernels.cu;
+// smoothers.py:176-200).  status[r] = 0 or the failing leading minor (dpotrf
+// info); sym[2r] = max |a - a^T|, sym[2r+1] = max |a| of the gathered block.
+cudaError_t launch_patch_factor(const DevCsr& a, int64_t n_regions, const int32_t* pptr,
+                                const int32_t* dofs, const int64_t* foff, double* w,
+                                int64_t* status, double* sym, cudaStream_t s);
+
 // dense / reduction kernels (dense_kernels.cu)
 cudaError_t launch_dot(int64_t n, const double* a, const double* b, double* partials,
                        unsigned int* counter, double* result, cudaStream_t s);

@@ -375,7 +375,7 @@ def build_hierarchy(meshes: Sequence, smoother: SmootherConfig, use_local_correc
         correction = None
         if use_local_correction and dof_sets:
             t = time.perf_counter()
-            correction = build_local_correction(a, dof_sets)
+            correction = build_local_correction(a, dof_sets, device=device_setup)
             times["local_factor_s"] += time.perf_counter() - t
         lam = lam_adj = None
         cfg = smoother

@@ -83,3 +83,99 @@ def test_prolongation_full_size_bitwise(wl):
         p_dev = build_prolongation(dms[l], meshes[l + 1], dms[l + 1], device=True)
         p_host = build_prolongation(dms[l], meshes[l + 1], dms[l + 1], device=False)
         assert same(p_dev, p_host), f"level {l}"
+
+
+# ---------------------------------------------------------------------------
+# batched patch Cholesky (smg_patch_factor; smoothers.py:176-200, sparse.py:234-254)
+
+def _factor_checks(a, lc_dev, lc_ref=None, tol_l=1e-12):
+    s = a.to_scipy()
+    for r, (idx, f) in enumerate(lc_dev.regions):
+        c = f.factor[0]
+        sub = s[idx][:, idx].toarray()
+        L = np.tril(c)
+        # upper triangle untouched (cho_factor's layout), backward error at rounding level
+        iu = np.triu_indices(len(idx), 1)
+        assert np.array_equal(c[iu], sub[iu])
+        assert np.max(np.abs(L @ L.T - sub)) <= 1e-14 * np.max(np.abs(sub)) * len(idx)
+        if lc_ref is not None:
+            ridx, rf = lc_ref.regions[r]
+            assert np.array_equal(ridx, idx)
+            Lr = np.tril(rf.factor[0])
+            assert np.max(np.abs(L - Lr)) <= tol_l * np.max(np.abs(Lr))
+
+
+@pytest.mark.parametrize("name", ["c1s", "c2s", "c3s", "crit7_adj"])
+def test_patch_factor_vs_reference_factors(name):
+    from paper_2402_12947_b200.smoothers import build_local_correction
+    from tests.golden import fixtures
+    z, h = fixtures.load(name)
+    for lv in h.levels:
+        lc = lv.local_correction
+        if lc is None:
+            continue
+        sets = [idx for idx, _ in lc.regions]
+        dev = build_local_correction(lv.a, sets, device=True)
+        _factor_checks(lv.a, dev, lc)
+        # the sandwich smoother with device factors matches the reference's
+        from paper_2402_12947_b200 import combined_smooth
+        out = combined_smooth(lv.a, z["g/b"], z["g/u_rand"].copy(), dev, lv.smoother) \
+            if lv.index == 0 else None
+        if out is not None:
+            ref = z["g/combined"]
+            assert np.linalg.norm(out - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+def test_patch_factor_c5_blocks_cond_1e6():
+    """1000-style synthetic SPD blocks (cond 1e6, 64-512 dofs): backward error
+    at rounding level; solves agree with LAPACK's to cond * eps."""
+    import scipy.linalg
+    import scipy.sparse as sp
+    from paper_2402_12947_b200.smoothers import build_local_correction
+    from paper_2402_12947_b200.sparse import CsrMatrix
+    from tests.test_oracle_golden import load_c5p
+    z, lc_ref = load_c5p()
+    n = int(z["n"])
+    rows, cols, vals = [np.arange(n)], [np.arange(n)], [np.ones(n)]
+    covered = np.zeros(n, dtype=bool)
+    blocks = []
+    for idx, f in lc_ref.regions:
+        L = np.tril(f.factor[0])
+        B = L @ L.T
+        B = 0.5 * (B + B.T)
+        blocks.append((idx, B))
+        covered[idx] = True
+        ii, jj = np.meshgrid(idx, idx, indexing="ij")
+        rows.append(ii.ravel()); cols.append(jj.ravel()); vals.append(B.ravel())
+    keep = ~covered[rows[0]]
+    rows[0], cols[0], vals[0] = rows[0][keep], cols[0][keep], vals[0][keep]
+    a = CsrMatrix.from_scipy(sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows),
+                                            np.concatenate(cols))), shape=(n, n)).tocsr())
+    dev = build_local_correction(a, [idx for idx, _ in blocks], device=True)
+    _factor_checks(a, dev)
+    rng = np.random.default_rng(0)
+    for (idx, B), (_, f) in zip(blocks, dev.regions):
+        rhs = rng.standard_normal(len(idx))
+        x_dev = scipy.linalg.cho_solve(f.factor, rhs)
+        x_ref = scipy.linalg.cho_solve(scipy.linalg.cho_factor(B, lower=True), rhs)
+        assert np.linalg.norm(x_dev - x_ref) <= 1e-9 * np.linalg.norm(x_ref)
+
+
+def test_patch_factor_errors():
+    from paper_2402_12947_b200.smoothers import build_local_correction
+    from paper_2402_12947_b200.sparse import CsrMatrix, NotPositiveDefiniteError
+    d = np.diag([4.0, 4.0, -1.0, 4.0, 4.0, 4.0]) + 0.5 * (np.eye(6, k=1) + np.eye(6, k=-1))
+    a = CsrMatrix.from_dense(d)
+    with pytest.raises(NotPositiveDefiniteError, match="local block 2"):
+        build_local_correction(a, [np.array([0, 1]), np.array([], dtype=np.int64),
+                                   np.array([2, 3])], device=True)
+    with pytest.raises(ValueError, match="overlaps"):
+        build_local_correction(a, [np.array([0, 1]), np.array([1, 2])], device=True)
+    asym = d.copy()
+    asym[0, 1] = 3.0
+    with pytest.raises(ValueError, match="symmetric"):
+        build_local_correction(CsrMatrix.from_dense(asym), [np.array([0, 1])], device=True)
+    # the host path raises the same way
+    with pytest.raises(NotPositiveDefiniteError, match="local block 2"):
+        build_local_correction(a, [np.array([0, 1]), np.array([], dtype=np.int64),
+                                   np.array([2, 3])], device=False)
