@@ -157,6 +157,19 @@ SMG_API int smg_correction_create(const smg_operator *a, int64_t n_regions,
 SMG_API int smg_correction_destroy(smg_correction *c);
 SMG_API int smg_correction_info(const smg_correction *c, int64_t *n_regions, int64_t *covered_dofs,
                         int *coupled, int64_t *device_bytes);
+/* ---- setup: coarse operator factor and inverse (mg.py:123 coarse_factor =
+ * sparse.py:234-254 dense_factor; the hot path's A_L^-1) --------------------
+ * smg_dense_cholesky: a (host, n x n row-major) -> c (host) in cho_factor's
+ * layout (L lower, A strict upper), on the device (cuSOLVER dpotrf).
+ * SMG_ERR_INVALID "… expects a symmetric matrix" when max|a - a^T| > 1e-10
+ * max|a|; SMG_ERR_NOT_SPD with *info = dpotrf's leading minor when not SPD
+ * (the reference then falls back to LU on the host).
+ * smg_cholesky_inverse: c (cho_factor layout, lower) -> the full symmetric
+ * A^-1 (host), as LAPACK dpotri on the same factor.                          */
+SMG_API int smg_dense_cholesky(int64_t n, const double *a, double *c, int64_t *info,
+                               void *stream);
+SMG_API int smg_cholesky_inverse(int64_t n, const double *c, double *inverse, void *stream);
+
 /* Factor every region's principal submatrix on the device (setup;
  * smoothers.py:176-200 build_local_correction -> sparse.py:234-254
  * dense_factor(lu_fallback=False) -> scipy cho_factor(lower=True)): one CTA per

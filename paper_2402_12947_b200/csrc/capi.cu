@@ -1064,6 +1064,47 @@ static int build_halo(const Operator& o, const std::vector<int32_t>& dof32,
   return SMG_OK;
 }
 
+static int dense_roundtrip(int64_t n, const double* in, double* out, bool invert, int64_t* info,
+                           void* stream)
+{
+  if (info) *info = 0;
+  if (n < 0) return fail("negative dimension");
+  if (n == 0) return SMG_OK;
+  if (!in || !out) return fail("NULL matrix");
+  const cudaStream_t st = as_stream(stream);
+  const size_t bytes = sizeof(double) * (size_t)n * (size_t)n;
+  double* d = nullptr;
+  SMG_CUDA(cudaMalloc(&d, bytes));
+  int rc = check_cuda(cudaMemcpyAsync(d, in, bytes, cudaMemcpyHostToDevice, st), "H2D");
+  double asym = 0.0, amax = 0.0;
+  int64_t inf = 0;
+  if (rc == SMG_OK)
+    rc = dense_cholesky_device(n, d, !invert, &asym, &amax, &inf, invert, st);
+  if (rc == SMG_OK && !invert && amax != 0.0 && asym > 1e-10 * amax)
+    rc = fail("dense_factor expects a symmetric matrix");
+  if (rc == SMG_OK && inf != 0) {
+    if (info) *info = inf;
+    set_error(invert ? "dpotri: the factor is singular (info " + std::to_string(inf) + ")"
+                     : "Cholesky failed: leading minor of order " + std::to_string(inf) +
+                           " is not positive");
+    rc = SMG_ERR_NOT_SPD;
+  }
+  if (rc == SMG_OK) rc = check_cuda(cudaMemcpy(out, d, bytes, cudaMemcpyDeviceToHost), "D2H");
+  cudaFree(d);
+  return rc;
+}
+
+int smg_dense_cholesky(int64_t n, const double* a, double* c, int64_t* info, void* stream)
+{
+  return dense_roundtrip(n, a, c, false, info, stream);
+}
+
+int smg_cholesky_inverse(int64_t n, const double* c, double* inverse, void* stream)
+{
+  int64_t info = 0;
+  return dense_roundtrip(n, c, inverse, true, &info, stream);
+}
+
 int smg_patch_factor(const smg_operator* a, int64_t n_regions, const int64_t* roff,
                      const int64_t* dofs, double* factors, int64_t* failed_region,
                      int64_t* failed_minor, void* stream)

@@ -201,6 +201,13 @@ cudaError_t launch_patch_factor(const DevCsr& a, int64_t n_regions, const int32_
                                 const int32_t* dofs, const int64_t* foff, double* w,
                                 int64_t* status, double* sym, cudaStream_t s);
 
+// dense Cholesky (invert=false: A -> cho_factor's c in place, *info = dpotrf
+// info) or inverse from such a factor (invert=true: dpotri, full symmetric);
+// row-major, cuSOLVER (coarse_factor.cu).  With check_symmetry the max|a - a^T|
+// and max|a| come back in *asym / *amax and an asymmetric input stops early.
+int dense_cholesky_device(int64_t n, double* d_a, bool check_symmetry, double* asym,
+                          double* amax, int64_t* info_out, bool invert, cudaStream_t s);
+
 // dense / reduction kernels (dense_kernels.cu)
 cudaError_t launch_dot(int64_t n, const double* a, const double* b, double* partials,
                        unsigned int* counter, double* result, cudaStream_t s);

@@ -90,15 +90,26 @@ class Hierarchy:
         return _device_for(self)
 
 
-def coarse_inverse(coarse_factor) -> np.ndarray:
-    """Dense A_L^{-1} from the reference's Cholesky factor (mg.py:123) via
-    LAPACK dpotri (setup).  ``coarse_factor.factor = (c, lower)``."""
+def coarse_inverse(coarse_factor, device: Optional[bool] = None) -> np.ndarray:
+    """Dense A_L^{-1} from the reference's Cholesky factor (mg.py:123) as
+    LAPACK dpotri forms it (setup).  ``coarse_factor.factor = (c, lower)``.
+    ``device`` (default: whenever a CUDA device exists): dpotri on the GPU
+    (``smg_cholesky_inverse``, cuSOLVER) from the same factor."""
     f = getattr(coarse_factor, "factor", coarse_factor)
     kind = getattr(coarse_factor, "kind", "cholesky")
     if kind != "cholesky":
         raise NotImplementedError("coarse operator is not SPD (LU fallback): not on the GPU hot path")
     c, lower = f
     c = np.asarray(c, dtype=np.float64)
+    if device is None:
+        device = bool(_dev.torch().cuda.is_available())
+    if device and c.size:
+        lib = _lib.load()
+        lo = np.ascontiguousarray(np.tril(c) if lower else np.triu(c).T)
+        inv = np.empty_like(lo)
+        _lib.check(lib.smg_cholesky_inverse(lo.shape[0], lo.ctypes.data_as(_f64p),
+                                            inv.ctypes.data_as(_f64p), _dev.stream_handle()))
+        return inv
     lo = np.asfortranarray(np.tril(c) if lower else np.triu(c).T)
     inv, info = scipy.linalg.lapack.dpotri(lo, lower=1)
     if info != 0:
@@ -388,7 +399,7 @@ def build_hierarchy(meshes: Sequence, smoother: SmootherConfig, use_local_correc
         prol = prolongations[l] if l < len(prolongations) else None
         levels.append(Level(l, mesh, dofmap, a, prol, cfg, regions, correction, None, lam, lam_adj))
     t = time.perf_counter()
-    coarse = dense_factor(operators[-1].to_dense())
+    coarse = dense_factor(operators[-1].to_dense(), device=device_setup)
     times["coarse_factor_s"] += time.perf_counter() - t
     h = Hierarchy(levels, coarse, system, coarse_refine)
     h.setup_times = dict(times, galerkin_device=bool(device_setup))

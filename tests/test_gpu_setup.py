@@ -179,3 +179,54 @@ def test_patch_factor_errors():
     with pytest.raises(NotPositiveDefiniteError, match="local block 2"):
         build_local_correction(a, [np.array([0, 1]), np.array([], dtype=np.int64),
                                    np.array([2, 3])], device=False)
+
+
+# ---------------------------------------------------------------------------
+# coarse factor and inverse (smg_dense_cholesky / smg_cholesky_inverse; mg.py:123)
+
+@pytest.mark.parametrize("name", ["c1s", "c2s", "c3s", "crit7_adj"])
+def test_coarse_factor_and_inverse_vs_lapack(name):
+    import scipy.linalg
+    from paper_2402_12947_b200.mg import coarse_inverse
+    from paper_2402_12947_b200.sparse import dense_factor
+    from tests.golden import fixtures
+    z, h = fixtures.load(name)
+    a = h.levels[-1].a.to_dense()
+    f = dense_factor(a, device=True)
+    assert f.kind == "cholesky"
+    c = f.factor[0]
+    cr = np.asarray(h.coarse_factor.factor[0])
+    iu = np.triu_indices(len(a), 1)
+    assert np.array_equal(c[iu], a[iu])               # cho_factor layout
+    L, Lr = np.tril(c), np.tril(cr)
+    assert np.max(np.abs(L - Lr)) <= 1e-13 * np.max(np.abs(Lr))
+    inv_d = coarse_inverse(h.coarse_factor, device=True)
+    inv_h = coarse_inverse(h.coarse_factor, device=False)
+    assert np.array_equal(inv_d, inv_d.T)
+    assert np.max(np.abs(inv_d - inv_h)) <= 1e-13 * np.linalg.cond(a) * np.max(np.abs(inv_h))
+    # the solve the hot path performs: x = A^-1 b vs LAPACK dpotrs on the reference factor
+    b = z["g/coarse_b"]
+    x_ref = scipy.linalg.cho_solve(h.coarse_factor.factor, b)
+    assert np.linalg.norm(inv_d @ b - x_ref) <= 1e-13 * np.linalg.cond(a) * np.linalg.norm(x_ref)
+
+
+def test_dense_factor_device_fallbacks():
+    from paper_2402_12947_b200.sparse import NotPositiveDefiniteError, dense_factor
+    rng = np.random.default_rng(1)
+    q, _ = np.linalg.qr(rng.standard_normal((300, 300)))
+    indef = (q * np.linspace(-1.0, 2.0, 300)) @ q.T
+    indef = 0.5 * (indef + indef.T)
+    f = dense_factor(indef, lu_fallback=True, device=True)
+    assert f.kind == "lu"
+    with pytest.raises(NotPositiveDefiniteError):
+        dense_factor(indef, lu_fallback=False, device=True)
+    asym = np.eye(5)
+    asym[0, 3] = 1.0
+    with pytest.raises(ValueError, match="symmetric"):
+        dense_factor(asym, device=True)
+    spd = (q * np.logspace(0, -8, 300)) @ q.T
+    spd = 0.5 * (spd + spd.T)
+    import scipy.linalg
+    c = dense_factor(spd, device=True).factor[0]
+    L = np.tril(c)
+    assert np.max(np.abs(L @ L.T - spd)) <= 1e-14 * np.max(np.abs(spd)) * 300
