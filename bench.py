@@ -403,8 +403,12 @@ def main():
     wl = configs.WORKLOADS[args.workload]
     t_setup = time.perf_counter()
     h, b_host, u0 = configs.build(wl)
+    t_upload = time.perf_counter()
     dh = DeviceHierarchy(h.levels, h.coarse_factor)
+    t_upload = time.perf_counter() - t_upload
     t_setup = time.perf_counter() - t_setup
+    setup_detail = dict(getattr(h, "setup_times", {}), device_hierarchy_s=t_upload,
+                        total_s=t_setup)
     lib = _lib.load()
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
@@ -605,6 +609,7 @@ def main():
             "clocks": clocks,
             "cpu_baseline": cpu,
             "setup_s": t_setup,
+            "setup": setup_detail,
         }
         print(json.dumps(line))
     if ws > 1:
