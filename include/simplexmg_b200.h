@@ -157,6 +157,23 @@ SMG_API int smg_correction_create(const smg_operator *a, int64_t n_regions,
 SMG_API int smg_correction_destroy(smg_correction *c);
 SMG_API int smg_correction_info(const smg_correction *c, int64_t *n_regions, int64_t *covered_dofs,
                         int *coupled, int64_t *device_bytes);
+/* ---- setup: Poisson stiffness assembly (fem.py:303-377 assemble, scalar
+ * P1/P2, homogeneous Dirichlet on the listed DOFs) ---------------------------
+ * Host inputs: vertices (n_vertices x dim), cells (n_cells x (dim+1), positively
+ * oriented), cell_dofs (n_cells x nodes per cell, the DofMap numbering),
+ * sorted dirichlet_dofs, and the reference gradients grad_ref (n_quad x nodes
+ * x dim) with weights (n_quad) of the stiffness quadrature (fem.py:63-95).
+ * *out = the assembled operator after symmetric elimination: Dirichlet rows
+ * and columns removed, unit diagonal (canonical CSR).  Values agree with the
+ * reference to rounding (element geometry by cofactors, duplicates summed in
+ * cell order).  SMG_ERR_INVALID with *bad_cell for a cell with det <= 0.      */
+SMG_API int smg_assemble_poisson(int dim, int degree, int64_t n_vertices, const double *vertices,
+                                 int64_t n_cells, const int64_t *cells, const int64_t *cell_dofs,
+                                 int64_t n_dofs, const int64_t *dirichlet_dofs,
+                                 int64_t n_dirichlet, const double *grad_ref,
+                                 const double *weights, int n_quad, smg_csr **out,
+                                 int64_t *bad_cell, void *stream);
+
 /* ---- setup: coarse operator factor and inverse (mg.py:123 coarse_factor =
  * sparse.py:234-254 dense_factor; the hot path's A_L^-1) --------------------
  * smg_dense_cholesky: a (host, n x n row-major) -> c (host) in cho_factor's

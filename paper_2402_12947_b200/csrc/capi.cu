@@ -1064,6 +1064,47 @@ static int build_halo(const Operator& o, const std::vector<int32_t>& dof32,
   return SMG_OK;
 }
 
+int smg_assemble_poisson(int dim, int degree, int64_t n_vertices, const double* vertices,
+                         int64_t n_cells, const int64_t* cells, const int64_t* cell_dofs,
+                         int64_t n_dofs, const int64_t* dirichlet_dofs, int64_t n_dirichlet,
+                         const double* grad_ref, const double* weights, int n_quad,
+                         smg_csr** out, int64_t* bad_cell, void* stream)
+{
+  if (!out) return fail("out is NULL");
+  *out = nullptr;
+  if (bad_cell) *bad_cell = -1;
+  if (dim != 2 && dim != 3) return fail("dim must be 2 or 3");
+  if (degree != 1 && degree != 2) return fail("element degree must be 1 or 2");
+  if (n_cells <= 0 || n_vertices <= 0 || n_dofs <= 0 || n_quad <= 0 || n_dirichlet < 0)
+    return fail("empty mesh or negative sizes");
+  if (n_dofs >= INT32_MAX || (uint64_t)n_dofs > (1ull << 31)) return fail("too many DOFs");
+  if (!vertices || !cells || !cell_dofs || !grad_ref || !weights ||
+      (n_dirichlet > 0 && !dirichlet_dofs))
+    return fail("NULL input array");
+  const int npc = degree == 1 ? dim + 1 : (dim + 1) * (dim + 2) / 2;
+  for (int64_t k = 0; k < n_cells * (dim + 1); ++k)
+    if (cells[k] < 0 || cells[k] >= n_vertices) return fail("cell vertex out of range");
+  for (int64_t k = 0; k < n_cells * npc; ++k)
+    if (cell_dofs[k] < 0 || cell_dofs[k] >= n_dofs) return fail("cell dof out of range");
+  std::vector<uint8_t> mask((size_t)n_dofs, 0);
+  for (int64_t k = 0; k < n_dirichlet; ++k) {
+    const int64_t d = dirichlet_dofs[k];
+    if (d < 0 || d >= n_dofs) return fail("Dirichlet dof out of range");
+    if (k > 0 && d <= dirichlet_dofs[k - 1]) return fail("Dirichlet dofs must be sorted and unique");
+    mask[(size_t)d] = 1;
+  }
+  auto c = std::make_unique<smg_csr>();
+  int64_t bad = -1;
+  const int rc = assemble_poisson_device(dim, degree, n_vertices, vertices, n_cells, cells,
+                                         cell_dofs, n_dofs, mask.data(), n_dirichlet,
+                                         dirichlet_dofs, grad_ref, weights, n_quad, &c->m, &bad,
+                                         as_stream(stream));
+  if (bad_cell) *bad_cell = bad;
+  SMG_TRY(rc);
+  *out = c.release();
+  return SMG_OK;
+}
+
 static int dense_roundtrip(int64_t n, const double* in, double* out, bool invert, int64_t* info,
                            void* stream)
 {

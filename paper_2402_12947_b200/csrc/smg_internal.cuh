@@ -208,6 +208,13 @@ cudaError_t launch_patch_factor(const DevCsr& a, int64_t n_regions, const int32_
 int dense_cholesky_device(int64_t n, double* d_a, bool check_symmetry, double* asym,
                           double* amax, int64_t* info_out, bool invert, cudaStream_t s);
 
+// Poisson stiffness with Dirichlet elimination (assembly_kernels.cu; fem.py:303-377)
+int assemble_poisson_device(int dim, int degree, int64_t n_vertices, const double* verts,
+                            int64_t n_cells, const int64_t* cells, const int64_t* cell_dofs,
+                            int64_t n_dofs, const uint8_t* dirichlet_mask, int64_t n_dir,
+                            const int64_t* dir_dofs, const double* gref, const double* wq, int nq,
+                            DevCsrOwned* out, int64_t* bad_cell_out, cudaStream_t s);
+
 // dense / reduction kernels (dense_kernels.cu)
 cudaError_t launch_dot(int64_t n, const double* a, const double* b, double* partials,
                        unsigned int* counter, double* result, cudaStream_t s);

@@ -144,12 +144,66 @@ def build_dofmap(mesh: SimplexMesh, degree: int) -> DofMap:
         return DofMap(mesh, 1, np.array(mesh.vertices), np.array(mesh.cells), None)
     local_edges = np.asarray(_EDGES[mesh.dim])
     pairs = np.sort(mesh.cells[:, local_edges], axis=2).reshape(-1, 2)
-    unique, inverse = np.unique(pairs, axis=0, return_inverse=True)
+    # np.unique(pairs, axis=0) order (lexicographic) via one int64 key per pair
+    nv = np.int64(mesh.n_vertices)
+    ukeys, inverse = np.unique(pairs[:, 0].astype(np.int64) * nv + pairs[:, 1],
+                               return_inverse=True)
+    unique = np.column_stack([ukeys // nv, ukeys % nv])
     edge_ids = inverse.reshape(mesh.n_cells, len(local_edges))
     midpoints = 0.5 * (mesh.vertices[unique[:, 0]] + mesh.vertices[unique[:, 1]])
     node_coords = np.vstack([mesh.vertices, midpoints])
     cell_nodes = np.hstack([mesh.cells, mesh.n_vertices + edge_ids])
     return DofMap(mesh, 2, node_coords, cell_nodes, unique.astype(np.int64))
+
+
+def _load_vector(mesh, dofmap, source, v0, jac, det) -> np.ndarray:
+    dim, degree = mesh.dim, dofmap.element_degree
+    b = np.zeros(dofmap.n_dofs)
+    qpts, qwts = quadrature(dim, 4)
+    vals = np.asarray([reference_values(degree, dim, p) for p in qpts])
+    coords = v0[:, None, :] + np.einsum("mde,qe->mqd", jac, qpts)
+    fvals = np.asarray(source(coords.reshape(-1, dim)), dtype=np.float64).reshape(coords.shape[:2])
+    b_local = np.einsum("q,m,qi,mq->mi", qwts, det, vals, fvals)
+    np.add.at(b, dofmap.cell_dofs.ravel(), b_local.ravel())
+    return b
+
+
+def _assemble_poisson_device(mesh, dofmap, source, dirichlet_all, grads_ref, wts):
+    import ctypes
+    from . import _lib
+    from . import device as _dev
+    _dev.require_cuda()
+    lib = _lib.load()
+    i64p = ctypes.POINTER(ctypes.c_int64)
+    f64p = ctypes.POINTER(ctypes.c_double)
+    verts = np.ascontiguousarray(mesh.vertices, dtype=np.float64)
+    cells = np.ascontiguousarray(mesh.cells, dtype=np.int64)
+    cdofs = np.ascontiguousarray(dofmap.cell_dofs, dtype=np.int64)
+    dir_dofs = dofmap.boundary_dofs() if dirichlet_all else np.empty(0, dtype=np.int64)
+    dd = np.ascontiguousarray(dir_dofs, dtype=np.int64)
+    g = np.ascontiguousarray(grads_ref, dtype=np.float64)
+    w = np.ascontiguousarray(wts, dtype=np.float64)
+    out = ctypes.c_void_p()
+    bad = ctypes.c_int64(-1)
+    rc = lib.smg_assemble_poisson(mesh.dim, int(dofmap.element_degree), len(verts),
+                                  verts.ctypes.data_as(f64p), len(cells), cells.ctypes.data_as(i64p),
+                                  cdofs.ctypes.data_as(i64p), int(dofmap.n_dofs),
+                                  dd.ctypes.data_as(i64p), len(dd), g.ctypes.data_as(f64p),
+                                  w.ctypes.data_as(f64p), len(w), ctypes.byref(out),
+                                  ctypes.byref(bad), _dev.stream_handle())
+    if rc != _lib.SMG_OK and bad.value >= 0:
+        raise ValueError("mesh contains a degenerate or inverted cell")
+    _lib.check(rc)
+    nr, nc, ptr, col, val = _dev._csr_result_to_host(lib, out)
+    a = CsrMatrix(nr, nc, ptr, col, val)
+    if source is not None:
+        v0, jac, det, _ = _cell_geometry(mesh)
+        b = _load_vector(mesh, dofmap, source, v0, jac, det)
+    else:
+        b = np.zeros(dofmap.n_dofs)
+    if len(dir_dofs):
+        b[dir_dofs] = 0.0
+    return AssembledSystem(a, b, dir_dofs)
 
 
 @dataclass(frozen=True)
@@ -170,14 +224,21 @@ def _cell_geometry(mesh: SimplexMesh):
 
 def assemble_poisson(mesh: SimplexMesh, dofmap: DofMap,
                      source: Optional[Callable[[np.ndarray], np.ndarray]] = None,
-                     dirichlet_all: bool = True) -> AssembledSystem:
+                     dirichlet_all: bool = True, device: bool = False) -> AssembledSystem:
     """Stiffness + load with homogeneous Dirichlet on every box face
-    (fem.py:303-377).  ``source`` is vectorised: (m, dim) points -> (m,)."""
+    (fem.py:303-377).  ``source`` is vectorised: (m, dim) points -> (m,).
+
+    ``device=True``: the stiffness matrix (element matrices, duplicate sums,
+    Dirichlet elimination) is assembled on the GPU (``smg_assemble_poisson``;
+    values agree with the host/reference to rounding, identical pattern); the
+    load vector stays on the host."""
     dim = mesh.dim
     degree = dofmap.element_degree
-    v0, jac, det, inv_jac = _cell_geometry(mesh)
     pts, wts = quadrature(dim, 1 if degree == 1 else 2)
     grads_ref = np.asarray([reference_gradients(degree, dim, p) for p in pts])
+    if device:
+        return _assemble_poisson_device(mesh, dofmap, source, dirichlet_all, grads_ref, wts)
+    v0, jac, det, inv_jac = _cell_geometry(mesh)
     grads = np.einsum("qie,med->mqid", grads_ref, inv_jac)
     local = np.einsum("q,m,mqid,mqjd->mij", wts, det, grads, grads)
 

@@ -365,7 +365,7 @@ def build_hierarchy(meshes: Sequence, smoother: SmootherConfig, use_local_correc
     dofmaps = [build_dofmap(m, element_degree) for m in meshes]
     times["dofmap_s"] += time.perf_counter() - t
     t = time.perf_counter()
-    system = assemble_poisson(meshes[0], dofmaps[0], source)
+    system = assemble_poisson(meshes[0], dofmaps[0], source, device=device_setup)
     times["assembly_s"] += time.perf_counter() - t
     operators = [system.a]
     prolongations = []

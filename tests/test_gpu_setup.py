@@ -230,3 +230,58 @@ def test_dense_factor_device_fallbacks():
     c = dense_factor(spd, device=True).factor[0]
     L = np.tril(c)
     assert np.max(np.abs(L @ L.T - spd)) <= 1e-14 * np.max(np.abs(spd)) * 300
+
+
+# ---------------------------------------------------------------------------
+# Poisson assembly (smg_assemble_poisson; fem.py:303-377)
+
+def _close_csr(a, r, tol=1e-13):
+    assert a.shape == r.shape
+    assert np.array_equal(a.row_offsets, r.row_offsets)
+    assert np.array_equal(a.col_indices, r.col_indices)
+    scale = np.max(np.abs(r.values))
+    assert np.max(np.abs(a.values - r.values)) <= tol * scale
+
+
+@pytest.mark.parametrize("name,wl,scale", CASES)
+def test_assembly_vs_reference_operator(name, wl, scale):
+    from paper_2402_12947_b200 import configs
+    from paper_2402_12947_b200.fem import assemble_poisson, build_dofmap
+    from tests.golden import fixtures
+    z, ref = fixtures.load(name)
+    w = getattr(configs, wl).scaled(scale)
+    m = configs.build_meshes(w)[0]
+    dm = build_dofmap(m, w.degree)
+    source = (lambda x: np.ones(len(x))) if w.rhs == "source-one" else None
+    sys_d = assemble_poisson(m, dm, source, device=True)
+    sys_h = assemble_poisson(m, dm, source, device=False)
+    _close_csr(sys_d.a, ref.levels[0].a)
+    _close_csr(sys_d.a, sys_h.a)
+    assert np.array_equal(sys_d.b, sys_h.b)
+    assert np.array_equal(sys_d.dirichlet_dofs, sys_h.dirichlet_dofs)
+
+
+@pytest.mark.parametrize("dim,degree,n", [(2, 1, 9), (2, 2, 7), (3, 1, 5), (3, 2, 4)])
+def test_assembly_all_elements_jittered(dim, degree, n):
+    from paper_2402_12947_b200 import configs
+    from paper_2402_12947_b200.fem import assemble_poisson, build_dofmap
+    from paper_2402_12947_b200.mesh import generate_simplex_grid
+    m = configs.jitter(generate_simplex_grid(dim, n), 0.15, np.random.default_rng(dim * 10 + degree))
+    dm = build_dofmap(m, degree)
+    _close_csr(assemble_poisson(m, dm, device=True).a, assemble_poisson(m, dm, device=False).a)
+    # no Dirichlet elimination: the plain stiffness (rows sum to zero)
+    a = assemble_poisson(m, dm, dirichlet_all=False, device=True).a
+    _close_csr(a, assemble_poisson(m, dm, dirichlet_all=False, device=False).a)
+    assert np.max(np.abs(a.to_scipy() @ np.ones(a.ncols))) <= 1e-12 * np.max(np.abs(a.values))
+
+
+def test_assembly_inverted_cell_raises():
+    from dataclasses import replace
+    from paper_2402_12947_b200.fem import assemble_poisson, build_dofmap
+    from paper_2402_12947_b200.mesh import generate_simplex_grid
+    m = generate_simplex_grid(2, 4)
+    cells = m.cells.copy()
+    cells[3, [1, 2]] = cells[3, [2, 1]]
+    bad = replace(m, cells=cells)
+    with pytest.raises(ValueError, match="degenerate or inverted"):
+        assemble_poisson(bad, build_dofmap(bad, 1), device=True)
