@@ -186,7 +186,9 @@ def run_reference(args):
     from paper_2402_12947_b200 import configs
     from oracle import oracle as O
     wl = configs.WORKLOADS[args.workload]
-    h, b, u0 = configs.build(wl)
+    # host setup (the reference's own construction, bit for bit): nothing of
+    # this package's device code runs on the reference arm
+    h, b, u0 = configs.build(wl, device_setup=False)
     threads = len(os.sched_getaffinity(0))
     O.set_threads(threads)
     u = u0.copy()

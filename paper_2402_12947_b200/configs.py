@@ -185,14 +185,18 @@ def build_meshes(wl: Workload) -> List[SimplexMesh]:
     return meshes
 
 
-def build(wl: Workload, use_local_correction: bool = True, coarse_refine: bool = False):
-    """Host hierarchy + (b, u0) for a workload.  Returns (hierarchy, b, u0)."""
+def build(wl: Workload, use_local_correction: bool = True, coarse_refine: bool = False,
+          device_setup=None):
+    """Host hierarchy + (b, u0) for a workload.  Returns (hierarchy, b, u0).
+    ``device_setup``: see mg.build_hierarchy (None = GPU setup when a device
+    exists; False = the host path, bit-identical to the reference's setup)."""
     from .mg import build_hierarchy
     meshes = build_meshes(wl)
     source = (lambda x: np.ones(len(x))) if wl.rhs == "source-one" else None
     smoother = wl.smoother
     h = build_hierarchy(meshes, smoother, use_local_correction, 0.1, wl.degree, source=source,
-                        region_layers=wl.region_layers, coarse_refine=coarse_refine)
+                        region_layers=wl.region_layers, coarse_refine=coarse_refine,
+                        device_setup=device_setup)
     n0 = h.fine.a.nrows
     if wl.rhs == "random":
         b = np.random.default_rng([wl.seed, 99]).standard_normal(n0)

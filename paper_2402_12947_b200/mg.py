@@ -392,8 +392,9 @@ def build_hierarchy(meshes: Sequence, smoother: SmootherConfig, use_local_correc
         cfg = smoother
         if smoother.kind == "chebyshev":
             t = time.perf_counter()
-            lam = jacobi_lambda_max(a, lambda_tol)
-            lam_adj = adjusted_lambda_max(a, dof_sets, lambda_tol) if dof_sets else lam
+            lam = jacobi_lambda_max(a, lambda_tol, device_setup)
+            lam_adj = (adjusted_lambda_max(a, dof_sets, lambda_tol, device_setup)
+                       if dof_sets else lam)
             cfg = replace(smoother, lambda_max=lam_adj if smoother.adjusted else lam)
             times["lambda_s"] += time.perf_counter() - t
         prol = prolongations[l] if l < len(prolongations) else None

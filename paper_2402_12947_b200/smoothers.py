@@ -272,21 +272,26 @@ def combined_smooth(a, b, u, correction, cfg, splitting=None):
     return _write_back(u, ut, host)
 
 
-def jacobi_lambda_max(a, tol: float = 1e-8) -> float:
-    """Largest eigenvalue of D^-1 A (smoothers.py:214-222; setup, host)."""
+def jacobi_lambda_max(a, tol: float = 1e-8, device: Optional[bool] = None) -> float:
+    """Largest eigenvalue of D^-1 A (smoothers.py:214-222; setup).  ``device``
+    (default: whenever a CUDA device exists) runs Lanczos on the GPU for
+    operators of at least DEVICE_LANCZOS_MIN_ROWS rows."""
     a = CsrMatrix.from_any(a)
     diag = a.diagonal()
     zero = np.nonzero(diag == 0.0)[0]
     if len(zero):
         raise ZeroDiagonalError(int(zero[0]))
     scale = 1.0 / np.sqrt(np.abs(diag))
-    if a.nrows >= DEVICE_LANCZOS_MIN_ROWS and _dev.torch().cuda.is_available():
+    if device is None:
+        device = bool(_dev.torch().cuda.is_available())
+    if a.nrows >= DEVICE_LANCZOS_MIN_ROWS and device:
         return estimate_lambda_max_device(a, scale, tol)
     s = a.to_scipy()
     return estimate_lambda_max(lambda x: scale * (s @ (scale * x)), a.nrows, tol)
 
 
-def adjusted_lambda_max(a, boundary_dof_sets: Sequence[np.ndarray], tol: float = 1e-8) -> float:
+def adjusted_lambda_max(a, boundary_dof_sets: Sequence[np.ndarray], tol: float = 1e-8,
+                        device: Optional[bool] = None) -> float:
     """smoothers.py:225-241 (setup)."""
     a = CsrMatrix.from_any(a)
     covered = np.zeros(a.nrows, dtype=bool)
@@ -296,5 +301,5 @@ def adjusted_lambda_max(a, boundary_dof_sets: Sequence[np.ndarray], tol: float =
     if len(keep) == 0:
         raise ValueError("excluded dofs cover the whole operator; nothing remains")
     if len(keep) == a.nrows:
-        return jacobi_lambda_max(a, tol)
-    return jacobi_lambda_max(a.principal_submatrix(keep), tol)
+        return jacobi_lambda_max(a, tol, device)
+    return jacobi_lambda_max(a.principal_submatrix(keep), tol, device)
