@@ -108,9 +108,9 @@ static int64_t tile_cap_for(int64_t nnz, int64_t nrows)
   return cap;
 }
 
-static std::vector<int32_t> make_tiles(int64_t nrows, const int64_t* rowptr)
+static std::vector<int32_t> make_tiles(int64_t nrows, const int64_t* rowptr, int64_t cap = 0)
 {
-  const int64_t cap = tile_cap_for(rowptr[nrows], nrows);
+  if (cap <= 0) cap = tile_cap_for(rowptr[nrows], nrows);
   std::vector<int32_t> t;
   t.reserve((size_t)(nrows / 64 + 2));
   t.push_back(0);
@@ -143,9 +143,25 @@ static int build_devcsr(std::vector<void*>& allocs, int64_t& bytes, int64_t nrow
   if (nnz) std::memcpy(valp.data(), val, sizeof(double) * (size_t)nnz);
   std::vector<int64_t> rpp((size_t)nrows + 3, nnz);
   std::memcpy(rpp.data(), rowptr, sizeof(int64_t) * (size_t)(nrows + 1));
-  std::vector<int32_t> tiles = make_tiles(nrows, rowptr);
+  // fixed-capacity tiles (DevCsr::fixed): shrink the capacity while whole
+  // tiles of kRowsPerTile average rows would not fill it (little padding)
+  int64_t cap = tile_cap_for(nnz, nrows);
+  static const bool fixed_env = [] {
+    const char* e = getenv("SMG_FIXED_TILES");
+    return !(e && e[0] == '0');
+  }();
+  // (multi-chunk operators keep the offset-table layout: with ~27 nonzeros per
+  // row their tiles are row-bound, and shrinking them to avoid padding measured
+  // slower on C5, profiles/r01/ab_fixed_tiles/)
+  bool fixed = fixed_env && nrows > 0 && !long_rows(nnz, nrows);
+  if (fixed) {
+    while (cap > 256 && kRowsPerTile * nnz < cap * nrows) cap /= 2;
+  }
+  std::vector<int32_t> tiles = make_tiles(nrows, rowptr, cap);
   std::vector<int64_t> tnz(tiles.size());
   for (size_t i = 0; i < tiles.size(); ++i) tnz[i] = rowptr[tiles[i]];
+  for (size_t i = 0; fixed && i + 1 < tiles.size(); ++i)
+    if (tnz[i + 1] - tnz[i] > cap) fixed = false;   // a single row longer than the capacity
   DevCsr d;
   d.nrows = nrows;
   d.ncols = ncols;
@@ -168,6 +184,32 @@ static int build_devcsr(std::vector<void*>& allocs, int64_t& bytes, int64_t nrow
   d.val = v;
   d.tile_row = tr;
   d.tile_nz = tz;
+  if (fixed) {
+    const size_t nt = tiles.size() - 1;
+    std::vector<int32_t> pc(nt * (size_t)cap + 4, 0);
+    std::vector<double> pv(nt * (size_t)cap + 2, 0.0);
+    std::vector<int32_t> rel((size_t)nrows);
+    for (size_t t = 0; t < nt; ++t) {
+      const int64_t b = tnz[t], e = tnz[t + 1];
+      for (int64_t j = b; j < e; ++j) {
+        pc[t * (size_t)cap + (size_t)(j - b)] = col32[(size_t)j];
+        pv[t * (size_t)cap + (size_t)(j - b)] = val[j];
+      }
+      for (int32_t r = tiles[t]; r < tiles[t + 1]; ++r)
+        rel[(size_t)r] = (int32_t)(rowptr[r + 1] - b);
+    }
+    int32_t* dpc = nullptr;
+    double* dpv = nullptr;
+    int32_t* drel = nullptr;
+    SMG_TRY(dev_upload(allocs, bytes, pc.data(), pc.size(), &dpc));
+    SMG_TRY(dev_upload(allocs, bytes, pv.data(), pv.size(), &dpv));
+    SMG_TRY(dev_upload(allocs, bytes, rel.data(), rel.size(), &drel));
+    d.fixed = true;
+    d.cap = (int32_t)cap;
+    d.pcol = dpc;
+    d.pval = dpv;
+    d.rel_end = drel;
+  }
   *out = d;
   return SMG_OK;
 }

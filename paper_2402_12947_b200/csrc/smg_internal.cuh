@@ -42,6 +42,15 @@ struct DevCsr {
   int32_t ntiles = 0;
   bool streaming = false;            // val+col exceed kStreamBytes: evict-first reads
   bool multichunk = false;           // long rows: tiles of up to kMaxTileChunks chunks
+  // fixed-capacity layout: tile t's nonzeros sit at [t*cap, (t+1)*cap) of the
+  // padded arrays (zero values / column 0 after the last row), so a CTA can
+  // issue its value/column loads without first loading its tile offset;
+  // rel_end[r] = end of row r relative to its tile's start
+  bool fixed = false;
+  int32_t cap = 0;
+  const int32_t* pcol = nullptr;
+  const double* pval = nullptr;
+  const int32_t* rel_end = nullptr;
 };
 
 // Host-side owner of one operator's device arrays.

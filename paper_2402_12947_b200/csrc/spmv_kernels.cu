@@ -114,7 +114,7 @@ __device__ __forceinline__ void epilogue(const EpiArgs& ea, int32_t row, double 
 #endif
 constexpr int kMinBlocks = SMG_SPMV_MIN_BLOCKS;
 
-template <Epi E, bool kPf, bool kMulti>
+template <Epi E, bool kPf, bool kMulti, bool kFixed>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
 csr_tile_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, int pf_dist)
 {
@@ -127,18 +127,18 @@ csr_tile_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, 
   const int t = blockIdx.x;
   const int tid = threadIdx.x;
   // ---- operator data (never written by any kernel): before the dependency wait
-  const int32_t r0 = m.tile_row[t];
-  const int32_t r1 = m.tile_row[t + 1];
-  const int64_t e0 = m.tile_nz[t];
-  const int64_t e1 = m.tile_nz[t + 1];
-  const int cnt = (int)(e1 - e0);
-  const int nq = (cnt + kTileNnz - 1) / kTileNnz;   // chunks of this tile
-  const int32_t row = r0 + tid;
-  const bool has_row = row < r1;
-  int64_t lo = 0, hi = 0;
-  if (has_row) {
-    lo = m.rowptr[row];
-    hi = m.rowptr[row + 1];
+  // fixed-capacity layout: the tile's nonzeros start at t * cap -- the value /
+  // column loads need no tile-offset load first (one dependent round trip less)
+  const int32_t* __restrict__ colp = kFixed ? m.pcol : m.col;
+  const double* __restrict__ valp = kFixed ? m.pval : m.val;
+  int64_t e0;
+  int cnt;
+  if constexpr (kFixed) {
+    e0 = (int64_t)t * m.cap;
+    cnt = m.cap;
+  } else {
+    e0 = m.tile_nz[t];
+    cnt = (int)(m.tile_nz[t + 1] - e0);
   }
   int32_t c[kItems];
   double v[kItems];
@@ -150,28 +150,45 @@ csr_tile_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, 
       v[i] = 0.0;
       if (k < cnt && k < q0 + kTileNnz) {
         if (m.streaming) {  // operator larger than L2 share: don't evict the small levels
-          c[i] = __ldcs(m.col + e0 + k);
-          v[i] = __ldcs(m.val + e0 + k);
+          c[i] = __ldcs(colp + e0 + k);
+          v[i] = __ldcs(valp + e0 + k);
         } else {
-          c[i] = __ldg(m.col + e0 + k);
-          v[i] = __ldg(m.val + e0 + k);
+          c[i] = __ldg(colp + e0 + k);
+          v[i] = __ldg(valp + e0 + k);
         }
       }
     }
   };
-  load_chunk(0);
+  if constexpr (kFixed) load_chunk(0);
+  const int32_t r0 = m.tile_row[t];
+  const int32_t r1 = m.tile_row[t + 1];
+  const int nq = (cnt + kTileNnz - 1) / kTileNnz;   // chunks of this tile
+  const int32_t row = r0 + tid;
+  const bool has_row = row < r1;
+  int64_t lo = 0, hi = 0;
+  if (has_row) {
+    if constexpr (kFixed) {
+      lo = tid > 0 ? m.rel_end[row - 1] : 0;
+      hi = m.rel_end[row];
+    } else {
+      lo = m.rowptr[row] - e0;
+      hi = m.rowptr[row + 1] - e0;
+    }
+  }
+  if constexpr (!kFixed) load_chunk(0);
   if constexpr (kPf) {
     // pull the tile that starts one resident wave later into L2 (bulk
     // prefetch: no registers, no shared memory), so its CTA's loads hit L2
     if (tid == 0) {
       const int tp = t + pf_dist;
       if (tp < m.ntiles) {
-        const int64_t p0 = m.tile_nz[tp], p1 = m.tile_nz[tp + 1];
+        const int64_t p0 = kFixed ? (int64_t)tp * m.cap : m.tile_nz[tp];
+        const int64_t p1 = kFixed ? p0 + m.cap : m.tile_nz[tp + 1];
         if (p1 - p0 <= kTileNnz * kMaxTileChunks && p1 > p0) {
           const int64_t va = p0 & ~int64_t(1), vb = (p1 + 1) & ~int64_t(1);
           const int64_t ca = p0 & ~int64_t(3), cb = (p1 + 3) & ~int64_t(3);
-          prefetch_l2(m.val + va, (uint32_t)((vb - va) * 8), m.streaming);
-          prefetch_l2(m.col + ca, (uint32_t)((cb - ca) * 4), m.streaming);
+          prefetch_l2(valp + va, (uint32_t)((vb - va) * 8), m.streaming);
+          prefetch_l2(colp + ca, (uint32_t)((cb - ca) * 4), m.streaming);
         }
       }
     }
@@ -192,7 +209,7 @@ csr_tile_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, 
     if constexpr (T::kDiag) inv = m.inv_diag[grow];
     if constexpr (T::kDiagVec) inv = ea.inv_diag[grow];
   }
-  const int a = (int)(lo - e0), bnd = (int)(hi - e0);   // this row's tile-relative range
+  const int a = (int)lo, bnd = (int)hi;   // this row's tile-relative range
   double sum = 0.0;
   for (int q = 0; q < nq; ++q) {
     const int q0 = q * kTileNnz;
@@ -254,11 +271,18 @@ static cudaError_t launch_t(const DevCsr& m, const double* x, const EpiArgs& ea,
   }();
   const int dist = g_sm_count * kMinBlocks * waves;  // resident waves ahead (default one)
   const bool pf = env_flag(g_prefetch, "SMG_L2_PREFETCH", 1);
+  if (m.fixed) {
+    if (m.multichunk)
+      return pf ? cudaLaunchKernelEx(&cfg, csr_tile_kernel<E, true, true, true>, m, x, ea, dist)
+                : cudaLaunchKernelEx(&cfg, csr_tile_kernel<E, false, true, true>, m, x, ea, dist);
+    return pf ? cudaLaunchKernelEx(&cfg, csr_tile_kernel<E, true, false, true>, m, x, ea, dist)
+              : cudaLaunchKernelEx(&cfg, csr_tile_kernel<E, false, false, true>, m, x, ea, dist);
+  }
   if (m.multichunk)
-    return pf ? cudaLaunchKernelEx(&cfg, csr_tile_kernel<E, true, true>, m, x, ea, dist)
-              : cudaLaunchKernelEx(&cfg, csr_tile_kernel<E, false, true>, m, x, ea, dist);
-  return pf ? cudaLaunchKernelEx(&cfg, csr_tile_kernel<E, true, false>, m, x, ea, dist)
-            : cudaLaunchKernelEx(&cfg, csr_tile_kernel<E, false, false>, m, x, ea, dist);
+    return pf ? cudaLaunchKernelEx(&cfg, csr_tile_kernel<E, true, true, false>, m, x, ea, dist)
+              : cudaLaunchKernelEx(&cfg, csr_tile_kernel<E, false, true, false>, m, x, ea, dist);
+  return pf ? cudaLaunchKernelEx(&cfg, csr_tile_kernel<E, true, false, false>, m, x, ea, dist)
+            : cudaLaunchKernelEx(&cfg, csr_tile_kernel<E, false, false, false>, m, x, ea, dist);
 }
 
 cudaError_t launch_csr_stream(const DevCsr& m, const double* x, Epi epi, const EpiArgs& ea,
