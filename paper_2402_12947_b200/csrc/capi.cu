@@ -184,6 +184,85 @@ static int build_devcsr(std::vector<void*>& allocs, int64_t& bytes, int64_t nrow
   d.val = v;
   d.tile_row = tr;
   d.tile_nz = tz;
+  // SMG_SELL: 0 = never, 1 = every operator, unset/2 = operators with short
+  // rows (avg < SMG_SELL_MAX_ROW, default 20) and at least SMG_SELL_MIN_WIN
+  // windows (default 296 = 2 per SM): SELL streams one row per thread, which
+  // wins on short rows and loses where long rows serialise each thread
+  // (profiles/r01/ab_sell/)
+  static const int sell_mode = [] {
+    const char* e = getenv("SMG_SELL");
+    return e ? atoi(e) : 2;
+  }();
+  static const int sell_max_row = [] {
+    const char* e = getenv("SMG_SELL_MAX_ROW");
+    return e ? atoi(e) : 20;
+  }();
+  static const int sell_min_win = [] {
+    const char* e = getenv("SMG_SELL_MIN_WIN");
+    return e ? atoi(e) : 296;
+  }();
+  const int64_t nwin_est = (nrows + kSellWindow - 1) / kSellWindow;
+  const bool use_sell = nrows > 0 &&
+                        (sell_mode == 1 || (sell_mode >= 2 && nnz < (int64_t)sell_max_row * nrows &&
+                                            nwin_est >= sell_min_win));
+  if (use_sell) {
+    // SELL-32-sigma256: per window of 256 rows, slots sorted by row length
+    // (stable, descending), 8 slices of 32 slots, column-major within a slice
+    const int64_t nw = (nrows + kSellWindow - 1) / kSellWindow;
+    std::vector<int16_t> perm((size_t)(nw * kSellWindow), -1);
+    std::vector<int64_t> sptr((size_t)(nw * kSellSlices + 1), 0);
+    std::vector<int32_t> idx(kSellWindow);
+    for (int64_t w = 0; w < nw; ++w) {
+      const int64_t r0 = w * kSellWindow;
+      const int cntw = (int)std::min<int64_t>(kSellWindow, nrows - r0);
+      for (int i = 0; i < cntw; ++i) idx[(size_t)i] = i;
+      std::stable_sort(idx.begin(), idx.begin() + cntw, [&](int a, int b) {
+        return rowptr[r0 + a + 1] - rowptr[r0 + a] > rowptr[r0 + b + 1] - rowptr[r0 + b];
+      });
+      for (int sl = 0; sl < cntw; ++sl) perm[(size_t)(r0 + sl)] = (int16_t)idx[(size_t)sl];
+      for (int k = 0; k < kSellSlices; ++k) {
+        int64_t width = 0;
+        for (int l = 0; l < 32; ++l) {
+          const int sl = k * 32 + l;
+          if (sl < cntw) {
+            const int64_t r = r0 + idx[(size_t)sl];
+            width = std::max<int64_t>(width, rowptr[r + 1] - rowptr[r]);
+          }
+        }
+        sptr[(size_t)(w * kSellSlices + k + 1)] = sptr[(size_t)(w * kSellSlices + k)] + 32 * width;
+      }
+    }
+    const int64_t total = sptr.back();
+    std::vector<int32_t> scol((size_t)total + 4, -1);
+    std::vector<double> sval((size_t)total + 2, 0.0);
+    for (int64_t w = 0; w < nw; ++w) {
+      const int64_t r0 = w * kSellWindow;
+      for (int sl = 0; sl < kSellWindow; ++sl) {
+        const int16_t pr = perm[(size_t)(r0 + sl)];
+        if (pr < 0) continue;
+        const int64_t r = r0 + pr;
+        const int64_t base = sptr[(size_t)(w * kSellSlices + sl / 32)] + (sl % 32);
+        for (int64_t j = rowptr[r]; j < rowptr[r + 1]; ++j) {
+          scol[(size_t)(base + (j - rowptr[r]) * 32)] = col32[(size_t)j];
+          sval[(size_t)(base + (j - rowptr[r]) * 32)] = val[j];
+        }
+      }
+    }
+    int64_t* dsp = nullptr;
+    int16_t* dperm = nullptr;
+    int32_t* dsc = nullptr;
+    double* dsv = nullptr;
+    SMG_TRY(dev_upload(allocs, bytes, sptr.data(), sptr.size(), &dsp));
+    SMG_TRY(dev_upload(allocs, bytes, perm.data(), perm.size(), &dperm));
+    SMG_TRY(dev_upload(allocs, bytes, scol.data(), scol.size(), &dsc));
+    SMG_TRY(dev_upload(allocs, bytes, sval.data(), sval.size(), &dsv));
+    d.sell = true;
+    d.sell_nwin = (int32_t)nw;
+    d.sell_ptr = dsp;
+    d.sell_perm = dperm;
+    d.sell_col = dsc;
+    d.sell_val = dsv;
+  }
   if (fixed) {
     const size_t nt = tiles.size() - 1;
     std::vector<int32_t> pc(nt * (size_t)cap + 4, 0);

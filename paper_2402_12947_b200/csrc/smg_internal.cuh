@@ -51,7 +51,19 @@ struct DevCsr {
   const int32_t* pcol = nullptr;
   const double* pval = nullptr;
   const int32_t* rel_end = nullptr;
+  // SELL-32-sigma256 layout (sell_kernel): windows of 256 consecutive rows,
+  // rows sorted by length inside the window (perm: slot -> row offset, -1 =
+  // no row), 8 slices of 32 slots per window stored column-major (entry j of
+  // the 32 slots contiguous; padding column -1), slice offsets in sell_ptr
+  bool sell = false;
+  int32_t sell_nwin = 0;
+  const int64_t* sell_ptr = nullptr;   // nwin * 8 + 1
+  const int16_t* sell_perm = nullptr;  // nwin * 256
+  const int32_t* sell_col = nullptr;
+  const double* sell_val = nullptr;
 };
+constexpr int kSellWindow = 256;
+constexpr int kSellSlices = kSellWindow / 32;
 
 // Host-side owner of one operator's device arrays.
 struct Operator {

@@ -231,6 +231,91 @@ csr_tile_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, 
   if (write) epilogue<E>(ea, grow, sum, inv, bv, uv, dv, ov);
 }
 
+// SELL-32-sigma256 (DevCsr::sell): one CTA per window of 256 rows, warp k =
+// slice k, lane = slot.  Each thread streams its own row -- entry j of the 32
+// slots is contiguous, so every load is coalesced -- and adds the products in
+// column order (scipy's order) without staging them in shared memory: no
+// barrier, few registers, 8 CTAs (64 warps) per SM.
+constexpr int kSellPre = 4;   // entries loaded before the dependency wait
+
+template <Epi E, bool kPf>
+__global__ void __launch_bounds__(kSellWindow, 8)
+sell_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, int pf_dist)
+{
+  using T = EpiTraits<E>;
+  const int w = blockIdx.x;
+  const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t sb = m.sell_ptr[(int64_t)w * kSellSlices + k];
+  const int64_t se = m.sell_ptr[(int64_t)w * kSellSlices + k + 1];
+  const int width = (int)((se - sb) >> 5);
+  const int rl = m.sell_perm[(int64_t)w * kSellWindow + threadIdx.x];
+  const int32_t* __restrict__ cp = m.sell_col + sb + lane;
+  const double* __restrict__ vp = m.sell_val + sb + lane;
+  int32_t c0[kSellPre];
+  double v0[kSellPre];
+#pragma unroll
+  for (int j = 0; j < kSellPre; ++j) {
+    c0[j] = -1;
+    v0[j] = 0.0;
+    if (j < width) {
+      if (m.streaming) {
+        c0[j] = __ldcs(cp + j * 32);
+        v0[j] = __ldcs(vp + j * 32);
+      } else {
+        c0[j] = __ldg(cp + j * 32);
+        v0[j] = __ldg(vp + j * 32);
+      }
+    }
+  }
+  if constexpr (kPf) {
+    if (threadIdx.x == 0) {
+      const int wp = w + pf_dist;
+      if (wp < m.sell_nwin) {
+        const int64_t p0 = m.sell_ptr[(int64_t)wp * kSellSlices];
+        const int64_t p1 = m.sell_ptr[(int64_t)(wp + 1) * kSellSlices];
+        if (p1 > p0 && p1 - p0 <= (int64_t)kTileNnz * 16) {
+          const int64_t va = p0 & ~int64_t(1), vb = (p1 + 1) & ~int64_t(1);
+          const int64_t ca = p0 & ~int64_t(3), cb = (p1 + 3) & ~int64_t(3);
+          prefetch_l2(m.sell_val + va, (uint32_t)((vb - va) * 8), m.streaming);
+          prefetch_l2(m.sell_col + ca, (uint32_t)((cb - ca) * 4), m.streaming);
+        }
+      }
+    }
+  }
+  pdl_wait();
+  pdl_trigger();
+  const int32_t grow = w * kSellWindow + rl;
+  const bool has_row = rl >= 0;
+  const bool write = has_row && !(ea.skip_rows && ea.skip_rows[grow]);
+  double bv = 0.0, uv = 0.0, dv = 0.0, ov = 0.0, inv = 0.0;
+  if (write) {
+    if constexpr (T::kB) bv = ea.b[grow];
+    if constexpr (T::kU) uv = ea.u_in[grow];
+    if constexpr (T::kD) dv = ea.d[grow];
+    if constexpr (T::kOut) ov = ea.out[grow];
+    if constexpr (T::kDiag) inv = m.inv_diag[grow];
+    if constexpr (T::kDiagVec) inv = ea.inv_diag[grow];
+  }
+  double sum = 0.0;
+#pragma unroll
+  for (int j = 0; j < kSellPre; ++j)
+    if (c0[j] >= 0) sum = __dadd_rn(sum, __dmul_rn(v0[j], __ldg(x + c0[j])));
+#pragma unroll 4
+  for (int j = kSellPre; j < width; ++j) {
+    int32_t c;
+    double v;
+    if (m.streaming) {
+      c = __ldcs(cp + j * 32);
+      v = __ldcs(vp + j * 32);
+    } else {
+      c = __ldg(cp + j * 32);
+      v = __ldg(vp + j * 32);
+    }
+    if (c >= 0) sum = __dadd_rn(sum, __dmul_rn(v, __ldg(x + c)));
+  }
+  if (write) epilogue<E>(ea, grow, sum, inv, bv, uv, dv, ov);
+}
+
 static int g_sm_count = 0;
 static int g_prefetch = -1;
 static int g_pdl = -1;
@@ -247,7 +332,7 @@ static bool env_flag(int& cache, const char* name, int dflt)
 template <Epi E>
 static cudaError_t launch_t(const DevCsr& m, const double* x, const EpiArgs& ea, cudaStream_t s)
 {
-  if (m.ntiles == 0) return cudaSuccess;
+  if (m.ntiles == 0 && !(m.sell && m.sell_nwin > 0)) return cudaSuccess;
   if (g_sm_count == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -271,6 +356,13 @@ static cudaError_t launch_t(const DevCsr& m, const double* x, const EpiArgs& ea,
   }();
   const int dist = g_sm_count * kMinBlocks * waves;  // resident waves ahead (default one)
   const bool pf = env_flag(g_prefetch, "SMG_L2_PREFETCH", 1);
+  if (m.sell) {
+    cfg.gridDim = dim3((unsigned)m.sell_nwin);
+    cfg.blockDim = dim3(kSellWindow);
+    const int sdist = g_sm_count * 8 * waves;
+    return pf ? cudaLaunchKernelEx(&cfg, sell_kernel<E, true>, m, x, ea, sdist)
+              : cudaLaunchKernelEx(&cfg, sell_kernel<E, false>, m, x, ea, sdist);
+  }
   if (m.fixed) {
     if (m.multichunk)
       return pf ? cudaLaunchKernelEx(&cfg, csr_tile_kernel<E, true, true, true>, m, x, ea, dist)

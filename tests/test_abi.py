@@ -46,7 +46,9 @@ def test_sass_is_sm100a_and_parity_kernels_have_no_fma():
     for epi in ("0", "1", "5"):
         names = [f for f in funcs if f.startswith(f"_ZN3smg15csr_tile_kernelILNS_3EpiE{epi}E")]
         assert names, f"csr_tile_kernel<{epi}> missing"
-        for name in names:  # with and without the L2-prefetch instantiation
+        sell = [f for f in funcs if f.startswith(f"_ZN3smg11sell_kernelILNS_3EpiE{epi}E")]
+        assert sell, f"sell_kernel<{epi}> missing"
+        for name in names + sell:  # every layout, with and without the L2 prefetch
             body = "\n".join(funcs[name])
             assert "DFMA" not in body, f"{name} contains DFMA"
             assert "DMUL" in body and "DADD" in body
