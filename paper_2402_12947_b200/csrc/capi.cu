@@ -184,27 +184,28 @@ static int build_devcsr(std::vector<void*>& allocs, int64_t& bytes, int64_t nrow
   d.val = v;
   d.tile_row = tr;
   d.tile_nz = tz;
-  // SMG_SELL: 0 = never, 1 = every operator, unset/2 = operators with short
-  // rows (avg < SMG_SELL_MAX_ROW, default 20) and at least SMG_SELL_MIN_WIN
-  // windows (default 296 = 2 per SM): SELL streams one row per thread, which
-  // wins on short rows and loses where long rows serialise each thread
-  // (profiles/r01/ab_sell/)
-  static const int sell_mode = [] {
-    const char* e = getenv("SMG_SELL");
-    return e ? atoi(e) : 2;
-  }();
-  static const int sell_max_row = [] {
-    const char* e = getenv("SMG_SELL_MAX_ROW");
-    return e ? atoi(e) : 20;
-  }();
-  static const int sell_min_win = [] {
-    const char* e = getenv("SMG_SELL_MIN_WIN");
-    return e ? atoi(e) : 296;
-  }();
+  // SMG_SELL: 0 = never, 1 = every operator, unset/2 = by measurement
+  // (profiles/r01/ab_sell/): short rows (avg < SMG_SELL_MAX_ROW = 20) with at
+  // least SMG_SELL_MIN_WIN = 296 windows run SELL with a 4-deep loop (8 CTAs
+  // per SM); longer rows with at least SMG_SELL_MIN_WIN_LONG = 592 windows run
+  // SELL with an SMG_SELL_LONG_UNROLL-deep loop (default 8; more loads in
+  // flight per thread); operators with fewer windows keep the tile kernel,
+  // whose CTAs share a row's products across all threads
+  auto env_int = [](const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
+  };
+  static const int sell_mode = env_int("SMG_SELL", 2);
+  static const int sell_max_row = env_int("SMG_SELL_MAX_ROW", 20);
+  static const int sell_min_win = env_int("SMG_SELL_MIN_WIN", 296);
+  static const int sell_min_win_long = env_int("SMG_SELL_MIN_WIN_LONG", 592);
+  static const int sell_long_unroll = env_int("SMG_SELL_LONG_UNROLL", 8);
   const int64_t nwin_est = (nrows + kSellWindow - 1) / kSellWindow;
-  const bool use_sell = nrows > 0 &&
-                        (sell_mode == 1 || (sell_mode >= 2 && nnz < (int64_t)sell_max_row * nrows &&
-                                            nwin_est >= sell_min_win));
+  const bool short_rows = nnz < (int64_t)sell_max_row * nrows;
+  const bool use_sell =
+      nrows > 0 && (sell_mode == 1 ||
+                    (sell_mode >= 2 && nwin_est >= (short_rows ? sell_min_win : sell_min_win_long)));
+  d.sell_unroll = short_rows ? 4 : sell_long_unroll;
   if (use_sell) {
     // SELL-32-sigma256: per window of 256 rows, slots sorted by row length
     // (stable, descending), 8 slices of 32 slots, column-major within a slice

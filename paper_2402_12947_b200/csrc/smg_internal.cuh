@@ -56,6 +56,7 @@ struct DevCsr {
   // no row), 8 slices of 32 slots per window stored column-major (entry j of
   // the 32 slots contiguous; padding column -1), slice offsets in sell_ptr
   bool sell = false;
+  int32_t sell_unroll = 4;             // loop unroll (4: 8 CTAs/SM; 8/16: long rows)
   int32_t sell_nwin = 0;
   const int64_t* sell_ptr = nullptr;   // nwin * 8 + 1
   const int16_t* sell_perm = nullptr;  // nwin * 256

@@ -238,8 +238,8 @@ csr_tile_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, 
 // barrier, few registers, 8 CTAs (64 warps) per SM.
 constexpr int kSellPre = 4;   // entries loaded before the dependency wait
 
-template <Epi E, bool kPf>
-__global__ void __launch_bounds__(kSellWindow, 8)
+template <Epi E, bool kPf, int kUnroll>
+__global__ void __launch_bounds__(kSellWindow, kUnroll <= 4 ? 8 : (kUnroll <= 8 ? 4 : 2))
 sell_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, int pf_dist)
 {
   using T = EpiTraits<E>;
@@ -300,7 +300,7 @@ sell_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, int 
 #pragma unroll
   for (int j = 0; j < kSellPre; ++j)
     if (c0[j] >= 0) sum = __dadd_rn(sum, __dmul_rn(v0[j], __ldg(x + c0[j])));
-#pragma unroll 4
+#pragma unroll kUnroll
   for (int j = kSellPre; j < width; ++j) {
     int32_t c;
     double v;
@@ -359,9 +359,19 @@ static cudaError_t launch_t(const DevCsr& m, const double* x, const EpiArgs& ea,
   if (m.sell) {
     cfg.gridDim = dim3((unsigned)m.sell_nwin);
     cfg.blockDim = dim3(kSellWindow);
+    if (m.sell_unroll >= 16) {
+      const int sdist = g_sm_count * 2 * waves;
+      return pf ? cudaLaunchKernelEx(&cfg, sell_kernel<E, true, 16>, m, x, ea, sdist)
+                : cudaLaunchKernelEx(&cfg, sell_kernel<E, false, 16>, m, x, ea, sdist);
+    }
+    if (m.sell_unroll >= 8) {
+      const int sdist = g_sm_count * 4 * waves;
+      return pf ? cudaLaunchKernelEx(&cfg, sell_kernel<E, true, 8>, m, x, ea, sdist)
+                : cudaLaunchKernelEx(&cfg, sell_kernel<E, false, 8>, m, x, ea, sdist);
+    }
     const int sdist = g_sm_count * 8 * waves;
-    return pf ? cudaLaunchKernelEx(&cfg, sell_kernel<E, true>, m, x, ea, sdist)
-              : cudaLaunchKernelEx(&cfg, sell_kernel<E, false>, m, x, ea, sdist);
+    return pf ? cudaLaunchKernelEx(&cfg, sell_kernel<E, true, 4>, m, x, ea, sdist)
+              : cudaLaunchKernelEx(&cfg, sell_kernel<E, false, 4>, m, x, ea, sdist);
   }
   if (m.fixed) {
     if (m.multichunk)
