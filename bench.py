@@ -179,6 +179,18 @@ def cpu_baseline(h, b, budget_s: float, threads: int):
     return n / el, n, el, O.num_threads()
 
 
+def _layout(lib, op) -> str:
+    """Name of the kernel/layout the operator's sweeps run on (smg_operator_layout)."""
+    import ctypes
+    lay, unr = ctypes.c_int(), ctypes.c_int()
+    if lib.smg_operator_layout(op.handle, ctypes.byref(lay), ctypes.byref(unr)) != 0:
+        return "unknown"
+    if lay.value == 2:
+        return f"sell_kernel (SELL-32-sigma256, {unr.value}-deep)"
+    kind = "fixed-capacity" if lay.value == 1 else "offset-table"
+    return f"csr_tile_kernel ({kind} tiles, {unr.value} chunk(s))"
+
+
 def run_reference(args):
     ws, rank, local = _dist()
     if rank != 0:
@@ -498,7 +510,8 @@ def main():
         k1.record(stream)
         torch.cuda.synchronize()
         us = k0.elapsed_time(k1) / 100 * 1e3
-        per_level.append({"level": li, "rows": nl, "nnz": zl, "us": round(us, 2),
+        per_level.append({"level": li, "rows": nl, "nnz": zl, "layout": _layout(lib, opl),
+                          "us": round(us, 2),
                           "gbs": round(bpl / us / 1e3, 1), "frac": round(bpl / us / 1e3 / _peaks()[0], 3)})
         del xa, xb, dl, bl
 
@@ -596,7 +609,7 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "traffic_source": traffic_src,
-                         "kernel": "csr_tile_kernel<ChebNext> (fine-level Chebyshev step)",
+                         "kernel": f"{_layout(lib, dh.ops[0])} <ChebNext> (fine-level Chebyshev step)",
                          "bytes_per_launch": bytes_per, "us_per_launch": 1e3 * k_ms,
                          "peak_source": peak_src, "nnz": z, "rows": nn,
                          "nnz_per_row": z / nn},

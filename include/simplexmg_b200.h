@@ -72,6 +72,17 @@ SMG_API int smg_operator_destroy(smg_operator *op);
 SMG_API int smg_operator_info(const smg_operator *op, int64_t *nrows, int64_t *ncols, int64_t *nnz,
                       int64_t *first_zero_diag, int64_t *device_bytes);
 
+/* Device layout the sweeps of an operator run on (chosen at upload from its
+ * row-length statistics; every layout is bit-identical):
+ *   SMG_LAYOUT_TILES        CSR tiles with an offset table (csr_tile_kernel)
+ *   SMG_LAYOUT_TILES_FIXED  fixed-capacity CSR tiles (csr_tile_kernel)
+ *   SMG_LAYOUT_SELL         SELL-32-sigma256 (sell_kernel); *unroll = loop depth
+ * For tiles *unroll is the chunks per tile (1, or 4 for long-row operators). */
+#define SMG_LAYOUT_TILES 0
+#define SMG_LAYOUT_TILES_FIXED 1
+#define SMG_LAYOUT_SELL 2
+SMG_API int smg_operator_layout(const smg_operator *op, int *layout, int *unroll);
+
 /* y = A x                       (sparse.py:135-140 spmv; bitwise)                */
 SMG_API int smg_spmv(const smg_operator *a, const double *x, double *y, void *stream);
 /* r = b - A u                   (smoothers.py:263,266; mg.py:141; bitwise)       */

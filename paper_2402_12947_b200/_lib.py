@@ -39,6 +39,7 @@ PROTOTYPES = {
     "smg_operator_create": (ctypes.c_int, [_i64, _i64, _i64p, _i64p, _f64p, ctypes.c_int, _pp]),
     "smg_operator_destroy": (ctypes.c_int, [_vp]),
     "smg_operator_info": (ctypes.c_int, [_vp, _i64p, _i64p, _i64p, _i64p, _i64p]),
+    "smg_operator_layout": (ctypes.c_int, [_vp, _intp, _intp]),
     "smg_spmv": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "smg_residual": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "smg_spmv_transpose": (ctypes.c_int, [_vp, _vp, _vp, _vp]),

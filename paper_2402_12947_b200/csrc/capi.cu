@@ -258,6 +258,7 @@ static int build_devcsr(std::vector<void*>& allocs, int64_t& bytes, int64_t nrow
     SMG_TRY(dev_upload(allocs, bytes, scol.data(), scol.size(), &dsc));
     SMG_TRY(dev_upload(allocs, bytes, sval.data(), sval.size(), &dsv));
     d.sell = true;
+    fixed = false;   // the sweeps run on the SELL arrays: no padded tile copy
     d.sell_nwin = (int32_t)nw;
     d.sell_ptr = dsp;
     d.sell_perm = dperm;
@@ -827,6 +828,15 @@ int smg_operator_info(const smg_operator* op, int64_t* nrows, int64_t* ncols, in
   if (nnz) *nnz = op->o.a.nnz;
   if (first_zero_diag) *first_zero_diag = op->o.first_zero_diag;
   if (device_bytes) *device_bytes = op->o.device_bytes;
+  return SMG_OK;
+}
+
+int smg_operator_layout(const smg_operator* op, int* layout, int* unroll)
+{
+  if (!op) return fail("operator is NULL");
+  const DevCsr& m = op->o.a;
+  if (layout) *layout = m.sell ? SMG_LAYOUT_SELL : (m.fixed ? SMG_LAYOUT_TILES_FIXED : SMG_LAYOUT_TILES);
+  if (unroll) *unroll = m.sell ? m.sell_unroll : (m.multichunk ? kMaxTileChunks : 1);
   return SMG_OK;
 }
 
