@@ -15,7 +15,7 @@ if ! $CMD > $OUT/plain_$TAG.log 2>&1; then echo "plain run failed"; exit 1; fi
 ncu --nvtx --nvtx-include "vcycle/" --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $OUT/launches_$TAG.csv $CMD > $OUT/ncu_launch_$TAG.log 2>&1
 echo "launch list: $?"
-ncu --nvtx --nvtx-include "sweeps/" -k regex:csr_tile_kernel --set full --clock-control none --import-source on \
+ncu --nvtx --nvtx-include "sweeps/" -k regex:"csr_tile_kernel|sell_kernel" --set full --clock-control none --import-source on \
     -o $OUT/prof_sweeps_$TAG $CMD > $OUT/ncu_sweeps_$TAG.log 2>&1
 echo "sweeps: $?"
 ncu --nvtx --nvtx-include "lc/" -k regex:patch_kernel --set full --clock-control none --import-source on \
