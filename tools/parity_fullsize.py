@@ -46,6 +46,28 @@ def main():
         sweeps.append(bool(np.array_equal(u, O.global_smooth(lv.a, b, ur.copy(), cfg))))
     out["fine_sweeps_bitwise"] = sweeps
     lib = _lib.load()
+    # every non-coarse level: one smoother call of the level's degree and the
+    # residual, bitwise, with the layout the level's sweeps run on
+    levels = []
+    for l, lvl in enumerate(h.levels[:-1]):
+        n = lvl.a.nrows
+        ul = np.random.default_rng(200 + l).standard_normal(n)
+        bl = np.random.default_rng(300 + l).standard_normal(n)
+        ug = ul.copy()
+        P.chebyshev_smooth(lvl.a, bl, ug, lvl.smoother.sweeps, lvl.smoother)
+        ok_s = bool(np.array_equal(ug, O.global_smooth(lvl.a, bl, ul.copy(), lvl.smoother)))
+        op = D.device_operator(lvl.a)
+        bt, ut = torch.from_numpy(bl).cuda(), torch.from_numpy(ul).cuda()
+        rt = torch.empty_like(bt)
+        _lib.check(lib.smg_residual(op.handle, D.ptr(bt), D.ptr(ut), D.ptr(rt), D.stream_handle()))
+        ok_r = bool(np.array_equal(rt.cpu().numpy(), bl - O.spmv(lvl.a, ul)))
+        import ctypes
+        lay, unr = ctypes.c_int(), ctypes.c_int()
+        _lib.check(lib.smg_operator_layout(op.handle, ctypes.byref(lay), ctypes.byref(unr)))
+        levels.append({"level": l, "rows": n, "nnz": lvl.a.nnz,
+                       "layout": ["tiles", "tiles-fixed", "sell"][lay.value], "unroll": unr.value,
+                       "smooth_bitwise": ok_s, "residual_bitwise": ok_r})
+    out["levels"] = levels
     transfers = []
     for l, lvl in enumerate(h.levels[:-1]):
         pm = lvl.prolongation.matrix
