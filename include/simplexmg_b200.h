@@ -82,6 +82,11 @@ SMG_API int smg_operator_info(const smg_operator *op, int64_t *nrows, int64_t *n
 #define SMG_LAYOUT_TILES_FIXED 1
 #define SMG_LAYOUT_SELL 2
 SMG_API int smg_operator_layout(const smg_operator *op, int *layout, int *unroll);
+/* Force a layout (and SELL loop depth 4/8/16; 0 = by the rule) for the
+ * operator and its stored transpose -- for tests and A/B runs; results are
+ * bit-identical in every layout.  Not thread-safe with concurrent launches on
+ * the operator; hierarchies built on it afterwards use the new layout.        */
+SMG_API int smg_operator_set_layout(smg_operator *op, int layout, int unroll);
 
 /* y = A x                       (sparse.py:135-140 spmv; bitwise)                */
 SMG_API int smg_spmv(const smg_operator *a, const double *x, double *y, void *stream);

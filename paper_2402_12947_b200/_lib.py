@@ -40,6 +40,7 @@ PROTOTYPES = {
     "smg_operator_destroy": (ctypes.c_int, [_vp]),
     "smg_operator_info": (ctypes.c_int, [_vp, _i64p, _i64p, _i64p, _i64p, _i64p]),
     "smg_operator_layout": (ctypes.c_int, [_vp, _intp, _intp]),
+    "smg_operator_set_layout": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int]),
     "smg_spmv": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "smg_residual": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "smg_spmv_transpose": (ctypes.c_int, [_vp, _vp, _vp, _vp]),

@@ -131,9 +131,11 @@ static bool stream_env()
   return !(v && v[0] == '0');
 }
 
+// forced_layout: -1 = by the measured rule, else SMG_LAYOUT_* (tests / A-B);
+// forced_unroll: SELL loop depth (0 = by the rule)
 static int build_devcsr(std::vector<void*>& allocs, int64_t& bytes, int64_t nrows, int64_t ncols,
                         const int64_t* rowptr, const int64_t* col64, const double* val,
-                        DevCsr* out)
+                        DevCsr* out, int forced_layout = -1, int forced_unroll = 0)
 {
   const int64_t nnz = rowptr[nrows];
   // padded so the TMA ring may read up to 16 B past the last element
@@ -154,7 +156,8 @@ static int build_devcsr(std::vector<void*>& allocs, int64_t& bytes, int64_t nrow
   // row their tiles are row-bound, and shrinking them to avoid padding measured
   // slower on C5, profiles/r01/ab_fixed_tiles/)
   bool fixed = fixed_env && nrows > 0 && !long_rows(nnz, nrows);
-  if (fixed) {
+  if (forced_layout >= 0) fixed = forced_layout == SMG_LAYOUT_TILES_FIXED && nrows > 0;
+  if (fixed && !long_rows(nnz, nrows)) {
     while (cap > 256 && kRowsPerTile * nnz < cap * nrows) cap /= 2;
   }
   std::vector<int32_t> tiles = make_tiles(nrows, rowptr, cap);
@@ -202,10 +205,12 @@ static int build_devcsr(std::vector<void*>& allocs, int64_t& bytes, int64_t nrow
   static const int sell_long_unroll = env_int("SMG_SELL_LONG_UNROLL", 8);
   const int64_t nwin_est = (nrows + kSellWindow - 1) / kSellWindow;
   const bool short_rows = nnz < (int64_t)sell_max_row * nrows;
-  const bool use_sell =
+  bool use_sell =
       nrows > 0 && (sell_mode == 1 ||
                     (sell_mode >= 2 && nwin_est >= (short_rows ? sell_min_win : sell_min_win_long)));
+  if (forced_layout >= 0) use_sell = forced_layout == SMG_LAYOUT_SELL && nrows > 0;
   d.sell_unroll = short_rows ? 4 : sell_long_unroll;
+  if (forced_unroll > 0) d.sell_unroll = forced_unroll >= 16 ? 16 : (forced_unroll >= 8 ? 8 : 4);
   if (use_sell) {
     // SELL-32-sigma256: per window of 256 rows, slots sorted by row length
     // (stable, descending), 8 slices of 32 slots, column-major within a slice
@@ -828,6 +833,38 @@ int smg_operator_info(const smg_operator* op, int64_t* nrows, int64_t* ncols, in
   if (nnz) *nnz = op->o.a.nnz;
   if (first_zero_diag) *first_zero_diag = op->o.first_zero_diag;
   if (device_bytes) *device_bytes = op->o.device_bytes;
+  return SMG_OK;
+}
+
+static int relayout(Operator& o, DevCsr& m, int layout, int unroll)
+{
+  const int64_t n = m.nrows, nnz = m.nnz;
+  std::vector<int64_t> rp((size_t)n + 1);
+  std::vector<int32_t> c32((size_t)std::max<int64_t>(nnz, 1));
+  std::vector<int64_t> c64((size_t)std::max<int64_t>(nnz, 1));
+  std::vector<double> v((size_t)std::max<int64_t>(nnz, 1));
+  SMG_CUDA(cudaMemcpy(rp.data(), m.rowptr, sizeof(int64_t) * (size_t)(n + 1), cudaMemcpyDeviceToHost));
+  if (nnz > 0) {
+    SMG_CUDA(cudaMemcpy(c32.data(), m.col, sizeof(int32_t) * (size_t)nnz, cudaMemcpyDeviceToHost));
+    SMG_CUDA(cudaMemcpy(v.data(), m.val, sizeof(double) * (size_t)nnz, cudaMemcpyDeviceToHost));
+  }
+  for (int64_t j = 0; j < nnz; ++j) c64[(size_t)j] = c32[(size_t)j];
+  DevCsr d;
+  SMG_TRY(build_devcsr(o.allocs, o.device_bytes, n, m.ncols, rp.data(), c64.data(), v.data(), &d,
+                       layout, unroll));
+  d.inv_diag = m.inv_diag;
+  d.row_map = m.row_map;
+  m = d;
+  return SMG_OK;
+}
+
+int smg_operator_set_layout(smg_operator* op, int layout, int unroll)
+{
+  if (!op) return fail("operator is NULL");
+  if (layout < SMG_LAYOUT_TILES || layout > SMG_LAYOUT_SELL) return fail("unknown layout");
+  SMG_CUDA(cudaDeviceSynchronize());
+  SMG_TRY(relayout(op->o, op->o.a, layout, unroll));
+  if (op->o.has_t) SMG_TRY(relayout(op->o, op->o.t, layout, unroll));
   return SMG_OK;
 }
 
