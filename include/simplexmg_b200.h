@@ -253,10 +253,21 @@ SMG_API int smg_hierarchy_set_graphs(smg_hierarchy *h, int enable);
  *                           patch-independent (interior) rows of the adjacent
  *                           smoother sweep; the halo rows follow (bit-identical,
  *                           default 0: the extra halo launch and the fork/join
- *                           cost more than the overlap saves on C1-C3) */
+ *                           cost more than the overlap saves on C1-C3)
+ *   SMG_OPT_LC_FOLLOW       1 = every local correction that follows a kernel
+ *                           producing u (the last smoother step, the
+ *                           prolong-add) runs concurrently with it: the
+ *                           producer skips the patch dofs, the correction
+ *                           recomputes the producer on its rings and writes
+ *                           them (bit-identical; default 1, but rings are
+ *                           only built for corrections created with the
+ *                           environment variable SMG_LC_FOLLOW=1: measured
+ *                           slower on C1-C4, a dependent launch cannot start
+ *                           before its producer's last wave) */
 #define SMG_OPT_GRAPHS 0
 #define SMG_OPT_FUSE_ZERO_GUESS 1
 #define SMG_OPT_LC_OVERLAP 2
+#define SMG_OPT_LC_FOLLOW 3
 SMG_API int smg_hierarchy_set_option(smg_hierarchy *h, int option, int value);
 /* kernels one V-cycle launches (for launch accounting) */
 SMG_API int smg_hierarchy_launches_per_vcycle(const smg_hierarchy *h, int64_t *launches);

@@ -339,39 +339,58 @@ static int cheb_scalars(int sweeps, double lambda_max, double frac, ChebScalars*
 
 // k steps ping-ponging between *cur and *alt (the reference computes the full
 // A u before updating u, so the gathering SpMV never writes its own input).
+// With `follow` the last step skips the patch dofs and leaves d alone (it is
+// dead after the last step), and the correction that follows the smoother
+// runs concurrently with that step (patch_kernel<kFollow>: it recomputes the
+// step on its rings, then writes u_out on the patch dofs); *followed reports
+// whether that happened (no step launched -> the caller corrects as usual).
 static int enqueue_global_smooth(const Operator& op, const double* b, double** cur, double** alt,
                                  double* d, int sweeps, const ChebScalars& cs, cudaStream_t st,
-                                 int64_t* launches, bool first_done = false)
+                                 int64_t* launches, bool first_done = false,
+                                 const Correction* follow = nullptr, bool* followed = nullptr)
 {
-  EpiArgs ea;
-  ea.b = b;
-  ea.theta = cs.theta;
-  ea.d = d;
+  if (followed) *followed = false;
+  std::vector<std::pair<Epi, std::pair<double, double>>> steps;
   if (cs.collapsed) {
-    for (int k = first_done ? 1 : 0; k < sweeps; ++k) {
-      ea.u_in = *cur;
-      ea.out = *alt;
-      SMG_CUDA(launch_csr_stream(op.a, *cur, Epi::kJacobi, ea, st));
-      std::swap(*cur, *alt);
-      ++*launches;
+    for (int k = first_done ? 1 : 0; k < sweeps; ++k) steps.push_back({Epi::kJacobi, {0.0, 0.0}});
+  } else {
+    if (!first_done) steps.push_back({Epi::kChebFirst, {0.0, 0.0}});
+    for (const auto& c : cs.steps) steps.push_back({Epi::kChebNext, c});
+  }
+  for (size_t k = 0; k < steps.size(); ++k) {
+    EpiArgs ea;
+    ea.b = b;
+    ea.theta = cs.theta;
+    ea.d = d;
+    ea.u_in = *cur;
+    ea.out = *alt;
+    ea.c1 = steps[k].second.first;
+    ea.c2 = steps[k].second.second;
+    const bool fol = follow && k + 1 == steps.size();
+    if (fol) {
+      ea.skip_rows = follow->bmask;
+      ea.keep_d = false;
     }
-    return SMG_OK;
-  }
-  if (!first_done) {
-    ea.u_in = *cur;
-    ea.out = *alt;
-    SMG_CUDA(launch_csr_stream(op.a, *cur, Epi::kChebFirst, ea, st));
-    std::swap(*cur, *alt);
+    SMG_CUDA(launch_csr_stream(op.a, *cur, steps[k].first, ea, st));
     ++*launches;
-  }
-  for (size_t k = 0; k < cs.steps.size(); ++k) {
-    ea.u_in = *cur;
-    ea.out = *alt;
-    ea.c1 = cs.steps[k].first;
-    ea.c2 = cs.steps[k].second;
-    SMG_CUDA(launch_csr_stream(op.a, *cur, Epi::kChebNext, ea, st));
+    if (fol) {
+      FollowArgs fa;
+      fa.epi = (int)steps[k].first;
+      fa.ring = follow->ringA;
+      fa.x = *cur;
+      fa.u_in = *cur;
+      fa.b = b;
+      fa.d = d;
+      fa.inv_diag = op.a.inv_diag;
+      fa.theta = cs.theta;
+      fa.c1 = ea.c1;
+      fa.c2 = ea.c2;
+      fa.out = *alt;
+      SMG_CUDA(launch_patch_follow(*follow, fa, st));
+      ++*launches;
+      if (followed) *followed = true;
+    }
     std::swap(*cur, *alt);
-    ++*launches;
   }
   return SMG_OK;
 }
@@ -444,6 +463,8 @@ struct HLevel {
   double* t = nullptr;   // ping-pong partner
   double* d = nullptr;   // Chebyshev direction
   double* r = nullptr;   // residual
+  RingRows ringP;        // P's rows on the correction rings (follow-mode prolong-add)
+  bool has_ringP = false;
 };
 
 struct Hierarchy {
@@ -458,6 +479,8 @@ struct Hierarchy {
   bool use_graphs = true;
   bool fuse_zero_guess = true;
   bool lc_overlap = false;  // measured slower: opt-in
+  bool lc_follow = true;    // corrections overlapped with their producer kernel
+                            // (only where rings were built: opt-in, see build_ring)
   cudaStream_t side = nullptr;       // local corrections overlapping interior sweeps
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   std::map<std::pair<const void*, void*>, cudaGraphExec_t> graphs;
@@ -495,15 +518,19 @@ struct Hierarchy {
 // halo rows run first, then the second correction overlaps its interior rows.
 // Every row is computed by exactly the arithmetic of the unsplit sweep, so the
 // result is bit-identical.
+// lc1_done: the first correction already ran, fused with the prolong-add.
 static int enqueue_smooth(Hierarchy& h, HLevel& L, const double* b, double** cur, double** alt,
-                          cudaStream_t st, int64_t* launches, bool first_done = false)
+                          cudaStream_t st, int64_t* launches, bool first_done = false,
+                          bool lc1_done = false)
 {
   const bool active = L.lc && L.lc->n_regions > 0;
   if (!active || first_done || !h.lc_overlap || !L.lc->has_halo) {
-    if (active) SMG_TRY(enqueue_local_correct(*L.lc, b, *cur, st, launches));
+    if (active && !lc1_done) SMG_TRY(enqueue_local_correct(*L.lc, b, *cur, st, launches));
+    const bool follow = active && h.lc_follow && L.lc->has_ring;
+    bool followed = false;
     SMG_TRY(enqueue_global_smooth(*L.a, b, cur, alt, L.d, L.sweeps, L.cs, st, launches,
-                                  first_done));
-    if (active) SMG_TRY(enqueue_local_correct(*L.lc, b, *cur, st, launches));
+                                  first_done, follow ? L.lc : nullptr, &followed));
+    if (active && !followed) SMG_TRY(enqueue_local_correct(*L.lc, b, *cur, st, launches));
     return SMG_OK;
   }
   const Correction& lc = *L.lc;
@@ -636,11 +663,32 @@ static int enqueue_vcycle(Hierarchy& h, const double* b0, double* u0, cudaStream
   }
   for (int l = nl - 2; l >= 0; --l) {
     HLevel& L = h.lv[l];
+    const bool follow = L.lc && L.lc->n_regions > 0 && L.lc->has_ring && L.has_ringP &&
+                        h.lc_follow && !h.lc_overlap;
     EpiArgs ea;
     ea.out = cur[l];
+    if (follow) {
+      // prolong-add out of place, skipping the patch dofs; the post-smoother's
+      // first correction recomputes it on its rings and runs concurrently
+      ea.u_in = cur[l];
+      ea.out = alt[l];
+      ea.skip_rows = L.lc->bmask;
+    }
     SMG_CUDA(launch_csr_stream(L.p->a, cur[l + 1], Epi::kAddTo, ea, st));
     ++*launches;
-    SMG_TRY(enqueue_smooth(h, L, bl[l], &cur[l], &alt[l], st, launches));
+    if (follow) {
+      FollowArgs fa;
+      fa.epi = (int)Epi::kAddTo;
+      fa.ring = L.ringP;
+      fa.x = cur[l + 1];
+      fa.u_in = cur[l];
+      fa.b = bl[l];
+      fa.out = alt[l];
+      SMG_CUDA(launch_patch_follow(*L.lc, fa, st));
+      ++*launches;
+      std::swap(cur[l], alt[l]);
+    }
+    SMG_TRY(enqueue_smooth(h, L, bl[l], &cur[l], &alt[l], st, launches, false, follow));
   }
   if (cur[0] != u0) {
     SMG_CUDA(cudaMemcpyAsync(u0, cur[0], sizeof(double) * (size_t)h.lv[0].n,
@@ -1399,6 +1447,94 @@ int smg_patch_factor(const smg_operator* a, int64_t n_regions, const int64_t* ro
   return SMG_OK;
 }
 
+// Gather the rows `rows` (device, m entries) of `a` into a compact CSR copy.
+static int gather_rows(std::vector<void*>& allocs, int64_t& bytes, const DevCsr& a,
+                       const int32_t* rows, int64_t m, RingRows* out)
+{
+  std::vector<void*> tmp;
+  int64_t tmp_bytes = 0;
+  int64_t* dlen = nullptr;
+  std::vector<int64_t> rp((size_t)m + 1, 0);
+  int rc = dev_alloc(tmp, tmp_bytes, (size_t)std::max<int64_t>(m, 1), &dlen);
+  if (rc == SMG_OK) rc = check_cuda(launch_patch_row_len(a, rows, m, dlen), "ring row lengths");
+  if (rc == SMG_OK)
+    rc = check_cuda(cudaMemcpy(rp.data() + 1, dlen, sizeof(int64_t) * (size_t)m,
+                               cudaMemcpyDeviceToHost), "ring row lengths D2H");
+  free_all(tmp);
+  SMG_TRY(rc);
+  for (int64_t k = 0; k < m; ++k) rp[(size_t)k + 1] += rp[(size_t)k];
+  int64_t* drp = nullptr;
+  int32_t* dcol = nullptr;
+  double* dval = nullptr;
+  SMG_TRY(dev_upload(allocs, bytes, rp.data(), rp.size(), &drp));
+  SMG_TRY(dev_alloc(allocs, bytes, (size_t)rp[(size_t)m] + 1, &dcol));
+  SMG_TRY(dev_alloc(allocs, bytes, (size_t)rp[(size_t)m] + 1, &dval));
+  SMG_TRY(check_cuda(launch_patch_row_gather(a, rows, m, drp, dcol, dval), "ring row gather"));
+  SMG_CUDA(cudaDeviceSynchronize());
+  out->rptr = drp;
+  out->rcol = dcol;
+  out->rval = dval;
+  return SMG_OK;
+}
+
+// Rings for follow-mode corrections (a correction overlapped with the kernel
+// producing the u it corrects): region d's ring is the
+// sorted set of columns of its rows (B_d included), plcol maps every gathered
+// patch-row entry to the ring position of its column, bpos every patch dof to
+// its own ring position.
+static int build_ring(const Operator& o, const std::vector<int32_t>& pptr,
+                      const std::vector<int32_t>& dof32, const std::vector<int64_t>& prow,
+                      const std::vector<int32_t>& hcol, Correction& c)
+{
+  // opt-in (SMG_LC_FOLLOW=1 when the correction is created): measured slower
+  // on C1-C4, profiles/r01/ab_follow/ 
+  const char* env = getenv("SMG_LC_FOLLOW");
+  if (!(env && env[0] == '1') || !o.a.inv_diag || c.n_regions == 0) return SMG_OK;
+  const int64_t nr = c.n_regions;
+  std::vector<int32_t> rptr((size_t)nr + 1, 0), rows, plcol(hcol.size()), bpos(dof32.size());
+  int32_t rmax = 0;
+  for (int64_t r = 0; r < nr; ++r) {
+    const int32_t k0 = pptr[(size_t)r], k1 = pptr[(size_t)r + 1];
+    std::vector<int32_t> ring(dof32.begin() + k0, dof32.begin() + k1);
+    for (int64_t j = prow[(size_t)k0]; j < prow[(size_t)k1]; ++j) ring.push_back(hcol[(size_t)j]);
+    std::sort(ring.begin(), ring.end());
+    ring.erase(std::unique(ring.begin(), ring.end()), ring.end());
+    auto pos = [&](int32_t g) {
+      return (int32_t)(std::lower_bound(ring.begin(), ring.end(), g) - ring.begin());
+    };
+    for (int32_t k = k0; k < k1; ++k) {
+      bpos[(size_t)k] = pos(dof32[(size_t)k]);
+      for (int64_t j = prow[(size_t)k]; j < prow[(size_t)k + 1]; ++j)
+        plcol[(size_t)j] = pos(hcol[(size_t)j]);
+    }
+    rmax = std::max<int32_t>(rmax, (int32_t)ring.size());
+    rows.insert(rows.end(), ring.begin(), ring.end());
+    rptr[(size_t)r + 1] = (int32_t)rows.size();
+  }
+  c.ring_max = rmax;
+  c.ring_total = (int64_t)rows.size();
+  c.has_ring = true;
+  if (!patch_follow_fits(c)) {
+    c.has_ring = false;
+    return SMG_OK;
+  }
+  std::vector<uint8_t> mask((size_t)o.a.nrows, 0);
+  for (int32_t g : dof32) mask[(size_t)g] = 1;
+  int32_t *drp = nullptr, *drows = nullptr, *dpl = nullptr, *dbp = nullptr;
+  uint8_t* dmask = nullptr;
+  SMG_TRY(dev_upload(c.allocs, c.device_bytes, rptr.data(), rptr.size(), &drp));
+  SMG_TRY(dev_upload(c.allocs, c.device_bytes, rows.data(), rows.size(), &drows));
+  SMG_TRY(dev_upload(c.allocs, c.device_bytes, plcol.data(), plcol.size(), &dpl));
+  SMG_TRY(dev_upload(c.allocs, c.device_bytes, bpos.data(), bpos.size(), &dbp));
+  SMG_TRY(dev_upload(c.allocs, c.device_bytes, mask.data(), mask.size(), &dmask));
+  c.ring_ptr = drp;
+  c.ring_rows = drows;
+  c.plcol = dpl;
+  c.bpos = dbp;
+  c.bmask = dmask;
+  return gather_rows(c.allocs, c.device_bytes, o.a, drows, c.ring_total, &c.ringA);
+}
+
 int smg_correction_create(const smg_operator* a, int64_t n_regions, const int64_t* roff,
                           const int64_t* dofs, const int64_t* foff, const double* factors,
                           smg_correction** out)
@@ -1531,6 +1667,7 @@ int smg_correction_create(const smg_operator* a, int64_t n_regions, const int64_
     c.pcol = dpcol;
     c.pval = dpval;
     if (rc == SMG_OK) rc = build_halo(o, dof32, hcol, c);
+    if (rc == SMG_OK) rc = build_ring(o, pptr, dof32, prow, hcol, c);
     if (rc == SMG_OK) {
       c.pptr = dp;
       c.dofs = dd;
@@ -1698,6 +1835,14 @@ int smg_hierarchy_create(int n_levels, const smg_operator* const* a, const smg_o
       if (rc == SMG_OK) rc = dev_alloc(h.allocs, h.bytes, n, &L.r);
     }
   }
+  // P's rows on the correction rings (follow-mode prolong-add + correction)
+  for (int l = 0; l < n_levels - 1 && rc == SMG_OK; ++l) {
+    HLevel& L = h.lv[(size_t)l];
+    if (L.lc && L.lc->has_ring && L.lc->n_global == L.n) {
+      rc = gather_rows(h.allocs, h.bytes, L.p->a, L.lc->ring_rows, L.lc->ring_total, &L.ringP);
+      L.has_ringP = rc == SMG_OK;
+    }
+  }
   if (rc == SMG_OK) rc = upload_sym_tiles(h.allocs, h.bytes, n_coarse, coarse_inverse, &h.coarse);
   h.n_coarse = n_coarse;
   h.coarse_refine = coarse_refine;
@@ -1732,6 +1877,8 @@ int smg_hierarchy_set_option(smg_hierarchy* h, int option, int value)
     H.fuse_zero_guess = value != 0;
   else if (option == SMG_OPT_LC_OVERLAP)
     H.lc_overlap = value != 0;
+  else if (option == SMG_OPT_LC_FOLLOW)
+    H.lc_follow = value != 0;
   else
     return fail("unknown hierarchy option");
   for (auto& kv : H.graphs) cudaGraphExecDestroy(kv.second);

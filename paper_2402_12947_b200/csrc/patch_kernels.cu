@@ -117,7 +117,7 @@ constexpr int kProdCap = 2048;                 // residual products staged per p
 constexpr int kProdItems = kProdCap / kSolveThreads;
 constexpr int64_t kSmemBudget = 220 * 1024;    // dynamic smem per CTA (of 227 KB)
 
-enum PatchMode : int { kAddResidualSolve = 0, kSolveFromBuf = 1, kResidualOnly = 2 };
+enum PatchMode : int { kAddResidualSolve = 0, kSolveFromBuf = 1, kResidualOnly = 2, kFollow = 3 };
 constexpr int kFlagStream = 1;      // factors larger than shared memory stream through a ring
 constexpr int kFlagL2Prefetch = 2;  // ... after an L2 prefetch of the whole factor
 
@@ -372,6 +372,8 @@ __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_
   }
 }
 
+__host__ __device__ __forceinline__ int nmax_ring(const FollowArgs& fa) { return fa.ring_max; }
+
 template <int kMode>
 __global__ void __launch_bounds__(kSolveThreads)
 patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
@@ -379,10 +381,17 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
              const int32_t* __restrict__ dofs,
              const int64_t* __restrict__ foff, const double* __restrict__ lfac,
              const double* __restrict__ b, const double* u_res, double* rbuf, double* target,
-             int scatter_add, int nmax, int flags, const int32_t* __restrict__ order)
+             int scatter_add, int nmax, int flags, const int32_t* __restrict__ order,
+             const FollowArgs fa, const int32_t* __restrict__ ring_ptr,
+             const int32_t* __restrict__ ring_rows, const int32_t* __restrict__ plcol,
+             const int32_t* __restrict__ bpos)
 {
   const bool allow_stream = (flags & kFlagStream) != 0;
   PTRACE(0);
+  // follow mode: the next kernel may start its static prologue at once; its
+  // dependency wait still covers the producer, because this grid completes
+  // only after waiting for the producer (end of the kernel)
+  if (kMode == kFollow) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ __align__(16) unsigned char psm[];
   __shared__ double s_red[kSolveWarps][32];
   __shared__ uint64_t s_bar;
@@ -410,7 +419,7 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   const int32_t g_own = threadIdx.x < n ? dofs[k0 + threadIdx.x] : 0;
   double b_own = 0.0, t_own = 0.0;
   auto fetch_own = [&]() {
-    if (threadIdx.x < n) {
+    if (kMode != kFollow && threadIdx.x < n) {
       if (kMode != kSolveFromBuf) b_own = b[g_own];
       if (kMode != kResidualOnly && scatter_add) t_own = target[g_own];
     }
@@ -437,7 +446,125 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   // every thread may only wait on the barrier after thread 0 has initialised it
   __syncthreads();
 
-  if (kMode != kSolveFromBuf) {
+  if (kMode == kFollow) {
+    // ---- follow mode: this kernel was launched (programmatic dependent
+    //      launch) as soon as every CTA of the producer kernel had passed its
+    //      own dependency wait, so the producer's INPUTS are complete; its
+    //      output is not.  Recompute the producer on the region's ring (the
+    //      columns of the patch rows) from those inputs -- the same
+    //      separately rounded products, sequential sums and epilogue as the
+    //      SpMV kernels, so the same bits -- then form the patch residual from
+    //      the ring.  Vectors written by earlier kernels are read through L2
+    //      (ld.global.cg, coherent), never from a possibly stale L1 line.
+    //      The ring rows stream like the patch residual's rows: coalesced
+    //      (column, value) chunks, exact products with the gathered x staged
+    //      in shared memory, then every ring row summed sequentially in
+    //      column order; the next chunk's loads are in flight during the sums.
+    double* s_ring = reinterpret_cast<double*>(psm + L_.bytes);
+    const int32_t q0 = ring_ptr[p];
+    const int nr = ring_ptr[p + 1] - q0;
+    int32_t* s_roff = reinterpret_cast<int32_t*>(s_ring + ((nmax_ring(fa) + 1) & ~1));
+    const int64_t rbase = fa.ring.rptr[q0];
+    const int rtotal = (int)(fa.ring.rptr[q0 + nr] - rbase);
+    int32_t cc[kProdItems];
+    double vv[kProdItems];
+    auto load_ring = [&](int c0) {
+#pragma unroll
+      for (int it = 0; it < kProdItems; ++it) {
+        const int e = c0 + it * kSolveThreads + threadIdx.x;
+        cc[it] = 0;
+        vv[it] = 0.0;
+        if (e < rtotal && e < c0 + kProdCap) {
+          cc[it] = __ldg(fa.ring.rcol + rbase + e);
+          vv[it] = __ldg(fa.ring.rval + rbase + e);
+        }
+      }
+    };
+    load_ring(0);
+    for (int q = threadIdx.x; q <= nr; q += kSolveThreads) {
+      s_roff[q] = (int)(fa.ring.rptr[q0 + q] - rbase);
+      if (q < nr) s_ring[q] = 0.0;
+    }
+    __syncthreads();
+    for (int c0 = 0; c0 < rtotal; c0 += kProdCap) {
+      const int cnt = min(kProdCap, rtotal - c0);
+#pragma unroll
+      for (int it = 0; it < kProdItems; ++it) {
+        const int e = it * kSolveThreads + threadIdx.x;
+        if (e < cnt) s_prod[e] = __dmul_rn(vv[it], __ldcg(fa.x + cc[it]));
+      }
+      if (c0 + kProdCap < rtotal) load_ring(c0 + kProdCap);
+      __syncthreads();
+      for (int q = threadIdx.x; q < nr; q += kSolveThreads) {
+        const int a0 = max(s_roff[q], c0), a1 = min(s_roff[q + 1], c0 + cnt);
+        double sum = s_ring[q];
+        for (int e = a0; e < a1; ++e) sum = __dadd_rn(sum, s_prod[e - c0]);
+        s_ring[q] = sum;
+      }
+      __syncthreads();
+    }
+    for (int q = threadIdx.x; q < nr; q += kSolveThreads) {
+      const int32_t g = ring_rows[q0 + q];
+      const double sum = s_ring[q];
+      double v;
+      if (fa.epi == (int)Epi::kAddTo) {
+        v = __dadd_rn(__ldcg(fa.u_in + g), sum);
+      } else {
+        const double t = __dmul_rn(__ldg(fa.inv_diag + g), __dsub_rn(__ldcg(fa.b + g), sum));
+        const double uv = __ldcg(fa.u_in + g);
+        if (fa.epi == (int)Epi::kJacobi) {
+          v = __dadd_rn(uv, __ddiv_rn(t, fa.theta));
+        } else if (fa.epi == (int)Epi::kChebFirst) {
+          v = __dadd_rn(uv, __ddiv_rn(t, fa.theta));
+        } else {  // kChebNext
+          const double d = __dadd_rn(__dmul_rn(fa.c1, __ldcg(fa.d + g)), __dmul_rn(fa.c2, t));
+          v = __dadd_rn(uv, d);
+        }
+      }
+      s_ring[q] = v;
+    }
+    // patch residual from the ring values: the same chunked products / row sums
+    const int64_t base = prow[k0];
+    const int total = (int)(prow[k0 + n] - base);
+    for (int i = threadIdx.x; i <= n; i += kSolveThreads) {
+      s_off[i] = (int)(prow[k0 + i] - base);
+      if (i < n) s_x[i] = 0.0;
+    }
+    auto load_patch = [&](int c0) {
+#pragma unroll
+      for (int it = 0; it < kProdItems; ++it) {
+        const int e = c0 + it * kSolveThreads + threadIdx.x;
+        cc[it] = 0;
+        vv[it] = 0.0;
+        if (e < total && e < c0 + kProdCap) {
+          cc[it] = __ldg(plcol + base + e);
+          vv[it] = __ldg(pval + base + e);
+        }
+      }
+    };
+    load_patch(0);
+    __syncthreads();
+    for (int c0 = 0; c0 < total; c0 += kProdCap) {
+      const int cnt = min(kProdCap, total - c0);
+#pragma unroll
+      for (int it = 0; it < kProdItems; ++it) {
+        const int e = it * kSolveThreads + threadIdx.x;
+        if (e < cnt) s_prod[e] = __dmul_rn(vv[it], s_ring[cc[it]]);
+      }
+      if (c0 + kProdCap < total) load_patch(c0 + kProdCap);
+      __syncthreads();
+      for (int i = threadIdx.x; i < n; i += kSolveThreads) {
+        const int a0 = max(s_off[i], c0), a1 = min(s_off[i + 1], c0 + cnt);
+        double sum = s_x[i];
+        for (int e = a0; e < a1; ++e) sum = __dadd_rn(sum, s_prod[e - c0]);
+        s_x[i] = sum;
+      }
+      __syncthreads();
+    }
+    for (int i = threadIdx.x; i < n; i += kSolveThreads)
+      s_x[i] = __dsub_rn(__ldcg(fa.b + dofs[k0 + i]), s_x[i]);
+    PTRACE(2);
+  } else if (kMode != kSolveFromBuf) {
     // ---- residual rows from the region's gathered row copy (prow/pcol/pval,
     //      built at upload): coalesced streamed products, then ordered sums.
     //      The copy is static, so its first chunk is requested before the
@@ -568,13 +695,22 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   }  // generic (staged / global) path
   PTRACE(5);
 
-  for (int i = threadIdx.x; i < n; i += kSolveThreads) {
-    const bool own = i == (int)threadIdx.x;
-    const int32_t g = own ? g_own : dofs[k0 + i];
-    if (scatter_add)
-      target[g] = __dadd_rn(own ? t_own : target[g], s_x[i]);
-    else
-      target[g] = s_x[i];
+  if constexpr (kMode == kFollow) {
+    double* s_ring = reinterpret_cast<double*>(psm + L_.bytes);
+    for (int i = threadIdx.x; i < n; i += kSolveThreads)
+      fa.out[dofs[k0 + i]] = __dadd_rn(s_ring[bpos[k0 + i]], s_x[i]);   // u += S_c r
+    // completion of this grid must imply completion of the producer (the next
+    // kernel waits on this one only)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  } else {
+    for (int i = threadIdx.x; i < n; i += kSolveThreads) {
+      const bool own = i == (int)threadIdx.x;
+      const int32_t g = own ? g_own : dofs[k0 + i];
+      if (scatter_add)
+        target[g] = __dadd_rn(own ? t_own : target[g], s_x[i]);
+      else
+        target[g] = s_x[i];
+    }
   }
   PTRACE(6);
 }
@@ -670,7 +806,43 @@ static cudaError_t launch_patch(const Correction& c, size_t smem, const double* 
   const int flags = (allow_stream ? kFlagStream : 0) | (l2pf ? kFlagL2Prefetch : 0);
   return cudaLaunchKernelEx(&cfg, patch_kernel<kMode>, c.prow, c.pcol, c.pval, c.pptr, c.dofs,
                             c.foff, c.lfac, b, u_res, c.rbuf, tgt, add, c.max_dofs, flags,
-                            lpt ? c.order : (const int32_t*)nullptr);
+                            lpt ? c.order : (const int32_t*)nullptr, FollowArgs(),
+                            (const int32_t*)nullptr, (const int32_t*)nullptr,
+                            (const int32_t*)nullptr, (const int32_t*)nullptr);
+}
+
+static size_t follow_smem(const Correction& c)
+{
+  const PatchSmem L = patch_smem_layout(c.max_dofs, !nostream_env());
+  return (size_t)L.bytes + 8 * (size_t)((c.ring_max + 1) & ~1) + 4 * (size_t)(c.ring_max + 2);
+}
+
+bool patch_follow_fits(const Correction& c) { return follow_smem(c) <= 227 * 1024; }
+
+// follow mode: launched right after its producer kernel (programmatic
+// dependent launch), runs concurrently with it, waits for it at the end
+cudaError_t launch_patch_follow(const Correction& c, const FollowArgs& fa, cudaStream_t s)
+{
+  if (c.n_regions == 0) return cudaSuccess;
+  const int st = nostream_env() ? 0 : 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)c.n_regions);
+  cfg.blockDim = dim3(kSolveThreads);
+  cfg.dynamicSmemBytes = follow_smem(c);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  static const int lpt = patch_env("SMG_PATCH_LPT", 1);
+  FollowArgs f = fa;
+  f.ring_max = c.ring_max;
+  return cudaLaunchKernelEx(&cfg, patch_kernel<kFollow>, c.prow, c.pcol, c.pval, c.pptr, c.dofs,
+                            c.foff, c.lfac, fa.b, (const double*)nullptr, c.rbuf, fa.out, 1,
+                            c.max_dofs, st ? kFlagStream : 0,
+                            lpt ? c.order : (const int32_t*)nullptr, f, c.ring_ptr, c.ring_rows,
+                            c.plcol, c.bpos);
 }
 
 // residual-only pass (coupled regions): rbuf[k] = (b - A u)[dofs[k]]
@@ -707,18 +879,26 @@ cudaError_t launch_patch_solve(const Correction& c, const double* b, const doubl
   return launch_patch<kSolveFromBuf>(c, smem, b, u_res, tgt, add, st, s);
 }
 
+// The attribute is per kernel, shared by every correction: it only ever grows
+// (a smaller correction created later must not lower it under a larger one's
+// launch size).
 cudaError_t configure_patch_solve_smem(const Correction& c)
 {
+  static int cur[4] = {0, 0, 0, 0};
   const PatchSmem L = patch_smem_layout(c.max_dofs, !nostream_env());
   const int bytes = (int)(L.bytes + smem_pad());
-  cudaError_t e = cudaFuncSetAttribute(patch_kernel<kAddResidualSolve>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(patch_kernel<kSolveFromBuf>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(patch_kernel<kResidualOnly>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.l_off);
+  cudaError_t e = cudaSuccess;
+  auto grow = [&](int mode, auto fn, int need) {
+    if (e == cudaSuccess && need > cur[mode]) {
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, need);
+      if (e == cudaSuccess) cur[mode] = need;
+    }
+  };
+  grow(kAddResidualSolve, patch_kernel<kAddResidualSolve>, bytes);
+  grow(kSolveFromBuf, patch_kernel<kSolveFromBuf>, bytes);
+  grow(kResidualOnly, patch_kernel<kResidualOnly>, (int)L.l_off);
+  if (c.has_ring && patch_follow_fits(c))
+    grow(kFollow, patch_kernel<kFollow>, (int)follow_smem(c));
   return e;
 }
 

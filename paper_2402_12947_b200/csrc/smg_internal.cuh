@@ -79,6 +79,14 @@ struct Operator {
   std::vector<void*> allocs;
 };
 
+// rows of a producer operator (A for a sweep, P for the prolong-add) on every
+// region's ring, gathered at upload (rptr indexes the concatenated ring rows)
+struct RingRows {
+  const int64_t* rptr = nullptr;
+  const int32_t* rcol = nullptr;
+  const double* rval = nullptr;
+};
+
 struct Correction {
   int64_t n_global = 0;
   int32_t n_regions = 0;
@@ -100,6 +108,19 @@ struct Correction {
   DevCsr halo;
   const uint8_t* halo_mask = nullptr;
   bool coupled = true;             // some A[B_d, B_d'] != 0 (d != d')
+  // follow mode (correction overlapped with the kernel producing its u): the
+  // ring of region d is the sorted set of columns of its rows (B_d included);
+  // the correction kernel recomputes the producer's output there from the
+  // producer's inputs, while the producer skips the patch dofs (bmask)
+  bool has_ring = false;
+  int32_t ring_max = 0;
+  int64_t ring_total = 0;
+  const int32_t* ring_ptr = nullptr;   // n_regions + 1
+  const int32_t* ring_rows = nullptr;  // ring_total global rows
+  const int32_t* plcol = nullptr;      // per gathered patch-row entry: ring position of its column
+  const int32_t* bpos = nullptr;       // per patch dof: its own ring position
+  const uint8_t* bmask = nullptr;      // per row: 1 = patch dof
+  RingRows ringA;                      // A's rows on the rings
   const Operator* op = nullptr;
   int64_t device_bytes = 0;
   std::vector<void*> allocs;
@@ -156,6 +177,23 @@ struct EpiArgs {
   const double* inv_diag = nullptr;  // kRestrictFirst: coarse operator 1/diagonal
   double* b_out = nullptr;        // kRestrictFirst: restricted right-hand side
   const uint8_t* skip_rows = nullptr;  // interior pass: rows flagged here are not written
+  bool keep_d = true;   // false: the last Chebyshev step of a smooth (d is dead) leaves d alone
+};
+
+// follow-mode correction (patch_kernels.cu): producer epilogue `epi` (kJacobi,
+// kChebFirst, kChebNext or kAddTo) recomputed on the rings, then
+// out[B_d] = producer(B_d) + (L L^T)^{-1} (b - A producer)[B_d]
+struct FollowArgs {
+  int epi = 0;
+  RingRows ring;
+  const double* x = nullptr;      // the producer's SpMV input (u_in / coarse u)
+  const double* u_in = nullptr;   // sweeps: u_in; prolong-add: the fine u before the add
+  const double* b = nullptr;      // the level's right-hand side
+  const double* d = nullptr;      // kChebNext: direction before the step
+  const double* inv_diag = nullptr;
+  double theta = 1.0, c1 = 0.0, c2 = 0.0;
+  double* out = nullptr;          // the producer's output vector
+  int ring_max = 0;               // set by the launcher (shared-memory carve-up)
 };
 
 cudaError_t launch_csr_stream(const DevCsr& m, const double* x, Epi epi, const EpiArgs& ea,
@@ -169,6 +207,8 @@ cudaError_t launch_gather(const int32_t* idx, int64_t m, const double* src, doub
 cudaError_t launch_patch_solve(const Correction& c, const double* b, const double* u_res,
                                double* u_add, double* out_scatter, bool fused, cudaStream_t s);
 cudaError_t configure_patch_solve_smem(const Correction& c);
+cudaError_t launch_patch_follow(const Correction& c, const FollowArgs& fa, cudaStream_t s);
+bool patch_follow_fits(const Correction& c);
 cudaError_t launch_patch_row_len(const DevCsr& a, const int32_t* dofs, int64_t m, int64_t* len);
 cudaError_t launch_patch_row_gather(const DevCsr& a, const int32_t* dofs, int64_t m,
                                     const int64_t* prow, int32_t* pcol, double* pval);

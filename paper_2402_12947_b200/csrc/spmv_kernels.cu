@@ -8,7 +8,8 @@
 //   Epi::kChebFirst     d = (D^-1 (b - A u))/theta; u' = u + d  smoothers.py:128-129
 //   Epi::kChebNext      z = D^-1 (b - A u); d = c1 d + c2 z; u' = u + d
 //                                                              smoothers.py:130-135
-//   Epi::kAddTo         u += P u_c                   mg.py:149 (prolong-add)
+//   Epi::kAddTo         u += P u_c                   mg.py:149 (prolong-add; out of
+//                       place into `out` when u_in is given)
 //   Epi::kRestrictFirst b_c = P^T r, then the coarse level's first sweep from
 //                       its zero initial guess (mg.py:142-143 + smoothers.py:128)
 //   (plain restriction P^T r runs kSpmv over the stored CSR(P^T), mg.py:142)
@@ -97,11 +98,11 @@ __device__ __forceinline__ void epilogue(const EpiArgs& ea, int32_t row, double 
       ea.out[row] = __dadd_rn(uv, __ddiv_rn(t, ea.theta));
     } else if constexpr (E == Epi::kChebFirst) {
       const double d = __ddiv_rn(t, ea.theta);
-      ea.d[row] = d;
+      if (ea.keep_d) ea.d[row] = d;
       ea.out[row] = __dadd_rn(uv, d);
     } else {  // kChebNext
       const double d = __dadd_rn(__dmul_rn(ea.c1, dv), __dmul_rn(ea.c2, t));
-      ea.d[row] = d;
+      if (ea.keep_d) ea.d[row] = d;
       ea.out[row] = __dadd_rn(uv, d);
     }
   }
@@ -205,7 +206,7 @@ csr_tile_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, 
     if constexpr (T::kB) bv = ea.b[grow];
     if constexpr (T::kU) uv = ea.u_in[grow];
     if constexpr (T::kD) dv = ea.d[grow];
-    if constexpr (T::kOut) ov = ea.out[grow];
+    if constexpr (T::kOut) ov = (ea.u_in ? ea.u_in : ea.out)[grow];  // prolong-add in or out of place
     if constexpr (T::kDiag) inv = m.inv_diag[grow];
     if constexpr (T::kDiagVec) inv = ea.inv_diag[grow];
   }
@@ -292,7 +293,7 @@ sell_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, int 
     if constexpr (T::kB) bv = ea.b[grow];
     if constexpr (T::kU) uv = ea.u_in[grow];
     if constexpr (T::kD) dv = ea.d[grow];
-    if constexpr (T::kOut) ov = ea.out[grow];
+    if constexpr (T::kOut) ov = (ea.u_in ? ea.u_in : ea.out)[grow];  // prolong-add in or out of place
     if constexpr (T::kDiag) inv = m.inv_diag[grow];
     if constexpr (T::kDiagVec) inv = ea.inv_diag[grow];
   }

@@ -190,6 +190,70 @@ def test_lc_overlap_is_bitwise(P, fx, graphs):
         assert launches[0] > launches[1]
 
 
+@pytest.mark.parametrize("graphs", [True, False])
+def test_lc_follow_is_bitwise(P, fx, graphs, monkeypatch):
+    """Corrections overlapped with the kernel producing their u (last smoother
+    step, prolong-add; SMG_OPT_LC_FOLLOW) give the sequential V-cycle bit for
+    bit, over repeated cycles, and stay within 1e-12 of the oracle."""
+    import torch
+    from oracle import oracle as O
+    from paper_2402_12947_b200.mg import DeviceHierarchy
+    name, z, h = fx
+    from paper_2402_12947_b200 import device as D
+    monkeypatch.setenv("SMG_LC_FOLLOW", "1")   # build the rings (opt-in) ...
+    monkeypatch.setattr(D, "_corr_cache", {})  # ... on freshly created corrections
+    b = torch.from_numpy(z["g/b"]).cuda()
+    res, launches = [], []
+    for follow in (1, 0):
+        dh = DeviceHierarchy(h.levels, h.coarse_factor, use_graphs=graphs)
+        dh.set_option(3, follow)
+        u = torch.from_numpy(z["g/u_rand"]).cuda()
+        for _ in range(3):
+            dh.vcycle(b, u)
+        res.append(u.cpu().numpy())
+        launches.append(dh.launches_per_vcycle())
+    assert np.array_equal(res[0], res[1])
+    assert launches[0] == launches[1]
+    ref = z["g/u_rand"].copy()
+    for _ in range(3):
+        ref = O.vcycle(h, z["g/b"], ref)
+    assert rel(res[0], ref) <= TOL_DENSE
+
+
+def test_lc_follow_coupled_regions(P, monkeypatch):
+    """Two regions coupled through A whose rings overlap: each
+    follow-mode correction still sees the pre-correction u (bitwise equal to
+    the sequential path)."""
+    import torch
+    from tests.golden import fixtures
+    from paper_2402_12947_b200.mg import DeviceHierarchy
+    from paper_2402_12947_b200 import smoothers as S
+    from paper_2402_12947_b200 import device as D
+    monkeypatch.setenv("SMG_LC_FOLLOW", "1")   # build the rings (opt-in) ...
+    monkeypatch.setattr(D, "_corr_cache", {})  # ... on freshly created corrections
+    z, h = fixtures.load("c1s")
+    lv0 = h.levels[0]
+    n = lv0.a.nrows
+    # adjacent dof sets: rows 40..47 and their first unclaimed neighbours
+    rp, ci = lv0.a.row_offsets, lv0.a.col_indices
+    b1 = list(range(n // 2, n // 2 + 6))
+    nb = sorted({int(c) for r in b1 for c in ci[rp[r]:rp[r + 1]]} - set(b1))[:6]
+    corr = S.build_local_correction(lv0.a, [np.array(b1), np.array(nb)])
+    levels = list(h.levels)
+    import dataclasses
+    levels[0] = dataclasses.replace(lv0, local_correction=corr)
+    b = torch.from_numpy(z["g/b"]).cuda()
+    res = []
+    for follow in (1, 0):
+        dh = DeviceHierarchy(levels, h.coarse_factor)
+        dh.set_option(3, follow)
+        u = torch.from_numpy(z["g/u_rand"]).cuda()
+        for _ in range(2):
+            dh.vcycle(b, u)
+        res.append(u.cpu().numpy())
+    assert np.array_equal(res[0], res[1])
+
+
 def test_pipelined_host_vcycles_match_single_calls(P, fx):
     """smg_vcycle_host_many (copies overlapping V-cycles, two staging slots)
     gives every pair exactly the single-call result."""
