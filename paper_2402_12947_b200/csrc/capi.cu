@@ -1585,6 +1585,16 @@ int smg_correction_create(const smg_operator* a, int64_t n_regions, const int64_
     for (int64_t i = 0; i < nd; ++i)
       for (int64_t j = 0; j <= i; ++j) *dst++ = f[i * nd + j];
     double* dinv = base + ((nd * (nd + 1) / 2 + 1) & ~int64_t(1));
+    if (patch_small(nd)) {   // the whole L^{-1}, row stride kLinvLd
+      for (int64_t j = 0; j < nd; ++j) {
+        for (int64_t i = j; i < nd; ++i) {
+          double sacc = (i == j) ? 1.0 : 0.0;
+          for (int64_t k = j; k < i; ++k) sacc -= f[i * nd + k] * dinv[k * kLinvLd + j];
+          dinv[i * kLinvLd + j] = sacc / f[i * nd + i];
+        }
+      }
+      continue;
+    }
     for (int64_t p0 = 0; p0 < nd; p0 += kPanel) {
       const int64_t pn = std::min<int64_t>(kPanel, nd - p0);
       double* D = dinv + (p0 / kPanel) * kDinvBlock;

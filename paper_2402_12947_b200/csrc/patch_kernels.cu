@@ -113,6 +113,42 @@ __device__ __forceinline__ void panel_gemv(const double* D, double* x, int pn, b
   __syncthreads();
 }
 
+// x[0:n] <- M x (or M^T x) for the whole inverse M = L^{-1} of a 33..64-dof
+// region (row stride kLinvLd, zero above the diagonal): warp w sums columns
+// [8w, 8w+8) for rows lane and lane+32, one thread per row adds the eight
+// partials (red: 8 x 64 doubles).  Called with x ready; returns after a barrier.
+__device__ __forceinline__ void gemv64(const double* M, double* x, int n, bool transposed,
+                                       double* red)
+{
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int j = warp * 8 + q;
+    if (j < n) {
+      const double xj = x[j];
+      if (transposed) {
+        a0 += M[j * kLinvLd + lane] * xj;
+        a1 += M[j * kLinvLd + lane + 32] * xj;
+      } else {
+        a0 += M[lane * kLinvLd + j] * xj;
+        a1 += M[(lane + 32) * kLinvLd + j] * xj;
+      }
+    }
+  }
+  red[warp * 64 + lane] = a0;
+  red[warp * 64 + lane + 32] = a1;
+  __syncthreads();
+  if (threadIdx.x < n) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w * 64 + threadIdx.x];
+    x[threadIdx.x] = t;
+  }
+  __syncthreads();
+}
+
 constexpr int kProdCap = 2048;                 // residual products staged per pass
 constexpr int kProdItems = kProdCap / kSolveThreads;
 constexpr int64_t kSmemBudget = 220 * 1024;    // dynamic smem per CTA (of 227 KB)
@@ -175,7 +211,7 @@ __host__ __device__ inline PatchSmem patch_smem_layout(int nmax, bool allow_stre
   int64_t cap = (kSmemBudget - p.l_off) / 8;
   if (cap < 0) cap = 0;
   cap &= ~int64_t(1);
-  const int64_t need = patch_slot_doubles(nmax);
+  const int64_t need = patch_slot_max(nmax);
   p.stage = 0;
   if (need <= cap || !allow_stream) {  // every region's slot (factor + inverted blocks) fits: stage it whole
     p.tri_cap = need;
@@ -633,7 +669,13 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   const double* L = staged ? s_L : Lg;
   const double* Dinv = L + patch_tri_even(n);   // inverted diagonal blocks, row stride 33
 
-  if (!staged && L_.stage > 0) {
+  if (patch_small(n)) {
+    // 33..64 dofs: x = L^{-T} (L^{-1} r), two GEMVs with the stored inverse
+    // (rows of M beyond n are never read: x[j >= n] does not enter, and the
+    // rows >= n of the padded block are not stored to)
+    gemv64(L + patch_tri_even(n), s_x, n, false, s_prod);
+    gemv64(L + patch_tri_even(n), s_x, n, true, s_prod);
+  } else if (!staged && L_.stage > 0) {
     stream_solve(Lg, s_L, L_.stage, n, s_x, s_prod, s_ring_bar, s_dinv_bar, s_red);
   } else {
 
