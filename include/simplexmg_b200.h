@@ -77,10 +77,13 @@ SMG_API int smg_operator_info(const smg_operator *op, int64_t *nrows, int64_t *n
  *   SMG_LAYOUT_TILES        CSR tiles with an offset table (csr_tile_kernel)
  *   SMG_LAYOUT_TILES_FIXED  fixed-capacity CSR tiles (csr_tile_kernel)
  *   SMG_LAYOUT_SELL         SELL-32-sigma256 (sell_kernel); *unroll = loop depth
+ *   SMG_LAYOUT_SELL4        SELL-8x4, 4 lanes per row, sigma 64 (sell4_kernel);
+ *                           *unroll = batches in flight (2 or 4)
  * For tiles *unroll is the chunks per tile (1, or 4 for long-row operators). */
 #define SMG_LAYOUT_TILES 0
 #define SMG_LAYOUT_TILES_FIXED 1
 #define SMG_LAYOUT_SELL 2
+#define SMG_LAYOUT_SELL4 3
 SMG_API int smg_operator_layout(const smg_operator *op, int *layout, int *unroll);
 /* Force a layout (and SELL loop depth 4/8/16; 0 = by the rule) for the
  * operator and its stored transpose -- for tests and A/B runs; results are

@@ -211,6 +211,78 @@ static int build_devcsr(std::vector<void*>& allocs, int64_t& bytes, int64_t nrow
   if (forced_layout >= 0) use_sell = forced_layout == SMG_LAYOUT_SELL && nrows > 0;
   d.sell_unroll = short_rows ? 4 : sell_long_unroll;
   if (forced_unroll > 0) d.sell_unroll = forced_unroll >= 16 ? 16 : (forced_unroll >= 8 ? 8 : 4);
+  // SELL-8x4 (SMG_SELL4: unset/0 = only when forced, 1 = every long-row
+  // operator the rule above leaves to the tiles).  Measured slower than the
+  // tiles on C1-C3 and even on C4 (profiles/r01/ab_sell4/): 64-row windows
+  // with 4 batches in flight fit 4 CTAs per SM, so C2 level 2 needs 1.7 waves,
+  // and the 2-batch build (8 CTAs per SM) spills and keeps too few loads in flight
+  static const int sell4_mode = env_int("SMG_SELL4", 0);
+  static const int sell4_min_row = env_int("SMG_SELL4_MIN_ROW", 20);
+  static const int sell4_unroll = env_int("SMG_SELL4_UNROLL", 2);
+  bool use_sell4 = nrows > 0 && !use_sell && sell4_mode >= 1 &&
+                   nnz >= (int64_t)sell4_min_row * nrows;
+  if (forced_layout >= 0) use_sell4 = forced_layout == SMG_LAYOUT_SELL4 && nrows > 0;
+  if (use_sell4) {
+    const int64_t nw = (nrows + kSell4Window - 1) / kSell4Window;
+    std::vector<int16_t> perm((size_t)(nw * kSell4Window), -1);
+    std::vector<int64_t> sptr((size_t)(nw * kSellSlices + 1), 0);
+    std::vector<int32_t> idx(kSell4Window);
+    for (int64_t w = 0; w < nw; ++w) {
+      const int64_t r0 = w * kSell4Window;
+      const int cntw = (int)std::min<int64_t>(kSell4Window, nrows - r0);
+      for (int i = 0; i < cntw; ++i) idx[(size_t)i] = i;
+      std::stable_sort(idx.begin(), idx.begin() + cntw, [&](int a, int b) {
+        return rowptr[r0 + a + 1] - rowptr[r0 + a] > rowptr[r0 + b + 1] - rowptr[r0 + b];
+      });
+      for (int sl = 0; sl < cntw; ++sl) perm[(size_t)(r0 + sl)] = (int16_t)idx[(size_t)sl];
+      for (int k = 0; k < kSellSlices; ++k) {
+        int64_t width = 0;   // batches of 4 entries
+        for (int l = 0; l < 8; ++l) {
+          const int sl = k * 8 + l;
+          if (sl < cntw) {
+            const int64_t r = r0 + idx[(size_t)sl];
+            width = std::max<int64_t>(width, (rowptr[r + 1] - rowptr[r] + 3) / 4);
+          }
+        }
+        sptr[(size_t)(w * kSellSlices + k + 1)] = sptr[(size_t)(w * kSellSlices + k)] + 32 * width;
+      }
+    }
+    const int64_t total = sptr.back();
+    std::vector<int32_t> scol((size_t)total + 4, -1);
+    std::vector<double> sval((size_t)total + 2, 0.0);
+    for (int64_t w = 0; w < nw; ++w) {
+      const int64_t r0 = w * kSell4Window;
+      for (int sl = 0; sl < kSell4Window; ++sl) {
+        const int16_t pr = perm[(size_t)(r0 + sl)];
+        if (pr < 0) continue;
+        const int64_t r = r0 + pr;
+        const int64_t base = sptr[(size_t)(w * kSellSlices + sl / 8)] + 4 * (sl % 8);
+        for (int64_t j = rowptr[r]; j < rowptr[r + 1]; ++j) {
+          const int64_t e = j - rowptr[r];
+          const int64_t at = base + (e / 4) * 32 + (e % 4);
+          scol[(size_t)at] = col32[(size_t)j];
+          sval[(size_t)at] = val[j];
+        }
+      }
+    }
+    int64_t* dsp = nullptr;
+    int16_t* dperm = nullptr;
+    int32_t* dsc = nullptr;
+    double* dsv = nullptr;
+    SMG_TRY(dev_upload(allocs, bytes, sptr.data(), sptr.size(), &dsp));
+    SMG_TRY(dev_upload(allocs, bytes, perm.data(), perm.size(), &dperm));
+    SMG_TRY(dev_upload(allocs, bytes, scol.data(), scol.size(), &dsc));
+    SMG_TRY(dev_upload(allocs, bytes, sval.data(), sval.size(), &dsv));
+    d.sell = true;
+    d.sell_lanes = 4;
+    d.sell_unroll = forced_unroll > 0 ? (forced_unroll >= 4 ? 4 : 2) : (sell4_unroll >= 4 ? 4 : 2);
+    fixed = false;
+    d.sell_nwin = (int32_t)nw;
+    d.sell_ptr = dsp;
+    d.sell_perm = dperm;
+    d.sell_col = dsc;
+    d.sell_val = dsv;
+  }
   if (use_sell) {
     // SELL-32-sigma256: per window of 256 rows, slots sorted by row length
     // (stable, descending), 8 slices of 32 slots, column-major within a slice
@@ -909,7 +981,7 @@ static int relayout(Operator& o, DevCsr& m, int layout, int unroll)
 int smg_operator_set_layout(smg_operator* op, int layout, int unroll)
 {
   if (!op) return fail("operator is NULL");
-  if (layout < SMG_LAYOUT_TILES || layout > SMG_LAYOUT_SELL) return fail("unknown layout");
+  if (layout < SMG_LAYOUT_TILES || layout > SMG_LAYOUT_SELL4) return fail("unknown layout");
   SMG_CUDA(cudaDeviceSynchronize());
   SMG_TRY(relayout(op->o, op->o.a, layout, unroll));
   if (op->o.has_t) SMG_TRY(relayout(op->o, op->o.t, layout, unroll));
@@ -920,7 +992,9 @@ int smg_operator_layout(const smg_operator* op, int* layout, int* unroll)
 {
   if (!op) return fail("operator is NULL");
   const DevCsr& m = op->o.a;
-  if (layout) *layout = m.sell ? SMG_LAYOUT_SELL : (m.fixed ? SMG_LAYOUT_TILES_FIXED : SMG_LAYOUT_TILES);
+  if (layout)
+    *layout = m.sell ? (m.sell_lanes == 4 ? SMG_LAYOUT_SELL4 : SMG_LAYOUT_SELL)
+                     : (m.fixed ? SMG_LAYOUT_TILES_FIXED : SMG_LAYOUT_TILES);
   if (unroll) *unroll = m.sell ? m.sell_unroll : (m.multichunk ? kMaxTileChunks : 1);
   return SMG_OK;
 }

@@ -56,6 +56,10 @@ struct DevCsr {
   // no row), 8 slices of 32 slots per window stored column-major (entry j of
   // the 32 slots contiguous; padding column -1), slice offsets in sell_ptr
   bool sell = false;
+  // lanes per row: 1 = SELL-32-sigma256 (sell_kernel); 4 = SELL-8x4 (sell4_kernel:
+  // windows of 64 rows, slices of 8 rows, 4 lanes per row -- entry 4b+t of
+  // slot r at slice offset 32b + 4r + t; sigma = 64)
+  int32_t sell_lanes = 1;
   int32_t sell_unroll = 4;             // loop unroll (4: 8 CTAs/SM; 8/16: long rows)
   int32_t sell_nwin = 0;
   const int64_t* sell_ptr = nullptr;   // nwin * 8 + 1
@@ -65,6 +69,7 @@ struct DevCsr {
 };
 constexpr int kSellWindow = 256;
 constexpr int kSellSlices = kSellWindow / 32;
+constexpr int kSell4Window = 64;    // SELL-8x4: 8 slices of 8 rows per window
 
 // Host-side owner of one operator's device arrays.
 struct Operator {

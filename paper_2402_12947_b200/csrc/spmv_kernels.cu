@@ -317,6 +317,108 @@ sell_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, int 
   if (write) epilogue<E>(ea, grow, sum, inv, bv, uv, dv, ov);
 }
 
+// SELL-8x4 (DevCsr::sell_lanes == 4): operators with long rows but too few
+// rows for one thread per row to fill the GPU (C2 levels 2-3, C3 level 1, C4
+// level 2).  One CTA per window of 64 rows, warp k = slice k of 8 rows, 4
+// lanes per row: the lanes of a row load entries 4b..4b+3 of batch b
+// (coalesced: a batch of the slice is 32 contiguous entries) and form their
+// products in parallel -- the serial load chain per row is a quarter of
+// sell_kernel's -- then the row's first lane adds the four products in column
+// order (shuffles; padding entries, column -1, are skipped via a ballot), so
+// every row is still one sequential sum in scipy's order, bit for bit.
+constexpr int kSell4Pre = 2;   // batches loaded before the dependency wait
+
+template <Epi E, bool kPf, int kUnroll>
+__global__ void __launch_bounds__(kThreads, kUnroll <= 2 ? 8 : 4)
+sell4_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, int pf_dist)
+{
+  using T = EpiTraits<E>;
+  const int w = blockIdx.x;
+  const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t sb = m.sell_ptr[(int64_t)w * kSellSlices + k];
+  const int64_t se = m.sell_ptr[(int64_t)w * kSellSlices + k + 1];
+  const int width = (int)((se - sb) >> 5);   // batches of 4 entries per row
+  const int g0 = lane & ~3;                  // first lane of this row's group
+  const int rl = m.sell_perm[(int64_t)w * kSell4Window + k * 8 + (lane >> 2)];
+  const int32_t* __restrict__ cp = m.sell_col + sb + lane;
+  const double* __restrict__ vp = m.sell_val + sb + lane;
+  auto ld = [&](int j, int32_t& c, double& v) {
+    c = -1;
+    v = 0.0;
+    if (j < width) {
+      if (m.streaming) {
+        c = __ldcs(cp + j * 32);
+        v = __ldcs(vp + j * 32);
+      } else {
+        c = __ldg(cp + j * 32);
+        v = __ldg(vp + j * 32);
+      }
+    }
+  };
+  int32_t c0[kSell4Pre];
+  double v0[kSell4Pre];
+#pragma unroll
+  for (int j = 0; j < kSell4Pre; ++j) ld(j, c0[j], v0[j]);
+  if constexpr (kPf) {
+    if (threadIdx.x == 0) {
+      const int wp = w + pf_dist;
+      if (wp < m.sell_nwin) {
+        const int64_t p0 = m.sell_ptr[(int64_t)wp * kSellSlices];
+        const int64_t p1 = m.sell_ptr[(int64_t)(wp + 1) * kSellSlices];
+        if (p1 > p0 && p1 - p0 <= (int64_t)kTileNnz * 16) {
+          const int64_t va = p0 & ~int64_t(1), vb = (p1 + 1) & ~int64_t(1);
+          const int64_t ca = p0 & ~int64_t(3), cb = (p1 + 3) & ~int64_t(3);
+          prefetch_l2(m.sell_val + va, (uint32_t)((vb - va) * 8), m.streaming);
+          prefetch_l2(m.sell_col + ca, (uint32_t)((cb - ca) * 4), m.streaming);
+        }
+      }
+    }
+  }
+  pdl_wait();
+  pdl_trigger();
+  const int32_t grow = w * kSell4Window + rl;
+  const bool owner = (lane & 3) == 0;
+  const bool write = owner && rl >= 0 && !(ea.skip_rows && ea.skip_rows[grow]);
+  double bv = 0.0, uv = 0.0, dv = 0.0, ov = 0.0, inv = 0.0;
+  if (write) {
+    if constexpr (T::kB) bv = ea.b[grow];
+    if constexpr (T::kU) uv = ea.u_in[grow];
+    if constexpr (T::kD) dv = ea.d[grow];
+    if constexpr (T::kOut) ov = (ea.u_in ? ea.u_in : ea.out)[grow];
+    if constexpr (T::kDiag) inv = m.inv_diag[grow];
+    if constexpr (T::kDiagVec) inv = ea.inv_diag[grow];
+  }
+  double sum = 0.0;
+  // the group's four products of one batch, added in entry (column) order
+  auto add4 = [&](double p, bool valid) {
+    const unsigned msk = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const double q = __shfl_sync(0xffffffffu, p, g0 + t);
+      if ((msk >> (g0 + t)) & 1u) sum = __dadd_rn(sum, q);
+    }
+  };
+  {
+    double p0[kSell4Pre];
+#pragma unroll
+    for (int j = 0; j < kSell4Pre; ++j)
+      p0[j] = c0[j] >= 0 ? __dmul_rn(v0[j], __ldg(x + c0[j])) : 0.0;
+#pragma unroll
+    for (int j = 0; j < kSell4Pre; ++j) add4(p0[j], c0[j] >= 0);
+  }
+  for (int j0 = kSell4Pre; j0 < width; j0 += kUnroll) {
+    int32_t c[kUnroll];
+    double v[kUnroll], p[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) ld(j0 + u, c[u], v[u]);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) p[u] = c[u] >= 0 ? __dmul_rn(v[u], __ldg(x + c[u])) : 0.0;
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) add4(p[u], c[u] >= 0);
+  }
+  if (write) epilogue<E>(ea, grow, sum, inv, bv, uv, dv, ov);
+}
+
 static int g_sm_count = 0;
 static int g_prefetch = -1;
 static int g_pdl = -1;
@@ -357,6 +459,18 @@ static cudaError_t launch_t(const DevCsr& m, const double* x, const EpiArgs& ea,
   }();
   const int dist = g_sm_count * kMinBlocks * waves;  // resident waves ahead (default one)
   const bool pf = env_flag(g_prefetch, "SMG_L2_PREFETCH", 1);
+  if (m.sell && m.sell_lanes == 4) {
+    cfg.gridDim = dim3((unsigned)m.sell_nwin);
+    cfg.blockDim = dim3(kThreads);
+    if (m.sell_unroll >= 4) {
+      const int sdist = g_sm_count * 4 * waves;
+      return pf ? cudaLaunchKernelEx(&cfg, sell4_kernel<E, true, 4>, m, x, ea, sdist)
+                : cudaLaunchKernelEx(&cfg, sell4_kernel<E, false, 4>, m, x, ea, sdist);
+    }
+    const int sdist = g_sm_count * 8 * waves;
+    return pf ? cudaLaunchKernelEx(&cfg, sell4_kernel<E, true, 2>, m, x, ea, sdist)
+              : cudaLaunchKernelEx(&cfg, sell4_kernel<E, false, 2>, m, x, ea, sdist);
+  }
   if (m.sell) {
     cfg.gridDim = dim3((unsigned)m.sell_nwin);
     cfg.blockDim = dim3(kSellWindow);
