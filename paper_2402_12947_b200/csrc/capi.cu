@@ -1626,14 +1626,15 @@ int smg_correction_create(const smg_operator* a, int64_t n_regions, const int64_
   std::vector<int32_t> dof32((size_t)m);
   std::vector<int64_t> poff((size_t)n_regions + 1, 0);
   int32_t max_dofs = 0;
+  for (int64_t r = 0; r < n_regions; ++r)
+    max_dofs = std::max<int32_t>(max_dofs, (int32_t)(roff[r + 1] - roff[r]));
   for (int64_t r = 0; r < n_regions; ++r) {
     const int64_t nd = roff[r + 1] - roff[r];
     if (nd <= 0) return fail("region " + std::to_string(r) + " is empty");
-    max_dofs = std::max<int32_t>(max_dofs, (int32_t)nd);
     pptr[(size_t)r] = (int32_t)roff[r];
     // slot = [packed L, even length][inverted 32x32 diagonal blocks]; 16-byte
     // aligned and even-length so one bulk copy stages the whole slot
-    poff[(size_t)r + 1] = poff[(size_t)r] + patch_slot_doubles(nd);
+    poff[(size_t)r + 1] = poff[(size_t)r] + patch_slot_doubles(nd, max_dofs);
     for (int64_t k = roff[r]; k < roff[r + 1]; ++k) {
       const int64_t g = dofs[k];
       if (g < 0 || g >= n)
@@ -1659,12 +1660,13 @@ int smg_correction_create(const smg_operator* a, int64_t n_regions, const int64_
     for (int64_t i = 0; i < nd; ++i)
       for (int64_t j = 0; j <= i; ++j) *dst++ = f[i * nd + j];
     double* dinv = base + ((nd * (nd + 1) / 2 + 1) & ~int64_t(1));
-    if (patch_small(nd)) {   // the whole L^{-1}, row stride kLinvLd
+    if (const int64_t B = patch_block(nd, max_dofs)) {   // the whole L^{-1}, row stride B + 1
+      const int64_t ld = B + 1;
       for (int64_t j = 0; j < nd; ++j) {
         for (int64_t i = j; i < nd; ++i) {
           double sacc = (i == j) ? 1.0 : 0.0;
-          for (int64_t k = j; k < i; ++k) sacc -= f[i * nd + k] * dinv[k * kLinvLd + j];
-          dinv[i * kLinvLd + j] = sacc / f[i * nd + i];
+          for (int64_t k = j; k < i; ++k) sacc -= f[i * nd + k] * dinv[k * ld + j];
+          dinv[i * ld + j] = sacc / f[i * nd + i];
         }
       }
       continue;

@@ -113,37 +113,40 @@ __device__ __forceinline__ void panel_gemv(const double* D, double* x, int pn, b
   __syncthreads();
 }
 
-// x[0:n] <- M x (or M^T x) for the whole inverse M = L^{-1} of a 33..64-dof
-// region (row stride kLinvLd, zero above the diagonal): warp w sums columns
-// [8w, 8w+8) for rows lane and lane+32, one thread per row adds the eight
-// partials (red: 8 x 64 doubles).  Called with x ready; returns after a barrier.
-__device__ __forceinline__ void gemv64(const double* M, double* x, int n, bool transposed,
-                                       double* red)
+// x[0:n] <- M x (or M^T x) for the whole inverse M = L^{-1} of a region
+// (B = 64 or 128 rows, row stride B + 1, zero above the diagonal): warp w sums
+// columns [w*B/8, (w+1)*B/8) for rows lane + 32q, then one thread per row adds
+// the eight partials (red: 8 x B doubles).  Rows and columns >= n are never
+// stored to / read from x.  Called with x ready; returns after a barrier.
+template <int B>
+__device__ __forceinline__ void gemv_inv(const double* M, double* x, int n, bool transposed,
+                                         double* red)
 {
+  constexpr int kLd = B + 1, kCols = B / kSolveWarps, kRows = B / 32;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  double a0 = 0.0, a1 = 0.0;
+  double acc[kRows];
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int j = warp * 8 + q;
+  for (int q = 0; q < kRows; ++q) acc[q] = 0.0;
+#pragma unroll
+  for (int c = 0; c < kCols; ++c) {
+    const int j = warp * kCols + c;
     if (j < n) {
       const double xj = x[j];
-      if (transposed) {
-        a0 += M[j * kLinvLd + lane] * xj;
-        a1 += M[j * kLinvLd + lane + 32] * xj;
-      } else {
-        a0 += M[lane * kLinvLd + j] * xj;
-        a1 += M[(lane + 32) * kLinvLd + j] * xj;
+#pragma unroll
+      for (int q = 0; q < kRows; ++q) {
+        const int i = lane + 32 * q;
+        acc[q] += (transposed ? M[j * kLd + i] : M[i * kLd + j]) * xj;
       }
     }
   }
-  red[warp * 64 + lane] = a0;
-  red[warp * 64 + lane + 32] = a1;
+#pragma unroll
+  for (int q = 0; q < kRows; ++q) red[warp * B + lane + 32 * q] = acc[q];
   __syncthreads();
   if (threadIdx.x < n) {
     double t = 0.0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) t += red[w * 64 + threadIdx.x];
+    for (int w = 0; w < kSolveWarps; ++w) t += red[w * B + threadIdx.x];
     x[threadIdx.x] = t;
   }
   __syncthreads();
@@ -446,7 +449,7 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   const int n = pptr[p + 1] - k0;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int64_t nslot = patch_slot_doubles(n);
+  const int64_t nslot = patch_slot_doubles(n, nmax);
   const bool staged = kMode != kResidualOnly && nslot <= L_.tri_cap;
   const double* __restrict__ Lg = lfac + foff[p];
   // this thread's own patch dof (rows < kSolveThreads): b and the scatter
@@ -669,12 +672,14 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   const double* L = staged ? s_L : Lg;
   const double* Dinv = L + patch_tri_even(n);   // inverted diagonal blocks, row stride 33
 
-  if (patch_small(n)) {
-    // 33..64 dofs: x = L^{-T} (L^{-1} r), two GEMVs with the stored inverse
-    // (rows of M beyond n are never read: x[j >= n] does not enter, and the
-    // rows >= n of the padded block are not stored to)
-    gemv64(L + patch_tri_even(n), s_x, n, false, s_prod);
-    gemv64(L + patch_tri_even(n), s_x, n, true, s_prod);
+  const int blk = patch_block(n, nmax);
+  if (blk == 2 * kPanel) {
+    // x = L^{-T} (L^{-1} r): two GEMVs with the stored inverse
+    gemv_inv<2 * kPanel>(L + patch_tri_even(n), s_x, n, false, s_prod);
+    gemv_inv<2 * kPanel>(L + patch_tri_even(n), s_x, n, true, s_prod);
+  } else if (blk == 4 * kPanel) {
+    gemv_inv<4 * kPanel>(L + patch_tri_even(n), s_x, n, false, s_prod);
+    gemv_inv<4 * kPanel>(L + patch_tri_even(n), s_x, n, true, s_prod);
   } else if (!staged && L_.stage > 0) {
     stream_solve(Lg, s_L, L_.stage, n, s_x, s_prod, s_ring_bar, s_dinv_bar, s_red);
   } else {

@@ -139,22 +139,28 @@ __host__ __device__ inline int64_t patch_tri_even(int64_t nd)
 {
   return (nd * (nd + 1) / 2 + 1) & ~int64_t(1);
 }
-// regions of 33..64 dofs carry the whole inverse of L (row stride kLinvLd,
-// zero above the diagonal) instead of two inverted diagonal blocks: each
-// triangular solve is then one 64-wide GEMV instead of three panel steps
-constexpr int kLinvLd = 65;
-constexpr int kLinvBlock = 2 * kPanel * kLinvLd;  // 4160 doubles (even)
-__host__ __device__ inline bool patch_small(int64_t nd) { return nd > kPanel && nd <= 2 * kPanel; }
-__host__ __device__ inline int64_t patch_slot_doubles(int64_t nd)
+// Regions of 33..64 dofs carry the whole inverse of L in a 64 x 65 block
+// (zero above the diagonal) instead of inverted 32 x 32 diagonal blocks, and so
+// do regions of 65..128 dofs (128 x 129 block) when no region of the
+// correction is larger (the slot then still fits shared memory): each
+// triangular solve is one GEMV instead of a chain of panel steps.
+__host__ __device__ inline int patch_block(int64_t nd, int64_t nmax)
 {
-  return patch_tri_even(nd) +
-         (patch_small(nd) ? (int64_t)kLinvBlock : ((nd + kPanel - 1) / kPanel) * kDinvBlock);
+  if (nd > kPanel && nd <= 2 * kPanel) return 2 * kPanel;
+  if (nd > 2 * kPanel && nd <= 4 * kPanel && nmax <= 4 * kPanel) return 4 * kPanel;
+  return 0;
+}
+__host__ __device__ inline int64_t patch_slot_doubles(int64_t nd, int64_t nmax)
+{
+  const int64_t B = patch_block(nd, nmax);
+  return patch_tri_even(nd) + (B ? B * (B + 1) : ((nd + kPanel - 1) / kPanel) * kDinvBlock);
 }
 // the largest slot of any region of at most nmax dofs (slots are not monotonic)
 __host__ __device__ inline int64_t patch_slot_max(int64_t nmax)
 {
-  const int64_t a = patch_slot_doubles(nmax);
-  const int64_t b = nmax > kPanel ? patch_slot_doubles(nmax < 2 * kPanel ? nmax : 2 * kPanel) : 0;
+  const int64_t a = patch_slot_doubles(nmax, nmax);
+  const int64_t b =
+      nmax > kPanel ? patch_slot_doubles(nmax < 2 * kPanel ? nmax : 2 * kPanel, nmax) : 0;
   return a > b ? a : b;
 }
 
