@@ -335,6 +335,12 @@ static int build_devcsr(std::vector<void*>& allocs, int64_t& bytes, int64_t nrow
     SMG_TRY(dev_upload(allocs, bytes, scol.data(), scol.size(), &dsc));
     SMG_TRY(dev_upload(allocs, bytes, sval.data(), sval.size(), &dsv));
     d.sell = true;
+    // software-pipelined loop for long rows up to SMG_SELL_PIPE_MAX_ROW (64)
+    // nonzeros per row: C2 level 1 (41) 28.2 -> 25.9 us, C4 level 0 (26.5)
+    // 547 -> 503 us; C4 level 1 (172) loses (363 -> 381 us), keeps the plain
+    // loop (profiles/r01/ab_pipe/)
+    static const int pipe_max_row = env_int("SMG_SELL_PIPE_MAX_ROW", 64);
+    d.sell_pipe = (d.sell_unroll == 8 && nnz < (int64_t)pipe_max_row * nrows) ? 6 : 0;
     fixed = false;   // the sweeps run on the SELL arrays: no padded tile copy
     d.sell_nwin = (int32_t)nw;
     d.sell_ptr = dsp;

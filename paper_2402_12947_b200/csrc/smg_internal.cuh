@@ -61,6 +61,7 @@ struct DevCsr {
   // slot r at slice offset 32b + 4r + t; sigma = 64)
   int32_t sell_lanes = 1;
   int32_t sell_unroll = 4;             // loop unroll (4: 8 CTAs/SM; 8/16: long rows)
+  int32_t sell_pipe = 0;               // 8-deep long rows: software-pipelined batch depth (0 = off)
   int32_t sell_nwin = 0;
   const int64_t* sell_ptr = nullptr;   // nwin * 8 + 1
   const int16_t* sell_perm = nullptr;  // nwin * 256
@@ -203,6 +204,8 @@ struct EpiArgs {
   double* b_out = nullptr;        // kRestrictFirst: restricted right-hand side
   const uint8_t* skip_rows = nullptr;  // interior pass: rows flagged here are not written
   bool keep_d = true;   // false: the last Chebyshev step of a smooth (d is dead) leaves d alone
+  bool stream_vec = false;  // set by the launcher: per-row vectors b, d, 1/a_ii read (and d
+                            // written) evict-first, so x keeps the L2 (SMG_EVICT_VEC)
 };
 
 // follow-mode correction (patch_kernels.cu): producer epilogue `epi` (kJacobi,

@@ -98,11 +98,15 @@ __device__ __forceinline__ void epilogue(const EpiArgs& ea, int32_t row, double 
       ea.out[row] = __dadd_rn(uv, __ddiv_rn(t, ea.theta));
     } else if constexpr (E == Epi::kChebFirst) {
       const double d = __ddiv_rn(t, ea.theta);
-      if (ea.keep_d) ea.d[row] = d;
+      if (ea.keep_d) {
+        if (ea.stream_vec) __stcs(ea.d + row, d); else ea.d[row] = d;
+      }
       ea.out[row] = __dadd_rn(uv, d);
     } else {  // kChebNext
       const double d = __dadd_rn(__dmul_rn(ea.c1, dv), __dmul_rn(ea.c2, t));
-      if (ea.keep_d) ea.d[row] = d;
+      if (ea.keep_d) {
+        if (ea.stream_vec) __stcs(ea.d + row, d); else ea.d[row] = d;
+      }
       ea.out[row] = __dadd_rn(uv, d);
     }
   }
@@ -239,8 +243,11 @@ csr_tile_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, 
 // barrier, few registers, 8 CTAs (64 warps) per SM.
 constexpr int kSellPre = 4;   // entries loaded before the dependency wait
 
-template <Epi E, bool kPf, int kUnroll>
-__global__ void __launch_bounds__(kSellWindow, kUnroll <= 4 ? 8 : (kUnroll <= 8 ? 4 : 2))
+// kPipe (long rows): the next kUnroll entries' columns and values are
+// requested before this batch's x gathers and sums, so the HBM stream never
+// waits on the gathers (software pipelining; SMG_SELL_PIPE)
+template <Epi E, bool kPf, int kUnroll, bool kPipe = false>
+__global__ void __launch_bounds__(kSellWindow, kPipe ? 4 : (kUnroll <= 4 ? 8 : (kUnroll <= 8 ? 4 : 2)))
 sell_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, int pf_dist)
 {
   using T = EpiTraits<E>;
@@ -290,17 +297,54 @@ sell_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, int 
   const bool write = has_row && !(ea.skip_rows && ea.skip_rows[grow]);
   double bv = 0.0, uv = 0.0, dv = 0.0, ov = 0.0, inv = 0.0;
   if (write) {
-    if constexpr (T::kB) bv = ea.b[grow];
+    if constexpr (T::kB) bv = ea.stream_vec ? __ldcs(ea.b + grow) : ea.b[grow];
     if constexpr (T::kU) uv = ea.u_in[grow];
-    if constexpr (T::kD) dv = ea.d[grow];
+    if constexpr (T::kD) dv = ea.stream_vec ? __ldcs(ea.d + grow) : ea.d[grow];
     if constexpr (T::kOut) ov = (ea.u_in ? ea.u_in : ea.out)[grow];  // prolong-add in or out of place
-    if constexpr (T::kDiag) inv = m.inv_diag[grow];
+    if constexpr (T::kDiag) inv = ea.stream_vec ? __ldcs(m.inv_diag + grow) : m.inv_diag[grow];
     if constexpr (T::kDiagVec) inv = ea.inv_diag[grow];
   }
   double sum = 0.0;
 #pragma unroll
   for (int j = 0; j < kSellPre; ++j)
     if (c0[j] >= 0) sum = __dadd_rn(sum, __dmul_rn(v0[j], __ldg(x + c0[j])));
+  if constexpr (kPipe) {
+    auto ldb = [&](int j0, int32_t* cc, double* vv) {
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int j = j0 + u;
+        cc[u] = -1;
+        vv[u] = 0.0;
+        if (j < width) {
+          if (m.streaming) {
+            cc[u] = __ldcs(cp + j * 32);
+            vv[u] = __ldcs(vp + j * 32);
+          } else {
+            cc[u] = __ldg(cp + j * 32);
+            vv[u] = __ldg(vp + j * 32);
+          }
+        }
+      }
+    };
+    int32_t c[kUnroll];
+    double v[kUnroll];
+    ldb(kSellPre, c, v);
+    for (int j0 = kSellPre; j0 < width; j0 += kUnroll) {
+      int32_t cn[kUnroll];
+      double vn[kUnroll];
+      ldb(j0 + kUnroll, cn, vn);
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u)
+        if (c[u] >= 0) sum = __dadd_rn(sum, __dmul_rn(v[u], __ldg(x + c[u])));
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        c[u] = cn[u];
+        v[u] = vn[u];
+      }
+    }
+    if (write) epilogue<E>(ea, grow, sum, inv, bv, uv, dv, ov);
+    return;
+  }
 #pragma unroll kUnroll
   for (int j = kSellPre; j < width; ++j) {
     int32_t c;
@@ -433,6 +477,10 @@ static bool env_flag(int& cache, const char* name, int dflt)
 }
 
 template <Epi E>
+static cudaError_t launch_t_sell(const DevCsr& m, const double* x, const EpiArgs& ea,
+                                 cudaLaunchConfig_t cfg, bool pf, int waves);
+
+template <Epi E>
 static cudaError_t launch_t(const DevCsr& m, const double* x, const EpiArgs& ea, cudaStream_t s)
 {
   if (m.ntiles == 0 && !(m.sell && m.sell_nwin > 0)) return cudaSuccess;
@@ -457,8 +505,26 @@ static cudaError_t launch_t(const DevCsr& m, const double* x, const EpiArgs& ea,
     const int w = v ? atoi(v) : 1;
     return w > 0 ? w : 1;
   }();
-  const int dist = g_sm_count * kMinBlocks * waves;  // resident waves ahead (default one)
   const bool pf = env_flag(g_prefetch, "SMG_L2_PREFETCH", 1);
+  // streamed SELL operators read their per-row vectors evict-first so x
+  // keeps the L2 (C2 fine step 31.5 -> 29.5 us; profiles/r01/ab_evictvec/)
+  static const int evict_vec = [] {
+    const char* v = getenv("SMG_EVICT_VEC");
+    return v ? atoi(v) : 1;
+  }();
+  if (m.sell && m.streaming && evict_vec) {
+    EpiArgs e2 = ea;
+    e2.stream_vec = true;
+    return launch_t_sell<E>(m, x, e2, cfg, pf, waves);
+  }
+  return launch_t_sell<E>(m, x, ea, cfg, pf, waves);
+}
+
+template <Epi E>
+static cudaError_t launch_t_sell(const DevCsr& m, const double* x, const EpiArgs& ea,
+                                 cudaLaunchConfig_t cfg, bool pf, int waves)
+{
+  const int dist = g_sm_count * kMinBlocks * waves;  // resident waves ahead (default one)
   if (m.sell && m.sell_lanes == 4) {
     cfg.gridDim = dim3((unsigned)m.sell_nwin);
     cfg.blockDim = dim3(kThreads);
@@ -481,6 +547,19 @@ static cudaError_t launch_t(const DevCsr& m, const double* x, const EpiArgs& ea,
     }
     if (m.sell_unroll >= 8) {
       const int sdist = g_sm_count * 4 * waves;
+      // SMG_SELL_PIPE: unset = per operator (DevCsr::sell_pipe, set at upload),
+      // 0 = never, 4 / 6 = that depth for every 8-deep operator
+      static const int pipe_env = [] {
+        const char* v = getenv("SMG_SELL_PIPE");
+        return v ? atoi(v) : -1;
+      }();
+      const int pipe = pipe_env >= 0 ? pipe_env : m.sell_pipe;
+      if (pipe >= 6)
+        return pf ? cudaLaunchKernelEx(&cfg, sell_kernel<E, true, 6, true>, m, x, ea, sdist)
+                  : cudaLaunchKernelEx(&cfg, sell_kernel<E, false, 6, true>, m, x, ea, sdist);
+      if (pipe > 0)
+        return pf ? cudaLaunchKernelEx(&cfg, sell_kernel<E, true, 4, true>, m, x, ea, sdist)
+                  : cudaLaunchKernelEx(&cfg, sell_kernel<E, false, 4, true>, m, x, ea, sdist);
       return pf ? cudaLaunchKernelEx(&cfg, sell_kernel<E, true, 8>, m, x, ea, sdist)
                 : cudaLaunchKernelEx(&cfg, sell_kernel<E, false, 8>, m, x, ea, sdist);
     }
