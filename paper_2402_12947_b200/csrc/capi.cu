@@ -729,14 +729,14 @@ static int enqueue_vcycle(Hierarchy& h, const double* b0, double* u0, cudaStream
   {
     HLevel& C = h.lv[nl - 1];
     SMG_CUDA(launch_sym_apply(h.coarse, bl[nl - 1], cur[nl - 1], false, st));
-    *launches += 2;
+    *launches += sym_apply_launches();
     if (h.coarse_refine) {
       EpiArgs ea;
       ea.b = bl[nl - 1];
       ea.out = h.coarse_r;
       SMG_CUDA(launch_csr_stream(C.a->a, cur[nl - 1], Epi::kResidual, ea, st));
       SMG_CUDA(launch_sym_apply(h.coarse, h.coarse_r, cur[nl - 1], true, st));
-      *launches += 3;
+      *launches += 1 + sym_apply_launches();
     }
   }
   for (int l = nl - 2; l >= 0; --l) {
@@ -1860,9 +1860,13 @@ static int upload_sym_tiles(std::vector<void*>& allocs, int64_t& bytes, int64_t 
   SMG_TRY(dev_upload(allocs, bytes, t.data(), t.size(), &dt));
   SMG_TRY(dev_upload(allocs, bytes, ti.data(), ti.size(), &dti));
   SMG_TRY(dev_alloc(allocs, bytes, (size_t)m.nb * m.nb * kSymTile, &dp));
+  unsigned int* dc = nullptr;
+  SMG_TRY(dev_alloc(allocs, bytes, (size_t)m.nb, &dc));
+  SMG_CUDA(cudaMemset(dc, 0, sizeof(unsigned int) * (size_t)m.nb));
   m.tiles = dt;
   m.tile_i = dti;
   m.partial = dp;
+  m.counter = dc;
   *out = m;
   return SMG_OK;
 }

@@ -15,6 +15,8 @@
 // finalisation in block order -> run-to-run deterministic results.
 #include "smg_internal.cuh"
 
+#include <cstdlib>
+
 namespace smg {
 
 __device__ __forceinline__ double warp_sum_d(double v)
@@ -28,19 +30,38 @@ __device__ __forceinline__ double warp_sum_d(double v)
 // Symmetric coarse operator applied from its lower triangle only (half the
 // bytes of the dense GEMV): A_L^{-1} is stored as 64 x 64 tiles (I, J), J <= I,
 // row-major inside a tile, zero-padded, tile (I, J) at index I(I+1)/2 + J.
-// Kernel 1, one CTA per tile: partial[I][J] = A_IJ x_J and, off the diagonal,
-// partial[J][I] = A_IJ^T x_I.  Kernel 2: y_i = sum_J partial[I][J][i] in
-// ascending J.  Every sum has a fixed order: run-to-run deterministic.
+// One kernel, one CTA per tile: partial[I][J] = A_IJ x_J and, off the
+// diagonal, partial[J][I] = A_IJ^T x_I.  Each block row I receives nb partials;
+// the CTA that delivers the last one (per-row counter) forms
+// y_i = sum_J partial[I][J][i] in ascending J and resets the counter -- a fixed
+// summation order whoever finalises, so the result is run-to-run
+// deterministic.  The tile (static data) is requested before the programmatic
+// dependency wait, x after it.
 constexpr int kSymThreads = 256;
 constexpr int kSymRowsPerThread = kSymTile * kSymTile / kSymThreads;   // 16
 
+__device__ __forceinline__ void sym_finish_row(int row, int nb, int64_t n,
+                                               const double* partial, double* y, bool add)
+{
+  const int tid = threadIdx.x;
+  if (tid >= kSymTile) return;
+  const int64_t i = (int64_t)row * kSymTile + tid;
+  if (i >= n) return;
+  const double* p = partial + (int64_t)row * nb * kSymTile + tid;
+  double s = 0.0;
+  for (int J = 0; J < nb; ++J) s += __ldcg(p + (int64_t)J * kSymTile);
+  y[i] = add ? y[i] + s : s;
+}
+
 __global__ void __launch_bounds__(kSymThreads)
 sym_tile_kernel(int nb, const int32_t* __restrict__ tile_i, const double* __restrict__ tiles,
-                const double* __restrict__ x, int64_t n, double* __restrict__ partial)
+                const double* __restrict__ x, int64_t n, double* __restrict__ partial,
+                unsigned int* __restrict__ counter, double* __restrict__ y, int add)
 {
   __shared__ double s_xi[kSymTile], s_xj[kSymTile];
   __shared__ double s_row[kSymTile][2];
   __shared__ double s_col[kSymThreads / kSymTile][kSymTile];
+  __shared__ int s_last[2];
   const int t = blockIdx.x;
   const int I = tile_i[t];
   const int J = t - I * (I + 1) / 2;
@@ -51,6 +72,8 @@ sym_tile_kernel(int nb, const int32_t* __restrict__ tile_i, const double* __rest
   double v[kSymRowsPerThread];
 #pragma unroll
   for (int i = 0; i < kSymRowsPerThread; ++i) v[i] = __ldcs(a + (g + 4 * i) * kSymTile + c);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (tid < kSymTile) {
     const int64_t gi = (int64_t)I * kSymTile + tid, gj = (int64_t)J * kSymTile + tid;
     s_xi[tid] = gi < n ? x[gi] : 0.0;
@@ -83,12 +106,39 @@ sym_tile_kernel(int nb, const int32_t* __restrict__ tile_i, const double* __rest
     for (int gg = 0; gg < kSymThreads / kSymTile; ++gg) q += s_col[gg][tid];
     partial[((int64_t)J * nb + I) * kSymTile + tid] = q;
   }
+  if (!counter) return;   // two-kernel mode: sym_reduce_kernel sums the rows
+  // deliver: the last contributor of a block row sums it (threadFenceReduction)
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    s_last[0] = atomicAdd(&counter[I], 1u) == (unsigned)(nb - 1);
+    s_last[1] = I != J && atomicAdd(&counter[J], 1u) == (unsigned)(nb - 1);
+  }
+  __syncthreads();
+  if (s_last[0]) {
+    __threadfence();
+    sym_finish_row(I, nb, n, partial, y, add != 0);
+    if (tid == 0) counter[I] = 0;
+  }
+  if (s_last[1]) {
+    __threadfence();
+    sym_finish_row(J, nb, n, partial, y, add != 0);
+    if (tid == 0) counter[J] = 0;
+  }
+}
+
+int sym_apply_launches()
+{
+  const char* v = getenv("SMG_COARSE_FUSED");
+  return (v && atoi(v)) ? 1 : 2;
 }
 
 template <bool kAdd>
 __global__ void sym_reduce_kernel(int nb, int64_t n, const double* __restrict__ partial,
                                   double* __restrict__ y)
 {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int64_t I = i / kSymTile, r = i % kSymTile;
@@ -105,15 +155,45 @@ cudaError_t launch_sym_apply(const SymTiles& m, const double* x, double* y, bool
                              cudaStream_t s)
 {
   if (m.n == 0) return cudaSuccess;
+  static const int fused = [] {
+    const char* v = getenv("SMG_COARSE_FUSED");
+    return v ? atoi(v) : 0;
+  }();
+  if (!fused) {
+    // two kernels, both programmatic dependents (counter == nullptr: the tile
+    // kernel only writes partials)
+    const int64_t ntiles = (int64_t)m.nb * (m.nb + 1) / 2;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)ntiles);
+    cfg.blockDim = dim3(kSymThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, sym_tile_kernel, m.nb, m.tile_i, m.tiles, x, m.n,
+                                       m.partial, (unsigned int*)nullptr, y, add ? 1 : 0);
+    if (e != cudaSuccess) return e;
+    cfg.gridDim = dim3((unsigned)((m.n + 255) / 256));
+    cfg.blockDim = dim3(256);
+    if (add) return cudaLaunchKernelEx(&cfg, sym_reduce_kernel<true>, m.nb, m.n,
+                                       (const double*)m.partial, y);
+    return cudaLaunchKernelEx(&cfg, sym_reduce_kernel<false>, m.nb, m.n,
+                              (const double*)m.partial, y);
+  }
   const int64_t ntiles = (int64_t)m.nb * (m.nb + 1) / 2;
-  sym_tile_kernel<<<(unsigned)ntiles, kSymThreads, 0, s>>>(m.nb, m.tile_i, m.tiles, x, m.n,
-                                                            m.partial);
-  const unsigned blocks = (unsigned)((m.n + 255) / 256);
-  if (add)
-    sym_reduce_kernel<true><<<blocks, 256, 0, s>>>(m.nb, m.n, m.partial, y);
-  else
-    sym_reduce_kernel<false><<<blocks, 256, 0, s>>>(m.nb, m.n, m.partial, y);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)ntiles);
+  cfg.blockDim = dim3(kSymThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, sym_tile_kernel, m.nb, m.tile_i, m.tiles, x, m.n, m.partial,
+                            m.counter, y, add ? 1 : 0);
 }
 
 // ---------------------------------------------------------------------------

@@ -250,9 +250,11 @@ struct SymTiles {
   const double* tiles = nullptr;     // nb(nb+1)/2 tiles of kSymTile^2 doubles
   const int32_t* tile_i = nullptr;   // block row of each tile
   double* partial = nullptr;         // nb * nb * kSymTile scratch
+  unsigned int* counter = nullptr;   // nb: partials delivered per block row (0 between calls)
 };
 cudaError_t launch_sym_apply(const SymTiles& m, const double* x, double* y, bool add,
                              cudaStream_t s);
+int sym_apply_launches();   // kernels one launch_sym_apply enqueues (1 fused, 2 default)
 
 // sparse matrix product C = X Y in scipy csr_matmat's order, bit-identical
 // (galerkin_kernels.cu; the Galerkin operator P^T (A P), sparse.py:147-154)
