@@ -50,7 +50,7 @@ __device__ __forceinline__ void sym_finish_row(int row, int nb, int64_t n,
   const double* p = partial + (int64_t)row * nb * kSymTile + tid;
   double s = 0.0;
   for (int J = 0; J < nb; ++J) s += __ldcg(p + (int64_t)J * kSymTile);
-  y[i] = add ? y[i] + s : s;
+  y[i] = (add & 1) ? y[i] + s : s;
 }
 
 __global__ void __launch_bounds__(kSymThreads)
@@ -71,7 +71,8 @@ sym_tile_kernel(int nb, const int32_t* __restrict__ tile_i, const double* __rest
   const double* __restrict__ a = tiles + (int64_t)t * kSymTile * kSymTile;
   double v[kSymRowsPerThread];
 #pragma unroll
-  for (int i = 0; i < kSymRowsPerThread; ++i) v[i] = __ldcs(a + (g + 4 * i) * kSymTile + c);
+  for (int i = 0; i < kSymRowsPerThread; ++i)
+    v[i] = add < 2 ? __ldcs(a + (g + 4 * i) * kSymTile + c) : __ldg(a + (g + 4 * i) * kSymTile + c);
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (tid < kSymTile) {
@@ -117,12 +118,12 @@ sym_tile_kernel(int nb, const int32_t* __restrict__ tile_i, const double* __rest
   __syncthreads();
   if (s_last[0]) {
     __threadfence();
-    sym_finish_row(I, nb, n, partial, y, add != 0);
+    sym_finish_row(I, nb, n, partial, y, (add & 1) != 0);
     if (tid == 0) counter[I] = 0;
   }
   if (s_last[1]) {
     __threadfence();
-    sym_finish_row(J, nb, n, partial, y, add != 0);
+    sym_finish_row(J, nb, n, partial, y, (add & 1) != 0);
     if (tid == 0) counter[J] = 0;
   }
 }
@@ -133,22 +134,32 @@ int sym_apply_launches()
   return (v && atoi(v)) ? 1 : 2;
 }
 
+// one CTA per 64-row block row: thread group q (of 4) sums the partials
+// J = q, q + 4, ... in ascending order, then the four group sums are added in
+// group order -- a fixed order, so run-to-run deterministic
 template <bool kAdd>
-__global__ void sym_reduce_kernel(int nb, int64_t n, const double* __restrict__ partial,
-                                  double* __restrict__ y)
+__global__ void __launch_bounds__(256) sym_reduce_kernel(int nb, int64_t n,
+                                                        const double* __restrict__ partial,
+                                                        double* __restrict__ y)
 {
+  __shared__ double s_part[4][kSymTile];
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int64_t I = i / kSymTile, r = i % kSymTile;
-  const double* p = partial + I * nb * kSymTile + r;
+  const int I = blockIdx.x;
+  const int r = threadIdx.x & (kSymTile - 1), q = threadIdx.x / kSymTile;
+  const double* p = partial + (int64_t)I * nb * kSymTile + r;
   double s = 0.0;
-  for (int J = 0; J < nb; ++J) s += p[(int64_t)J * kSymTile];
-  if (kAdd)
-    y[i] += s;
-  else
-    y[i] = s;
+  for (int J = q; J < nb; J += 4) s += p[(int64_t)J * kSymTile];
+  s_part[q][r] = s;
+  __syncthreads();
+  const int64_t i = (int64_t)I * kSymTile + threadIdx.x;
+  if (threadIdx.x < kSymTile && i < n) {
+    const double t = ((s_part[0][r] + s_part[1][r]) + s_part[2][r]) + s_part[3][r];
+    if (kAdd)
+      y[i] += t;
+    else
+      y[i] = t;
+  }
 }
 
 cudaError_t launch_sym_apply(const SymTiles& m, const double* x, double* y, bool add,
@@ -172,10 +183,17 @@ cudaError_t launch_sym_apply(const SymTiles& m, const double* x, double* y, bool
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    // SMG_COARSE_KEEP=1: tiles read with normal L2 priority (they may stay
+    // resident between V-cycles when small); default evict-first
+    static const int keep = [] {
+      const char* v = getenv("SMG_COARSE_KEEP");
+      return v ? atoi(v) : 0;
+    }();
+    const int mode = (add ? 1 : 0) | (keep ? 2 : 0);
     cudaError_t e = cudaLaunchKernelEx(&cfg, sym_tile_kernel, m.nb, m.tile_i, m.tiles, x, m.n,
-                                       m.partial, (unsigned int*)nullptr, y, add ? 1 : 0);
+                                       m.partial, (unsigned int*)nullptr, y, mode);
     if (e != cudaSuccess) return e;
-    cfg.gridDim = dim3((unsigned)((m.n + 255) / 256));
+    cfg.gridDim = dim3((unsigned)m.nb);
     cfg.blockDim = dim3(256);
     if (add) return cudaLaunchKernelEx(&cfg, sym_reduce_kernel<true>, m.nb, m.n,
                                        (const double*)m.partial, y);
