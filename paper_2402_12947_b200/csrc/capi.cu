@@ -211,16 +211,21 @@ static int build_devcsr(std::vector<void*>& allocs, int64_t& bytes, int64_t nrow
   if (forced_layout >= 0) use_sell = forced_layout == SMG_LAYOUT_SELL && nrows > 0;
   d.sell_unroll = short_rows ? 4 : sell_long_unroll;
   if (forced_unroll > 0) d.sell_unroll = forced_unroll >= 16 ? 16 : (forced_unroll >= 8 ? 8 : 4);
-  // SELL-8x4 (SMG_SELL4: unset/0 = only when forced, 1 = every long-row
+  // SELL-8x4 (SMG_SELL4: 0 = only when forced, 1 = every long-row
   // operator the rule above leaves to the tiles).  Measured slower than the
   // tiles on C1-C3 and even on C4 (profiles/r01/ab_sell4/): 64-row windows
   // with 4 batches in flight fit 4 CTAs per SM, so C2 level 2 needs 1.7 waves,
   // and the 2-batch build (8 CTAs per SM) spills and keeps too few loads in flight
+  // 2: only very long rows (>= SMG_SELL4_AUTO_ROW = 200 per row, C4 level 2),
+  // 4 batches in flight -- its sweep gets faster (158 -> 152 us) but the C4
+  // V-cycle does not (178.2 -> 176.5 /s; profiles/r01/ab_sell4/auto_*), so the
+  // default stays 0.
   static const int sell4_mode = env_int("SMG_SELL4", 0);
   static const int sell4_min_row = env_int("SMG_SELL4_MIN_ROW", 20);
-  static const int sell4_unroll = env_int("SMG_SELL4_UNROLL", 2);
+  static const int sell4_auto_row = env_int("SMG_SELL4_AUTO_ROW", 200);
+  static const int sell4_unroll = env_int("SMG_SELL4_UNROLL", sell4_mode == 2 ? 4 : 2);
   bool use_sell4 = nrows > 0 && !use_sell && sell4_mode >= 1 &&
-                   nnz >= (int64_t)sell4_min_row * nrows;
+                   nnz >= (int64_t)(sell4_mode == 2 ? sell4_auto_row : sell4_min_row) * nrows;
   if (forced_layout >= 0) use_sell4 = forced_layout == SMG_LAYOUT_SELL4 && nrows > 0;
   if (use_sell4) {
     const int64_t nw = (nrows + kSell4Window - 1) / kSell4Window;
