@@ -19,8 +19,9 @@ from .smoothers import (LocalCorrection, SmootherConfig, ZeroDiagonalError,
                         adjusted_lambda_max, apply_local_correction, build_local_correction,
                         chebyshev_smooth, combined_smooth, dofs_for_regions, jacobi_lambda_max,
                         sgs_sweep)
-from .mg import (DeviceHierarchy, Hierarchy, Level, Prolongation, as_preconditioner,
-                 build_hierarchy, solve_stationary, vcycle)
+from .mg import (DeviceHierarchy, Hierarchy, Level, ProblemSpec, Prolongation,
+                 as_preconditioner, build_hierarchy, solve_stationary, vcycle)
+from .transfer import PointLocationError, locate_point, prolong_add, restrict_residual
 
 __all__ = [
     "CsrMatrix", "DenseFactor", "EigenEstimateError", "IndefiniteOperatorError",
@@ -29,5 +30,6 @@ __all__ = [
     "adjusted_lambda_max", "apply_local_correction", "build_local_correction",
     "chebyshev_smooth", "combined_smooth", "dofs_for_regions", "jacobi_lambda_max", "sgs_sweep",
     "DeviceHierarchy", "Hierarchy", "Level", "Prolongation", "as_preconditioner",
-    "build_hierarchy", "solve_stationary", "vcycle",
+    "build_hierarchy", "solve_stationary", "vcycle", "ProblemSpec", "PointLocationError",
+    "locate_point", "prolong_add", "restrict_residual",
 ]

@@ -185,18 +185,29 @@ def build_meshes(wl: Workload) -> List[SimplexMesh]:
     return meshes
 
 
+def problem_spec(wl: Workload):
+    """Poisson, homogeneous Dirichlet on every box face (fem.py:230-262);
+    f = 1 for the source-one workloads (vectorised), else no source (the
+    random right-hand side is drawn directly)."""
+    from .mg import ProblemSpec
+    zero = lambda x: 0.0
+    source = (lambda x: np.ones(len(x))) if wl.rhs == "source-one" else None
+    return ProblemSpec("poisson", source=source,
+                       dirichlet=tuple((m, zero) for m in range(1, 2 * wl.dim + 1)),
+                       vectorized_source=True)
+
+
 def build(wl: Workload, use_local_correction: bool = True, coarse_refine: bool = False,
-          device_setup=None):
+          device_setup=None, device_assembly: bool = False):
     """Host hierarchy + (b, u0) for a workload.  Returns (hierarchy, b, u0).
     ``device_setup``: see mg.build_hierarchy (None = GPU setup when a device
-    exists; False = the host path, bit-identical to the reference's setup)."""
+    exists; False = the host path).  Either way the fine operator is the
+    reference's construction bit for bit unless ``device_assembly``."""
     from .mg import build_hierarchy
     meshes = build_meshes(wl)
-    source = (lambda x: np.ones(len(x))) if wl.rhs == "source-one" else None
-    smoother = wl.smoother
-    h = build_hierarchy(meshes, smoother, use_local_correction, 0.1, wl.degree, source=source,
-                        region_layers=wl.region_layers, coarse_refine=coarse_refine,
-                        device_setup=device_setup)
+    h = build_hierarchy(meshes, problem_spec(wl), wl.smoother, use_local_correction, 0.1,
+                        wl.degree, region_layers=wl.region_layers, coarse_refine=coarse_refine,
+                        device_setup=device_setup, device_assembly=device_assembly)
     n0 = h.fine.a.nrows
     if wl.rhs == "random":
         b = np.random.default_rng([wl.seed, 99]).standard_normal(n0)

@@ -576,9 +576,17 @@ struct Hierarchy {
   cudaStream_t copy_in = nullptr, copy_out = nullptr;
   cudaEvent_t pipe_ev[6] = {};
   DotScratch dots;
+  // concurrent vcycle calls on one shared hierarchy are safe:
+  // every entry point that touches the per-level scratch, the staging
+  // buffers, the dot scratch or the graph cache holds `mu`, and device work is
+  // ordered across callers' streams by `done_ev` (each call waits for the
+  // previous call's last kernel before it starts, then records its own).
+  std::recursive_mutex mu;
+  cudaEvent_t done_ev = nullptr;
 
   ~Hierarchy()
   {
+    if (done_ev) cudaEventDestroy(done_ev);
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     if (capture_stream) cudaStreamDestroy(capture_stream);
     if (side) cudaStreamDestroy(side);
@@ -779,6 +787,36 @@ static int enqueue_vcycle(Hierarchy& h, const double* b0, double* u0, cudaStream
   }
   return SMG_OK;
 }
+
+// Cross-stream ordering of the shared scratch (see Hierarchy::mu): wait for
+// the previous caller's work, run, record.  Skipped while the caller's stream
+// is being captured (an event recorded outside a capture cannot be waited on
+// inside it; a captured graph is ordered by whoever launches it).
+struct ScratchOrder {
+  Hierarchy* hp;
+  cudaStream_t st;
+  bool active = false;
+  int begin()
+  {
+    if (!hp) return SMG_OK;
+    Hierarchy& h = *hp;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    SMG_CUDA(cudaStreamIsCapturing(st, &cs));
+    active = cs == cudaStreamCaptureStatusNone;
+    if (!active) return SMG_OK;
+    if (!h.done_ev) {
+      SMG_CUDA(cudaEventCreateWithFlags(&h.done_ev, cudaEventDisableTiming));
+      return SMG_OK;   // nothing recorded yet
+    }
+    SMG_CUDA(cudaStreamWaitEvent(st, h.done_ev, 0));
+    return SMG_OK;
+  }
+  int end()
+  {
+    if (hp && active) SMG_CUDA(cudaEventRecord(hp->done_ev, st));
+    return SMG_OK;
+  }
+};
 
 static int run_vcycle(Hierarchy& h, const double* b, double* u, cudaStream_t st)
 {
@@ -1830,6 +1868,15 @@ int smg_combined_smooth(const smg_operator* a, const double* b, double* u, const
                         void* stream)
 {
   if (!a) return fail("operator is NULL");
+  if (c && c->c.n_regions > 0 && c->c.op != &a->o) {
+    // the correction forms its patch residuals from the rows of the operator
+    // it was created with (smg_correction_create); another operator would
+    // give the residual of a different matrix
+    set_error("correction of size " + std::to_string(c->c.n_global) +
+              " was created for another operator; it does not match this " +
+              std::to_string(a->o.a.nrows) + "-row operator");
+    return SMG_ERR_DIMENSION;
+  }
   return smooth_standalone(a->o, b, u, c ? &c->c : nullptr, kind, sweeps, lambda_max, frac, work,
                            as_stream(stream));
 }
@@ -1906,6 +1953,9 @@ int smg_hierarchy_create(int n_levels, const smg_operator* const* a, const smg_o
       if (L.p->a.nrows != L.n || L.p->a.ncols != a[l + 1]->o.a.nrows)
         return bail(fail("dimension mismatch between prolongation and level operators"));
       L.lc = corrections ? (corrections[l] ? &corrections[l]->c : nullptr) : nullptr;
+      if (L.lc && L.lc->n_regions > 0 && L.lc->op != L.a)
+        return bail(fail("level " + std::to_string(l) +
+                         ": the correction was created for another operator (does not match)"));
       L.kind = kinds[l];
       L.sweeps = sweeps[l];
       L.lambda_max = lambda_max[l];
@@ -1964,6 +2014,7 @@ int smg_hierarchy_destroy(smg_hierarchy* h)
 int smg_hierarchy_set_graphs(smg_hierarchy* h, int enable)
 {
   if (!h) return fail("hierarchy is NULL");
+  std::lock_guard<std::recursive_mutex> lk(h->h.mu);
   h->h.use_graphs = enable != 0;
   return SMG_OK;
 }
@@ -1972,6 +2023,7 @@ int smg_hierarchy_set_option(smg_hierarchy* h, int option, int value)
 {
   if (!h) return fail("hierarchy is NULL");
   Hierarchy& H = h->h;
+  std::lock_guard<std::recursive_mutex> lk(H.mu);
   if (option == SMG_OPT_GRAPHS)
     H.use_graphs = value != 0;
   else if (option == SMG_OPT_FUSE_ZERO_GUESS)
@@ -1997,19 +2049,27 @@ int smg_hierarchy_launches_per_vcycle(const smg_hierarchy* h, int64_t* launches)
 int smg_vcycle(smg_hierarchy* h, const double* b, double* u, void* stream)
 {
   if (!h) return fail("hierarchy is NULL");
-  return run_vcycle(h->h, b, u, as_stream(stream));
+  std::lock_guard<std::recursive_mutex> lk(h->h.mu);
+  ScratchOrder ord{&h->h, as_stream(stream)};
+  SMG_TRY(ord.begin());
+  SMG_TRY(run_vcycle(h->h, b, u, as_stream(stream)));
+  return ord.end();
 }
 
 int smg_vcycle_host(smg_hierarchy* h, const double* b_host, double* u_host, void* stream)
 {
   if (!h) return fail("hierarchy is NULL");
   Hierarchy& H = h->h;
+  std::lock_guard<std::recursive_mutex> lk(H.mu);
   cudaStream_t st = as_stream(stream);
+  ScratchOrder ord{&H, st};
+  SMG_TRY(ord.begin());
   const size_t bytes = sizeof(double) * (size_t)H.lv[0].n;
   SMG_CUDA(cudaMemcpyAsync(H.stage_b, b_host, bytes, cudaMemcpyHostToDevice, st));
   SMG_CUDA(cudaMemcpyAsync(H.stage_u, u_host, bytes, cudaMemcpyHostToDevice, st));
   SMG_TRY(run_vcycle(H, H.stage_b, H.stage_u, st));
   SMG_CUDA(cudaMemcpyAsync(u_host, H.stage_u, bytes, cudaMemcpyDeviceToHost, st));
+  SMG_TRY(ord.end());
   SMG_CUDA(cudaStreamSynchronize(st));
   return SMG_OK;
 }
@@ -2024,7 +2084,10 @@ int smg_vcycle_host_many(smg_hierarchy* h, int64_t count, const double* const* b
   if (count < 0) return fail("negative count");
   if (count > 0 && (!b_host || !u_host)) return fail("NULL host pointer arrays");
   Hierarchy& H = h->h;
+  std::lock_guard<std::recursive_mutex> lk(H.mu);
   cudaStream_t st = as_stream(stream);
+  ScratchOrder ord{&H, st};
+  SMG_TRY(ord.begin());
   if (!H.stage_b2) {
     SMG_TRY(dev_alloc(H.allocs, H.bytes, (size_t)H.lv[0].n, &H.stage_b2));
     SMG_TRY(dev_alloc(H.allocs, H.bytes, (size_t)H.lv[0].n, &H.stage_u2));
@@ -2055,6 +2118,7 @@ int smg_vcycle_host_many(smg_hierarchy* h, int64_t count, const double* const* b
     SMG_CUDA(cudaMemcpyAsync(u_host[i], su[s], bytes, cudaMemcpyDeviceToHost, H.copy_out));
     SMG_CUDA(cudaEventRecord(out_done[s], H.copy_out));
   }
+  SMG_TRY(ord.end());
   SMG_CUDA(cudaStreamSynchronize(H.copy_out));
   SMG_CUDA(cudaStreamSynchronize(st));
   return SMG_OK;
@@ -2065,7 +2129,14 @@ int smg_solve_stationary(smg_hierarchy* h, const double* b, double* u, double rt
 {
   if (!h || !history || !n_history) return fail("NULL argument");
   Hierarchy& H = h->h;
+  std::lock_guard<std::recursive_mutex> lk(H.mu);
   cudaStream_t st = as_stream(stream);
+  ScratchOrder ord{&H, st};
+  SMG_TRY(ord.begin());
+  struct End {
+    ScratchOrder& o;
+    ~End() { o.end(); }
+  } end_guard{ord};
   HLevel& L0 = H.lv[0];
   const int64_t n = L0.n;
   double rr = 0, bb = 0;
@@ -2103,7 +2174,22 @@ int smg_cg(smg_hierarchy* h, const smg_operator* a, const double* b, double* x, 
   if (!a || !history || !n_history) return fail("NULL argument");
   const Operator& A = a->o;
   const int64_t n = A.a.nrows;
+  if (A.a.nrows != A.a.ncols) return fail("cg needs a square operator");
+  if (h && h->h.lv[0].n != n) {
+    set_error("dimension mismatch: the preconditioner's fine level has " +
+              std::to_string(h->h.lv[0].n) + " dofs, the operator " + std::to_string(n) +
+              " (does not match)");
+    return SMG_ERR_DIMENSION;
+  }
   cudaStream_t st = as_stream(stream);
+  std::unique_lock<std::recursive_mutex> lk;
+  if (h) lk = std::unique_lock<std::recursive_mutex>(h->h.mu);
+  ScratchOrder ord{h ? &h->h : nullptr, st};
+  SMG_TRY(ord.begin());
+  struct End {
+    ScratchOrder& o;
+    ~End() { o.end(); }
+  } end_guard{ord};
   std::vector<void*> tmp;
   int64_t bytes = 0;
   double *r = nullptr, *z = nullptr, *d = nullptr, *q = nullptr;

@@ -155,8 +155,20 @@ def device_operator(m, with_transpose: bool = False) -> DeviceOperator:
 
 
 def device_correction(a, correction) -> DeviceCorrection:
+    """Device copy of ``correction`` bound to the operator ``a`` (its patch
+    residuals are formed from a's rows, so the cache is keyed on both)."""
+    n = int(getattr(a, "nrows"))
+    if int(correction.n_global) != n:
+        raise ValueError(f"correction size {int(correction.n_global)} does not match the "
+                         f"{n}-row operator")
     op = device_operator(a)
-    return _cached(_corr_cache, correction, lambda: DeviceCorrection(op, correction))
+    per_op = _cached(_corr_cache, correction, dict)
+    hit = per_op.get(id(op))
+    if hit is None or hit.op is not op:
+        hit = DeviceCorrection(op, correction)
+        per_op.clear()          # one operator per correction at a time (bounded)
+        per_op[id(op)] = hit
+    return hit
 
 
 def _csr_result_to_host(lib, h):

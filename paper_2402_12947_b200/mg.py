@@ -336,25 +336,99 @@ def as_preconditioner(h) -> Callable:
 # ---------------------------------------------------------------------------
 # setup (host): mg.py:72-124 restated over this package's vectorised builders
 
-def build_hierarchy(meshes: Sequence, smoother: SmootherConfig, use_local_correction: bool,
-                    quality_threshold: float = 0.1, element_degree: int = 1,
-                    source=None, region_layers: int = 1,
-                    lambda_tol: float = 1e-8, coarse_refine: bool = False,
-                    device_setup: Optional[bool] = None) -> Hierarchy:
-    """Poisson with homogeneous Dirichlet on every box face; fine to coarse meshes.
+@dataclass(frozen=True)
+class ProblemSpec:
+    """The reference's problem data (fem.py:230-262), restricted to what the
+    GPU setup assembles: Poisson with homogeneous Dirichlet data on every box
+    face.  ``source``: f(x) for one point (as the reference evaluates it,
+    fem.py:288-300) or, with ``vectorized_source=True``, f(points) for an
+    (m, dim) array."""
 
-    ``device_setup``: prolongations (point location, ``smg_prolongation_build``)
-    and Galerkin products (``smg_galerkin``) on the GPU, both bit-identical to
-    the reference's; default: whenever a CUDA device exists.
-    Host-only setup (no GPU, e.g. the CPU test suite) uses the reference's own
-    scipy product."""
+    kind: str = "poisson"
+    source: Optional[Callable] = None
+    dirichlet: tuple = ()
+    neumann: tuple = ()
+    material: Optional[dict] = None
+    vectorized_source: bool = False
+
+
+def _vector_source(problem):
+    """A vectorised (m, dim) -> (m,) source from a reference-style ProblemSpec."""
+    f = getattr(problem, "source", None)
+    if f is None:
+        return None
+    if getattr(problem, "vectorized_source", False):
+        return f
+    return lambda pts: np.fromiter((float(f(p)) for p in pts), dtype=np.float64, count=len(pts))
+
+
+def _check_problem(problem, dim: int) -> None:
+    kind = getattr(problem, "kind", None)
+    if kind != "poisson":
+        raise NotImplementedError(f"problem kind {kind!r}: the GPU setup assembles Poisson only "
+                                  "(elasticity is outside the hot path, SURVEY.md section 2)")
+    if tuple(getattr(problem, "neumann", ()) or ()):
+        raise NotImplementedError("Neumann data is outside the GPU setup (homogeneous Dirichlet "
+                                  "on every box face)")
+    markers = sorted(int(m) for m, _ in getattr(problem, "dirichlet", ()))
+    if markers != list(range(1, 2 * dim + 1)):
+        raise NotImplementedError("the GPU setup eliminates Dirichlet conditions on every box face "
+                                  f"(markers 1..{2 * dim}); got {markers}")
+    probe = np.full(dim, 0.5)
+    for _, fn in problem.dirichlet:
+        val = np.asarray(fn(probe), dtype=np.float64)
+        if np.any(val != 0.0):
+            raise NotImplementedError("only homogeneous Dirichlet data is supported")
+
+
+def _own_mesh(m):
+    from .mesh import SimplexMesh
+    if isinstance(m, SimplexMesh):
+        return m
+    return SimplexMesh(int(m.dim), np.asarray(m.vertices, dtype=np.float64),
+                       np.asarray(m.cells, dtype=np.int64), np.asarray(m.boundary_facets, dtype=np.int64),
+                       np.asarray(m.facet_markers, dtype=np.int64))
+
+
+def build_hierarchy(meshes: Sequence, problem, smoother: SmootherConfig,
+                    use_local_correction: bool, quality_threshold: float = 0.1,
+                    element_degree: int = 1, *, region_layers: int = 1,
+                    lambda_tol: float = 1e-8, coarse_refine: bool = False,
+                    device_setup: Optional[bool] = None,
+                    device_assembly: bool = False) -> Hierarchy:
+    """``build_hierarchy(meshes, problem, smoother, use_local_correction,
+    quality_threshold=0.1, element_degree=1)`` as the reference (mg.py:72-124);
+    meshes fine to coarse (reference ``SimplexMesh`` objects are accepted),
+    ``problem`` a Poisson ``ProblemSpec`` (the reference's or this package's)
+    with homogeneous Dirichlet data on every box face.
+
+    ``device_setup``: prolongations (point location, ``smg_prolongation_build``),
+    Galerkin products (``smg_galerkin``), patch Cholesky factors, the coarse
+    factor and Lanczos on levels >= 200k rows run on the GPU (default:
+    whenever a CUDA device exists).  The fine operator is assembled on the
+    host by default -- the reference's own element arithmetic (numpy einsum /
+    LAPACK det and inv) and scipy's duplicate summation, so A_0 and therefore
+    every Galerkin level are bit-identical to the reference's construction;
+    ``device_assembly=True`` assembles on the GPU instead (same pattern,
+    values within ~1e-13, so exact-zero Galerkin sums can differ).
+    Host-only setup (no GPU, e.g. the CPU test suite) uses the reference's
+    own scipy products."""
+    if isinstance(problem, SmootherConfig) or hasattr(problem, "sweeps"):
+        raise TypeError("build_hierarchy(meshes, problem, smoother, use_local_correction, ...): "
+                        "the second argument is the ProblemSpec (mg.py:72-75)")
+    meshes = [_own_mesh(m) for m in meshes]
+    if len(meshes) < 2:
+        raise ValueError(f"a hierarchy needs at least 2 meshes, got {len(meshes)}")
+    if len({m.dim for m in meshes}) != 1:
+        raise ValueError("all meshes must share the same dimension")
+    _check_problem(problem, meshes[0].dim)
+    source = _vector_source(problem)
+    smoother = SmootherConfig.from_any(smoother)
     from .fem import assemble_poisson, build_dofmap
     from .mesh import identify_regions
     from .smoothers import (adjusted_lambda_max, build_local_correction, dofs_for_regions,
                             jacobi_lambda_max)
     from .transfer import build_prolongation, coarsen_system
-    if len(meshes) < 2:
-        raise ValueError(f"a hierarchy needs at least 2 meshes, got {len(meshes)}")
     if device_setup is None:
         from .device import torch
         device_setup = bool(torch().cuda.is_available())
@@ -365,7 +439,8 @@ def build_hierarchy(meshes: Sequence, smoother: SmootherConfig, use_local_correc
     dofmaps = [build_dofmap(m, element_degree) for m in meshes]
     times["dofmap_s"] += time.perf_counter() - t
     t = time.perf_counter()
-    system = assemble_poisson(meshes[0], dofmaps[0], source, device=device_setup)
+    system = assemble_poisson(meshes[0], dofmaps[0], source,
+                              device=bool(device_setup and device_assembly))
     times["assembly_s"] += time.perf_counter() - t
     operators = [system.a]
     prolongations = []
@@ -403,5 +478,6 @@ def build_hierarchy(meshes: Sequence, smoother: SmootherConfig, use_local_correc
     coarse = dense_factor(operators[-1].to_dense(), device=device_setup)
     times["coarse_factor_s"] += time.perf_counter() - t
     h = Hierarchy(levels, coarse, system, coarse_refine)
-    h.setup_times = dict(times, galerkin_device=bool(device_setup))
+    h.setup_times = dict(times, galerkin_device=bool(device_setup),
+                         assembly_device=bool(device_setup and device_assembly))
     return h

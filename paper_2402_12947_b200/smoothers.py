@@ -28,7 +28,7 @@ import numpy as np
 from . import _lib
 from . import device as _dev
 from .sparse import (DEVICE_LANCZOS_MIN_ROWS, CsrMatrix, DenseFactor, NotPositiveDefiniteError,
-                     dense_factor, estimate_lambda_max, estimate_lambda_max_device)
+                     dense_factor, device_matvec, estimate_lambda_max)
 
 
 class ZeroDiagonalError(ValueError):
@@ -274,8 +274,10 @@ def combined_smooth(a, b, u, correction, cfg, splitting=None):
 
 def jacobi_lambda_max(a, tol: float = 1e-8, device: Optional[bool] = None) -> float:
     """Largest eigenvalue of D^-1 A (smoothers.py:214-222; setup).  ``device``
-    (default: whenever a CUDA device exists) runs Lanczos on the GPU for
-    operators of at least DEVICE_LANCZOS_MIN_ROWS rows."""
+    (default: whenever a CUDA device exists) runs the Lanczos matvecs of
+    operators with at least DEVICE_LANCZOS_MIN_ROWS rows on the GPU (bitwise
+    equal SpMV, so the estimate is the host path's, which is the
+    reference's)."""
     a = CsrMatrix.from_any(a)
     diag = a.diagonal()
     zero = np.nonzero(diag == 0.0)[0]
@@ -285,7 +287,7 @@ def jacobi_lambda_max(a, tol: float = 1e-8, device: Optional[bool] = None) -> fl
     if device is None:
         device = bool(_dev.torch().cuda.is_available())
     if a.nrows >= DEVICE_LANCZOS_MIN_ROWS and device:
-        return estimate_lambda_max_device(a, scale, tol)
+        return estimate_lambda_max(device_matvec(a, scale), a.nrows, tol)
     s = a.to_scipy()
     return estimate_lambda_max(lambda x: scale * (s @ (scale * x)), a.nrows, tol)
 

@@ -184,3 +184,55 @@ def coarsen_system(a_fine, p, device: bool = True) -> CsrMatrix:
     path (the reference's scipy product)."""
     m = getattr(p, "matrix", p)
     return triple_product(m, a_fine) if device else host_triple_product(m, a_fine)
+
+
+def locate_point(mesh: SimplexMesh, x, tol: float = 1e-10):
+    """One-shot point location (transfer.py:99-101): (cell index, clamped
+    barycentric coordinates), lowest-index containing cell on ties."""
+    pt = np.asarray(x, dtype=np.float64).reshape(1, mesh.dim)
+    cells, bary = CellLocator(mesh, tol=tol).locate(pt)
+    return int(cells[0]), bary[0]
+
+
+def _prolongation_operator(p):
+    from . import device as _dev
+    m = getattr(p, "matrix", p)
+    return m, _dev.device_operator(m, with_transpose=True)
+
+
+def restrict_residual(p, r_fine):
+    """``P^T r`` (transfer.py:158-162; the restriction inside vcycle, mg.py:142)
+    on the GPU: stored CSR(P^T) rows summed in ascending fine order, bitwise
+    equal to scipy's csc_matvec.  numpy in -> numpy out; CUDA tensor in ->
+    CUDA tensor out."""
+    from . import _lib, device as _dev
+    m, op = _prolongation_operator(p)
+    t = _dev.torch()
+    is_tensor = isinstance(r_fine, t.Tensor)
+    if tuple(np.shape(r_fine)) != (m.nrows,):
+        raise ValueError(f"residual length {tuple(r_fine.shape)} does not match fine size "
+                         f"{m.nrows}")
+    rt, _ = _dev.as_device_vector(r_fine, m.nrows, "r_fine")
+    out = t.empty(m.ncols, dtype=t.float64, device=rt.device)
+    _lib.check(_lib.load().smg_spmv_transpose(op.handle, _dev.ptr(rt), _dev.ptr(out),
+                                              _dev.stream_handle()))
+    return out if is_tensor else out.cpu().numpy()
+
+
+def prolong_add(p, u_coarse, u_fine):
+    """``u_fine += P u_coarse`` in place (transfer.py:165-172; mg.py:149) on the
+    GPU (row-sequential sums, bitwise equal to scipy's csr_matvec + add)."""
+    from . import _lib, device as _dev
+    m, op = _prolongation_operator(p)
+    t = _dev.torch()
+    if tuple(np.shape(u_coarse)) != (m.ncols,):
+        raise ValueError(f"coarse vector length {tuple(u_coarse.shape)} does not match {m.ncols}")
+    if tuple(np.shape(u_fine)) != (m.nrows,):
+        raise ValueError(f"fine vector length {tuple(u_fine.shape)} does not match {m.nrows}")
+    ct, _ = _dev.as_device_vector(u_coarse, m.ncols, "u_coarse")
+    ft, host = _dev.as_device_vector(u_fine, m.nrows, "u_fine")
+    _lib.check(_lib.load().smg_prolong_add(op.handle, _dev.ptr(ct), _dev.ptr(ft),
+                                           _dev.stream_handle()))
+    if host is not None and not isinstance(u_fine, t.Tensor):
+        u_fine[...] = ft.cpu().numpy()
+    return u_fine

@@ -97,3 +97,24 @@ def load(name: str):
     z = dict(np.load(path(name), allow_pickle=False))
     h = load_hierarchy(z) if "h/n_levels" in z else None
     return z, h
+
+
+#: every fixture that stores a whole reference-built hierarchy and its outputs
+HIERARCHY_FIXTURES = ["crit7_adj", "crit7_ref", "c1s", "c2s", "c3s", "c4s",
+                      "cpl_p1", "cpl_p2", "unc_p2"]
+#: fixtures whose fine level holds several local-correction regions, and
+#: whether those regions are coupled through A
+MULTI_REGION_FIXTURES = {"cpl_p1": True, "cpl_p2": True, "unc_p2": False}
+
+
+def workload(name: str):
+    """The paper_2402_12947_b200.configs construction a baseline fixture was
+    generated from (tests/golden/make_golden.py ``baseline_small``)."""
+    from dataclasses import replace
+    from paper_2402_12947_b200 import configs
+    return {
+        "c1s": configs.C1.scaled(4),
+        "c2s": configs.C2.scaled(8),
+        "c3s": configs.C3.scaled(4),
+        "c4s": replace(configs.C4, name="C4-3d-p2-cheb2/s", grids=(12, 6, 3, 2), n_clusters=2),
+    }[name]

@@ -18,9 +18,18 @@ Every output vector here comes from the reference's own functions
   damped-Jacobi branch (lambda_max = 1.5, fraction 1 => omega = 2/3,
   smoothers.py:120-124); C2 uses 2-layer regions computed harness-side and
   factored by the reference's build_local_correction.
+* c4s -- BASELINE C4 construction (3D P2, flattened tets, Chebyshev
+  degree 2) at grids 12/6/3/2 with two clusters: two 279-dof regions, past
+  the shared-memory cap, so the streamed-factor patch path runs.
 * c5p -- C5-style batched patch solves: dense SPD blocks of 64/200/512 dofs,
   cond 1e6, embedded in an otherwise-identity operator; reference
   apply_local_correction outputs.
+* cpl_p1, cpl_p2, unc_p2 -- several local-correction regions on one level
+  (SURVEY.md A4), every step by the reference: a 16x16 grid whose flattened
+  vertices (the reference's _apply_clusters) sit 4 cells apart (two regions
+  coupled through A; P1 and P2), or far apart (three uncoupled regions).
+
+``python tests/golden/make_golden.py c4s cpl_p1`` regenerates only those.
 """
 
 from __future__ import annotations
@@ -233,14 +242,93 @@ def c5_patches():
     print("c5p", sizes)
 
 
+def _coupling(a, regions):
+    """1 if any two regions are coupled through A (A[B_d, B_d'] != 0)."""
+    s = a.to_scipy()
+    owner = -np.ones(a.nrows, dtype=np.int64)
+    for k, (idx, _) in enumerate(regions):
+        owner[idx] = k
+    for k, (idx, _) in enumerate(regions):
+        sub = s[idx]
+        cols = sub.indices[sub.data != 0.0]
+        o = owner[cols]
+        if np.any((o >= 0) & (o != k)):
+            return 1
+    return 0
+
+
+def multi_region(name, degree, centers, grids=(16, 8, 4), jacobi_theta=None, sweeps=2):
+    """Several local-correction regions on the fine level, built entirely by
+    the reference: structured grids (mesh.py:136), two or more flattened
+    vertices by the reference's own cluster routine (experiments.py:175-263,
+    one vertex per cluster, seeded), regions / dofs / factors / lambda by
+    build_hierarchy (mg.py:72-124).  SURVEY.md A4: with the flattened vertices
+    4 cells apart at n = 16 the two regions are disjoint but coupled through A
+    (additive S_c must read the pre-correction u); far apart they are not."""
+    sm = _ref()
+    ex = sm.experiments
+    meshes = []
+    for lvl, n in enumerate(grids):
+        m = sm.mesh.generate_simplex_grid(2, n)
+        if lvl == 0:
+            clusters = [ex.ClusterSpec(c, 1e-4, 1) for c in centers]
+            m = ex._apply_clusters(m, clusters, np.random.default_rng([5, lvl]))
+        meshes.append(m)
+    zero = lambda x: 0.0
+    problem = sm.fem.ProblemSpec("poisson", source=lambda x: 1.0,
+                                 dirichlet=tuple((m, zero) for m in range(1, 5)))
+    smoother = sm.smoothers.SmootherConfig("chebyshev", sweeps)
+    h = sm.mg.build_hierarchy(meshes, problem, smoother, True, 0.1, degree)
+    if jacobi_theta is not None:
+        for lv in h.levels:
+            lv.smoother = sm.smoothers.SmootherConfig("chebyshev", sweeps, lambda_max=jacobi_theta,
+                                                      lambda_min_fraction=1.0)
+    lv0 = h.levels[0]
+    lc = lv0.local_correction
+    n0 = lv0.a.nrows
+    b = np.array(h.system.b)
+    d = fixtures.hierarchy_arrays(h)
+    _common_goldens(sm, h, b, np.zeros(n0), d)
+    d["coupled"] = np.array(_coupling(lv0.a, lc.regions))
+    d["lambda_max"] = np.array([lv.lambda_max for lv in h.levels])
+    d["lambda_max_adjusted"] = np.array([lv.lambda_max_adjusted for lv in h.levels])
+    d["meta/grids"] = np.array(grids)
+    _versions(d)
+    np.savez_compressed(fixtures.path(name), **d)
+    print(name, [lv.a.nrows for lv in h.levels], "regions", lc.n_regions,
+          [len(i) for i, _ in lc.regions], "coupled", int(d["coupled"]),
+          "stat iters", int(d["g/stat_iters"]), "cg iters", int(d["g/cg_iters"]))
+
+
 def main():
-    from paper_2402_12947_b200 import configs
     t = time.time()
-    crit7()
-    baseline_small("c1s", configs.C1.scaled(4), jacobi_theta=1.5)
-    baseline_small("c2s", configs.C2.scaled(8), layers=2)
-    baseline_small("c3s", configs.C3.scaled(4), jacobi_theta=1.5)
-    c5_patches()
+    which = set(sys.argv[1:])
+
+    def want(name):
+        return not which or name in which
+
+    if want("crit7"):
+        crit7()
+    if want("c1s"):
+        baseline_small("c1s", fixtures.workload("c1s"), jacobi_theta=1.5)
+    if want("c2s"):
+        baseline_small("c2s", fixtures.workload("c2s"), layers=2)
+    if want("c3s"):
+        baseline_small("c3s", fixtures.workload("c3s"), jacobi_theta=1.5)
+    if want("c4s"):
+        # BASELINE C4 construction (3D P2, jitter 0.15h, flattened tets,
+        # Chebyshev degree 2) at grids 12/6/3/2 with two clusters: P2 patches
+        # of ~200 dofs (SURVEY.md finding 6) on a 15,625-dof fine level
+        baseline_small("c4s", fixtures.workload("c4s"))
+    if want("c5p"):
+        c5_patches()
+    # multi-region local corrections (SURVEY.md A4; pkg/tests/test_smoothers.py:89-99)
+    if want("cpl_p1"):
+        multi_region("cpl_p1", 1, [(0.3125, 0.5), (0.5625, 0.5)], jacobi_theta=1.5)
+    if want("cpl_p2"):
+        multi_region("cpl_p2", 2, [(0.3125, 0.5), (0.5625, 0.5)])
+    if want("unc_p2"):
+        multi_region("unc_p2", 2, [(0.25, 0.25), (0.75, 0.75), (0.25, 0.75)])
     print(f"done in {time.time() - t:.1f}s")
 
 

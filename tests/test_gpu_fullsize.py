@@ -1,6 +1,9 @@
-"""BASELINE-size parity: C1 (16,641 DOFs), C2 (1,050,625) and C3 (274,625) hierarchies
-built by this repo's setup, GPU path vs the CPU oracle on identical inputs,
-plus size-independent properties of the V-cycle.
+"""BASELINE-size parity: C1 (16,641 DOFs), C2 (1,050,625), C3 (274,625) and
+C4 (7,189,057; 3D P2) hierarchies built by this repo's setup, GPU path vs the
+CPU oracle on identical inputs, plus size-independent properties of the
+V-cycle.  (The hierarchies are the reference's construction: the device setup
+equals the host setup, test_gpu_setup.py::test_device_setup_equals_host_setup_c2,
+and the host setup equals the reference's, tests/test_setup.py.)
 
 Bars: per-sweep vectors, restriction and prolongation bitwise; V-cycle
 <= 1e-12 relative; identical stationary and CG iteration counts (rtol 1e-10);
@@ -17,11 +20,12 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
-@pytest.fixture(scope="module", params=["C1", "C2", "C3"])
+@pytest.fixture(scope="module", params=["C1", "C2", "C3", "C4"])
 def case(request):
     from paper_2402_12947_b200 import configs
     h, b, u0 = configs.build(configs.WORKLOADS[request.param])
-    return request.param, h, b, u0
+    yield request.param, h, b, u0
+    del h
 
 
 def test_fine_level_sweeps_bitwise(case):

@@ -10,11 +10,13 @@ sums every entry in scipy csr_matmat's order and drops exact zeros as it does).
 import numpy as np
 import pytest
 
+from tests.golden import fixtures
+
 from tests.test_oracle_golden import random_int_csr
 
 pytestmark = pytest.mark.gpu
 
-NAMES = ["crit7_adj", "crit7_ref", "c1s", "c2s", "c3s"]
+NAMES = fixtures.HIERARCHY_FIXTURES
 
 
 def same(m, ptr, col, val) -> bool:

@@ -10,9 +10,11 @@ CG iteration counts at rtol 1e-10; bit-identical reruns (criterion 10).
 import numpy as np
 import pytest
 
+from tests.golden import fixtures
+
 pytestmark = pytest.mark.gpu
 
-NAMES = ["crit7_adj", "crit7_ref", "c1s", "c2s", "c3s"]
+NAMES = fixtures.HIERARCHY_FIXTURES
 TOL_DENSE = 1e-12
 
 

@@ -285,3 +285,56 @@ def test_assembly_inverted_cell_raises():
     bad = replace(m, cells=cells)
     with pytest.raises(ValueError, match="degenerate or inverted"):
         assemble_poisson(bad, build_dofmap(bad, 1), device=True)
+
+
+# ---------------------------------------------------------------------------
+# the whole device setup == the reference construction (BENCH same_config)
+
+def _assert_same_hierarchy(hd, hh, factor_tol=1e-12):
+    """Device-built vs host-built hierarchy: operators, prolongations, region
+    dof sets and smoother lambdas bit for bit; Cholesky factors (device
+    kernel / cuSOLVER vs LAPACK) to a stated tolerance."""
+    assert len(hd.levels) == len(hh.levels)
+    for ld, lh in zip(hd.levels, hh.levels):
+        for x, y in ((ld.a, lh.a),) + (((ld.prolongation.matrix, lh.prolongation.matrix),)
+                                        if lh.prolongation is not None else ()):
+            assert np.array_equal(x.row_offsets, y.row_offsets)
+            assert np.array_equal(x.col_indices, y.col_indices)
+            assert np.array_equal(x.values, y.values)
+        assert ld.smoother.lambda_max == lh.smoother.lambda_max
+        cd, ch = ld.local_correction, lh.local_correction
+        assert (cd is None) == (ch is None)
+        if ch is not None:
+            assert len(cd.regions) == len(ch.regions)
+            for (i1, f1), (i2, f2) in zip(cd.regions, ch.regions):
+                assert np.array_equal(i1, i2)
+                l1, l2 = np.tril(f1.factor[0]), np.tril(f2.factor[0])
+                assert np.max(np.abs(l1 - l2)) <= factor_tol * np.max(np.abs(l2))
+    c1, c2 = np.tril(hd.coarse_factor.factor[0]), np.tril(hh.coarse_factor.factor[0])
+    assert np.max(np.abs(c1 - c2)) <= 1e-12 * np.max(np.abs(c2))
+
+
+@pytest.mark.parametrize("name", ["c1s", "c2s", "c4s"])
+def test_device_setup_equals_reference_fixture(name):
+    from paper_2402_12947_b200 import configs
+    from tests.golden import fixtures
+    z, ref = fixtures.load(name)
+    h, b, _ = configs.build(fixtures.workload(name), device_setup=True)
+    if name == "c1s":   # C1 runs the reference's Jacobi branch: lambda is set, not estimated
+        for lv, rl in zip(h.levels, ref.levels):
+            lv.smoother = rl.smoother
+    _assert_same_hierarchy(h, ref)
+    assert np.array_equal(b, z["g/b"])
+
+
+@pytest.mark.slow
+def test_device_setup_equals_host_setup_c2():
+    """Full BASELINE C2: the GPU-built hierarchy the bench times is the host
+    (= reference) construction -- every level's nnz and values, P, regions
+    and lambda identical."""
+    from paper_2402_12947_b200 import configs
+    hd, bd, _ = configs.build(configs.C2, device_setup=True)
+    hh, bh, _ = configs.build(configs.C2, device_setup=False)
+    assert [lv.a.nnz for lv in hd.levels] == [lv.a.nnz for lv in hh.levels]
+    _assert_same_hierarchy(hd, hh)
+    assert np.array_equal(bd, bh)

@@ -14,7 +14,7 @@ import pytest
 from oracle import oracle as O
 from tests.golden import fixtures
 
-NAMES = ["crit7_adj", "crit7_ref", "c1s", "c2s", "c3s"]
+NAMES = fixtures.HIERARCHY_FIXTURES
 TOL_DENSE = 1e-12
 
 
