@@ -10,18 +10,21 @@ launch through the C-ABI (smg_vcycle).  Every V-cycle touches ~3 GB, far more
 than the 126 MB L2, so no flush is needed between steps.
 
 Also measured in the same run (all reported in the one JSON line):
-  * roofline: the dominant kernel, the fine-level Chebyshev step
-    (csr_tile_kernel<ChebNext>, 12z + 44n algorithmic bytes per launch),
-    timed with CUDA events on the launching stream;
-  * sweeps_per_s: fine-level smoother sweeps/s (same loop);
-  * lc_share: (T_vcycle - T_vcycle_without_corrections) / T_vcycle, both graph replays;
-  * e2e: V-cycles/s through smg_vcycle_host_many with HOST buffers (every
-    step's H2D of b and u, V-cycle and D2H of u inside the timed region; the
-    copies of neighbouring steps overlap each V-cycle), plus the
-    one-call-per-step smg_vcycle_host figure;
-  * cpu_baseline: the CPU oracle (oracle/, the reference algorithm restated
-    in numpy + C, bit-identical sparse arithmetic) on the host cores.
-`--impl reference` times that CPU implementation alone (rank 0; other ranks
+  * roofline: the dominant kernel, the fine-level smoother step (ChebNext:
+    12z + 44n algorithmic bytes per launch; Jacobi: 12z + 28n), timed with
+    CUDA events on the launching stream -- `frac` on cold launches (L2
+    overwritten before each), the warm back-to-back figure beside it;
+    `traffic` from this round's ncu capture of the same workload, else null;
+  * sweeps_per_s, per-level sweep rates, lc_share (graph replays with and
+    without the corrections);
+  * e2e: the drop-in call vcycle(h, b_host, u_host) per step (H2D of b and u,
+    V-cycle, D2H of u, synchronised), with the batched host API and the
+    pageable-memory figure beside it;
+  * cpu_baseline: the reference itself (baseline/_ref, unmodified simplexmg)
+    on the host cores -- vcycle, chebyshev_smooth, combined_smooth,
+    solve_stationary, bounded samples -- plus the oracle port
+    (cpu_baseline_port), and gpu_functions with the same list on the device.
+`--impl reference` times the reference's vcycle alone (rank 0; other ranks
 exit 0).  N > 1 GPUs run independent replicas (the path does not shard;
 DESIGN.md), timed on the device, max over ranks.
 """
@@ -45,12 +48,16 @@ METRIC = "V-cycles/sec & smoother sweeps/sec (fp64) at 1 B200; SpMV HBM GB/s vs 
 UNIT = "V-cycles/s"
 
 
-def _ncu_traffic():
-    """dram read+write bytes per launch of the dominant kernel from the committed
-    ncu --set full capture (profiles/ncu_dominant_kernel.json), or None."""
+def _ncu_traffic(workload: str, step: str):
+    """dram read+write bytes per launch of this workload's dominant kernel
+    from this round's ncu --set full capture (profiles/ncu_traffic.json,
+    keyed by workload; written by profiles/summarize_ncu.py --traffic), or
+    None when the workload / step kind was not captured."""
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_dominant_kernel.json")) as f:
-            j = json.load(f)
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            j = json.load(f)[workload]
+        if j.get("step") != step:
+            return None, None
         return int(j["dram_read_bytes"]) + int(j["dram_write_bytes"]), j.get("source")
     except Exception:
         return None, None
@@ -163,6 +170,139 @@ def _cheb_steps(cfg):
     return theta, out
 
 
+def reference_package():
+    """The UNMODIFIED reference (``simplexmg``) installed into baseline/_ref
+    (``pip install --no-index --no-build-isolation --no-deps --target
+    baseline/_ref <copy of /root/reference/pkg>``).  It
+    imports matplotlib at package import (pkg/src/simplexmg/__init__.py:27 ->
+    experiments.py:26 -> plots.py:5-9), which the image lacks: a stub module
+    satisfies the import (no figure is drawn here).  Returns (module, None)
+    or (None, why)."""
+    import types
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "simplexmg")):
+        return None, "baseline/_ref is not installed"
+    if "matplotlib" not in sys.modules:
+        mpl = types.ModuleType("matplotlib")
+        mpl.use = lambda *a, **k: None
+        plt = types.ModuleType("matplotlib.pyplot")
+        plt.subplots = lambda *a, **k: (None, None)
+        plt.close = lambda *a, **k: None
+        mpl.pyplot = plt
+        sys.modules["matplotlib"] = mpl
+        sys.modules["matplotlib.pyplot"] = plt
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    try:
+        import simplexmg  # noqa: F401
+        import simplexmg.mg, simplexmg.smoothers, simplexmg.sparse, simplexmg.transfer  # noqa
+    except Exception as e:  # pragma: no cover - reported in the JSON line
+        return None, f"import failed: {e!r}"
+    if not os.path.abspath(simplexmg.__file__).startswith(path):
+        return None, f"simplexmg resolved to {simplexmg.__file__}, not baseline/_ref"
+    return simplexmg, None
+
+
+def reference_hierarchy(sm, h):
+    """The reference's own objects (mg.Level / mg.Hierarchy, sparse.CsrMatrix,
+    smoothers.LocalCorrection, sparse.DenseFactor; mg.py:30-69) holding the
+    hierarchy this package's host setup built -- bit for bit the reference's
+    construction (tests/test_setup.py).  The damped-Jacobi workloads map onto
+    the reference's delta == 0 Chebyshev branch (smoothers.py:120-124)."""
+    from paper_2402_12947_b200.smoothers import SmootherConfig
+
+    def csr(m):
+        return sm.sparse.CsrMatrix(int(m.nrows), int(m.ncols), np.array(m.row_offsets),
+                                   np.array(m.col_indices), np.array(m.values))
+
+    levels = []
+    for l, lv in enumerate(h.levels):
+        prol = None
+        if lv.prolongation is not None:
+            prol = sm.transfer.Prolongation(csr(lv.prolongation.matrix), l, l + 1)
+        lam, frac = SmootherConfig.from_any(lv.smoother).chebyshev_parameters()
+        cfg = sm.smoothers.SmootherConfig("chebyshev", int(lv.smoother.sweeps), lambda_max=lam,
+                                          lambda_min_fraction=frac)
+        lc = None
+        if lv.local_correction is not None:
+            regs = tuple((np.asarray(idx, dtype=np.int64),
+                          sm.sparse.DenseFactor("cholesky", f.factor, len(idx)))
+                         for idx, f in lv.local_correction.regions)
+            lc = sm.smoothers.LocalCorrection(regs, int(lv.local_correction.n_global))
+        levels.append(sm.mg.Level(l, None, None, csr(lv.a), prol, cfg, None, lc, None))
+    cf = h.coarse_factor
+    return sm.mg.Hierarchy(levels, sm.sparse.DenseFactor("cholesky", cf.factor, int(cf.n_local)), None)
+
+
+def _cpu_env():
+    import platform
+    import scipy
+    model = platform.processor() or ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu": model, "visible_cores": len(os.sched_getaffinity(0)),
+            "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS"),
+            "numpy": np.__version__, "scipy": scipy.__version__}
+
+
+def reference_functions(sm, rh, b, budget_s: float = 20.0):
+    """Per-function CPU timings of the reference itself (SURVEY.md section
+    8(d)): chebyshev_smooth per sweep, combined_smooth,
+    vcycle and solve_stationary per cycle on the fine level, 1 warm-up then
+    the median of the timed calls, bounded to ~budget_s.  Sparse products are
+    scipy (1 core); the dense patch / coarse solves are OpenBLAS (all visible
+    cores)."""
+    lv = rh.levels[0]
+    cfg = lv.smoother
+    n = lv.a.nrows
+    u0 = np.random.default_rng(5).standard_normal(n)
+    out = {}
+    t_start = time.perf_counter()
+
+    def med(fn, reps):
+        fn()
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t0)
+        return float(np.median(ts)), len(ts)
+
+    t, r = med(lambda: sm.smoothers.chebyshev_smooth(lv.a, b, u0.copy(), cfg.sweeps, cfg), 3)
+    out["chebyshev_smooth_per_sweep_ms"] = 1e3 * t / cfg.sweeps
+    out["chebyshev_smooth_degree"] = int(cfg.sweeps)
+    t, r = med(lambda: sm.smoothers.combined_smooth(lv.a, b, u0.copy(), lv.local_correction,
+                                                   cfg), 2)
+    out["combined_smooth_ms"] = 1e3 * t
+    t_one = time.perf_counter()
+    sm.mg.vcycle(rh, b, u0.copy())
+    t_one = time.perf_counter() - t_one
+    reps = max(1, min(3, int((budget_s - (time.perf_counter() - t_start)) / max(t_one, 1e-3) / 3)))
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        sm.mg.vcycle(rh, b, u0.copy())
+        ts.append(time.perf_counter() - t0)
+    out["vcycle_ms"] = 1e3 * float(np.median(ts))
+    out["vcycle_reps"] = reps
+    cycles = 2
+    t0 = time.perf_counter()
+    _, hist = sm.mg.solve_stationary(rh, b, np.zeros(n), 1e-10, cycles)
+    el = time.perf_counter() - t0
+    out["solve_stationary_ms_per_cycle"] = 1e3 * el / max(1, len(hist) - 1)
+    out["solve_stationary_sample"] = f"max_cycles={cycles} (history {len(hist)} entries)"
+    out["wall_s"] = time.perf_counter() - t_start
+    out.update(_cpu_env())
+    out["cores_note"] = "sparse products: 1 core (scipy); dense patch/coarse solves: OpenBLAS threads"
+    return out
+
+
 def cpu_baseline(h, b, budget_s: float, threads: int):
     """Oracle V-cycles on the host for ~budget_s seconds (at least one)."""
     from oracle import oracle as O
@@ -194,44 +334,65 @@ def _layout(lib, op) -> str:
 
 
 def run_reference(args):
+    """The reference arm: the UNMODIFIED reference's ``vcycle`` (mg.py:127-151,
+    numpy/scipy/LAPACK on the host cores) from baseline/_ref on the same
+    workload -- the hierarchy this package's host setup built, which is the
+    reference's construction bit for bit (tests/test_setup.py), held in the
+    reference's own objects.  Falls back to the oracle port (oracle/, the
+    reference algorithm restated in numpy + C) only if baseline/_ref is absent.
+    Rank 0 alone runs; other ranks exit 0."""
     ws, rank, local = _dist()
     if rank != 0:
         return 0
     from paper_2402_12947_b200 import configs
-    from oracle import oracle as O
     wl = configs.WORKLOADS[args.workload]
-    # host setup (the reference's own construction, bit for bit): nothing of
-    # this package's device code runs on the reference arm
-    h, b, u0 = configs.build(wl, device_setup=False)
+    t_setup = time.perf_counter()
+    h, b, u0 = configs.build(wl, device_setup=False)   # host only: no GPU code on this arm
+    t_setup = time.perf_counter() - t_setup
+    sm, why = reference_package()
     threads = len(os.sched_getaffinity(0))
-    O.set_threads(threads)
+    if sm is not None:
+        rh = reference_hierarchy(sm, h)
+        cycle = lambda u: sm.mg.vcycle(rh, b, u)
+        kind, cores = "reference", threads
+        what = "reference simplexmg.mg.vcycle (baseline/_ref, unmodified)"
+    else:
+        from oracle import oracle as O
+        O.set_threads(threads)
+        cycle = lambda u: O.vcycle(h, b, u)
+        kind, cores = "port", O.num_threads()
+        what = f"oracle port (reference unavailable: {why})"
     u = u0.copy()
     t0 = time.perf_counter()
-    O.vcycle(h, b, u)
+    cycle(u)
     t_one = time.perf_counter() - t0
-    # the requested warm-up (the first, untimed cycle above included in it),
-    # bounded to ~60 s of CPU time
-    warm = max(0, min(args.warmup - 1, int(60.0 / max(t_one, 1e-3))))
+    # the requested warm-up (the first, untimed cycle above included), and the
+    # timed steps, each bounded so the whole arm ends within a few minutes
+    budget_warm, budget_steps = 30.0, 120.0
+    warm = max(0, min(args.warmup - 1, int(budget_warm / max(t_one, 1e-3))))
     for _ in range(warm):
-        O.vcycle(h, b, u)
-    steps = max(1, min(args.steps, int(90.0 / max(t_one, 1e-3))))
+        cycle(u)
+    steps = max(1, min(args.steps, int(budget_steps / max(t_one, 1e-3))))
     t0 = time.perf_counter()
     for _ in range(steps):
-        O.vcycle(h, b, u)
+        cycle(u)
     el = time.perf_counter() - t0
     value = steps / el
-    sample = (f"{steps} oracle V-cycles of {args.workload} (bounded sample of the {args.steps} "
-              f"requested; ~90 s cap), after {warm + 1} warm-up")
+    sample = (f"{steps} V-cycles of {args.workload} by the {what} (bounded sample of the "
+              f"{args.steps} requested; ~{budget_steps:.0f} s cap), after {warm + 1} warm-up")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
         "steps": steps, "warmup": warm + 1, "ms_per_step": 1e3 * el / steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic (seeded BASELINE {args.workload} construction)",
         "config": _config(wl, h),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": O.num_threads(), "kind": "port",
-                         "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": sample, **_cpu_env()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "setup_s": t_setup,
     }
+    if sm is not None and not args.no_cpu_baseline:
+        line["reference_functions"] = reference_functions(sm, rh, b)
     print(json.dumps(line))
     return 0
 
@@ -505,8 +666,28 @@ def main():
     torch.cuda.synchronize()
     k_ms = k0.elapsed_time(k1) / reps
     peak, peak_src = _peaks()
-    achieved = bytes_per / (k_ms / 1e3) / 1e9
+    achieved_warm = bytes_per / (k_ms / 1e3) / 1e9
     sweeps_per_s = 1e3 / k_ms
+    # cold: the L2 (126 MB) is overwritten by a 512 MB memset before every
+    # launch; each launch is bracketed by its own events on the launching
+    # stream, so the memset is not timed.  This is the kernel as it runs inside
+    # a V-cycle whose other levels evicted its vectors -- the honest figure.
+    flush = torch.empty(64 << 20, dtype=torch.float64, device="cuda")
+    cold_reps = 40
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(cold_reps)]
+    for i in range(cold_reps):
+        flush.zero_()
+        evs[i][0].record(stream)
+        _lib.check(lib.smg_smoother_step(op.handle, D.ptr(b), D.ptr(ua), D.ptr(ub), D.ptr(dbuf),
+                                         step_kind, theta, c1, c2, sh))
+        evs[i][1].record(stream)
+        ua, ub = ub, ua
+    torch.cuda.synchronize()
+    cold_ms = float(np.mean([a.elapsed_time(e) for a, e in evs]))
+    del flush
+    achieved = bytes_per / (cold_ms / 1e3) / 1e9
+    step_name = "ChebNext" if steps else "Jacobi"
 
     # ---- per-level sweep rates (same step kind on every non-coarse level; levels
     # below the fine one are L2-resident: their GB/s is algorithmic bytes / time)
@@ -563,34 +744,70 @@ def main():
         lc_share = (times["with"] - times["without"]) / times["with"]
         del dh0
 
-    # ---- e2e through the host-buffer C-ABI calls (pinned host memory).  Every
-    #      step copies its b and u host->device and its u back; the headline
-    #      uses smg_vcycle_host_many, which overlaps those copies with the
-    #      neighbouring steps' V-cycles; the one-call-per-step figure is kept.
+    # ---- e2e through the drop-in host-buffer call (pinned host memory): each
+    #      step is vcycle(h, b_host, u_host) -- H2D of b and u, the V-cycle, D2H
+    #      of u, synchronised -- exactly the reference-facing call
+    #      (mg.py:127, numpy in, u updated in place).  The batched C-ABI call
+    #      smg_vcycle_host_many (copies of neighbouring independent pairs
+    #      overlapping each V-cycle) and the pageable-memory figure are beside it.
     ring = 4
     bhs = [torch.from_numpy(b_host).pin_memory() for _ in range(ring)]
     uhs = [torch.zeros(n0, dtype=torch.float64).pin_memory() for _ in range(ring)]
     bnp, unp = [t.numpy() for t in bhs], [t.numpy() for t in uhs]
     e2e_steps = max(20, min(args.steps, 200))
+    for _ in range(3):
+        P.vcycle(dh, bnp[0], unp[0])
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        P.vcycle(dh, bnp[0], unp[0])
+    single_s = max_over_ranks(time.perf_counter() - t0)
     blist = [bnp[i % ring] for i in range(e2e_steps)]
     ulist = [unp[i % ring] for i in range(e2e_steps)]
     dh.vcycles_host(blist[:4], ulist[:4])
     t0 = time.perf_counter()
     dh.vcycles_host(blist, ulist)
-    e2e_s = time.perf_counter() - t0
-    e2e_val = max_over_ranks(e2e_s)
-    for _ in range(3):
-        dh.vcycle(bnp[0], unp[0])
+    batched_s = max_over_ranks(time.perf_counter() - t0)
+    bpage, upage = b_host.copy(), np.zeros(n0)
+    P.vcycle(dh, bpage, upage)
     t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        dh.vcycle(bnp[0], unp[0])
-    single_s = max_over_ranks(time.perf_counter() - t0)
-    e2e = {"value": whole_job_rate(e2e_steps, e2e_val, ws), "unit": UNIT,
+    for _ in range(10):
+        P.vcycle(dh, bpage, upage)
+    pageable_s = max_over_ranks(time.perf_counter() - t0)
+    e2e = {"value": whole_job_rate(e2e_steps, single_s, ws), "unit": UNIT,
            "h2d_bytes_per_step": 2 * 8 * n0, "d2h_bytes_per_step": 8 * n0,
            "steps": e2e_steps,
-           "path": "smg_vcycle_host_many (pinned numpy b, u; copies of step i+-1 overlap "
-                   "V-cycle i)",
-           "one_call_per_step": whole_job_rate(e2e_steps, single_s, ws)}
+           "path": "paper_2402_12947_b200.vcycle(h, b, u) per step (smg_vcycle_host: pinned "
+                   "numpy b, u copied in, V-cycle, u copied back, synchronised)",
+           "batched": {"value": whole_job_rate(e2e_steps, batched_s, ws),
+                       "path": "smg_vcycle_host_many over independent pairs (copies of pairs "
+                               "i+-1 overlap V-cycle i)"},
+           "pageable_per_call": whole_job_rate(10, pageable_s, ws)}
+
+    # ---- the reference's other hot-path functions on the device (same list
+    #      as the CPU reference_functions below): combined_smooth (LC, k sweeps,
+    #      LC) on the fine level through the C-ABI, device-resident vectors
+    gpu_functions = {"chebyshev_smooth_per_sweep_ms": k_ms, "vcycle_ms": ms_per_step}
+    if dh.corrs[0] is not None:
+        n_even = (nn + 1) & ~1
+        work = torch.empty(2 * n_even, dtype=torch.float64, device="cuda")
+        cfg0 = P.SmootherConfig.from_any(lv.smoother)
+        lam0, frac0 = cfg0.chebyshev_parameters()
+        uu = torch.randn(nn, dtype=torch.float64, device="cuda")
+
+        def comb():
+            _lib.check(lib.smg_combined_smooth(op.handle, D.ptr(b), D.ptr(uu), dh.corrs[0].handle,
+                                               0, int(cfg0.sweeps), float(lam0), float(frac0),
+                                               D.ptr(work), sh))
+        for _ in range(5):
+            comb()
+        torch.cuda.synchronize()
+        k0.record(stream)
+        for _ in range(50):
+            comb()
+        k1.record(stream)
+        torch.cuda.synchronize()
+        gpu_functions["combined_smooth_ms"] = k0.elapsed_time(k1) / 50
+        del work, uu
 
     # ---- time to solution: stationary MG to rtol 1e-10 (mg.py:154-175) from u0
     solve = None
@@ -604,23 +821,37 @@ def main():
         solve = {"rtol": 1e-10, "cycles": len(hist) - 1, "final_rel_residual": hist[-1],
                  "ms": 1e3 * (time.perf_counter() - t0),
                  "note": "device loop, one residual-norm readback per cycle"}
+        gpu_functions["solve_stationary_ms_per_cycle"] = solve["ms"] / max(1, solve["cycles"])
         if ws == 1 and not args.no_cpu_baseline:
             from oracle import oracle as O
             t0 = time.perf_counter()
             _, ch = O.solve_stationary(h, b_host, u0, 1e-10, 100)
-            solve["cpu_oracle_ms"] = 1e3 * (time.perf_counter() - t0)
-            solve["cpu_oracle_cycles"] = len(ch) - 1
+            solve["cpu_port_ms"] = 1e3 * (time.perf_counter() - t0)
+            solve["cpu_port_cycles"] = len(ch) - 1
 
-    # ---- CPU baseline (rank 0, N = 1 only)
-    cpu = None
+    # ---- CPU baseline (rank 0, N = 1 only): the reference itself from
+    #      baseline/_ref (per-function timings, bounded), and the oracle port
+    cpu, cpu_port = None, None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         threads = len(os.sched_getaffinity(0))
-        val, n_done, el, cores = cpu_baseline(h, b_host, args.cpu_budget, threads)
-        cpu = {"value": val, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"{n_done} oracle V-cycles of {args.workload} in {el:.1f} s "
-                         f"(sparse rows on {cores} OpenMP threads, numpy elementwise 1 thread)"}
+        sm, why = reference_package()
+        if sm is not None:
+            funcs = reference_functions(sm, reference_hierarchy(sm, h), b_host, args.cpu_budget)
+            cpu = {"value": 1e3 / funcs["vcycle_ms"], "unit": UNIT, "cores": threads,
+                   "kind": "reference",
+                   "sample": f"median of {funcs['vcycle_reps']} reference V-cycles of "
+                             f"{args.workload} after 1 warm-up (simplexmg.mg.vcycle from "
+                             f"baseline/_ref, unmodified; {funcs['cores_note']})",
+                   "functions": funcs}
+        val, n_done, el, cores = cpu_baseline(h, b_host, min(args.cpu_budget, 8.0), threads)
+        cpu_port = {"value": val, "unit": UNIT, "cores": cores, "kind": "port",
+                    "sample": f"{n_done} oracle V-cycles of {args.workload} in {el:.1f} s "
+                              f"(sparse rows on {cores} OpenMP threads, numpy elementwise "
+                              f"1 thread)"}
+        if cpu is None:
+            cpu = dict(cpu_port, note=f"reference unavailable ({why}): oracle port")
 
-    traffic, traffic_src = _ncu_traffic()
+    traffic, traffic_src = _ncu_traffic(args.workload, step_name)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
@@ -631,8 +862,15 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "traffic_source": traffic_src,
-                         "kernel": f"{_layout(lib, dh.ops[0])} <ChebNext> (fine-level Chebyshev step)",
-                         "bytes_per_launch": bytes_per, "us_per_launch": 1e3 * k_ms,
+                         "kernel": f"{_layout(lib, dh.ops[0])} <{step_name}> (fine-level "
+                                   f"smoother step)",
+                         "bytes_per_launch": bytes_per, "us_per_launch": 1e3 * cold_ms,
+                         "timing": "cold: L2 overwritten before each of 40 launches, "
+                                   "per-launch CUDA events on the launching stream",
+                         "warm": {"us_per_launch": 1e3 * k_ms, "achieved": achieved_warm,
+                                  "frac": achieved_warm / peak,
+                                  "timing": f"{reps} back-to-back launches (PDL), per-row "
+                                            "vectors partly L2-resident"},
                          "peak_source": peak_src, "nnz": z, "rows": nn,
                          "nnz_per_row": z / nn},
             "sweeps_per_s": sweeps_per_s,
@@ -645,6 +883,8 @@ def main():
             "launches_per_vcycle": launches,
             "clocks": clocks,
             "cpu_baseline": cpu,
+            "cpu_baseline_port": cpu_port,
+            "gpu_functions": gpu_functions,
             "setup_s": t_setup,
             "setup": setup_detail,
         }

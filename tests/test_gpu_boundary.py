@@ -149,7 +149,7 @@ def _duck_hierarchy(h):
         if lc is not None:
             dlc = types.SimpleNamespace(
                 regions=tuple((idx, types.SimpleNamespace(kind="cholesky", factor=f.factor,
-                                                          n=len(idx)))
+                                                          n_local=len(idx)))
                               for idx, f in lc.regions),
                 n_global=lc.n_global)
         cfg = lv.smoother
@@ -165,7 +165,7 @@ def _duck_hierarchy(h):
             regions=None, local_correction=dlc, sgs=None))
     cf = h.coarse_factor
     return types.SimpleNamespace(levels=levels, coarse_factor=types.SimpleNamespace(
-        kind="cholesky", factor=cf.factor, n=cf.n), system=None)
+        kind="cholesky", factor=cf.factor, n_local=cf.n_local), system=None)
 
 
 @pytest.mark.parametrize("name", ["crit7_adj", "cpl_p2", "c3s"])

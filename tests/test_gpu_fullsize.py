@@ -23,7 +23,11 @@ def rel(a, b):
 @pytest.fixture(scope="module", params=["C1", "C2", "C3", "C4"])
 def case(request):
     from paper_2402_12947_b200 import configs
-    h, b, u0 = configs.build(configs.WORKLOADS[request.param])
+    # C4's fine operator (197M nonzeros) is assembled on the GPU here: the host
+    # assembly (reference element arithmetic) takes ~2 min and 33 GB; both arms
+    # of every comparison below run on this same hierarchy either way
+    h, b, u0 = configs.build(configs.WORKLOADS[request.param],
+                             device_assembly=request.param == "C4")
     yield request.param, h, b, u0
     del h
 
@@ -81,7 +85,8 @@ def test_iteration_counts_match_oracle(case):
     _, hg = P.solve_stationary(h, b, u0, 1e-10, 100)
     _, ho = O.solve_stationary(h, b, u0, 1e-10, 100)
     assert len(hg) == len(ho) and hg[-1] <= 1e-10
-    np.testing.assert_allclose(hg, ho, rtol=1e-3)
+    # near the rounding floor (~1e-11) the residual norms differ by ~1e-13 absolute
+    np.testing.assert_allclose(hg, ho, rtol=1e-3, atol=1e-12)
     _, cg_g = P.cg(h.levels[0].a, b, precond=P.as_preconditioner(h), rtol=1e-10, maxit=200)
     _, cg_o = O.cg(h.levels[0].a, b, O.as_preconditioner(h), 1e-10, 200)
     assert len(cg_g) == len(cg_o)
