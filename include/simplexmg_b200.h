@@ -176,6 +176,20 @@ SMG_API int smg_correction_create(const smg_operator *a, int64_t n_regions,
 SMG_API int smg_correction_destroy(smg_correction *c);
 SMG_API int smg_correction_info(const smg_correction *c, int64_t *n_regions, int64_t *covered_dofs,
                         int *coupled, int64_t *device_bytes);
+/* ---- setup: stiffness from element matrices, scipy's exact order
+ * (fem.py:339-375 assemble: coo_matrix((local, (rows, cols))).tocsr(), then the
+ * symmetric Dirichlet elimination).  local: n_cells x nloc x nloc element
+ * matrices (the reference's arithmetic, computed by the caller), cell_dofs:
+ * n_cells x nloc.  Duplicates are summed in the order scipy's coo->csr uses
+ * (entries bucketed by row in input order, then libstdc++ std::sort of every
+ * row's (column, value) pairs unless all rows are already sorted, then runs
+ * added sequentially), so *out is the reference's matrix bit for bit:
+ * canonical CSR, rows/columns of the sorted dirichlet_dofs removed and a unit
+ * diagonal in their place.                                                     */
+SMG_API int smg_assemble_elements(int64_t n_dofs, int64_t n_cells, int nloc,
+                                  const int64_t *cell_dofs, const double *local,
+                                  const int64_t *dirichlet_dofs, int64_t n_dirichlet,
+                                  smg_csr **out, void *stream);
 /* ---- setup: Poisson stiffness assembly (fem.py:303-377 assemble, scalar
  * P1/P2, homogeneous Dirichlet on the listed DOFs) ---------------------------
  * Host inputs: vertices (n_vertices x dim), cells (n_cells x (dim+1), positively
@@ -224,7 +238,9 @@ SMG_API int smg_apply_local_correction(const smg_correction *c, const double *r,
                                void *stream);
 /* u += S_c (b - A u)            (smoothers.py:263 / :266)                          */
 SMG_API int smg_local_correct(const smg_correction *c, const double *b, double *u, void *stream);
-/* sandwich smoother             (smoothers.py:252-267); c may be NULL             */
+/* sandwich smoother             (smoothers.py:252-267); c may be NULL.  c must
+ * have been created for this operator a (its patch residuals read a's rows):
+ * another operator is SMG_ERR_DIMENSION.                                          */
 SMG_API int smg_combined_smooth(const smg_operator *a, const double *b, double *u,
                         const smg_correction *c, int kind, int sweeps, double lambda_max,
                         double lambda_min_fraction, double *work, void *stream);
@@ -275,7 +291,13 @@ SMG_API int smg_hierarchy_set_option(smg_hierarchy *h, int option, int value);
 /* kernels one V-cycle launches (for launch accounting) */
 SMG_API int smg_hierarchy_launches_per_vcycle(const smg_hierarchy *h, int64_t *launches);
 
-/* u <- one V-cycle on u (mg.py:127-151; in place)                                 */
+/* u <- one V-cycle on u (mg.py:127-151; in place).
+ * Thread safety ("concurrent vcycle calls on distinct arrays over
+ * one shared Hierarchy are safe"): every call below that runs the hierarchy
+ * (smg_vcycle*, smg_solve_stationary, smg_cg with a preconditioner, option
+ * setters) holds a per-hierarchy mutex while it enqueues, and orders its
+ * device work after the previous call's through an event, whatever stream
+ * the callers use; results equal the sequential calls.                          */
 SMG_API int smg_vcycle(smg_hierarchy *h, const double *b, double *u, void *stream);
 /* same with HOST b/u: H2D copies, V-cycle, D2H of u (the e2e path)                */
 SMG_API int smg_vcycle_host(smg_hierarchy *h, const double *b_host, double *u_host, void *stream);
@@ -292,7 +314,8 @@ SMG_API int smg_solve_stationary(smg_hierarchy *h, const double *b, double *u, d
 /* MG-preconditioned CG (sparse.py:168-211 with mg.py:178-184 as precond).
  * h == NULL: unpreconditioned.  x holds x0 on entry when x0_given != 0, else
  * it is zeroed.  history: capacity maxit + 1.  On SMG_ERR_INDEFINITE,
- * *bad_iteration / *bad_curvature describe the failure. */
+ * *bad_iteration / *bad_curvature describe the failure.  A preconditioner
+ * whose fine level is not a's size is SMG_ERR_DIMENSION (nothing launched). */
 SMG_API int smg_cg(smg_hierarchy *h, const smg_operator *a, const double *b, double *x, int x0_given,
            double rtol, int maxit, double *history, int *n_history, int64_t *bad_iteration,
            double *bad_curvature, void *stream);

@@ -80,6 +80,8 @@ PROTOTYPES = {
     "smg_assemble_poisson": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _i64, _f64p, _i64, _i64p,
                                             _i64p, _i64, _i64p, _i64, _f64p, _f64p, ctypes.c_int,
                                             _pp, _i64p, _vp]),
+    "smg_assemble_elements": (ctypes.c_int, [_i64, _i64, ctypes.c_int, _i64p, _f64p, _i64p, _i64,
+                                             _pp, _vp]),
     "smg_patch_factor": (ctypes.c_int, [_vp, _i64, _i64p, _i64p, _f64p, _i64p, _i64p, _vp]),
     "smg_prolongation_build": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _i64, _f64p, _i64, _f64p,
                                               _f64p, _i64p, _i64, ctypes.c_int, _f64p, _f64p,

@@ -198,11 +198,11 @@ def problem_spec(wl: Workload):
 
 
 def build(wl: Workload, use_local_correction: bool = True, coarse_refine: bool = False,
-          device_setup=None, device_assembly: bool = False):
+          device_setup=None, device_assembly=None):
     """Host hierarchy + (b, u0) for a workload.  Returns (hierarchy, b, u0).
     ``device_setup``: see mg.build_hierarchy (None = GPU setup when a device
-    exists; False = the host path).  Either way the fine operator is the
-    reference's construction bit for bit unless ``device_assembly``."""
+    exists; False = the host path).  Either way the hierarchy is the
+    reference's construction bit for bit unless ``device_assembly="kernel"``."""
     from .mg import build_hierarchy
     meshes = build_meshes(wl)
     h = build_hierarchy(meshes, problem_spec(wl), wl.smoother, use_local_correction, 0.1,

@@ -1445,6 +1445,38 @@ int smg_assemble_poisson(int dim, int degree, int64_t n_vertices, const double* 
   return SMG_OK;
 }
 
+int smg_assemble_elements(int64_t n_dofs, int64_t n_cells, int nloc, const int64_t* cell_dofs,
+                          const double* local, const int64_t* dirichlet_dofs, int64_t n_dirichlet,
+                          smg_csr** out, void* stream)
+{
+  if (!out) return fail("out is NULL");
+  *out = nullptr;
+  if (n_dofs <= 0 || n_cells < 0 || nloc <= 0 || n_dirichlet < 0)
+    return fail("empty space or negative sizes");
+  if (n_dofs >= INT32_MAX) return fail("too many DOFs");
+  if (n_cells * (int64_t)nloc * nloc >= (int64_t)UINT32_MAX)
+    return fail("too many element entries for one call");
+  if ((n_cells > 0 && (!cell_dofs || !local)) || (n_dirichlet > 0 && !dirichlet_dofs))
+    return fail("NULL input array");
+  for (int64_t k = 0; k < n_cells * nloc; ++k)
+    if (cell_dofs[k] < 0 || cell_dofs[k] >= n_dofs) return fail("cell dof out of range");
+  std::vector<uint8_t> mask;
+  if (n_dirichlet > 0) {
+    mask.assign((size_t)n_dofs, 0);
+    for (int64_t k = 0; k < n_dirichlet; ++k) {
+      const int64_t d = dirichlet_dofs[k];
+      if (d < 0 || d >= n_dofs) return fail("Dirichlet dof out of range");
+      if (k > 0 && d <= dirichlet_dofs[k - 1]) return fail("Dirichlet dofs must be sorted and unique");
+      mask[(size_t)d] = 1;
+    }
+  }
+  auto c = std::make_unique<smg_csr>();
+  SMG_TRY(assemble_elements_device(n_dofs, n_cells, nloc, cell_dofs, local,
+                                   mask.empty() ? nullptr : mask.data(), &c->m, as_stream(stream)));
+  *out = c.release();
+  return SMG_OK;
+}
+
 static int dense_roundtrip(int64_t n, const double* in, double* out, bool invert, int64_t* info,
                            void* stream)
 {

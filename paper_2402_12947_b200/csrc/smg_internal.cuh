@@ -307,6 +307,13 @@ int assemble_poisson_device(int dim, int degree, int64_t n_vertices, const doubl
                             const int64_t* dir_dofs, const double* gref, const double* wq, int nq,
                             DevCsrOwned* out, int64_t* bad_cell_out, cudaStream_t s);
 
+// element matrices (host, the reference's arithmetic) -> canonical CSR with
+// scipy's duplicate order and the Dirichlet elimination (coo_kernels.cu;
+// fem.py:339-375).  dirichlet_mask: host, n_dofs bytes, or nullptr.
+int assemble_elements_device(int64_t n_dofs, int64_t n_cells, int nloc, const int64_t* cell_dofs,
+                             const double* local, const uint8_t* dirichlet_mask, DevCsrOwned* out,
+                             cudaStream_t s);
+
 // dense / reduction kernels (dense_kernels.cu)
 cudaError_t launch_dot(int64_t n, const double* a, const double* b, double* partials,
                        unsigned int* counter, double* result, cudaStream_t s);

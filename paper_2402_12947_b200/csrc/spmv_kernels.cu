@@ -41,6 +41,7 @@
 // recorded in DESIGN.md section 3 with their measurements.
 #include "smg_internal.cuh"
 
+#include <algorithm>
 #include <cstdlib>
 
 namespace smg {
@@ -248,7 +249,8 @@ constexpr int kSellPre = 4;   // entries loaded before the dependency wait
 // waits on the gathers (software pipelining; SMG_SELL_PIPE)
 template <Epi E, bool kPf, int kUnroll, bool kPipe = false>
 __global__ void __launch_bounds__(kSellWindow, kPipe ? 4 : (kUnroll <= 4 ? 8 : (kUnroll <= 8 ? 4 : 2)))
-sell_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, int pf_dist)
+sell_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, int pf_dist,
+            int xpf_chunk)
 {
   using T = EpiTraits<E>;
   const int w = blockIdx.x;
@@ -292,6 +294,18 @@ sell_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, int 
   }
   pdl_wait();
   pdl_trigger();
+  // SMG_X_PREFETCH: the first CTAs pull the gathered vector x (produced by the
+  // previous kernel, so only after the dependency wait) into L2 in
+  // xpf_chunk-byte pieces -- a cold x would otherwise be gathered from HBM
+  // with a dependent round trip per entry
+  if (xpf_chunk > 0 && threadIdx.x == 32) {
+    const int64_t xb = m.ncols * 8;
+    const int64_t off = (int64_t)w * xpf_chunk;
+    if (off < xb) {
+      const int64_t len = min((int64_t)xpf_chunk, xb - off) & ~int64_t(15);
+      if (len > 0) prefetch_l2(reinterpret_cast<const char*>(x) + off, (uint32_t)len, false);
+    }
+  }
   const int32_t grow = w * kSellWindow + rl;
   const bool has_row = rl >= 0;
   const bool write = has_row && !(ea.skip_rows && ea.skip_rows[grow]);
@@ -540,10 +554,20 @@ static cudaError_t launch_t_sell(const DevCsr& m, const double* x, const EpiArgs
   if (m.sell) {
     cfg.gridDim = dim3((unsigned)m.sell_nwin);
     cfg.blockDim = dim3(kSellWindow);
+    // SMG_X_PREFETCH (0 = off, 1 = on): x in chunks over the first resident wave
+    static const int xpf_env = [] {
+      const char* v = getenv("SMG_X_PREFETCH");
+      return v ? atoi(v) : 0;
+    }();
+    int xpf = 0;
+    if (xpf_env && ((uintptr_t)x & 15) == 0) {
+      const int64_t ctas = std::min<int64_t>(m.sell_nwin, (int64_t)g_sm_count * 4);
+      xpf = (int)(((m.ncols * 8 + ctas - 1) / ctas + 15) & ~int64_t(15));
+    }
     if (m.sell_unroll >= 16) {
       const int sdist = g_sm_count * 2 * waves;
-      return pf ? cudaLaunchKernelEx(&cfg, sell_kernel<E, true, 16>, m, x, ea, sdist)
-                : cudaLaunchKernelEx(&cfg, sell_kernel<E, false, 16>, m, x, ea, sdist);
+      return pf ? cudaLaunchKernelEx(&cfg, sell_kernel<E, true, 16>, m, x, ea, sdist, xpf)
+                : cudaLaunchKernelEx(&cfg, sell_kernel<E, false, 16>, m, x, ea, sdist, xpf);
     }
     if (m.sell_unroll >= 8) {
       const int sdist = g_sm_count * 4 * waves;
@@ -555,17 +579,17 @@ static cudaError_t launch_t_sell(const DevCsr& m, const double* x, const EpiArgs
       }();
       const int pipe = pipe_env >= 0 ? pipe_env : m.sell_pipe;
       if (pipe >= 6)
-        return pf ? cudaLaunchKernelEx(&cfg, sell_kernel<E, true, 6, true>, m, x, ea, sdist)
-                  : cudaLaunchKernelEx(&cfg, sell_kernel<E, false, 6, true>, m, x, ea, sdist);
+        return pf ? cudaLaunchKernelEx(&cfg, sell_kernel<E, true, 6, true>, m, x, ea, sdist, xpf)
+                  : cudaLaunchKernelEx(&cfg, sell_kernel<E, false, 6, true>, m, x, ea, sdist, xpf);
       if (pipe > 0)
-        return pf ? cudaLaunchKernelEx(&cfg, sell_kernel<E, true, 4, true>, m, x, ea, sdist)
-                  : cudaLaunchKernelEx(&cfg, sell_kernel<E, false, 4, true>, m, x, ea, sdist);
-      return pf ? cudaLaunchKernelEx(&cfg, sell_kernel<E, true, 8>, m, x, ea, sdist)
-                : cudaLaunchKernelEx(&cfg, sell_kernel<E, false, 8>, m, x, ea, sdist);
+        return pf ? cudaLaunchKernelEx(&cfg, sell_kernel<E, true, 4, true>, m, x, ea, sdist, xpf)
+                  : cudaLaunchKernelEx(&cfg, sell_kernel<E, false, 4, true>, m, x, ea, sdist, xpf);
+      return pf ? cudaLaunchKernelEx(&cfg, sell_kernel<E, true, 8>, m, x, ea, sdist, xpf)
+                : cudaLaunchKernelEx(&cfg, sell_kernel<E, false, 8>, m, x, ea, sdist, xpf);
     }
     const int sdist = g_sm_count * 8 * waves;
-    return pf ? cudaLaunchKernelEx(&cfg, sell_kernel<E, true, 4>, m, x, ea, sdist)
-              : cudaLaunchKernelEx(&cfg, sell_kernel<E, false, 4>, m, x, ea, sdist);
+    return pf ? cudaLaunchKernelEx(&cfg, sell_kernel<E, true, 4>, m, x, ea, sdist, xpf)
+              : cudaLaunchKernelEx(&cfg, sell_kernel<E, false, 4>, m, x, ea, sdist, xpf);
   }
   if (m.fixed) {
     if (m.multichunk)

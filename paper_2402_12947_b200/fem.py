@@ -222,25 +222,72 @@ def _cell_geometry(mesh: SimplexMesh):
     return v[:, 0, :], jac, det, np.linalg.inv(jac)
 
 
+def _element_matrices(mesh: SimplexMesh, degree: int, grads_ref, wts):
+    """The reference's element stiffness matrices, with its own arithmetic
+    (fem.py:312-322: LAPACK det / inv via numpy, then two einsums)."""
+    v0, jac, det, inv_jac = _cell_geometry(mesh)
+    grads = np.einsum("qie,med->mqid", grads_ref, inv_jac)
+    local = np.einsum("q,m,mqid,mqjd->mij", wts, det, grads, grads)
+    return local, (v0, jac, det)
+
+
+def _assemble_elements_device(mesh, dofmap, source, dirichlet_all, grads_ref, wts):
+    """Element matrices on the host (the reference's arithmetic), then the
+    COO -> CSR summation in scipy's exact duplicate order and the Dirichlet
+    elimination on the GPU (``smg_assemble_elements``): bit-identical to the
+    host path."""
+    import ctypes
+    from . import _lib
+    from . import device as _dev
+    _dev.require_cuda()
+    lib = _lib.load()
+    i64p = ctypes.POINTER(ctypes.c_int64)
+    f64p = ctypes.POINTER(ctypes.c_double)
+    local, (v0, jac, det) = _element_matrices(mesh, dofmap.element_degree, grads_ref, wts)
+    local = np.ascontiguousarray(local, dtype=np.float64)
+    cdofs = np.ascontiguousarray(dofmap.cell_dofs, dtype=np.int64)
+    dir_dofs = dofmap.boundary_dofs() if dirichlet_all else np.empty(0, dtype=np.int64)
+    dd = np.ascontiguousarray(dir_dofs, dtype=np.int64)
+    out = ctypes.c_void_p()
+    _lib.check(lib.smg_assemble_elements(int(dofmap.n_dofs), len(cdofs), int(cdofs.shape[1]),
+                                         cdofs.ctypes.data_as(i64p), local.ctypes.data_as(f64p),
+                                         dd.ctypes.data_as(i64p), len(dd), ctypes.byref(out),
+                                         _dev.stream_handle()))
+    nr, nc, ptr, col, val = _dev._csr_result_to_host(lib, out)
+    a = CsrMatrix(nr, nc, ptr, col, val)
+    b = np.zeros(dofmap.n_dofs)
+    if source is not None:
+        b = _load_vector(mesh, dofmap, source, v0, jac, det)
+    if len(dir_dofs):
+        # homogeneous data: the reference's b -= A u_bc (u_bc = 0) leaves b as
+        # it is up to the sign of zeros, which -= 0.0 keeps (fem.py:362-366)
+        b -= 0.0
+        b[dir_dofs] = 0.0
+    return AssembledSystem(a, b, dir_dofs)
+
+
 def assemble_poisson(mesh: SimplexMesh, dofmap: DofMap,
                      source: Optional[Callable[[np.ndarray], np.ndarray]] = None,
-                     dirichlet_all: bool = True, device: bool = False) -> AssembledSystem:
+                     dirichlet_all: bool = True, device=False) -> AssembledSystem:
     """Stiffness + load with homogeneous Dirichlet on every box face
     (fem.py:303-377).  ``source`` is vectorised: (m, dim) points -> (m,).
 
-    ``device=True``: the stiffness matrix (element matrices, duplicate sums,
-    Dirichlet elimination) is assembled on the GPU (``smg_assemble_poisson``;
-    values agree with the host/reference to rounding, identical pattern); the
-    load vector stays on the host."""
+    ``device``: False = all on the host (numpy / scipy, the reference's own
+    calls); True = element matrices on the host with the reference's
+    arithmetic, the duplicate summation (scipy's order) and the Dirichlet
+    elimination on the GPU (``smg_assemble_elements``) -- both bit-identical
+    to the reference; ``"kernel"`` = element matrices too on the GPU
+    (``smg_assemble_poisson``: cofactor geometry, values within ~1e-13, same
+    pattern)."""
     dim = mesh.dim
     degree = dofmap.element_degree
     pts, wts = quadrature(dim, 1 if degree == 1 else 2)
     grads_ref = np.asarray([reference_gradients(degree, dim, p) for p in pts])
-    if device:
+    if device == "kernel":
         return _assemble_poisson_device(mesh, dofmap, source, dirichlet_all, grads_ref, wts)
-    v0, jac, det, inv_jac = _cell_geometry(mesh)
-    grads = np.einsum("qie,med->mqid", grads_ref, inv_jac)
-    local = np.einsum("q,m,mqid,mqjd->mij", wts, det, grads, grads)
+    if device:
+        return _assemble_elements_device(mesh, dofmap, source, dirichlet_all, grads_ref, wts)
+    local, (v0, jac, det) = _element_matrices(mesh, degree, grads_ref, wts)
 
     cell_dofs = dofmap.cell_dofs
     rows = np.repeat(cell_dofs, cell_dofs.shape[1], axis=1).ravel()

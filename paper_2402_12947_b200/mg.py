@@ -395,7 +395,7 @@ def build_hierarchy(meshes: Sequence, problem, smoother: SmootherConfig,
                     element_degree: int = 1, *, region_layers: int = 1,
                     lambda_tol: float = 1e-8, coarse_refine: bool = False,
                     device_setup: Optional[bool] = None,
-                    device_assembly: bool = False) -> Hierarchy:
+                    device_assembly=None) -> Hierarchy:
     """``build_hierarchy(meshes, problem, smoother, use_local_correction,
     quality_threshold=0.1, element_degree=1)`` as the reference (mg.py:72-124);
     meshes fine to coarse (reference ``SimplexMesh`` objects are accepted),
@@ -405,12 +405,15 @@ def build_hierarchy(meshes: Sequence, problem, smoother: SmootherConfig,
     ``device_setup``: prolongations (point location, ``smg_prolongation_build``),
     Galerkin products (``smg_galerkin``), patch Cholesky factors, the coarse
     factor and Lanczos on levels >= 200k rows run on the GPU (default:
-    whenever a CUDA device exists).  The fine operator is assembled on the
-    host by default -- the reference's own element arithmetic (numpy einsum /
-    LAPACK det and inv) and scipy's duplicate summation, so A_0 and therefore
-    every Galerkin level are bit-identical to the reference's construction;
-    ``device_assembly=True`` assembles on the GPU instead (same pattern,
-    values within ~1e-13, so exact-zero Galerkin sums can differ).
+    whenever a CUDA device exists).  The fine operator's element matrices
+    are always formed on the host with the reference's own arithmetic (numpy
+    einsum / LAPACK det and inv); with device setup the duplicate summation
+    (in scipy's exact order) and the Dirichlet elimination run on the GPU
+    (``smg_assemble_elements``), so A_0 and therefore every Galerkin level
+    are bit-identical to the reference's construction either way.
+    ``device_assembly="kernel"`` forms the element matrices on the GPU too
+    (``smg_assemble_poisson``: same pattern, values within ~1e-13, so
+    exact-zero Galerkin sums can differ -- a setup-time shortcut only).
     Host-only setup (no GPU, e.g. the CPU test suite) uses the reference's
     own scipy products."""
     if isinstance(problem, SmootherConfig) or hasattr(problem, "sweeps"):
@@ -439,8 +442,10 @@ def build_hierarchy(meshes: Sequence, problem, smoother: SmootherConfig,
     dofmaps = [build_dofmap(m, element_degree) for m in meshes]
     times["dofmap_s"] += time.perf_counter() - t
     t = time.perf_counter()
+    if device_assembly is None:
+        device_assembly = bool(device_setup)
     system = assemble_poisson(meshes[0], dofmaps[0], source,
-                              device=bool(device_setup and device_assembly))
+                              device=device_assembly if device_setup else False)
     times["assembly_s"] += time.perf_counter() - t
     operators = [system.a]
     prolongations = []
@@ -479,5 +484,5 @@ def build_hierarchy(meshes: Sequence, problem, smoother: SmootherConfig,
     times["coarse_factor_s"] += time.perf_counter() - t
     h = Hierarchy(levels, coarse, system, coarse_refine)
     h.setup_times = dict(times, galerkin_device=bool(device_setup),
-                         assembly_device=bool(device_setup and device_assembly))
+                         assembly_device=str(device_assembly) if device_setup else "host")
     return h

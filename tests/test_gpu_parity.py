@@ -215,7 +215,12 @@ def test_lc_follow_is_bitwise(P, fx, graphs, monkeypatch):
         res.append(u.cpu().numpy())
         launches.append(dh.launches_per_vcycle())
     assert np.array_equal(res[0], res[1])
-    assert launches[0] == launches[1]
+    # a followed correction is one kernel; a coupled correction's plain path is
+    # two (residual-only pass, then the solves)
+    if fixtures.MULTI_REGION_FIXTURES.get(name):
+        assert launches[0] < launches[1]
+    else:
+        assert launches[0] == launches[1]
     ref = z["g/u_rand"].copy()
     for _ in range(3):
         ref = O.vcycle(h, z["g/b"], ref)

@@ -243,8 +243,18 @@ def _close_csr(a, r, tol=1e-13):
     assert np.max(np.abs(a.values - r.values)) <= tol * scale
 
 
+def _same_csr(a, r):
+    assert a.shape == r.shape
+    assert np.array_equal(a.row_offsets, r.row_offsets)
+    assert np.array_equal(a.col_indices, r.col_indices)
+    assert np.array_equal(a.values, r.values)
+
+
 @pytest.mark.parametrize("name,wl,scale", CASES)
 def test_assembly_vs_reference_operator(name, wl, scale):
+    """device=True (element matrices with the reference's arithmetic, then
+    scipy-order duplicate sums + Dirichlet elimination on the GPU) is the
+    reference's operator bit for bit; the all-GPU kernel path to 1e-13."""
     from paper_2402_12947_b200 import configs
     from paper_2402_12947_b200.fem import assemble_poisson, build_dofmap
     from tests.golden import fixtures
@@ -255,9 +265,12 @@ def test_assembly_vs_reference_operator(name, wl, scale):
     source = (lambda x: np.ones(len(x))) if w.rhs == "source-one" else None
     sys_d = assemble_poisson(m, dm, source, device=True)
     sys_h = assemble_poisson(m, dm, source, device=False)
-    _close_csr(sys_d.a, ref.levels[0].a)
-    _close_csr(sys_d.a, sys_h.a)
+    sys_k = assemble_poisson(m, dm, source, device="kernel")
+    _same_csr(sys_d.a, ref.levels[0].a)
+    _same_csr(sys_h.a, ref.levels[0].a)
+    _close_csr(sys_k.a, ref.levels[0].a)
     assert np.array_equal(sys_d.b, sys_h.b)
+    assert np.array_equal(sys_k.b, sys_h.b)
     assert np.array_equal(sys_d.dirichlet_dofs, sys_h.dirichlet_dofs)
 
 
@@ -268,11 +281,54 @@ def test_assembly_all_elements_jittered(dim, degree, n):
     from paper_2402_12947_b200.mesh import generate_simplex_grid
     m = configs.jitter(generate_simplex_grid(dim, n), 0.15, np.random.default_rng(dim * 10 + degree))
     dm = build_dofmap(m, degree)
-    _close_csr(assemble_poisson(m, dm, device=True).a, assemble_poisson(m, dm, device=False).a)
+    host = assemble_poisson(m, dm, device=False).a
+    _same_csr(assemble_poisson(m, dm, device=True).a, host)
+    _close_csr(assemble_poisson(m, dm, device="kernel").a, host)
     # no Dirichlet elimination: the plain stiffness (rows sum to zero)
     a = assemble_poisson(m, dm, dirichlet_all=False, device=True).a
-    _close_csr(a, assemble_poisson(m, dm, dirichlet_all=False, device=False).a)
+    _same_csr(a, assemble_poisson(m, dm, dirichlet_all=False, device=False).a)
     assert np.max(np.abs(a.to_scipy() @ np.ones(a.ncols))) <= 1e-12 * np.max(np.abs(a.values))
+
+
+@pytest.mark.parametrize("seed,n_dofs,n_cells,nloc,ncol", [
+    (0, 7, 200, 6, 7), (1, 40, 500, 10, 40), (2, 3, 400, 4, 3), (3, 1, 50, 8, 1),
+    (4, 300, 2000, 6, 300), (5, 25, 3000, 10, 5)])
+def test_scipy_order_duplicate_sums(seed, n_dofs, n_cells, nloc, ncol):
+    """smg_assemble_elements on adversarial element data -- rows of up to
+    thousands of duplicates of a handful of columns, values spanning 16
+    decades so every summation order rounds differently -- equals scipy's
+    coo_matrix(...).tocsr() (+ the Dirichlet elimination) bit for bit: the
+    device reproduces libstdc++'s std::sort permutation of equal columns."""
+    import ctypes
+    import scipy.sparse as sp
+    from paper_2402_12947_b200 import _lib, device as D
+    g = np.random.default_rng(seed)
+    cdofs = np.ascontiguousarray(g.integers(0, ncol, size=(n_cells, nloc)) % n_dofs, dtype=np.int64)
+    local = np.ascontiguousarray(g.standard_normal((n_cells, nloc, nloc)) *
+                                 10.0 ** g.integers(-8, 8, size=(n_cells, nloc, nloc)))
+    rows = np.repeat(cdofs, nloc, axis=1).ravel()
+    cols = np.tile(cdofs, (1, nloc)).ravel()
+    ref = sp.coo_matrix((local.ravel(), (rows, cols)), shape=(n_dofs, n_dofs)).tocsr()
+    ref.sum_duplicates()
+    dirs = np.unique(g.integers(0, n_dofs, size=max(1, n_dofs // 5))) if n_dofs > 2 else \
+        np.empty(0, dtype=np.int64)
+    mask = np.zeros(n_dofs, dtype=bool)
+    mask[dirs] = True
+    coo = ref.tocoo()
+    keep = ~(mask[coo.row] | mask[coo.col])
+    from paper_2402_12947_b200.sparse import CsrMatrix
+    want = CsrMatrix.from_coo(n_dofs, n_dofs, np.concatenate([coo.row[keep], dirs]),
+                              np.concatenate([coo.col[keep], dirs]),
+                              np.concatenate([coo.data[keep], np.ones(len(dirs))]))
+    lib = _lib.load()
+    i64p, f64p = ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_double)
+    dd = np.ascontiguousarray(dirs, dtype=np.int64)
+    out = ctypes.c_void_p()
+    _lib.check(lib.smg_assemble_elements(n_dofs, n_cells, nloc, cdofs.ctypes.data_as(i64p),
+                                         local.ctypes.data_as(f64p), dd.ctypes.data_as(i64p),
+                                         len(dd), ctypes.byref(out), D.stream_handle()))
+    nr, nc, ptr, col, val = D._csr_result_to_host(lib, out)
+    _same_csr(CsrMatrix(nr, nc, ptr, col, val), want)
 
 
 def test_assembly_inverted_cell_raises():
@@ -285,6 +341,8 @@ def test_assembly_inverted_cell_raises():
     bad = replace(m, cells=cells)
     with pytest.raises(ValueError, match="degenerate or inverted"):
         assemble_poisson(bad, build_dofmap(bad, 1), device=True)
+    with pytest.raises(ValueError, match="degenerate or inverted"):
+        assemble_poisson(bad, build_dofmap(bad, 1), device="kernel")
 
 
 # ---------------------------------------------------------------------------
