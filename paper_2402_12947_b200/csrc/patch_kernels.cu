@@ -191,7 +191,8 @@ static bool nostream_env()
 // shared-memory carve-up for a region of at most nmax dofs
 struct PatchSmem {
   int64_t x_off, lo_off, off_off, prod_off, l_off, tri_cap, bytes;
-  int64_t stage;   // > 0: streaming ring of kRingStages stages of `stage` doubles at l_off
+  int64_t stage;   // > 0: streaming ring of `nst` stages of `stage` doubles at l_off
+  int nst;
 };
 
 constexpr int kChunkRows = 8;   // factor rows per streamed chunk (divides the 32-row panel)
@@ -199,11 +200,29 @@ constexpr int kChunkRows = 8;   // factor rows per streamed chunk (divides the 3
 // 4 x 4 rows, a variable-size byte ring holding 2-4 longest chunks (282-475
 // us) and an L2 prefetch window 2-6 chunks ahead (265 vs 247 us): the
 // streamed solve is bound by its per-chunk arithmetic, not by copy latency
-constexpr int kRingStages = 2;
+constexpr int kRingStages = 2;      // default depth (SMG_PATCH_STAGES overrides)
+constexpr int kMaxRingStages = 8;
+constexpr int kFlagStagesShift = 8; // launch flags bits 8..11: ring depth
 
-__host__ __device__ inline PatchSmem patch_smem_layout(int nmax, bool allow_stream = true)
+// ring depth for streamed factors (SMG_PATCH_STAGES, default kRingStages)
+static int stages_env()
+{
+  static int st = -1;
+  if (st < 0) {
+    const char* v = getenv("SMG_PATCH_STAGES");
+    st = v ? atoi(v) : kRingStages;
+    if (st < 2) st = 2;
+    if (st > kMaxRingStages) st = kMaxRingStages;
+  }
+  return st;
+}
+
+
+__host__ __device__ inline PatchSmem patch_smem_layout(int nmax, bool allow_stream = true,
+                                                       int nst = kRingStages)
 {
   PatchSmem p;
+  p.nst = nst < 2 ? 2 : (nst > kMaxRingStages ? kMaxRingStages : nst);
   const int64_t n2 = (nmax + 2) & ~int64_t(1);
   p.x_off = 0;                                   // double[n2]
   p.lo_off = p.x_off + 8 * n2;                   // int64[n2]
@@ -221,7 +240,9 @@ __host__ __device__ inline PatchSmem patch_smem_layout(int nmax, bool allow_stre
     p.bytes = p.l_off + 8 * need;
   } else {            // stream factor rows through a ring (smaller regions still staged)
     p.stage = ((int64_t)kChunkRows * (nmax + 2) + 1) & ~int64_t(1);
-    p.tri_cap = kRingStages * p.stage;
+    // deeper rings only while they fit the budget
+    while (p.nst > 2 && p.l_off + 8 * p.nst * p.stage > kSmemBudget) --p.nst;
+    p.tri_cap = p.nst * p.stage;
     p.bytes = p.l_off + 8 * p.tri_cap;
   }
   return p;
@@ -278,12 +299,12 @@ __device__ __forceinline__ int n_chunks(int n)
 
 // chunk seq -> ring stage seq % kRingStages (one mbarrier per stage)
 __device__ __forceinline__ void ring_issue(const double* Lg, double* ring, int64_t stage, int n,
-                                           int seq, uint64_t* bars)
+                                           int seq, uint64_t* bars, int nst)
 {
   const ChunkInfo c = chunk_of(seq, n);
   const int64_t a = tri(c.i0) & ~int64_t(1);
   const int64_t b = (tri(c.i0 + c.rows) + 1) & ~int64_t(1);
-  const int s = seq % kRingStages;
+  const int s = seq % nst;
   uint64_t* bar = &bars[s];
   const uint32_t bytes = (uint32_t)((b - a) * 8);
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(psmem_u32(bar)),
@@ -327,8 +348,8 @@ __device__ __forceinline__ void dinv_issue(const double* Dinv, double* s_dinv, i
       : "memory");
 }
 
-__device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_t stage, int n,
-                             double* s_x, double* s_dinv, uint64_t* bars, uint64_t* dbars,
+__device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_t stage, int nst,
+                             int n, double* s_x, double* s_dinv, uint64_t* bars, uint64_t* dbars,
                              double (*red)[32])
 {
   const int lane = threadIdx.x & 31;
@@ -339,12 +360,12 @@ __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_
   const int total = 2 * C;
   int dq = 0;  // next inverted block to consume
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kRingStages; ++s)
+    for (int s = 0; s < nst; ++s)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(psmem_u32(&bars[s])) : "memory");
     for (int s = 0; s < 2; ++s)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(psmem_u32(&dbars[s])) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int q = 0; q < kRingStages && q < total; ++q) ring_issue(Lg, ring, stage, n, q, bars);
+    for (int q = 0; q < nst && q < total; ++q) ring_issue(Lg, ring, stage, n, q, bars, nst);
     for (int q = 0; q < 2 && q < 2 * nb; ++q) dinv_issue(Dinv, s_dinv, q, nb, dbars);
   }
   __syncthreads();
@@ -365,8 +386,8 @@ __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_
     const bool fwd = seq < C;
     if (seq == C) PTRACE(4);
     if (!fwd && c.i0 == p0) panel_solve(p0, pn, true);   // backward: own block first
-    ring_wait(&bars[seq % kRingStages], (uint32_t)((seq / kRingStages) & 1));
-    const double* rows = ring + (seq % kRingStages) * stage + (tri(c.i0) & 1) - tri(c.i0);
+    ring_wait(&bars[seq % nst], (uint32_t)((seq / nst) & 1));
+    const double* rows = ring + (seq % nst) * stage + (tri(c.i0) & 1) - tri(c.i0);
     if (fwd) {
       // x_i -= L[i, 0:p0] . x[0:p0] for the chunk's rows (one warp per row)
       if (warp < c.rows && p0 > 0) {
@@ -403,9 +424,9 @@ __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_
       }
     }
     __syncthreads();
-    if (threadIdx.x == 0 && seq + kRingStages < total) {  // stage free: next chunk into it
+    if (threadIdx.x == 0 && seq + nst < total) {  // stage free: next chunk into it
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      ring_issue(Lg, ring, stage, n, seq + kRingStages, bars);
+      ring_issue(Lg, ring, stage, n, seq + nst, bars, nst);
     }
     if (fwd && c.i0 + c.rows == p0 + pn) panel_solve(p0, pn, false);  // forward: panel done
   }
@@ -434,9 +455,9 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   extern __shared__ __align__(16) unsigned char psm[];
   __shared__ double s_red[kSolveWarps][32];
   __shared__ uint64_t s_bar;
-  __shared__ uint64_t s_ring_bar[kRingStages];
+  __shared__ uint64_t s_ring_bar[kMaxRingStages];
   __shared__ uint64_t s_dinv_bar[2];
-  const PatchSmem L_ = patch_smem_layout(nmax, allow_stream);
+  const PatchSmem L_ = patch_smem_layout(nmax, allow_stream, (flags >> kFlagStagesShift) & 15);
   double* s_x = reinterpret_cast<double*>(psm + L_.x_off);
   int32_t* s_off = reinterpret_cast<int32_t*>(psm + L_.off_off);
   double* s_prod = reinterpret_cast<double*>(psm + L_.prod_off);
@@ -681,7 +702,7 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
     gemv_inv<4 * kPanel>(L + patch_tri_even(n), s_x, n, false, s_prod);
     gemv_inv<4 * kPanel>(L + patch_tri_even(n), s_x, n, true, s_prod);
   } else if (!staged && L_.stage > 0) {
-    stream_solve(Lg, s_L, L_.stage, n, s_x, s_prod, s_ring_bar, s_dinv_bar, s_red);
+    stream_solve(Lg, s_L, L_.stage, L_.nst, n, s_x, s_prod, s_ring_bar, s_dinv_bar, s_red);
   } else {
 
   // ---- forward: L y = r (left-looking over 32-row panels)
@@ -850,7 +871,8 @@ static cudaError_t launch_patch(const Correction& c, size_t smem, const double* 
   cfg.numAttrs = 1;
   static const int l2pf = patch_env("SMG_PATCH_L2PF", 0);  // measured slower on C5 (222 vs 240 us)
   static const int lpt = patch_env("SMG_PATCH_LPT", 1);
-  const int flags = (allow_stream ? kFlagStream : 0) | (l2pf ? kFlagL2Prefetch : 0);
+  const int flags = (allow_stream ? kFlagStream : 0) | (l2pf ? kFlagL2Prefetch : 0) |
+                    (stages_env() << kFlagStagesShift);
   return cudaLaunchKernelEx(&cfg, patch_kernel<kMode>, c.prow, c.pcol, c.pval, c.pptr, c.dofs,
                             c.foff, c.lfac, b, u_res, c.rbuf, tgt, add, c.max_dofs, flags,
                             lpt ? c.order : (const int32_t*)nullptr, FollowArgs(),
@@ -860,7 +882,7 @@ static cudaError_t launch_patch(const Correction& c, size_t smem, const double* 
 
 static size_t follow_smem(const Correction& c)
 {
-  const PatchSmem L = patch_smem_layout(c.max_dofs, !nostream_env());
+  const PatchSmem L = patch_smem_layout(c.max_dofs, !nostream_env(), stages_env());
   return (size_t)L.bytes + 8 * (size_t)((c.ring_max + 1) & ~1) + 4 * (size_t)(c.ring_max + 2);
 }
 
@@ -887,7 +909,7 @@ cudaError_t launch_patch_follow(const Correction& c, const FollowArgs& fa, cudaS
   f.ring_max = c.ring_max;
   return cudaLaunchKernelEx(&cfg, patch_kernel<kFollow>, c.prow, c.pcol, c.pval, c.pptr, c.dofs,
                             c.foff, c.lfac, fa.b, (const double*)nullptr, c.rbuf, fa.out, 1,
-                            c.max_dofs, st ? kFlagStream : 0,
+                            c.max_dofs, (st ? kFlagStream : 0) | (stages_env() << kFlagStagesShift),
                             lpt ? c.order : (const int32_t*)nullptr, f, c.ring_ptr, c.ring_rows,
                             c.plcol, c.bpos);
 }
@@ -918,7 +940,7 @@ cudaError_t launch_patch_solve(const Correction& c, const double* b, const doubl
 {
   if (c.n_regions == 0) return cudaSuccess;
   const int st = nostream_env() ? 0 : 1;
-  const PatchSmem L = patch_smem_layout(c.max_dofs, st != 0);
+  const PatchSmem L = patch_smem_layout(c.max_dofs, st != 0, stages_env());
   double* tgt = u_add ? u_add : out_scatter;
   const int add = u_add ? 1 : 0;
   const size_t smem = (size_t)L.bytes + smem_pad();
@@ -932,7 +954,7 @@ cudaError_t launch_patch_solve(const Correction& c, const double* b, const doubl
 cudaError_t configure_patch_solve_smem(const Correction& c)
 {
   static int cur[4] = {0, 0, 0, 0};
-  const PatchSmem L = patch_smem_layout(c.max_dofs, !nostream_env());
+  const PatchSmem L = patch_smem_layout(c.max_dofs, !nostream_env(), stages_env());
   const int bytes = (int)(L.bytes + smem_pad());
   cudaError_t e = cudaSuccess;
   auto grow = [&](int mode, auto fn, int need) {
