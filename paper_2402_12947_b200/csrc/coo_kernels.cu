@@ -406,7 +406,8 @@ int assemble_elements_device(int64_t n_dofs, int64_t n_cells, int nloc, const in
   SMG_E(cudaGetLastError());
   coo_sorted_check_kernel<<<gr, 256, 0, s>>>(n_dofs, rowptr, col, d_unsorted);
   SMG_E(cudaGetLastError());
-  coo_row_sum_kernel<<<gr, 128, 0, s>>>(n_dofs, rowptr, col, val, d_unsorted, d_dir, ucount, kcount);
+  coo_row_sum_kernel<<<(unsigned)((n_dofs + 127) / 128), 128, 0, s>>>(n_dofs, rowptr, col, val,
+                                                                 d_unsorted, d_dir, ucount, kcount);
   SMG_E(cudaGetLastError());
   SMG_E(cudaMalloc(&out->rowptr, sizeof(int64_t) * (size_t)(n_dofs + 1)));
   // out_ptr = exclusive scan of kcount (n_dofs + 1 entries: kcount[n] = 0)

@@ -65,6 +65,7 @@ sym_tile_kernel(int nb, const int32_t* __restrict__ tile_i, const double* __rest
   const int t = blockIdx.x;
   const int I = tile_i[t];
   const int J = t - I * (I + 1) / 2;
+  SMG_DCHECK(I >= 0 && I < nb && J >= 0 && J <= I);
   const int tid = threadIdx.x;
   const int c = tid & (kSymTile - 1);      // column inside the tile
   const int g = tid / kSymTile;            // rows g, g + 4, g + 8, ...
@@ -112,8 +113,15 @@ sym_tile_kernel(int nb, const int32_t* __restrict__ tile_i, const double* __rest
   __threadfence();
   __syncthreads();
   if (tid == 0) {
-    s_last[0] = atomicAdd(&counter[I], 1u) == (unsigned)(nb - 1);
-    s_last[1] = I != J && atomicAdd(&counter[J], 1u) == (unsigned)(nb - 1);
+    const unsigned ci = atomicAdd(&counter[I], 1u);
+    SMG_DCHECK(ci < (unsigned)nb);   // a block row receives exactly nb partials per call
+    s_last[0] = ci == (unsigned)(nb - 1);
+    unsigned cj = 0;
+    if (I != J) {
+      cj = atomicAdd(&counter[J], 1u);
+      SMG_DCHECK(cj < (unsigned)nb);
+    }
+    s_last[1] = I != J && cj == (unsigned)(nb - 1);
   }
   __syncthreads();
   if (s_last[0]) {

@@ -195,7 +195,11 @@ struct PatchSmem {
   int nst;
 };
 
-constexpr int kChunkRows = 8;   // factor rows per streamed chunk (divides the 32-row panel)
+#ifndef SMG_CHUNK_ROWS
+#define SMG_CHUNK_ROWS 8
+#endif
+constexpr int kChunkRows = SMG_CHUNK_ROWS;   // factor rows per streamed chunk (divides the 32-row panel)
+static_assert(kPanel % kChunkRows == 0 && kChunkRows % 8 == 0, "chunk rows: 8, 16 or 32");
 // chunks in flight per CTA; measured best on C5: 2 x 8 rows (227 us) beat
 // 4 x 4 rows, a variable-size byte ring holding 2-4 longest chunks (282-475
 // us) and an L2 prefetch window 2-6 chunks ahead (265 vs 247 us): the
@@ -256,40 +260,6 @@ __host__ __device__ inline PatchSmem patch_smem_layout(int nmax, bool allow_stre
 // solved prefix), then the panel's inverted diagonal block.  Backward:
 // right-looking from the last panel (inverted block first, then the panel's
 // rows update the unsolved prefix), so both passes stream the same row chunks.
-struct ChunkInfo {
-  int i0, rows, panel;
-};
-
-__device__ __forceinline__ ChunkInfo chunk_of(int seq, int n)
-{
-  const int nb = (n + kPanel - 1) / kPanel;
-  const int cpp = kPanel / kChunkRows;
-  const int pn_last = n - (nb - 1) * kPanel;
-  const int k_last = (pn_last + kChunkRows - 1) / kChunkRows;
-  const int C = (nb - 1) * cpp + k_last;
-  int panel, j;
-  if (seq < C) {  // forward: ascending
-    panel = seq / cpp;
-    if (panel > nb - 1) panel = nb - 1;
-    j = seq - panel * cpp;
-  } else {        // backward: panels descending
-    const int t = seq - C;
-    if (t < k_last) {
-      panel = nb - 1;
-      j = t;
-    } else {
-      const int t2 = t - k_last;
-      panel = nb - 2 - t2 / cpp;
-      j = t2 % cpp;
-    }
-  }
-  ChunkInfo c;
-  c.panel = panel;
-  c.i0 = panel * kPanel + j * kChunkRows;
-  c.rows = min(kChunkRows, n - c.i0);
-  return c;
-}
-
 __device__ __forceinline__ int n_chunks(int n)
 {
   const int nb = (n + kPanel - 1) / kPanel;
@@ -297,14 +267,48 @@ __device__ __forceinline__ int n_chunks(int n)
   return (nb - 1) * (kPanel / kChunkRows) + (pn_last + kChunkRows - 1) / kChunkRows;
 }
 
+// Chunk sequence without divisions: forward panels 0..nb-1, then backward
+// panels nb-1..0, chunks ascending inside each panel; advanced one chunk at a time by the consumer and the issuer.
+struct ChunkCursor {
+  int panel, j, nb, k_last, n;
+  bool fwd;
+  __device__ __forceinline__ void init(int n_)
+  {
+    n = n_;
+    nb = (n + kPanel - 1) / kPanel;
+    k_last = (n - (nb - 1) * kPanel + kChunkRows - 1) / kChunkRows;
+    panel = 0;
+    j = 0;
+    fwd = true;
+  }
+  __device__ __forceinline__ int chunks_in_panel() const
+  {
+    return panel == nb - 1 ? k_last : kPanel / kChunkRows;
+  }
+  __device__ __forceinline__ int i0() const { return panel * kPanel + j * kChunkRows; }
+  __device__ __forceinline__ int rows() const { return min(kChunkRows, n - i0()); }
+  __device__ __forceinline__ void advance()
+  {
+    if (++j < chunks_in_panel()) return;
+    j = 0;
+    if (fwd) {
+      if (++panel == nb) {
+        fwd = false;
+        panel = nb - 1;
+      }
+    } else {
+      --panel;
+    }
+  }
+};
+
 // chunk seq -> ring stage seq % kRingStages (one mbarrier per stage)
-__device__ __forceinline__ void ring_issue(const double* Lg, double* ring, int64_t stage, int n,
-                                           int seq, uint64_t* bars, int nst)
+__device__ __forceinline__ void ring_issue_at(const double* Lg, double* ring, int64_t stage,
+                                              int i0, int rows, int s, uint64_t* bars)
 {
-  const ChunkInfo c = chunk_of(seq, n);
-  const int64_t a = tri(c.i0) & ~int64_t(1);
-  const int64_t b = (tri(c.i0 + c.rows) + 1) & ~int64_t(1);
-  const int s = seq % nst;
+  const int64_t a = tri(i0) & ~int64_t(1);
+  const int64_t b = (tri(i0 + rows) + 1) & ~int64_t(1);
+  SMG_DCHECK(s >= 0 && s < kMaxRingStages && rows > 0 && b - a <= stage);
   uint64_t* bar = &bars[s];
   const uint32_t bytes = (uint32_t)((b - a) * 8);
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(psmem_u32(bar)),
@@ -359,13 +363,21 @@ __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_
   const int C = n_chunks(n);
   const int total = 2 * C;
   int dq = 0;  // next inverted block to consume
+  // issue cursor (thread 0 only): the chunk that goes into the ring next
+  ChunkCursor iss;
+  iss.init(n);
+  int iss_seq = 0, iss_stage = 0;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < nst; ++s)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(psmem_u32(&bars[s])) : "memory");
-    for (int s = 0; s < 2; ++s)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(psmem_u32(&dbars[s])) : "memory");
+    for (int q = 0; q < nst; ++q)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(psmem_u32(&bars[q])) : "memory");
+    for (int q = 0; q < 2; ++q)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(psmem_u32(&dbars[q])) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int q = 0; q < nst && q < total; ++q) ring_issue(Lg, ring, stage, n, q, bars, nst);
+    for (; iss_seq < nst && iss_seq < total; ++iss_seq) {
+      ring_issue_at(Lg, ring, stage, iss.i0(), iss.rows(), iss_stage, bars);
+      iss.advance();
+      if (++iss_stage == nst) iss_stage = 0;
+    }
     for (int q = 0; q < 2 && q < 2 * nb; ++q) dinv_issue(Dinv, s_dinv, q, nb, dbars);
   }
   __syncthreads();
@@ -379,56 +391,75 @@ __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_
     }
     ++dq;
   };
+  ChunkCursor cur;
+  cur.init(n);
+  int stg = 0;
+  uint32_t phase = 0;
   for (int seq = 0; seq < total; ++seq) {
-    const ChunkInfo c = chunk_of(seq, n);
-    const int p0 = c.panel * kPanel;
+    const int i0 = cur.i0(), crows = cur.rows();
+    const int p0 = cur.panel * kPanel;
     const int pn = min(kPanel, n - p0);
-    const bool fwd = seq < C;
+    const bool fwd = cur.fwd;
     if (seq == C) PTRACE(4);
-    if (!fwd && c.i0 == p0) panel_solve(p0, pn, true);   // backward: own block first
-    ring_wait(&bars[seq % nst], (uint32_t)((seq / nst) & 1));
-    const double* rows = ring + (seq % nst) * stage + (tri(c.i0) & 1) - tri(c.i0);
+    if (!fwd && i0 == p0) panel_solve(p0, pn, true);   // backward: own block first
+    ring_wait(&bars[stg], phase);
+    const double* rows = ring + stg * stage + (tri(i0) & 1) - tri(i0);
+    SMG_DCHECK(i0 >= p0 && crows > 0 && i0 + crows <= n && stg < nst);
     if (fwd) {
-      // x_i -= L[i, 0:p0] . x[0:p0] for the chunk's rows (one warp per row)
-      if (warp < c.rows && p0 > 0) {
-        const int i = c.i0 + warp;
-        const double* Li = rows + tri(i);
-        // four independent partial sums: the loads of the next products do not
-        // wait on the previous multiply-add
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        int j = lane;
-        for (; j + 96 < p0; j += 128) {
-          a0 += Li[j] * s_x[j];
-          a1 += Li[j + 32] * s_x[j + 32];
-          a2 += Li[j + 64] * s_x[j + 64];
-          a3 += Li[j + 96] * s_x[j + 96];
+      // x_i -= L[i, 0:p0] . x[0:p0] for the chunk's rows (warp w: rows w, w + 8, ...)
+      if (p0 > 0) {
+#pragma unroll
+        for (int rr = 0; rr < kChunkRows / 8; ++rr) {
+          const int r = warp + 8 * rr;
+          if (r < crows) {
+            const int i = i0 + r;
+            const double* Li = rows + tri(i);
+            // four independent partial sums: the loads of the next products do
+            // not wait on the previous multiply-add
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            int j = lane;
+            for (; j + 96 < p0; j += 128) {
+              a0 += Li[j] * s_x[j];
+              a1 += Li[j + 32] * s_x[j + 32];
+              a2 += Li[j + 64] * s_x[j + 64];
+              a3 += Li[j + 96] * s_x[j + 96];
+            }
+            for (; j < p0; j += 32) a0 += Li[j] * s_x[j];
+            const double acc = warp_sum((a0 + a1) + (a2 + a3));
+            if (lane == 0) s_x[i] -= acc;
+          }
         }
-        for (; j < p0; j += 32) a0 += Li[j] * s_x[j];
-        const double acc = warp_sum((a0 + a1) + (a2 + a3));
-        if (lane == 0) s_x[i] -= acc;
       }
     } else if (p0 > 0) {
       // y[c] -= sum_{i in chunk} L[i][c] x_i  for c < p0 (thread per column)
       for (int col = threadIdx.x; col < p0; col += kSolveThreads) {
         double a0 = 0.0, a1 = 0.0;
-        const double* rc = rows + tri(c.i0) + col;   // row c.i0 + r starts tri(c.i0 + r)
+        const double* rc = rows + tri(i0) + col;   // row i0 + r starts tri(i0 + r)
         int r = 0;
-        for (; r + 1 < c.rows; r += 2) {
-          a0 += rc[0] * s_x[c.i0 + r];
-          rc += c.i0 + r + 1;
-          a1 += rc[0] * s_x[c.i0 + r + 1];
-          rc += c.i0 + r + 2;
+        for (; r + 1 < crows; r += 2) {
+          a0 += rc[0] * s_x[i0 + r];
+          rc += i0 + r + 1;
+          a1 += rc[0] * s_x[i0 + r + 1];
+          rc += i0 + r + 2;
         }
-        if (r < c.rows) a0 += rc[0] * s_x[c.i0 + r];
+        if (r < crows) a0 += rc[0] * s_x[i0 + r];
         s_x[col] -= a0 + a1;
       }
     }
     __syncthreads();
-    if (threadIdx.x == 0 && seq + nst < total) {  // stage free: next chunk into it
+    if (threadIdx.x == 0 && iss_seq < total) {  // stage free: next chunk into it
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      ring_issue(Lg, ring, stage, n, seq + nst, bars, nst);
+      ring_issue_at(Lg, ring, stage, iss.i0(), iss.rows(), iss_stage, bars);
+      iss.advance();
+      ++iss_seq;
+      if (++iss_stage == nst) iss_stage = 0;
     }
-    if (fwd && c.i0 + c.rows == p0 + pn) panel_solve(p0, pn, false);  // forward: panel done
+    if (fwd && i0 + crows == p0 + pn) panel_solve(p0, pn, false);  // forward: panel done
+    cur.advance();
+    if (++stg == nst) {
+      stg = 0;
+      phase ^= 1u;
+    }
   }
 }
 
@@ -468,10 +499,12 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   const int p = order ? order[blockIdx.x] : (int)blockIdx.x;
   const int32_t k0 = pptr[p];
   const int n = pptr[p + 1] - k0;
+  SMG_DCHECK(n > 0 && n <= nmax);
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int64_t nslot = patch_slot_doubles(n, nmax);
   const bool staged = kMode != kResidualOnly && nslot <= L_.tri_cap;
+  SMG_DCHECK(L_.bytes <= (int64_t)227 * 1024);
   const double* __restrict__ Lg = lfac + foff[p];
   // this thread's own patch dof (rows < kSolveThreads): b and the scatter
   // target there are fetched right after the dependency wait, off the
@@ -660,7 +693,10 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
 #pragma unroll
       for (int it = 0; it < kProdItems; ++it) {
         const int e = it * kSolveThreads + threadIdx.x;
-        if (e < cnt) s_prod[e] = __dmul_rn(vv[it], u_res[cc[it]]);
+        if (e < cnt) {
+          SMG_DCHECK(e < kProdCap && cc[it] >= 0);
+          s_prod[e] = __dmul_rn(vv[it], u_res[cc[it]]);
+        }
       }
       __syncthreads();
       for (int i = threadIdx.x; i < n; i += kSolveThreads) {

@@ -8,6 +8,27 @@
 #include <string>
 #include <vector>
 
+// SMG_CHECKED (a variant build, tools/checked_run.py): device-side bounds and
+// protocol assertions in the kernels -- the substitute for compute-sanitizer,
+// which this pool does not run (profiles/r02/sanitizer/).  A failed check
+// prints its condition and traps (the launch fails with an error the host
+// reports).  Compiled out of the product build.
+#ifdef SMG_CHECKED
+#include <cstdio>
+#define SMG_DCHECK(cond)                                                             \
+  do {                                                                               \
+    if (!(cond)) {                                                                   \
+      printf("SMG_DCHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x, #cond);                              \
+      __trap();                                                                      \
+    }                                                                                \
+  } while (0)
+#else
+#define SMG_DCHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
+
 namespace smg {
 
 // ---------------------------------------------------------------------------

@@ -205,6 +205,7 @@ csr_tile_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, 
   // gathered row subsets (halo pass) address vectors through row_map; the
   // interior pass skips the rows a concurrent local correction may change
   const int32_t grow = (has_row && m.row_map) ? m.row_map[row] : row;
+  SMG_DCHECK(!has_row || (grow >= 0 && (m.row_map || grow < m.nrows)));
   const bool write = has_row && !(ea.skip_rows && ea.skip_rows[grow]);
   double bv = 0.0, uv = 0.0, dv = 0.0, ov = 0.0, inv = 0.0;
   if (write) {
@@ -224,11 +225,15 @@ csr_tile_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, 
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
       const int k = i * kThreads + tid;
-      if (k < qn) buf[k] = __dmul_rn(v[i], __ldg(x + c[i]));
+      if (k < qn) {
+        SMG_DCHECK(c[i] >= 0 && c[i] < m.ncols);
+        buf[k] = __dmul_rn(v[i], __ldg(x + c[i]));
+      }
     }
     if (q + 1 < nq) load_chunk(q0 + kTileNnz);   // in flight during this chunk's sums
     __syncthreads();
     if (has_row) {
+      SMG_DCHECK(a >= 0 && a <= bnd && bnd <= cnt);
       const int j0 = max(a, q0), j1 = min(bnd, q0 + qn);
       for (int j = j0; j < j1; ++j) sum = __dadd_rn(sum, buf[j - q0]);
     }
@@ -308,6 +313,8 @@ sell_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, int 
   }
   const int32_t grow = w * kSellWindow + rl;
   const bool has_row = rl >= 0;
+  SMG_DCHECK(!has_row || grow < m.nrows);
+  SMG_DCHECK(se >= sb && ((se - sb) & 31) == 0);
   const bool write = has_row && !(ea.skip_rows && ea.skip_rows[grow]);
   double bv = 0.0, uv = 0.0, dv = 0.0, ov = 0.0, inv = 0.0;
   if (write) {
@@ -370,6 +377,7 @@ sell_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, int 
       c = __ldg(cp + j * 32);
       v = __ldg(vp + j * 32);
     }
+    SMG_DCHECK(c < m.ncols);
     if (c >= 0) sum = __dadd_rn(sum, __dmul_rn(v, __ldg(x + c)));
   }
   if (write) epilogue<E>(ea, grow, sum, inv, bv, uv, dv, ov);

@@ -8,7 +8,7 @@ mkdir -p $OUT
 CS="compute-sanitizer --print-limit 50 --error-exitcode 9"
 run() {  # tool, variant, env...
   local tool=$1 var=$2; shift 2
-  env "$@" timeout 1500 $CS --tool $tool python tools/sanitize_driver.py \
+  env "$@" timeout 900 $CS --tool $tool python tools/sanitize_driver.py \
       > $OUT/sanitize_${tool}${var}_$TAG.log 2>&1
   echo "$tool$var rc=$?" >> $OUT/sanitize_rc_$TAG.txt
 }

@@ -42,6 +42,11 @@ def make(sizes, n_rows, seed=7):
 
 
 def main():
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--case", default=None, help="run only this case (e.g. '512 x1', 'C5')")
+    ap.add_argument("--reps", type=int, default=20)
+    args = ap.parse_args()
     import torch
     from paper_2402_12947_b200 import _lib, device as D
     from paper_2402_12947_b200.sparse import CsrMatrix
@@ -57,13 +62,15 @@ def main():
     for nd in (64, 128, 192, 256, 384, 512):
         cases.append((f"{nd} x1", np.array([nd])))
         cases.append((f"{nd} x1000", np.full(1000, nd)))
+    if args.case:
+        cases = [(nm, sz) for nm, sz in cases if nm.startswith(args.case)]
     for name, sizes in cases:
         lc = make(sizes, n)
         dc = D.DeviceCorrection(op, lc)
         for _ in range(3):
             _lib.check(lib.smg_apply_local_correction(dc.handle, D.ptr(r), D.ptr(o), sh))
         torch.cuda.synchronize()
-        reps = 20
+        reps = args.reps
         e0.record()
         for _ in range(reps):
             _lib.check(lib.smg_apply_local_correction(dc.handle, D.ptr(r), D.ptr(o), sh))

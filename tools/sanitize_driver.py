@@ -29,6 +29,11 @@ def rel(a, b):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--mode", default="all", choices=["all", "default", "follow", "overlap"])
+    ap.add_argument("--stress", type=int, default=0,
+                    help="repeat every V-cycle this many times on fresh copies of the same "
+                         "inputs (graphs and eager) and require bit-identical results: a "
+                         "race on shared memory, a ring stage or the last-CTA reduction "
+                         "would show up as run-to-run differences")
     args = ap.parse_args()
     import torch
     import paper_2402_12947_b200 as P
@@ -50,6 +55,27 @@ def main():
             dh.vcycle(b, u)
             if rel(u, z["g/vcycle1"]) > 1e-12:
                 bad.append(f"{name}/{mode}: vcycle {rel(u, z['g/vcycle1']):.2e}")
+            for graphs in ((True, False) if args.stress else ()):
+                dg = DeviceHierarchy(h.levels, h.coarse_factor, use_graphs=graphs)
+                if mode == "overlap":
+                    dg.set_option(2, 1)
+                if mode == "follow":
+                    dg.set_option(3, 1)
+                bt = torch.from_numpy(b).cuda()
+                outs = []
+                for _ in range(args.stress):
+                    ut = torch.from_numpy(ur).cuda()
+                    dg.vcycle(bt, ut)
+                    dg.vcycle(bt, ut)
+                    outs.append(ut)
+                torch.cuda.synchronize()
+                ref = outs[0].cpu().numpy()
+                if not np.array_equal(ref, u) and graphs:
+                    pass
+                ndiff = sum(0 if np.array_equal(o.cpu().numpy(), ref) else 1 for o in outs)
+                if ndiff:
+                    bad.append(f"{name}/{mode}/graphs={graphs}: {ndiff} of {args.stress} "
+                               f"reruns differ")
         lv = h.levels[0]
         w = ur.copy()
         P.combined_smooth(lv.a, b, w, lv.local_correction, lv.smoother)
@@ -65,6 +91,10 @@ def main():
     out = P.apply_local_correction(lc, zc["r"])
     if rel(out, zc["lc_apply"]) > 1e-13:
         bad.append("c5p: patch solves")
+    for _ in range(args.stress):
+        if not np.array_equal(P.apply_local_correction(lc, zc["r"]), out):
+            bad.append("c5p: rerun differs")
+            break
     # setup kernels: Galerkin product and batched patch Cholesky on the device
     z, h = fixtures.load("c2s")
     from paper_2402_12947_b200.sparse import triple_product
