@@ -28,7 +28,6 @@ FLAGS = [
     "-Xcompiler", "-fPIC,-ffp-contract=off,-fvisibility=hidden",
     "-Xptxas", "-v",
     "-shared",
-    "-lcusolver", "-lcublas",
     "-Xlinker", "-rpath=/usr/local/cuda/lib64",
 ]
 
