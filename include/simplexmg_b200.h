@@ -210,7 +210,8 @@ SMG_API int smg_assemble_poisson(int dim, int degree, int64_t n_vertices, const 
 /* ---- setup: coarse operator factor and inverse (mg.py:123 coarse_factor =
  * sparse.py:234-254 dense_factor; the hot path's A_L^-1) --------------------
  * smg_dense_cholesky: a (host, n x n row-major) -> c (host) in cho_factor's
- * layout (L lower, A strict upper), on the device (cuSOLVER dpotrf).
+ * layout (L lower, A strict upper), on the device (hand-written blocked dpotrf,
+ * csrc/coarse_factor.cu).
  * SMG_ERR_INVALID "… expects a symmetric matrix" when max|a - a^T| > 1e-10
  * max|a|; SMG_ERR_NOT_SPD with *info = dpotrf's leading minor when not SPD
  * (the reference then falls back to LU on the host).

@@ -94,7 +94,8 @@ def coarse_inverse(coarse_factor, device: Optional[bool] = None) -> np.ndarray:
     """Dense A_L^{-1} from the reference's Cholesky factor (mg.py:123) as
     LAPACK dpotri forms it (setup).  ``coarse_factor.factor = (c, lower)``.
     ``device`` (default: whenever a CUDA device exists): dpotri on the GPU
-    (``smg_cholesky_inverse``, cuSOLVER) from the same factor."""
+    (``smg_cholesky_inverse``, hand-written blocked dtrtri + dlauum) from the
+    same factor."""
     f = getattr(coarse_factor, "factor", coarse_factor)
     kind = getattr(coarse_factor, "kind", "cholesky")
     if kind != "cholesky":

@@ -351,7 +351,7 @@ def test_assembly_inverted_cell_raises():
 def _assert_same_hierarchy(hd, hh, factor_tol=1e-12):
     """Device-built vs host-built hierarchy: operators, prolongations, region
     dof sets and smoother lambdas bit for bit; Cholesky factors (device
-    kernel / cuSOLVER vs LAPACK) to a stated tolerance."""
+    kernels vs LAPACK) to a stated tolerance."""
     assert len(hd.levels) == len(hh.levels)
     for ld, lh in zip(hd.levels, hh.levels):
         for x, y in ((ld.a, lh.a),) + (((ld.prolongation.matrix, lh.prolongation.matrix),)

@@ -1,5 +1,6 @@
 """Time the coarse factor + inverse on the device (smg_dense_cholesky +
-smg_cholesky_inverse, cuSOLVER) against scipy cho_factor + LAPACK dpotri on
+smg_cholesky_inverse: the hand-written blocked dpotrf / dtrtri / dlauum of
+csrc/coarse_factor.cu) against scipy cho_factor + LAPACK dpotri on
 the host, for a dense SPD matrix of the coarsest-level size of a workload
 (C4: n_L = 15,625; the reference's mg.py:123 plus this package's A_L^-1).
 
@@ -28,7 +29,7 @@ def main():
     rng = np.random.default_rng(0)
     g = rng.standard_normal((n, n)) / np.sqrt(n)
     a = g @ g.T + np.eye(n)
-    dense_factor(a[:64, :64].copy(), device=True)  # warm-up (cuSOLVER handle)
+    dense_factor(a[:64, :64].copy(), device=True)  # warm-up (context, kernel attributes)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     f = dense_factor(a, device=True)
@@ -39,12 +40,15 @@ def main():
     t3 = time.perf_counter()
     inv_h = coarse_inverse(c, device=False) if False else None
     lo = np.asfortranarray(np.tril(c[0]))
-    scipy.linalg.lapack.dpotri(lo, lower=1)
+    inv_lapack, _ = scipy.linalg.lapack.dpotri(lo, lower=1)
     t4 = time.perf_counter()
+    inv_lapack = np.tril(inv_lapack) + np.tril(inv_lapack, -1).T
+    inv_rel = float(np.max(np.abs(inv_d - inv_lapack)) / np.max(np.abs(inv_lapack)))
     rel = float(np.max(np.abs(np.tril(f.factor[0]) - np.tril(c[0]))) / np.max(np.abs(np.tril(c[0]))))
     rec = {"n": n, "gpu_factor_ms": (t1 - t0) * 1e3, "gpu_inverse_ms": (t2 - t1) * 1e3,
            "cpu_factor_ms": (t3 - t2) * 1e3, "cpu_inverse_ms": (t4 - t3) * 1e3,
-           "max_rel_L_diff": rel, "gpu_includes": "H2D + cuSOLVER + D2H of n^2 doubles",
+           "max_rel_L_diff": rel, "max_rel_inverse_diff": inv_rel,
+           "gpu_includes": "H2D + hand-written kernels + D2H of n^2 doubles",
            "cpu_threads": os.cpu_count()}
     print(json.dumps(rec), flush=True)
     if out:
