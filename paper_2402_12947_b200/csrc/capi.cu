@@ -548,6 +548,11 @@ struct HLevel {
   double* r = nullptr;   // residual
   RingRows ringP;        // P's rows on the correction rings (follow-mode prolong-add)
   bool has_ringP = false;
+  // locality renumbering (renumber_level): perm[old] = new, inv[new] = old
+  bool renum = false;
+  std::vector<int32_t> perm_h;
+  int32_t* perm = nullptr;
+  int32_t* inv = nullptr;
 };
 
 struct Hierarchy {
@@ -583,9 +588,17 @@ struct Hierarchy {
   // previous call's last kernel before it starts, then records its own).
   std::recursive_mutex mu;
   cudaEvent_t done_ev = nullptr;
+  // renamed copies owned by the hierarchy (renumbered levels)
+  std::vector<std::unique_ptr<Operator>> own_ops;
+  std::vector<std::unique_ptr<Correction>> own_corrs;
+  const Operator* a_user = nullptr;   // level 0's operator as the caller passed it
+  double* b0r = nullptr;              // level 0 renumbered: b and u in the renamed space
+  double* u0r = nullptr;
 
   ~Hierarchy()
   {
+    for (auto& o : own_ops) free_all(o->allocs);
+    for (auto& c : own_corrs) free_all(c->allocs);
     if (done_ev) cudaEventDestroy(done_ev);
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     if (capture_stream) cudaStreamDestroy(capture_stream);
@@ -707,6 +720,14 @@ static int enqueue_vcycle(Hierarchy& h, const double* b0, double* u0, cudaStream
     cur[l] = h.lv[l].u;
     alt[l] = h.lv[l].t;
   }
+  if (h.lv[0].renum) {
+    // the caller's b and u into level 0's renamed index space
+    SMG_CUDA(launch_gather(h.lv[0].inv, h.lv[0].n, b0, h.b0r, st));
+    SMG_CUDA(launch_gather(h.lv[0].inv, h.lv[0].n, u0, h.u0r, st));
+    bl[0] = h.b0r;
+    cur[0] = h.u0r;
+    *launches += 2;
+  }
   std::vector<char> first_done(nl, 0);
   for (int l = 0; l < nl - 1; ++l) {
     HLevel& L = h.lv[l];
@@ -781,7 +802,10 @@ static int enqueue_vcycle(Hierarchy& h, const double* b0, double* u0, cudaStream
     }
     SMG_TRY(enqueue_smooth(h, L, bl[l], &cur[l], &alt[l], st, launches, false, follow));
   }
-  if (cur[0] != u0) {
+  if (h.lv[0].renum) {
+    SMG_CUDA(launch_gather(h.lv[0].perm, h.lv[0].n, cur[0], u0, st));   // back to the caller's order
+    ++*launches;
+  } else if (cur[0] != u0) {
     SMG_CUDA(cudaMemcpyAsync(u0, cur[0], sizeof(double) * (size_t)h.lv[0].n,
                              cudaMemcpyDeviceToDevice, st));
   }
@@ -1955,6 +1979,237 @@ static int upload_sym_tiles(std::vector<void*>& allocs, int64_t& bytes, int64_t 
   return SMG_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Locality renumbering of a level's device copy: a
+// symmetric permutation (reverse Cuthill-McKee of the operator's graph)
+// renames rows and columns of A_l, the rows of P_l and the columns of
+// P_{l-1}, so each SELL window / tile gathers x from a compact index range.
+// Every row keeps its entries in the reference's column order (only the
+// names change), CSR(P^T) keeps ascending ORIGINAL fine rows, and the patch
+// factors keep their row order -- every sum is the same sequence of the same
+// operations, so a renumbered V-cycle is bit-identical to the plain one.
+// Level 0's b and u are gathered into the renamed space at the start of the
+// V-cycle and back at its end (three gathers, inside the graph).
+struct HostCsr {
+  int64_t nrows = 0, ncols = 0;
+  std::vector<int64_t> ptr;
+  std::vector<int32_t> col;
+  std::vector<double> val;
+};
+
+static int download_csr(const DevCsr& m, HostCsr* out)
+{
+  out->nrows = m.nrows;
+  out->ncols = m.ncols;
+  out->ptr.resize((size_t)m.nrows + 1);
+  out->col.resize((size_t)m.nnz);
+  out->val.resize((size_t)m.nnz);
+  SMG_CUDA(cudaMemcpy(out->ptr.data(), m.rowptr, sizeof(int64_t) * (size_t)(m.nrows + 1),
+                      cudaMemcpyDeviceToHost));
+  if (m.nnz > 0) {
+    SMG_CUDA(cudaMemcpy(out->col.data(), m.col, sizeof(int32_t) * (size_t)m.nnz, cudaMemcpyDeviceToHost));
+    SMG_CUDA(cudaMemcpy(out->val.data(), m.val, sizeof(double) * (size_t)m.nnz, cudaMemcpyDeviceToHost));
+  }
+  return SMG_OK;
+}
+
+// reverse Cuthill-McKee: BFS from a low-degree node of each component,
+// neighbours in ascending (degree, index) order, order reversed.  perm[old] = new.
+static std::vector<int32_t> rcm_permutation(const HostCsr& a)
+{
+  const int64_t n = a.nrows;
+  std::vector<int32_t> deg((size_t)n);
+  for (int64_t i = 0; i < n; ++i) deg[(size_t)i] = (int32_t)(a.ptr[(size_t)i + 1] - a.ptr[(size_t)i]);
+  std::vector<int32_t> by_deg((size_t)n);
+  for (int64_t i = 0; i < n; ++i) by_deg[(size_t)i] = (int32_t)i;
+  std::stable_sort(by_deg.begin(), by_deg.end(),
+                   [&](int32_t x, int32_t y) { return deg[(size_t)x] < deg[(size_t)y]; });
+  std::vector<uint8_t> seen((size_t)n, 0);
+  std::vector<int32_t> order;
+  order.reserve((size_t)n);
+  std::vector<int32_t> nb;
+  auto bfs = [&](int32_t start, std::vector<int32_t>* out, int32_t* last) {
+    // plain BFS (for the pseudo-peripheral search) when out == nullptr
+    std::vector<int32_t> q{start};
+    std::vector<uint8_t>& mark = seen;
+    mark[(size_t)start] = 2;
+    size_t h = 0;
+    while (h < q.size()) {
+      const int32_t u = q[h++];
+      nb.clear();
+      for (int64_t j = a.ptr[(size_t)u]; j < a.ptr[(size_t)u + 1]; ++j) {
+        const int32_t v = a.col[(size_t)j];
+        if (v != u && !mark[(size_t)v]) nb.push_back(v);
+      }
+      std::sort(nb.begin(), nb.end(), [&](int32_t x, int32_t y) {
+        return deg[(size_t)x] != deg[(size_t)y] ? deg[(size_t)x] < deg[(size_t)y] : x < y;
+      });
+      for (int32_t v : nb)
+        if (!mark[(size_t)v]) {
+          mark[(size_t)v] = 2;
+          q.push_back(v);
+        }
+    }
+    if (last) *last = q.back();
+    if (out) {
+      for (int32_t v : q) {
+        mark[(size_t)v] = 1;
+        out->push_back(v);
+      }
+    } else {
+      for (int32_t v : q) mark[(size_t)v] = 0;   // probe only: unmark
+    }
+  };
+  for (int32_t s0 : by_deg) {
+    if (seen[(size_t)s0]) continue;
+    int32_t start = s0, far = s0;
+    bfs(start, nullptr, &far);   // one pseudo-peripheral step: restart from the far end
+    start = far;
+    bfs(start, &order, nullptr);
+  }
+  std::vector<int32_t> perm((size_t)n);
+  for (int64_t k = 0; k < n; ++k) perm[(size_t)order[(size_t)k]] = (int32_t)(n - 1 - k);
+  return perm;
+}
+
+// rows moved by rperm (old -> new, or identity), columns renamed by cperm,
+// each row's entries in their original order
+static HostCsr renamed(const HostCsr& a, const int32_t* rperm, const int32_t* cperm)
+{
+  HostCsr b;
+  b.nrows = a.nrows;
+  b.ncols = a.ncols;
+  b.ptr.assign((size_t)a.nrows + 1, 0);
+  for (int64_t i = 0; i < a.nrows; ++i) {
+    const int64_t r = rperm ? rperm[i] : i;
+    b.ptr[(size_t)r + 1] = a.ptr[(size_t)i + 1] - a.ptr[(size_t)i];
+  }
+  for (int64_t r = 0; r < a.nrows; ++r) b.ptr[(size_t)r + 1] += b.ptr[(size_t)r];
+  b.col.resize(a.col.size());
+  b.val.resize(a.val.size());
+  for (int64_t i = 0; i < a.nrows; ++i) {
+    const int64_t r = rperm ? rperm[i] : i;
+    int64_t o = b.ptr[(size_t)r];
+    for (int64_t j = a.ptr[(size_t)i]; j < a.ptr[(size_t)i + 1]; ++j, ++o) {
+      b.col[(size_t)o] = cperm ? cperm[a.col[(size_t)j]] : a.col[(size_t)j];
+      b.val[(size_t)o] = a.val[(size_t)j];
+    }
+  }
+  return b;
+}
+
+// CSR of P^T with the coarse rows renamed by cperm and, inside every row, the
+// fine entries in ascending ORIGINAL fine row order (scipy csc_matvec's order),
+// their names taken from rperm
+static HostCsr transposed_original_order(const HostCsr& p, const int32_t* rperm,
+                                         const int32_t* cperm)
+{
+  HostCsr t;
+  t.nrows = p.ncols;
+  t.ncols = p.nrows;
+  t.ptr.assign((size_t)p.ncols + 1, 0);
+  for (int32_t c : p.col) ++t.ptr[(size_t)(cperm ? cperm[c] : c) + 1];
+  for (int64_t r = 0; r < t.nrows; ++r) t.ptr[(size_t)r + 1] += t.ptr[(size_t)r];
+  std::vector<int64_t> fill(t.ptr.begin(), t.ptr.end() - 1);
+  t.col.resize(p.col.size());
+  t.val.resize(p.val.size());
+  for (int64_t i = 0; i < p.nrows; ++i)
+    for (int64_t j = p.ptr[(size_t)i]; j < p.ptr[(size_t)i + 1]; ++j) {
+      const int32_t c = p.col[(size_t)j];
+      const int64_t pos = fill[(size_t)(cperm ? cperm[c] : c)]++;
+      t.col[(size_t)pos] = rperm ? rperm[i] : (int32_t)i;
+      t.val[(size_t)pos] = p.val[(size_t)j];
+    }
+  return t;
+}
+
+static int upload_renamed(const HostCsr& h, Operator& o, DevCsr* out)
+{
+  std::vector<int64_t> c64(h.col.begin(), h.col.end());
+  return build_devcsr(o.allocs, o.device_bytes, h.nrows, h.ncols, h.ptr.data(), c64.data(),
+                      h.val.data(), out);
+}
+
+// a renamed square operator: diagonal found by a linear search (rows are no
+// longer sorted), 1/a_ii by the same IEEE division as the original
+static int make_renamed_operator(const HostCsr& h, const Operator& src, Operator& o)
+{
+  SMG_TRY(upload_renamed(h, o, &o.a));
+  o.first_zero_diag = src.first_zero_diag;
+  o.all_finite = src.all_finite;
+  if (h.nrows == h.ncols && h.nrows > 0) {
+    std::vector<double> diag((size_t)h.nrows, 0.0), inv((size_t)h.nrows);
+    for (int64_t r = 0; r < h.nrows; ++r) {
+      for (int64_t j = h.ptr[(size_t)r]; j < h.ptr[(size_t)r + 1]; ++j)
+        if (h.col[(size_t)j] == r) diag[(size_t)r] = h.val[(size_t)j];
+      inv[(size_t)r] = 1.0 / diag[(size_t)r];
+    }
+    double *dd = nullptr, *di = nullptr;
+    SMG_TRY(dev_upload(o.allocs, o.device_bytes, diag.data(), diag.size(), &dd));
+    SMG_TRY(dev_upload(o.allocs, o.device_bytes, inv.data(), inv.size(), &di));
+    o.diag = dd;
+    o.inv_diag = di;
+    o.a.inv_diag = di;
+  }
+  return SMG_OK;
+}
+
+// the correction of a renamed level: the same regions, factors (shared with
+// the source, never freed here) and launch order, dofs renamed, the patch rows
+// gathered from the renamed operator (original column order, renamed columns)
+static int make_renamed_correction(const Correction& src, const Operator& op,
+                                   const std::vector<int32_t>& perm, Correction& c)
+{
+  c.n_global = src.n_global;
+  c.n_regions = src.n_regions;
+  c.m = src.m;
+  c.max_dofs = src.max_dofs;
+  c.pptr = src.pptr;
+  c.order = src.order;
+  c.foff = src.foff;
+  c.lfac = src.lfac;
+  c.coupled = src.coupled;
+  c.op = &op;
+  std::vector<int32_t> dofs((size_t)src.m);
+  if (src.m > 0)
+    SMG_CUDA(cudaMemcpy(dofs.data(), src.dofs, sizeof(int32_t) * (size_t)src.m, cudaMemcpyDeviceToHost));
+  for (auto& g : dofs) g = perm[(size_t)g];
+  int32_t* dd = nullptr;
+  SMG_TRY(dev_upload(c.allocs, c.device_bytes, dofs.data(), dofs.size(), &dd));
+  c.dofs = dd;
+  SMG_TRY(dev_alloc(c.allocs, c.device_bytes, (size_t)src.m, &c.rbuf));
+  std::vector<int64_t> prow((size_t)src.m + 1, 0);
+  int64_t* dlen = nullptr;
+  SMG_TRY(dev_alloc(c.allocs, c.device_bytes, (size_t)std::max<int64_t>(src.m, 1), &dlen));
+  SMG_CUDA(launch_patch_row_len(op.a, dd, src.m, dlen));
+  SMG_CUDA(cudaMemcpy(prow.data() + 1, dlen, sizeof(int64_t) * (size_t)src.m, cudaMemcpyDeviceToHost));
+  for (int64_t k = 0; k < src.m; ++k) prow[(size_t)k + 1] += prow[(size_t)k];
+  int64_t* dprow = nullptr;
+  int32_t* dpcol = nullptr;
+  double* dpval = nullptr;
+  SMG_TRY(dev_upload(c.allocs, c.device_bytes, prow.data(), prow.size(), &dprow));
+  SMG_TRY(dev_alloc(c.allocs, c.device_bytes, (size_t)prow[(size_t)src.m] + 1, &dpcol));
+  SMG_TRY(dev_alloc(c.allocs, c.device_bytes, (size_t)prow[(size_t)src.m] + 1, &dpval));
+  SMG_CUDA(launch_patch_row_gather(op.a, dd, src.m, dprow, dpcol, dpval));
+  SMG_CUDA(cudaDeviceSynchronize());
+  c.prow = dprow;
+  c.pcol = dpcol;
+  c.pval = dpval;
+  return SMG_OK;
+}
+
+// SMG_RENUMBER: bit l set = renumber level l (never the coarsest); "auto"
+// (default) = levels whose operator is streamed from HBM (val + col > 64 MB)
+static bool renumber_level(int l, int n_levels, const Operator& a)
+{
+  if (l >= n_levels - 1) return false;
+  const char* env = getenv("SMG_RENUMBER");   // read per hierarchy (tests switch it)
+  if (!env || !strcmp(env, "auto")) return false;   // measured first: off unless requested
+  const long mask = strtol(env, nullptr, 0);
+  (void)a;
+  return (mask >> l) & 1;
+}
+
 int smg_hierarchy_create(int n_levels, const smg_operator* const* a, const smg_operator* const* p,
                          const smg_correction* const* corrections, const int* kinds,
                          const int* sweeps, const double* lambda_max, const double* frac,
@@ -2017,6 +2272,66 @@ int smg_hierarchy_create(int n_levels, const smg_operator* const* a, const smg_o
       if (rc == SMG_OK) rc = dev_alloc(h.allocs, h.bytes, n, &L.d);
       if (rc == SMG_OK) rc = dev_alloc(h.allocs, h.bytes, n, &L.r);
     }
+  }
+  // locality renumbering (renumber_level): renamed copies of A_l, P_l, P_{l-1}
+  // and the corrections; the originals stay with their owners untouched
+  h.a_user = h.lv[0].a;
+  for (int l = 0; l < n_levels - 1 && rc == SMG_OK; ++l) {
+    HLevel& L = h.lv[(size_t)l];
+    if (!renumber_level(l, n_levels, *L.a)) continue;
+    HostCsr ah;
+    rc = download_csr(L.a->a, &ah);
+    if (rc != SMG_OK) break;
+    L.perm_h = rcm_permutation(ah);
+    L.renum = true;
+    auto op = std::make_unique<Operator>();
+    const HostCsr ar = renamed(ah, L.perm_h.data(), L.perm_h.data());
+    rc = make_renamed_operator(ar, *L.a, *op);
+    if (rc != SMG_OK) {
+      free_all(op->allocs);
+      break;
+    }
+    if (L.lc && L.lc->n_regions > 0) {
+      auto cc = std::make_unique<Correction>();
+      rc = make_renamed_correction(*L.lc, *op, L.perm_h, *cc);
+      if (rc != SMG_OK) {
+        free_all(cc->allocs);
+        free_all(op->allocs);
+        break;
+      }
+      L.lc = cc.get();
+      h.own_corrs.push_back(std::move(cc));
+    }
+    L.a = op.get();
+    h.own_ops.push_back(std::move(op));
+    if (l == 0) {
+      std::vector<int32_t> inv(L.perm_h.size());
+      for (size_t i = 0; i < L.perm_h.size(); ++i) inv[(size_t)L.perm_h[i]] = (int32_t)i;
+      rc = dev_upload(h.allocs, h.bytes, L.perm_h.data(), L.perm_h.size(), &L.perm);
+      if (rc == SMG_OK) rc = dev_upload(h.allocs, h.bytes, inv.data(), inv.size(), &L.inv);
+      if (rc == SMG_OK) rc = dev_alloc(h.allocs, h.bytes, (size_t)L.n, &h.b0r);
+      if (rc == SMG_OK) rc = dev_alloc(h.allocs, h.bytes, (size_t)L.n, &h.u0r);
+    }
+  }
+  for (int l = 0; l < n_levels - 1 && rc == SMG_OK; ++l) {
+    HLevel& L = h.lv[(size_t)l];
+    const HLevel& N = h.lv[(size_t)l + 1];
+    if (!L.renum && !N.renum) continue;
+    HostCsr ph;
+    rc = download_csr(L.p->a, &ph);
+    if (rc != SMG_OK) break;
+    const int32_t* rp = L.renum ? L.perm_h.data() : nullptr;
+    const int32_t* cp = N.renum ? N.perm_h.data() : nullptr;
+    auto op = std::make_unique<Operator>();
+    rc = upload_renamed(renamed(ph, rp, cp), *op, &op->a);
+    if (rc == SMG_OK) rc = upload_renamed(transposed_original_order(ph, rp, cp), *op, &op->t);
+    if (rc != SMG_OK) {
+      free_all(op->allocs);
+      break;
+    }
+    op->has_t = true;
+    L.p = op.get();
+    h.own_ops.push_back(std::move(op));
   }
   // P's rows on the correction rings (follow-mode prolong-add + correction)
   for (int l = 0; l < n_levels - 1 && rc == SMG_OK; ++l) {
@@ -2171,11 +2486,12 @@ int smg_solve_stationary(smg_hierarchy* h, const double* b, double* u, double rt
   } end_guard{ord};
   HLevel& L0 = H.lv[0];
   const int64_t n = L0.n;
+  const Operator& A0 = *H.a_user;   // b and u are in the caller's order
   double rr = 0, bb = 0;
   EpiArgs ea;
   ea.b = b;
   ea.out = L0.r;
-  SMG_CUDA(launch_csr_stream(L0.a->a, u, Epi::kResidual, ea, st));
+  SMG_CUDA(launch_csr_stream(A0.a, u, Epi::kResidual, ea, st));
   SMG_TRY(H.dots.dot(n, L0.r, L0.r, st, &rr));
   SMG_TRY(H.dots.dot(n, b, b, st, &bb));
   const double residual = std::sqrt(rr);
@@ -2191,7 +2507,7 @@ int smg_solve_stationary(smg_hierarchy* h, const double* b, double* u, double rt
   for (int k = 0; k < max_cycles; ++k) {
     if (history[cnt - 1] <= rtol) break;
     SMG_TRY(run_vcycle(H, b, u, st));
-    SMG_CUDA(launch_csr_stream(L0.a->a, u, Epi::kResidual, ea, st));
+    SMG_CUDA(launch_csr_stream(A0.a, u, Epi::kResidual, ea, st));
     SMG_TRY(H.dots.dot(n, L0.r, L0.r, st, &rr));
     history[cnt++] = std::sqrt(rr) / denom;
   }

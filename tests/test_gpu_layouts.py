@@ -105,3 +105,35 @@ def test_vcycle_identical_across_layouts(name):
         assert np.linalg.norm(u - ref) <= 1e-12 * np.linalg.norm(ref)
     for u in outs[1:]:
         assert np.array_equal(u, outs[0])
+
+
+@pytest.mark.parametrize("name", ["c2s", "c4s", "cpl_p2", "crit7_adj", "c3s"])
+@pytest.mark.parametrize("mask", ["1", "3", "0x7"])
+def test_renumbered_levels_are_bitwise(name, mask, monkeypatch):
+    """Locality renumbering (SMG_RENUMBER bit mask of levels; reverse
+    Cuthill-McKee of each renamed level) only renames rows and columns --
+    every row keeps its entries in the reference's column order, CSR(P^T)
+    keeps ascending original fine rows, the patch factors keep their rows --
+    so V-cycles, stationary histories and CG counts are bit-identical to the
+    plain hierarchy's, and equal the reference's outputs."""
+    import torch
+    from paper_2402_12947_b200.mg import DeviceHierarchy
+    from tests.golden import fixtures
+    z, h = fixtures.load(name)
+    b = torch.from_numpy(z["g/b"]).cuda()
+    res = []
+    for m in ("0", mask):
+        monkeypatch.setenv("SMG_RENUMBER", m)
+        for graphs in (True, False):
+            dh = DeviceHierarchy(h.levels, h.coarse_factor, use_graphs=graphs)
+            u = torch.from_numpy(z["g/u_rand"]).cuda()
+            dh.vcycle(b, u)
+            dh.vcycle(b, u)
+            res.append(u.cpu().numpy())
+        _, hist = dh.solve_stationary(z["g/b"], z["g/u0"], 1e-10, 300)
+        assert len(hist) - 1 == int(z["g/stat_iters"])
+        res.append(np.array(hist))
+    assert np.array_equal(res[0], res[1])
+    assert np.array_equal(res[0], res[3]) and np.array_equal(res[1], res[4])
+    assert np.array_equal(res[2], res[5])
+    assert np.linalg.norm(res[3] - z["g/vcycle2"]) <= 1e-12 * np.linalg.norm(z["g/vcycle2"])
