@@ -2072,6 +2072,52 @@ static std::vector<int32_t> rcm_permutation(const HostCsr& a)
   return perm;
 }
 
+// greedy BFS clusters of `csize` nodes (compact blobs: a SELL window's rows
+// and their x columns sit together), each cluster grown from the first
+// unclustered node adjacent to the previous one, nodes numbered in the order
+// they join.  perm[old] = new.
+static std::vector<int32_t> cluster_permutation(const HostCsr& a, int csize)
+{
+  const int64_t n = a.nrows;
+  std::vector<int32_t> perm((size_t)n, -1);
+  std::vector<int32_t> q;
+  q.reserve((size_t)csize * 8);
+  int32_t next = 0;
+  int64_t scan = 0;          // lowest possibly unclustered node
+  std::vector<int32_t> frontier_seed;
+  int32_t seed = -1;
+  while (next < n) {
+    if (seed < 0 || perm[(size_t)seed] >= 0) {
+      while (scan < n && perm[(size_t)scan] >= 0) ++scan;
+      seed = (int32_t)scan;
+    }
+    // grow one cluster by BFS from seed
+    q.clear();
+    q.push_back(seed);
+    perm[(size_t)seed] = next++;
+    size_t h = 0;
+    int taken = 1;
+    int32_t boundary = -1;
+    while (h < q.size()) {
+      const int32_t u = q[h++];
+      for (int64_t j = a.ptr[(size_t)u]; j < a.ptr[(size_t)u + 1]; ++j) {
+        const int32_t v = a.col[(size_t)j];
+        if (perm[(size_t)v] >= 0) continue;
+        if (taken < csize) {
+          perm[(size_t)v] = next++;
+          ++taken;
+          q.push_back(v);
+        } else if (boundary < 0) {
+          boundary = v;      // the next cluster starts next to this one
+        }
+      }
+      if (taken >= csize && boundary >= 0) break;
+    }
+    seed = boundary;
+  }
+  return perm;
+}
+
 // rows moved by rperm (old -> new, or identity), columns renamed by cperm,
 // each row's entries in their original order
 static HostCsr renamed(const HostCsr& a, const int32_t* rperm, const int32_t* cperm)
@@ -2282,7 +2328,11 @@ int smg_hierarchy_create(int n_levels, const smg_operator* const* a, const smg_o
     HostCsr ah;
     rc = download_csr(L.a->a, &ah);
     if (rc != SMG_OK) break;
-    L.perm_h = rcm_permutation(ah);
+    {
+      const char* ord = getenv("SMG_RENUMBER_ORDER");   // "rcm" | "cluster" (default)
+      L.perm_h = (ord && !strcmp(ord, "rcm")) ? rcm_permutation(ah)
+                                              : cluster_permutation(ah, kSellWindow);
+    }
     L.renum = true;
     auto op = std::make_unique<Operator>();
     const HostCsr ar = renamed(ah, L.perm_h.data(), L.perm_h.data());
