@@ -291,6 +291,11 @@ SMG_API int smg_hierarchy_set_graphs(smg_hierarchy *h, int enable);
 SMG_API int smg_hierarchy_set_option(smg_hierarchy *h, int option, int value);
 /* kernels one V-cycle launches (for launch accounting) */
 SMG_API int smg_hierarchy_launches_per_vcycle(const smg_hierarchy *h, int64_t *launches);
+/* x_c = A_L^{-1} b_c on the coarsest level, exactly as the V-cycle applies it
+ * (mg.py:145 h.coarse_factor.solve; symmetric 64 x 64 tiles of A_L^{-1},
+ * deterministic reduction, plus the refinement step when the hierarchy was
+ * created with coarse_refine).  Device vectors of the coarsest size.          */
+SMG_API int smg_coarse_solve(smg_hierarchy *h, const double *b_c, double *x_c, void *stream);
 
 /* u <- one V-cycle on u (mg.py:127-151; in place).
  * Thread safety ("concurrent vcycle calls on distinct arrays over

@@ -62,6 +62,7 @@ PROTOTYPES = {
     "smg_hierarchy_set_graphs": (ctypes.c_int, [_vp, ctypes.c_int]),
     "smg_hierarchy_set_option": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int]),
     "smg_hierarchy_launches_per_vcycle": (ctypes.c_int, [_vp, _i64p]),
+    "smg_coarse_solve": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "smg_vcycle": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "smg_vcycle_host": (ctypes.c_int, [_vp, _f64p, _f64p, _vp]),
     "smg_vcycle_host_many": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp]),

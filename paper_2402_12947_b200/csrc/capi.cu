@@ -2436,6 +2436,25 @@ int smg_hierarchy_set_option(smg_hierarchy* h, int option, int value)
   return SMG_OK;
 }
 
+int smg_coarse_solve(smg_hierarchy* h, const double* b_c, double* x_c, void* stream)
+{
+  if (!h || !b_c || !x_c) return fail("NULL argument");
+  Hierarchy& H = h->h;
+  std::lock_guard<std::recursive_mutex> lk(H.mu);
+  cudaStream_t st = as_stream(stream);
+  ScratchOrder ord{&H, st};
+  SMG_TRY(ord.begin());
+  SMG_CUDA(launch_sym_apply(H.coarse, b_c, x_c, false, st));
+  if (H.coarse_refine) {
+    EpiArgs ea;
+    ea.b = b_c;
+    ea.out = H.coarse_r;
+    SMG_CUDA(launch_csr_stream(H.lv.back().a->a, x_c, Epi::kResidual, ea, st));
+    SMG_CUDA(launch_sym_apply(H.coarse, H.coarse_r, x_c, true, st));
+  }
+  return ord.end();
+}
+
 int smg_hierarchy_launches_per_vcycle(const smg_hierarchy* h, int64_t* launches)
 {
   if (!h || !launches) return fail("NULL argument");

@@ -262,6 +262,16 @@ class DeviceHierarchy:
     def as_preconditioner(self) -> Callable:
         return as_preconditioner(self)
 
+    def coarse_solve(self, b_c):
+        """x_c = A_L^-1 b_c as the V-cycle applies it (mg.py:145;
+        smg_coarse_solve).  numpy in -> numpy out; CUDA tensor -> tensor."""
+        t = _dev.torch()
+        bt, host = _dev.as_device_vector(b_c, self.n[-1], "b_c")
+        x = t.empty_like(bt)
+        _lib.check(_lib.load().smg_coarse_solve(self.handle, _dev.ptr(bt), _dev.ptr(x),
+                                                _dev.stream_handle()))
+        return x.cpu().numpy() if host is not None and not isinstance(b_c, t.Tensor) else x
+
 
 def _signature(h) -> tuple:
     sig = []

@@ -412,3 +412,16 @@ def test_long_row_operators_multichunk(P):
     u = x.copy()
     P.chebyshev_smooth(a, b, u, 3, cfg)
     assert np.array_equal(u, O.global_smooth(a, b, x.copy(), cfg))
+
+
+def test_coarse_solve_vs_reference(P, fx):
+    """The coarse solve the V-cycle performs (A_L^-1 from the reference's
+    factor, symmetric tiles, deterministic reduction) against the reference's
+    own h.coarse_factor.solve (LAPACK dpotrs, mg.py:145) at a fixed bar, and
+    bit-identical on reruns."""
+    from paper_2402_12947_b200.mg import DeviceHierarchy
+    name, z, h = fx
+    dh = DeviceHierarchy(h.levels, h.coarse_factor)
+    x = dh.coarse_solve(z["g/coarse_b"])
+    assert rel(x, z["g/coarse_x"]) <= TOL_DENSE
+    assert np.array_equal(x, dh.coarse_solve(z["g/coarse_b"]))

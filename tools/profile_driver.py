@@ -27,6 +27,7 @@ def main():
     args = ap.parse_args()
     import torch
     from paper_2402_12947_b200 import _lib, configs, device as D
+    from paper_2402_12947_b200.smoothers import SmootherConfig
     from paper_2402_12947_b200.mg import DeviceHierarchy
     h, b_host, _ = configs.build(configs.WORKLOADS[args.workload])
     dh = DeviceHierarchy(h.levels, h.coarse_factor)
@@ -59,9 +60,9 @@ def main():
         xb = torch.empty_like(xa)
         d = torch.zeros_like(xa)
         bl = torch.randn(n, dtype=torch.float64, device="cuda")
-        lam = float(cfg.lambda_max)
-        theta = 0.5 * (lam + cfg.lambda_min_fraction * lam)
-        kind = 2 if cfg.lambda_min_fraction < 1.0 else 0
+        lam, frac = SmootherConfig.from_any(cfg).chebyshev_parameters()
+        theta = 0.5 * (lam + frac * lam)
+        kind = 2 if frac < 1.0 else 0   # ChebNext, or the Jacobi step
         _lib.check(lib.smg_smoother_step(op.handle, D.ptr(bl), D.ptr(xa), D.ptr(xb), D.ptr(d),
                                          kind, theta, 0.3, 0.7, sh))
         offsets["sweeps"].append({"level": li, "launch": k, "rows": n, "nnz": op.nnz,
