@@ -18,7 +18,7 @@ from paper_2402_12947_b200 import build_lib  # noqa: E402
 def main():
     tag, defines = sys.argv[1], sys.argv[2:]
     out = os.path.join(build_lib.LIBDIR, f"libsimplexmg_b200_{tag}.so")
-    res = subprocess.run([build_lib.NVCC] + build_lib.FLAGS + defines + ["-o", out]
+    res = subprocess.run([build_lib.NVCC] + build_lib.COMPILE_FLAGS + build_lib.LINK_FLAGS[2:] + defines + ["-o", out]
                          + build_lib.sources(), capture_output=True, text=True)
     if res.returncode:
         sys.exit(res.stderr[-4000:])
