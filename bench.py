@@ -327,6 +327,8 @@ def _layout(lib, op) -> str:
         return "unknown"
     if lay.value == 2:
         return f"sell_kernel (SELL-32-sigma256, {unr.value}-deep)"
+    if lay.value == 4:
+        return f"sell_kernel (SELL-32-sigma256, 16-bit delta-coded columns, {unr.value}-deep)"
     if lay.value == 3:
         return f"sell4_kernel (SELL-8x4, 4 lanes per row, {unr.value} batches)"
     kind = "fixed-capacity" if lay.value == 1 else "offset-table"

@@ -79,11 +79,16 @@ SMG_API int smg_operator_info(const smg_operator *op, int64_t *nrows, int64_t *n
  *   SMG_LAYOUT_SELL         SELL-32-sigma256 (sell_kernel); *unroll = loop depth
  *   SMG_LAYOUT_SELL4        SELL-8x4, 4 lanes per row, sigma 64 (sell4_kernel);
  *                           *unroll = batches in flight (2 or 4)
+ *   SMG_LAYOUT_SELL_D16     SELL-32-sigma256 with 16-bit delta-coded columns
+ *                           (10 instead of 12 bytes per entry; same sums);
+ *                           chosen by the rule for SELL operators whose rows
+ *                           need at most two escapes
  * For tiles *unroll is the chunks per tile (1, or 4 for long-row operators). */
 #define SMG_LAYOUT_TILES 0
 #define SMG_LAYOUT_TILES_FIXED 1
 #define SMG_LAYOUT_SELL 2
 #define SMG_LAYOUT_SELL4 3
+#define SMG_LAYOUT_SELL_D16 4
 SMG_API int smg_operator_layout(const smg_operator *op, int *layout, int *unroll);
 /* Force a layout (and SELL loop depth 4/8/16; 0 = by the rule) for the
  * operator and its stored transpose -- for tests and A/B runs; results are

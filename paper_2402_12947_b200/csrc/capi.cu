@@ -8,11 +8,13 @@
 #include "smg_internal.cuh"
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <map>
 #include <memory>
 #include <mutex>
+#include <thread>
 #include <utility>
 
 namespace smg {
@@ -208,7 +210,8 @@ static int build_devcsr(std::vector<void*>& allocs, int64_t& bytes, int64_t nrow
   bool use_sell =
       nrows > 0 && (sell_mode == 1 ||
                     (sell_mode >= 2 && nwin_est >= (short_rows ? sell_min_win : sell_min_win_long)));
-  if (forced_layout >= 0) use_sell = forced_layout == SMG_LAYOUT_SELL && nrows > 0;
+  if (forced_layout >= 0)
+    use_sell = (forced_layout == SMG_LAYOUT_SELL || forced_layout == SMG_LAYOUT_SELL_D16) && nrows > 0;
   d.sell_unroll = short_rows ? 4 : sell_long_unroll;
   if (forced_unroll > 0) d.sell_unroll = forced_unroll >= 16 ? 16 : (forced_unroll >= 8 ? 8 : 4);
   // SELL-8x4 (SMG_SELL4: 0 = only when forced, 1 = every long-row
@@ -331,13 +334,81 @@ static int build_devcsr(std::vector<void*>& allocs, int64_t& bytes, int64_t nrow
         }
       }
     }
+    // SELL-d16 (SMG_LAYOUT_SELL_D16; by the rule only with SMG_SELL_DELTA=1):
+    // 16-bit column codes where every row needs at most two escapes and the
+    // column stream shrinks by >= 10 %.  Measured slower than int32 columns on
+    // C2 (fine sweep 29.1 -> 34.2 us, level 1 25.8 -> 29.5 us, 1,637 -> 1,489
+    // V-cycles/s; profiles/r02/SUMMARY.md): the sweeps are latency-bound, and
+    // the decode sits between the column load and the gather.  Kept as a
+    // forced layout (bit-identical, tests/test_gpu_layouts.py).
+    static const int delta_env = env_int("SMG_SELL_DELTA", 0);
+    const bool delta_forced = forced_layout == SMG_LAYOUT_SELL_D16;
+    bool delta = delta_forced || (delta_env >= 1 && forced_layout < 0);
+    int planes = 0;
+    std::vector<uint16_t> dcol;
+    std::vector<int32_t> c0v, escv;
+    if (delta) {
+      const size_t nslot = (size_t)(nw * kSellWindow);
+      dcol.assign((size_t)total + 8, (uint16_t)0xFFFE);
+      c0v.assign(nslot, 0);
+      escv.assign(2 * nslot, 0);
+      for (int64_t w = 0; w < nw && delta; ++w) {
+        const int64_t r0 = w * kSellWindow;
+        for (int sl = 0; sl < kSellWindow && delta; ++sl) {
+          const int16_t pr = perm[(size_t)(r0 + sl)];
+          if (pr < 0) continue;
+          const int64_t r = r0 + pr;
+          const int64_t base = sptr[(size_t)(w * kSellSlices + sl / 32)] + (sl % 32);
+          int ne = 0;
+          int64_t prev = 0;
+          for (int64_t j = rowptr[r]; j < rowptr[r + 1]; ++j) {
+            const int64_t cj = col32[(size_t)j];
+            uint16_t code;
+            if (j == rowptr[r]) {
+              c0v[(size_t)(r0 + sl)] = (int32_t)cj;
+              code = 0;
+            } else if (cj - prev >= 0 && cj - prev <= 0xFFFD) {
+              code = (uint16_t)(cj - prev);
+            } else if (ne < 2) {
+              escv[(size_t)ne * nslot + (size_t)(r0 + sl)] = (int32_t)cj;
+              ++ne;
+              code = 0xFFFF;
+            } else {
+              delta = false;   // a row with three far jumps: keep int32 columns
+              break;
+            }
+            prev = cj;
+            dcol[(size_t)(base + (j - rowptr[r]) * 32)] = code;
+          }
+          planes = std::max(planes, ne);
+        }
+      }
+      // worth it only if the column stream really shrinks
+      if (delta && !delta_forced &&
+          10 * (2 * total + 4 * nw * kSellWindow * (1 + planes)) > 9 * 4 * total)
+        delta = false;
+    }
     int64_t* dsp = nullptr;
     int16_t* dperm = nullptr;
     int32_t* dsc = nullptr;
     double* dsv = nullptr;
     SMG_TRY(dev_upload(allocs, bytes, sptr.data(), sptr.size(), &dsp));
     SMG_TRY(dev_upload(allocs, bytes, perm.data(), perm.size(), &dperm));
-    SMG_TRY(dev_upload(allocs, bytes, scol.data(), scol.size(), &dsc));
+    if (delta) {
+      uint16_t* ddc = nullptr;
+      int32_t *dc0 = nullptr, *desc = nullptr;
+      escv.resize((size_t)std::max(planes, 1) * (size_t)(nw * kSellWindow));
+      SMG_TRY(dev_upload(allocs, bytes, dcol.data(), dcol.size(), &ddc));
+      SMG_TRY(dev_upload(allocs, bytes, c0v.data(), c0v.size(), &dc0));
+      SMG_TRY(dev_upload(allocs, bytes, escv.data(), escv.size(), &desc));
+      d.sell_delta = true;
+      d.sell_esc_planes = planes;
+      d.sell_dcol = ddc;
+      d.sell_c0 = dc0;
+      d.sell_esc = desc;
+    } else {
+      SMG_TRY(dev_upload(allocs, bytes, scol.data(), scol.size(), &dsc));
+    }
     SMG_TRY(dev_upload(allocs, bytes, sval.data(), sval.size(), &dsv));
     d.sell = true;
     // software-pipelined loop for long rows up to SMG_SELL_PIPE_MAX_ROW (64)
@@ -1054,7 +1125,7 @@ static int relayout(Operator& o, DevCsr& m, int layout, int unroll)
 int smg_operator_set_layout(smg_operator* op, int layout, int unroll)
 {
   if (!op) return fail("operator is NULL");
-  if (layout < SMG_LAYOUT_TILES || layout > SMG_LAYOUT_SELL4) return fail("unknown layout");
+  if (layout < SMG_LAYOUT_TILES || layout > SMG_LAYOUT_SELL_D16) return fail("unknown layout");
   SMG_CUDA(cudaDeviceSynchronize());
   SMG_TRY(relayout(op->o, op->o.a, layout, unroll));
   if (op->o.has_t) SMG_TRY(relayout(op->o, op->o.t, layout, unroll));
@@ -1066,7 +1137,8 @@ int smg_operator_layout(const smg_operator* op, int* layout, int* unroll)
   if (!op) return fail("operator is NULL");
   const DevCsr& m = op->o.a;
   if (layout)
-    *layout = m.sell ? (m.sell_lanes == 4 ? SMG_LAYOUT_SELL4 : SMG_LAYOUT_SELL)
+    *layout = m.sell ? (m.sell_lanes == 4 ? SMG_LAYOUT_SELL4
+                                          : (m.sell_delta ? SMG_LAYOUT_SELL_D16 : SMG_LAYOUT_SELL))
                      : (m.fixed ? SMG_LAYOUT_TILES_FIXED : SMG_LAYOUT_TILES);
   if (unroll) *unroll = m.sell ? m.sell_unroll : (m.multichunk ? kMaxTileChunks : 1);
   return SMG_OK;
@@ -1714,6 +1786,42 @@ static int build_ring(const Operator& o, const std::vector<int32_t>& pptr,
   return gather_rows(c.allocs, c.device_bytes, o.a, drows, c.ring_total, &c.ringA);
 }
 
+// Packed lower triangle (row-major, even length) of (L L^T)^{-1} from the
+// reference's factor c (cho_factor layout, nd x nd row-major, lower triangle
+// valid): M = L^{-1} by row-oriented forward substitution, then
+// A^{-1} = M^T M accumulated row by row of M -- LAPACK dpotri's two steps
+// (dtrtri, dlauum) with contiguous inner loops.
+static void packed_spd_inverse(int64_t nd, const double* f, double* out, std::vector<double>& m)
+{
+  m.assign((size_t)(nd * (nd + 1) / 2 + nd), 0.0);
+  double* tmp = m.data() + nd * (nd + 1) / 2;
+  auto T = [](int64_t i) { return i * (i + 1) / 2; };
+  for (int64_t i = 0; i < nd; ++i) {
+    // row i of M: M[i][j] = -(sum_{k=j}^{i-1} L[i][k] M[k][j]) / L[i][i], M[i][i] = 1 / L[i][i]
+    for (int64_t j = 0; j < i; ++j) tmp[j] = 0.0;
+    for (int64_t k = 0; k < i; ++k) {
+      const double lik = f[i * nd + k];
+      const double* mk = m.data() + T(k);
+      for (int64_t j = 0; j <= k; ++j) tmp[j] += lik * mk[j];
+    }
+    const double inv = 1.0 / f[i * nd + i];
+    double* mi = m.data() + T(i);
+    for (int64_t j = 0; j < i; ++j) mi[j] = -tmp[j] * inv;
+    mi[i] = inv;
+  }
+  const int64_t len = (nd * (nd + 1) / 2 + 1) & ~int64_t(1);
+  for (int64_t q = 0; q < len; ++q) out[q] = 0.0;
+  for (int64_t k = 0; k < nd; ++k) {
+    // A^{-1}[i][j] += M[k][i] M[k][j] for j <= i <= k
+    const double* mk = m.data() + T(k);
+    for (int64_t i = 0; i <= k; ++i) {
+      const double s = mk[i];
+      double* oi = out + T(i);
+      for (int64_t j = 0; j <= i; ++j) oi[j] += s * mk[j];
+    }
+  }
+}
+
 int smg_correction_create(const smg_operator* a, int64_t n_regions, const int64_t* roff,
                           const int64_t* dofs, const int64_t* foff, const double* factors,
                           smg_correction** out)
@@ -1733,13 +1841,16 @@ int smg_correction_create(const smg_operator* a, int64_t n_regions, const int64_
   int32_t max_dofs = 0;
   for (int64_t r = 0; r < n_regions; ++r)
     max_dofs = std::max<int32_t>(max_dofs, (int32_t)(roff[r + 1] - roff[r]));
+  // SMG_PATCH_SYM=0: keep the factor (panel substitution) for the larger regions
+  const char* sym_env = getenv("SMG_PATCH_SYM");
+  const bool sym = !(sym_env && sym_env[0] == '0');
   for (int64_t r = 0; r < n_regions; ++r) {
     const int64_t nd = roff[r + 1] - roff[r];
     if (nd <= 0) return fail("region " + std::to_string(r) + " is empty");
     pptr[(size_t)r] = (int32_t)roff[r];
     // slot = [packed L, even length][inverted 32x32 diagonal blocks]; 16-byte
     // aligned and even-length so one bulk copy stages the whole slot
-    poff[(size_t)r + 1] = poff[(size_t)r] + patch_slot_doubles(nd, max_dofs);
+    poff[(size_t)r + 1] = poff[(size_t)r] + patch_slot_doubles(nd, max_dofs, sym);
     for (int64_t k = roff[r]; k < roff[r + 1]; ++k) {
       const int64_t g = dofs[k];
       if (g < 0 || g >= n)
@@ -1755,12 +1866,18 @@ int smg_correction_create(const smg_operator* a, int64_t n_regions, const int64_
   }
   pptr[(size_t)n_regions] = (int32_t)m;
   // pack lower triangles (row-major) and invert each 32x32 diagonal block
-  // (row stride kDinvLd) so the panel triangle solves become small GEMVs
+  // (row stride kDinvLd) so the panel triangle solves become small GEMVs;
+  // symmetric-inverse regions get the packed lower triangle of A[B,B]^{-1}
   std::vector<double> packed((size_t)poff[(size_t)n_regions], 0.0);
+  std::vector<int64_t> sym_regions;
   for (int64_t r = 0; r < n_regions; ++r) {
     const int64_t nd = roff[r + 1] - roff[r];
     const double* f = factors + foff[r];
     double* base = packed.data() + poff[(size_t)r];
+    if (patch_is_sym(nd, max_dofs, sym)) {
+      sym_regions.push_back(r);
+      continue;
+    }
     double* dst = base;
     for (int64_t i = 0; i < nd; ++i)
       for (int64_t j = 0; j <= i; ++j) *dst++ = f[i * nd + j];
@@ -1788,12 +1905,35 @@ int smg_correction_create(const smg_operator* a, int64_t n_regions, const int64_
       }
     }
   }
+  if (!sym_regions.empty()) {
+    // largest first, a few host threads (C5: 1000 regions of up to 512 dofs)
+    std::stable_sort(sym_regions.begin(), sym_regions.end(), [&](int64_t x, int64_t y) {
+      return roff[x + 1] - roff[x] > roff[y + 1] - roff[y];
+    });
+    std::atomic<size_t> next{0};
+    auto work = [&]() {
+      std::vector<double> scratch;
+      for (size_t q; (q = next.fetch_add(1)) < sym_regions.size();) {
+        const int64_t r = sym_regions[q];
+        const int64_t nd = roff[r + 1] - roff[r];
+        packed_spd_inverse(nd, factors + foff[r], packed.data() + poff[(size_t)r], scratch);
+      }
+    };
+    unsigned nt = std::thread::hardware_concurrency();
+    nt = std::max(1u, std::min(nt, 32u));
+    nt = (unsigned)std::min<size_t>(nt, sym_regions.size());
+    std::vector<std::thread> pool;
+    for (unsigned t = 1; t < nt; ++t) pool.emplace_back(work);
+    work();
+    for (auto& th : pool) th.join();
+  }
   auto* cc = new smg_correction();
   Correction& c = cc->c;
   c.n_global = n;
   c.n_regions = (int32_t)n_regions;
   c.m = m;
   c.max_dofs = max_dofs;
+  c.sym = sym;
   c.op = &o;
   int32_t* dp = nullptr;
   int32_t* dd = nullptr;
@@ -2215,6 +2355,7 @@ static int make_renamed_correction(const Correction& src, const Operator& op,
   c.foff = src.foff;
   c.lfac = src.lfac;
   c.coupled = src.coupled;
+  c.sym = src.sym;
   c.op = &op;
   std::vector<int32_t> dofs((size_t)src.m);
   if (src.m > 0)

@@ -159,20 +159,31 @@ constexpr int64_t kSmemBudget = 220 * 1024;    // dynamic smem per CTA (of 227 K
 enum PatchMode : int { kAddResidualSolve = 0, kSolveFromBuf = 1, kResidualOnly = 2, kFollow = 3 };
 constexpr int kFlagStream = 1;      // factors larger than shared memory stream through a ring
 constexpr int kFlagL2Prefetch = 2;  // ... after an L2 prefetch of the whole factor
+constexpr int kFlagSym = 4;         // the correction holds packed A[B,B]^{-1} for its larger regions
+constexpr int kFlagSymStageShift = 12;  // launch flags bits 12..30: symmetric ring stage, in pairs of doubles
 
 // Phase timestamps (SM clock) of the first 256 CTAs, compiled in only for the
 // tools/trace_patch.py build (-DSMG_PATCH_TRACE); no cost otherwise.
 #ifdef SMG_PATCH_TRACE
-__device__ unsigned long long g_patch_trace[256][8];
+__device__ unsigned long long g_patch_trace[256][16];
 #define PTRACE(k)                                                  \
   do {                                                             \
     if (threadIdx.x == 0 && blockIdx.x < 256)                      \
       g_patch_trace[blockIdx.x][k] = (unsigned long long)clock64(); \
   } while (0)
+#define PTRACE_ACC(k, v)                                            \
+  do {                                                              \
+    if (threadIdx.x == 0 && blockIdx.x < 256) g_patch_trace[blockIdx.x][k] += (unsigned long long)(v); \
+  } while (0)
+#define PTRACE_CLK() clock64()
 #else
 #define PTRACE(k) \
   do {            \
   } while (0)
+#define PTRACE_ACC(k, v) \
+  do {                   \
+  } while (0)
+#define PTRACE_CLK() 0ll
 #endif
 
 static int patch_env(const char* name, int dflt)
@@ -193,6 +204,8 @@ struct PatchSmem {
   int64_t x_off, lo_off, off_off, prod_off, l_off, tri_cap, bytes;
   int64_t stage;   // > 0: streaming ring of `nst` stages of `stage` doubles at l_off
   int nst;
+  int64_t y_off, z_off;   // symmetric-inverse path: column sums / row dots (double[n2] each)
+  bool sym;               // ring carries packed A^{-1} rows (sym_apply), not factor rows
 };
 
 #ifndef SMG_CHUNK_ROWS
@@ -222,8 +235,14 @@ static int stages_env()
 }
 
 
+// symmetric-inverse ring geometry: a stage holds one chunk of 4 rows
+// (4 (nmax + 2) doubles), as many stages (2..8) as fit SMG_SYM_RING_KB
+// (default 66 KB: four stages and two CTAs per SM for 512-dof regions)
+constexpr int kSymRowsLayout = 4;   // rows per chunk of the symmetric-inverse ring (= kSymRows)
+
 __host__ __device__ inline PatchSmem patch_smem_layout(int nmax, bool allow_stream = true,
-                                                       int nst = kRingStages)
+                                                       int nst = kRingStages, bool sym = false,
+                                                       int64_t sym_stage = 0, int sym_nst = 0)
 {
   PatchSmem p;
   p.nst = nst < 2 ? 2 : (nst > kMaxRingStages ? kMaxRingStages : nst);
@@ -234,11 +253,27 @@ __host__ __device__ inline PatchSmem patch_smem_layout(int nmax, bool allow_stre
   p.prod_off = p.off_off + ((4 * (n2 + 2) + 15) & ~int64_t(15));  // double[kProdCap]
   // the product buffer doubles as the streamed path's inverted-block double buffer
   p.l_off = p.prod_off + 8 * (kProdCap > 2 * kDinvBlock ? kProdCap : 2 * kDinvBlock);
+  p.y_off = p.z_off = 0;
+  p.sym = sym && nmax > 4 * kPanel;
+  p.stage = 0;
+  if (p.sym) {
+    // regions of more than 128 dofs (and 65..128 beside them) stream the packed
+    // lower triangle of their inverse through the ring; smaller ones are staged
+    p.y_off = p.l_off;
+    p.z_off = p.y_off + 8 * n2;
+    p.l_off = p.z_off + 8 * n2;
+    (void)sym_stage;
+    p.stage = ((int64_t)kSymRowsLayout * (nmax + 2) + 1) & ~int64_t(1);
+    p.nst = sym_nst < 2 ? 2 : (sym_nst > kMaxRingStages ? kMaxRingStages : sym_nst);
+    const int64_t need = patch_slot_max(nmax, true);
+    p.tri_cap = p.nst * p.stage > need ? p.nst * p.stage : need;
+    p.bytes = p.l_off + 8 * p.tri_cap;
+    return p;
+  }
   int64_t cap = (kSmemBudget - p.l_off) / 8;
   if (cap < 0) cap = 0;
   cap &= ~int64_t(1);
-  const int64_t need = patch_slot_max(nmax);
-  p.stage = 0;
+  const int64_t need = patch_slot_max(nmax, false);
   if (need <= cap || !allow_stream) {  // every region's slot (factor + inverted blocks) fits: stage it whole
     p.tri_cap = need;
     p.bytes = p.l_off + 8 * need;
@@ -463,10 +498,194 @@ __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_
   }
 }
 
+// ---------------------------------------------------------------------------
+// Symmetric-inverse correction: x = A[B,B]^{-1} r from the packed lower
+// triangle M of the inverse (row-major, row i = M[i][0..i]), read from HBM
+// once.  Chunks of kSymRows = 4 rows -- contiguous in the packed layout -- flow
+// HBM -> shared memory by 1D bulk copies through a ring of "full" (bytes
+// landed) and "empty" (all eight warps done) mbarriers; there is no CTA-wide
+// barrier per chunk, so warps drift and the copies stay ahead.  A chunk with
+// rows [i0, i0 + 4) is a strip of 32-column blocks; warp w owns the blocks
+// cb = w, w + 8, ... and lane l the column j = 32 cb + l of each:
+//   column part  y_j += sum_{i in chunk, i > j} M[i][j] r_i   (private to the lane;
+//                one running sum per column over the whole solve)
+//   row part     a_k += M[i0+k][j] r_j  for the 4 rows (j <= i), accumulated
+//                over the warp's blocks, then ONE 4-value butterfly per warp
+//                per chunk (6 exchanges instead of 4 x 5) leaves the warp's
+//                partial of row i0 + k on a lane.
+// Chunk c is closed by warp c mod 8: it waits for the chunk's "empty" phase,
+// adds the eight warps' row partials in warp order (z), and requests chunk
+// c + nst into the freed stage.  At the end x = y + z.  Nothing in a chunk
+// depends on another chunk's result: the ring is the only chain.  Fixed order
+// everywhere: deterministic, independent of the ring depth.
+constexpr int kSymRows = 4;
+static_assert(kSymRows == kSymRowsLayout, "ring stage size and chunk rows must agree");
+
+struct SymIssue {
+  int i0 = 0;      // first row of the next chunk to request
+  int stage = 0;   // ring stage it goes into
+};
+
+// 32-bit triangle numbers (regions are far below 65k dofs)
+__device__ __forceinline__ int tri32(int i) { return (i * (i + 1)) >> 1; }
+
+__device__ __forceinline__ void sym_issue_next(const double* Mg, double* ring, int S, int nst,
+                                               int n, SymIssue& si, uint64_t* bars)
+{
+  const int i1 = min(si.i0 + kSymRows, n);
+  const int a = tri32(si.i0) & ~1;
+  const int b = (tri32(i1) + 1) & ~1;
+  SMG_DCHECK(b - a <= S && i1 > si.i0 && si.stage < nst);
+  uint64_t* bar = &bars[si.stage];
+  const uint32_t bytes = (uint32_t)(b - a) * 8u;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(psmem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(psmem_u32(ring + si.stage * S)),
+      "l"(Mg + a), "r"(bytes), "r"(psmem_u32(bar))
+      : "memory");
+  si.i0 = i1;
+  if (++si.stage == nst) si.stage = 0;
+}
+
+// thread 0, at kernel entry (the inverse is static data: before the
+// dependency wait, overlapping the residual): barriers + the first nst chunks
+__device__ __forceinline__ void sym_ring_start(const double* Mg, double* ring, int S, int nst,
+                                               int n, SymIssue& si, uint64_t* full, uint64_t* empty)
+{
+  for (int q = 0; q < nst; ++q) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(psmem_u32(&full[q])) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(psmem_u32(&empty[q])),
+                 "r"(kSolveWarps)
+                 : "memory");
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  for (int q = 0; q < nst && si.i0 < n; ++q) sym_issue_next(Mg, ring, S, nst, n, si, full);
+}
+
+// s_x holds r on entry (visible to all threads) and x on return (after a
+// barrier).  part: nst x kSymRows x kSolveWarps doubles (per-warp row partials
+// of the chunks in flight).
+__device__ void sym_apply(const double* __restrict__ Mg, double* ring, int S, int nst, int n,
+                          double* s_x, double* s_y, double* s_z, double* part, uint64_t* full,
+                          uint64_t* empty)
+{
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  // this lane's columns are 32 (warp + 8 q) + lane: zero their running sums
+  for (int j = warp * 32 + lane; j < n; j += kSolveThreads) s_y[j] = 0.0;
+  const int nchunks = (n + kSymRows - 1) / kSymRows;
+  int stg = 0, closer = 0;
+  uint32_t phase = 0;
+  for (int c = 0; c < nchunks; ++c) {
+    const int i0 = c * kSymRows;
+    const int crows = min(kSymRows, n - i0);
+    ring_wait(&full[stg], phase);
+    // M[i0 + k][j] = base[roff[k] + j]
+    const double* base = ring + stg * S - (tri32(i0) & ~1);
+    int roff[kSymRows];
+    double ri[kSymRows], a[kSymRows];
+#pragma unroll
+    for (int k = 0; k < kSymRows; ++k) {
+      roff[k] = tri32(i0 + k);
+      ri[k] = k < crows ? s_x[i0 + k] : 0.0;
+      a[k] = 0.0;
+    }
+    const int last = i0 + crows - 1;   // last column any row of the chunk reaches
+    for (int c0 = warp * 32; c0 <= last; c0 += kSolveWarps * 32) {
+      const int j = c0 + lane;
+      double m[kSymRows];
+      if (c0 + 31 < i0) {
+        // the block lies strictly left of every row's diagonal: no predicates
+#pragma unroll
+        for (int k = 0; k < kSymRows; ++k) m[k] = k < crows ? base[roff[k] + j] : 0.0;
+        const double rj = s_x[j];
+        double y = s_y[j];
+#pragma unroll
+        for (int k = 0; k < kSymRows; ++k) {
+          a[k] += m[k] * rj;
+          y += m[k] * ri[k];
+        }
+        s_y[j] = y;
+      } else {
+        // block crossing the diagonal: row part j <= i, column part j < i
+#pragma unroll
+        for (int k = 0; k < kSymRows; ++k)
+          m[k] = (k < crows && j <= i0 + k) ? base[roff[k] + j] : 0.0;
+        const double rj = j < n ? s_x[j] : 0.0;
+        double y = j < n ? s_y[j] : 0.0;
+#pragma unroll
+        for (int k = 0; k < kSymRows; ++k) {
+          a[k] += m[k] * rj;
+          if (j < i0 + k) y += m[k] * ri[k];
+        }
+        if (j < n) s_y[j] = y;
+      }
+    }
+    // 4-value butterfly: after it the lanes with (lane & 7) == 0 hold the
+    // warp's partial of row i0 + 2 b4 + b3 (b = bits of the lane)
+    {
+      const bool u16 = (lane & 16) != 0;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const double send = u16 ? a[k] : a[k + 2];
+        const double keep = u16 ? a[k + 2] : a[k];
+        a[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+      }
+      const bool u8 = (lane & 8) != 0;
+      const double send = u8 ? a[0] : a[1];
+      const double keep = u8 ? a[1] : a[0];
+      double v = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      if ((lane & 7) == 0) {
+        const int row = ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
+        part[(stg * kSymRows + row) * kSolveWarps + warp] = v;
+      }
+    }
+    // this warp is done with the stage (its reads and its partials are
+    // ordered before the arrival: release)
+    __syncwarp();
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(psmem_u32(&empty[stg]))
+                   : "memory");
+    if (warp == closer) {
+      // close the chunk: every warp has arrived (acquire) -> z, then the refill
+      ring_wait(&empty[stg], phase);
+      if (lane < crows) {
+        const double* pp = part + (stg * kSymRows + lane) * kSolveWarps;
+        double z = 0.0;
+#pragma unroll
+        for (int w = 0; w < kSolveWarps; ++w) z += pp[w];
+        s_z[i0 + lane] = z;
+      }
+      __syncwarp();
+      if (lane == 0 && c + nst < nchunks) {
+        SymIssue si;
+        si.i0 = (c + nst) * kSymRows;
+        si.stage = stg;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        sym_issue_next(Mg, ring, S, nst, n, si, full);
+      }
+    }
+    if (++closer == kSolveWarps) closer = 0;
+    if (++stg == nst) {
+      stg = 0;
+      phase ^= 1u;
+    }
+  }
+  __syncthreads();   // every chunk closed: z complete, y owned per lane
+  for (int j = threadIdx.x; j < n; j += kSolveThreads) s_x[j] = s_z[j] + s_y[j];
+  __syncthreads();
+}
+
 __host__ __device__ __forceinline__ int nmax_ring(const FollowArgs& fa) { return fa.ring_max; }
 
 template <int kMode>
-__global__ void __launch_bounds__(kSolveThreads)
+__global__ void __launch_bounds__(kSolveThreads, 2)
 patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
              const double* __restrict__ pval, const int32_t* __restrict__ pptr,
              const int32_t* __restrict__ dofs,
@@ -488,7 +707,11 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   __shared__ uint64_t s_bar;
   __shared__ uint64_t s_ring_bar[kMaxRingStages];
   __shared__ uint64_t s_dinv_bar[2];
-  const PatchSmem L_ = patch_smem_layout(nmax, allow_stream, (flags >> kFlagStagesShift) & 15);
+  __shared__ uint64_t s_sym_empty[kMaxRingStages];
+  const bool sym_on = (flags & kFlagSym) != 0;
+  const PatchSmem L_ = patch_smem_layout(nmax, allow_stream, (flags >> kFlagStagesShift) & 15, sym_on,
+                                         (int64_t)((unsigned)flags >> kFlagSymStageShift) * 2,
+                                         (flags >> kFlagStagesShift) & 15);
   double* s_x = reinterpret_cast<double*>(psm + L_.x_off);
   int32_t* s_off = reinterpret_cast<int32_t*>(psm + L_.off_off);
   double* s_prod = reinterpret_cast<double*>(psm + L_.prod_off);
@@ -502,8 +725,9 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   SMG_DCHECK(n > 0 && n <= nmax);
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int64_t nslot = patch_slot_doubles(n, nmax);
-  const bool staged = kMode != kResidualOnly && nslot <= L_.tri_cap;
+  const int64_t nslot = patch_slot_doubles(n, nmax, sym_on);
+  const bool is_sym = kMode != kResidualOnly && patch_is_sym(n, nmax, sym_on);
+  const bool staged = kMode != kResidualOnly && !is_sym && nslot <= L_.tri_cap;
   SMG_DCHECK(L_.bytes <= (int64_t)227 * 1024);
   const double* __restrict__ Lg = lfac + foff[p];
   // this thread's own patch dof (rows < kSolveThreads): b and the scatter
@@ -521,11 +745,15 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   // bulk copy stages the whole factor while the residual is formed
   if (staged && threadIdx.x == 0)
     factor_bulk_load(s_L, Lg, (uint32_t)(nslot * 8), &s_bar);
+  // symmetric-inverse region: the first chunks of the inverse are requested now
+  SymIssue sym_iss;
+  if (is_sym && threadIdx.x == 0)
+    sym_ring_start(Lg, s_L, (int)L_.stage, L_.nst, n, sym_iss, s_ring_bar, s_sym_empty);
   // a factor streamed through the ring: pull all of it towards L2 now, so the
   // ring's dependent copies hit L2 instead of paying HBM latency one chunk at
   // a time (the slot is contiguous, 16-byte aligned, even length)
-  if (!staged && kMode != kResidualOnly && L_.stage > 0 && (flags & kFlagL2Prefetch) &&
-      warp == 0) {
+  if (!staged && !is_sym && kMode != kResidualOnly && L_.stage > 0 &&
+      (flags & kFlagL2Prefetch) && warp == 0) {
     const int64_t total = nslot * 8;
     constexpr int64_t kPiece = 32 * 1024;
     for (int64_t off = (int64_t)lane * kPiece; off < total; off += 32 * kPiece) {
@@ -730,7 +958,11 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   const double* Dinv = L + patch_tri_even(n);   // inverted diagonal blocks, row stride 33
 
   const int blk = patch_block(n, nmax);
-  if (blk == 2 * kPanel) {
+  if (is_sym) {
+    // (the residual's product buffer is free now: per-warp row partials)
+    sym_apply(Lg, s_L, (int)L_.stage, L_.nst, n, s_x, reinterpret_cast<double*>(psm + L_.y_off),
+              reinterpret_cast<double*>(psm + L_.z_off), s_prod, s_ring_bar, s_sym_empty);
+  } else if (blk == 2 * kPanel) {
     // x = L^{-T} (L^{-1} r): two GEMVs with the stored inverse
     gemv_inv<2 * kPanel>(L + patch_tri_even(n), s_x, n, false, s_prod);
     gemv_inv<2 * kPanel>(L + patch_tri_even(n), s_x, n, true, s_prod);
@@ -890,9 +1122,36 @@ cudaError_t launch_gather(const int32_t* idx, int64_t m, const double* src, doub
   return cudaGetLastError();
 }
 
+// launch flags and shared-memory carve-up of a correction (host side; the
+// kernel rebuilds the same layout from the flags)
+struct PatchGeom {
+  int flags;
+  PatchSmem L;
+};
+
+static PatchGeom patch_geom(const Correction& c)
+{
+  static const int l2pf = patch_env("SMG_PATCH_L2PF", 0);  // measured slower on C5 (222 vs 240 us)
+  // read per launch (tests vary it); a graph bakes the value of its capture
+  const int sym_ring_kb = patch_env("SMG_SYM_RING_KB", 66);
+  const bool st = !nostream_env();
+  int nst = stages_env();
+  int64_t S = 0;
+  if (c.sym && c.max_dofs > 4 * kPanel) {
+    S = ((int64_t)kSymRowsLayout * (c.max_dofs + 2) + 1) & ~int64_t(1);
+    int64_t q = (int64_t)sym_ring_kb * 1024 / (8 * S);
+    nst = (int)(q < 2 ? 2 : (q > kMaxRingStages ? kMaxRingStages : q));
+  }
+  PatchGeom g;
+  g.flags = (st ? kFlagStream : 0) | (l2pf ? kFlagL2Prefetch : 0) | (nst << kFlagStagesShift) |
+            (c.sym ? kFlagSym : 0) | (int)((S / 2) << kFlagSymStageShift);
+  g.L = patch_smem_layout(c.max_dofs, st, nst, c.sym, S, nst);
+  return g;
+}
+
 template <int kMode>
 static cudaError_t launch_patch(const Correction& c, size_t smem, const double* b,
-                                const double* u_res, double* tgt, int add, int allow_stream,
+                                const double* u_res, double* tgt, int add, int flags,
                                 cudaStream_t s)
 {
   cudaLaunchConfig_t cfg = {};
@@ -905,10 +1164,7 @@ static cudaError_t launch_patch(const Correction& c, size_t smem, const double* 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  static const int l2pf = patch_env("SMG_PATCH_L2PF", 0);  // measured slower on C5 (222 vs 240 us)
   static const int lpt = patch_env("SMG_PATCH_LPT", 1);
-  const int flags = (allow_stream ? kFlagStream : 0) | (l2pf ? kFlagL2Prefetch : 0) |
-                    (stages_env() << kFlagStagesShift);
   return cudaLaunchKernelEx(&cfg, patch_kernel<kMode>, c.prow, c.pcol, c.pval, c.pptr, c.dofs,
                             c.foff, c.lfac, b, u_res, c.rbuf, tgt, add, c.max_dofs, flags,
                             lpt ? c.order : (const int32_t*)nullptr, FollowArgs(),
@@ -918,7 +1174,7 @@ static cudaError_t launch_patch(const Correction& c, size_t smem, const double* 
 
 static size_t follow_smem(const Correction& c)
 {
-  const PatchSmem L = patch_smem_layout(c.max_dofs, !nostream_env(), stages_env());
+  const PatchSmem L = patch_geom(c).L;
   return (size_t)L.bytes + 8 * (size_t)((c.ring_max + 1) & ~1) + 4 * (size_t)(c.ring_max + 2);
 }
 
@@ -929,7 +1185,6 @@ bool patch_follow_fits(const Correction& c) { return follow_smem(c) <= 227 * 102
 cudaError_t launch_patch_follow(const Correction& c, const FollowArgs& fa, cudaStream_t s)
 {
   if (c.n_regions == 0) return cudaSuccess;
-  const int st = nostream_env() ? 0 : 1;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)c.n_regions);
   cfg.blockDim = dim3(kSolveThreads);
@@ -945,7 +1200,7 @@ cudaError_t launch_patch_follow(const Correction& c, const FollowArgs& fa, cudaS
   f.ring_max = c.ring_max;
   return cudaLaunchKernelEx(&cfg, patch_kernel<kFollow>, c.prow, c.pcol, c.pval, c.pptr, c.dofs,
                             c.foff, c.lfac, fa.b, (const double*)nullptr, c.rbuf, fa.out, 1,
-                            c.max_dofs, (st ? kFlagStream : 0) | (stages_env() << kFlagStagesShift),
+                            c.max_dofs, patch_geom(c).flags,
                             lpt ? c.order : (const int32_t*)nullptr, f, c.ring_ptr, c.ring_rows,
                             c.plcol, c.bpos);
 }
@@ -956,8 +1211,10 @@ cudaError_t launch_patch_residual(const DevCsr& a, const Correction& c, const do
 {
   (void)a;
   if (c.n_regions == 0) return cudaSuccess;
-  const PatchSmem L = patch_smem_layout(c.max_dofs);
-  return launch_patch<kResidualOnly>(c, (size_t)L.l_off, b, u, nullptr, 0, 1, s);
+  const PatchGeom g = patch_geom(c);
+  // only the residual buffers (everything before the factor / ring area)
+  const size_t smem = (size_t)(g.L.sym ? g.L.y_off : g.L.l_off);
+  return launch_patch<kResidualOnly>(c, smem, b, u, nullptr, 0, g.flags, s);
 }
 
 static size_t smem_pad()
@@ -975,13 +1232,12 @@ cudaError_t launch_patch_solve(const Correction& c, const double* b, const doubl
                                double* u_add, double* out_scatter, bool fused, cudaStream_t s)
 {
   if (c.n_regions == 0) return cudaSuccess;
-  const int st = nostream_env() ? 0 : 1;
-  const PatchSmem L = patch_smem_layout(c.max_dofs, st != 0, stages_env());
+  const PatchGeom g = patch_geom(c);
   double* tgt = u_add ? u_add : out_scatter;
   const int add = u_add ? 1 : 0;
-  const size_t smem = (size_t)L.bytes + smem_pad();
-  if (fused) return launch_patch<kAddResidualSolve>(c, smem, b, u_res, tgt, add, st, s);
-  return launch_patch<kSolveFromBuf>(c, smem, b, u_res, tgt, add, st, s);
+  const size_t smem = (size_t)g.L.bytes + smem_pad();
+  if (fused) return launch_patch<kAddResidualSolve>(c, smem, b, u_res, tgt, add, g.flags, s);
+  return launch_patch<kSolveFromBuf>(c, smem, b, u_res, tgt, add, g.flags, s);
 }
 
 // The attribute is per kernel, shared by every correction: it only ever grows
@@ -990,7 +1246,7 @@ cudaError_t launch_patch_solve(const Correction& c, const double* b, const doubl
 cudaError_t configure_patch_solve_smem(const Correction& c)
 {
   static int cur[4] = {0, 0, 0, 0};
-  const PatchSmem L = patch_smem_layout(c.max_dofs, !nostream_env(), stages_env());
+  const PatchSmem L = patch_geom(c).L;
   const int bytes = (int)(L.bytes + smem_pad());
   cudaError_t e = cudaSuccess;
   auto grow = [&](int mode, auto fn, int need) {
@@ -1001,7 +1257,7 @@ cudaError_t configure_patch_solve_smem(const Correction& c)
   };
   grow(kAddResidualSolve, patch_kernel<kAddResidualSolve>, bytes);
   grow(kSolveFromBuf, patch_kernel<kSolveFromBuf>, bytes);
-  grow(kResidualOnly, patch_kernel<kResidualOnly>, (int)L.l_off);
+  grow(kResidualOnly, patch_kernel<kResidualOnly>, (int)(L.sym ? L.y_off : L.l_off));
   if (c.has_ring && patch_follow_fits(c))
     grow(kFollow, patch_kernel<kFollow>, (int)follow_smem(c));
   return e;

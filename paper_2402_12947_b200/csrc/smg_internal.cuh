@@ -88,6 +88,15 @@ struct DevCsr {
   const int16_t* sell_perm = nullptr;  // nwin * 256
   const int32_t* sell_col = nullptr;
   const double* sell_val = nullptr;
+  // SELL-d16 (sell_delta): 16-bit column codes at the positions of sell_col
+  // (which is then not uploaded): delta to the row's previous column, 0xFFFE
+  // padding, 0xFFFF = take the slot's next escape column; first column and
+  // escapes per slot (sell_esc: sell_esc_planes planes of nwin * 256)
+  bool sell_delta = false;
+  int32_t sell_esc_planes = 0;
+  const uint16_t* sell_dcol = nullptr;
+  const int32_t* sell_c0 = nullptr;
+  const int32_t* sell_esc = nullptr;
 };
 constexpr int kSellWindow = 256;
 constexpr int kSellSlices = kSellWindow / 32;
@@ -135,6 +144,7 @@ struct Correction {
   DevCsr halo;
   const uint8_t* halo_mask = nullptr;
   bool coupled = true;             // some A[B_d, B_d'] != 0 (d != d')
+  bool sym = false;                // regions past the L^{-1} sizes hold packed A[B,B]^{-1}
   // follow mode (correction overlapped with the kernel producing its u): the
   // ring of region d is the sorted set of columns of its rows (B_d included);
   // the correction kernel recomputes the producer's output there from the
@@ -172,17 +182,30 @@ __host__ __device__ inline int patch_block(int64_t nd, int64_t nmax)
   if (nd > 2 * kPanel && nd <= 4 * kPanel && nmax <= 4 * kPanel) return 4 * kPanel;
   return 0;
 }
-__host__ __device__ inline int64_t patch_slot_doubles(int64_t nd, int64_t nmax)
+// Symmetric-inverse regions (round 2, SMG_PATCH_SYM, default on): a region
+// that would otherwise run the panel substitution (more than 32 dofs and no
+// whole-L^{-1} block) stores the packed lower triangle of A[B,B]^{-1} =
+// L^{-T} L^{-1} instead of L: the correction is one symmetric matrix-vector
+// product streamed from HBM once, with no serial panel chain.
+__host__ __device__ inline bool patch_is_sym(int64_t nd, int64_t nmax, bool sym)
 {
+  return sym && nd > kPanel && patch_block(nd, nmax) == 0;
+}
+__host__ __device__ inline int64_t patch_slot_doubles(int64_t nd, int64_t nmax, bool sym)
+{
+  if (patch_is_sym(nd, nmax, sym)) return patch_tri_even(nd);
   const int64_t B = patch_block(nd, nmax);
   return patch_tri_even(nd) + (B ? B * (B + 1) : ((nd + kPanel - 1) / kPanel) * kDinvBlock);
 }
-// the largest slot of any region of at most nmax dofs (slots are not monotonic)
-__host__ __device__ inline int64_t patch_slot_max(int64_t nmax)
+// the largest slot that is staged whole in shared memory for regions of at
+// most nmax dofs (slots are not monotonic; symmetric-inverse regions stream)
+__host__ __device__ inline int64_t patch_slot_max(int64_t nmax, bool sym)
 {
-  const int64_t a = patch_slot_doubles(nmax, nmax);
+  if (sym && nmax > 4 * kPanel)   // staged: <= 32 dofs (L + one block) and 33..64 (L + 64 x 65)
+    return patch_slot_doubles(2 * kPanel, nmax, sym);
+  const int64_t a = patch_slot_doubles(nmax, nmax, sym);
   const int64_t b =
-      nmax > kPanel ? patch_slot_doubles(nmax < 2 * kPanel ? nmax : 2 * kPanel, nmax) : 0;
+      nmax > kPanel ? patch_slot_doubles(nmax < 2 * kPanel ? nmax : 2 * kPanel, nmax, sym) : 0;
   return a > b ? a : b;
 }
 

@@ -252,12 +252,29 @@ constexpr int kSellPre = 4;   // entries loaded before the dependency wait
 // kPipe (long rows): the next kUnroll entries' columns and values are
 // requested before this batch's x gathers and sums, so the HBM stream never
 // waits on the gathers (software pipelining; SMG_SELL_PIPE)
-template <Epi E, bool kPf, int kUnroll, bool kPipe = false>
-__global__ void __launch_bounds__(kSellWindow, kPipe ? 4 : (kUnroll <= 4 ? 8 : (kUnroll <= 8 ? 4 : 2)))
+// kDelta (DevCsr::sell_delta, "SELL-d16"): the column stream is 16-bit codes
+// in the same positions -- code = column - previous column of the row
+// (0..0xFFFD), 0xFFFE = padding, 0xFFFF = the next of the row's (at most two)
+// escape columns, held per slot in sell_esc; the row's first column comes
+// from sell_c0.  A thread walks its row in order anyway, so decoding is one
+// integer add on the gather address; the sums are unchanged (same products,
+// same order), the operator stream is 10 instead of 12 bytes per entry.
+#ifndef SMG_D16_RELAX
+#define SMG_D16_RELAX 0   // 1: delta kernels get 6 / 3 CTAs per SM (40 / 80 registers, no spills)
+#endif
+constexpr int sell_min_blocks(int unroll, bool pipe, bool delta)
+{
+  if (SMG_D16_RELAX && delta) return pipe ? 3 : (unroll <= 4 ? 6 : (unroll <= 8 ? 3 : 2));
+  return pipe ? 4 : (unroll <= 4 ? 8 : (unroll <= 8 ? 4 : 2));
+}
+
+template <Epi E, bool kPf, int kUnroll, bool kPipe = false, bool kDelta = false>
+__global__ void __launch_bounds__(kSellWindow, sell_min_blocks(kUnroll, kPipe, kDelta))
 sell_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, int pf_dist,
             int xpf_chunk)
 {
   using T = EpiTraits<E>;
+  constexpr int32_t kPad = kDelta ? 0xFFFE : -1;
   const int w = blockIdx.x;
   const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t sb = m.sell_ptr[(int64_t)w * kSellSlices + k];
@@ -265,21 +282,51 @@ sell_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, int 
   const int width = (int)((se - sb) >> 5);
   const int rl = m.sell_perm[(int64_t)w * kSellWindow + threadIdx.x];
   const int32_t* __restrict__ cp = m.sell_col + sb + lane;
+  const uint16_t* __restrict__ dp = m.sell_dcol + sb + lane;
   const double* __restrict__ vp = m.sell_val + sb + lane;
+  // raw column-stream item j of this slot: a column (or -1), or a 16-bit code
+  auto ldraw = [&](int j) -> int32_t {
+    if constexpr (kDelta)
+      return m.streaming ? (int32_t)__ldcs(dp + j * 32) : (int32_t)__ldg(dp + j * 32);
+    else
+      return m.streaming ? __ldcs(cp + j * 32) : __ldg(cp + j * 32);
+  };
+  auto ldval = [&](int j) -> double {
+    return m.streaming ? __ldcs(vp + j * 32) : __ldg(vp + j * 32);
+  };
+  // decoder state (kDelta): current column, escapes consumed, the slot's escapes
+  int32_t ccur = 0, e0 = 0, e1 = 0;
+  int ek = 0;
+  if constexpr (kDelta) {
+    const int64_t slot = (int64_t)w * kSellWindow + threadIdx.x;
+    ccur = __ldg(m.sell_c0 + slot);
+    if (m.sell_esc_planes > 0) e0 = __ldg(m.sell_esc + slot);
+    if (m.sell_esc_planes > 1) e1 = __ldg(m.sell_esc + (int64_t)m.sell_nwin * kSellWindow + slot);
+  }
+  // items must be decoded in entry order; returns the column, or -1 for padding
+  auto decode = [&](int32_t raw) -> int32_t {
+    if constexpr (!kDelta) {
+      return raw;
+    } else {
+      if (raw == 0xFFFE) return -1;
+      if (raw == 0xFFFF) {
+        ccur = ek == 0 ? e0 : e1;
+        ++ek;
+      } else {
+        ccur += raw;
+      }
+      return ccur;
+    }
+  };
   int32_t c0[kSellPre];
   double v0[kSellPre];
 #pragma unroll
   for (int j = 0; j < kSellPre; ++j) {
-    c0[j] = -1;
+    c0[j] = kPad;
     v0[j] = 0.0;
     if (j < width) {
-      if (m.streaming) {
-        c0[j] = __ldcs(cp + j * 32);
-        v0[j] = __ldcs(vp + j * 32);
-      } else {
-        c0[j] = __ldg(cp + j * 32);
-        v0[j] = __ldg(vp + j * 32);
-      }
+      c0[j] = ldraw(j);
+      v0[j] = ldval(j);
     }
   }
   if constexpr (kPf) {
@@ -290,9 +337,14 @@ sell_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, int 
         const int64_t p1 = m.sell_ptr[(int64_t)(wp + 1) * kSellSlices];
         if (p1 > p0 && p1 - p0 <= (int64_t)kTileNnz * 16) {
           const int64_t va = p0 & ~int64_t(1), vb = (p1 + 1) & ~int64_t(1);
-          const int64_t ca = p0 & ~int64_t(3), cb = (p1 + 3) & ~int64_t(3);
           prefetch_l2(m.sell_val + va, (uint32_t)((vb - va) * 8), m.streaming);
-          prefetch_l2(m.sell_col + ca, (uint32_t)((cb - ca) * 4), m.streaming);
+          if constexpr (kDelta) {
+            const int64_t ca = p0 & ~int64_t(7), cb = (p1 + 7) & ~int64_t(7);
+            prefetch_l2(m.sell_dcol + ca, (uint32_t)((cb - ca) * 2), m.streaming);
+          } else {
+            const int64_t ca = p0 & ~int64_t(3), cb = (p1 + 3) & ~int64_t(3);
+            prefetch_l2(m.sell_col + ca, (uint32_t)((cb - ca) * 4), m.streaming);
+          }
         }
       }
     }
@@ -327,23 +379,21 @@ sell_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, int 
   }
   double sum = 0.0;
 #pragma unroll
-  for (int j = 0; j < kSellPre; ++j)
-    if (c0[j] >= 0) sum = __dadd_rn(sum, __dmul_rn(v0[j], __ldg(x + c0[j])));
+  for (int j = 0; j < kSellPre; ++j) {
+    const int32_t c = decode(c0[j]);
+    SMG_DCHECK(c < m.ncols);
+    if (c >= 0) sum = __dadd_rn(sum, __dmul_rn(v0[j], __ldg(x + c)));
+  }
   if constexpr (kPipe) {
     auto ldb = [&](int j0, int32_t* cc, double* vv) {
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
         const int j = j0 + u;
-        cc[u] = -1;
+        cc[u] = kPad;
         vv[u] = 0.0;
         if (j < width) {
-          if (m.streaming) {
-            cc[u] = __ldcs(cp + j * 32);
-            vv[u] = __ldcs(vp + j * 32);
-          } else {
-            cc[u] = __ldg(cp + j * 32);
-            vv[u] = __ldg(vp + j * 32);
-          }
+          cc[u] = ldraw(j);
+          vv[u] = ldval(j);
         }
       }
     };
@@ -355,8 +405,10 @@ sell_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, int 
       double vn[kUnroll];
       ldb(j0 + kUnroll, cn, vn);
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u)
-        if (c[u] >= 0) sum = __dadd_rn(sum, __dmul_rn(v[u], __ldg(x + c[u])));
+      for (int u = 0; u < kUnroll; ++u) {
+        const int32_t cu = decode(c[u]);
+        if (cu >= 0) sum = __dadd_rn(sum, __dmul_rn(v[u], __ldg(x + cu)));
+      }
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
         c[u] = cn[u];
@@ -368,15 +420,9 @@ sell_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, int 
   }
 #pragma unroll kUnroll
   for (int j = kSellPre; j < width; ++j) {
-    int32_t c;
-    double v;
-    if (m.streaming) {
-      c = __ldcs(cp + j * 32);
-      v = __ldcs(vp + j * 32);
-    } else {
-      c = __ldg(cp + j * 32);
-      v = __ldg(vp + j * 32);
-    }
+    const int32_t raw = ldraw(j);
+    const double v = ldval(j);
+    const int32_t c = decode(raw);
     SMG_DCHECK(c < m.ncols);
     if (c >= 0) sum = __dadd_rn(sum, __dmul_rn(v, __ldg(x + c)));
   }
@@ -572,10 +618,17 @@ static cudaError_t launch_t_sell(const DevCsr& m, const double* x, const EpiArgs
       const int64_t ctas = std::min<int64_t>(m.sell_nwin, (int64_t)g_sm_count * 4);
       xpf = (int)(((m.ncols * 8 + ctas - 1) / ctas + 15) & ~int64_t(15));
     }
+#define SMG_SELL_LAUNCH(U, P)                                                              \
+  do {                                                                                     \
+    if (m.sell_delta)                                                                      \
+      return pf ? cudaLaunchKernelEx(&cfg, sell_kernel<E, true, U, P, true>, m, x, ea, sdist, xpf) \
+                : cudaLaunchKernelEx(&cfg, sell_kernel<E, false, U, P, true>, m, x, ea, sdist, xpf); \
+    return pf ? cudaLaunchKernelEx(&cfg, sell_kernel<E, true, U, P, false>, m, x, ea, sdist, xpf) \
+              : cudaLaunchKernelEx(&cfg, sell_kernel<E, false, U, P, false>, m, x, ea, sdist, xpf); \
+  } while (0)
     if (m.sell_unroll >= 16) {
       const int sdist = g_sm_count * 2 * waves;
-      return pf ? cudaLaunchKernelEx(&cfg, sell_kernel<E, true, 16>, m, x, ea, sdist, xpf)
-                : cudaLaunchKernelEx(&cfg, sell_kernel<E, false, 16>, m, x, ea, sdist, xpf);
+      SMG_SELL_LAUNCH(16, false);
     }
     if (m.sell_unroll >= 8) {
       const int sdist = g_sm_count * 4 * waves;
@@ -586,18 +639,13 @@ static cudaError_t launch_t_sell(const DevCsr& m, const double* x, const EpiArgs
         return v ? atoi(v) : -1;
       }();
       const int pipe = pipe_env >= 0 ? pipe_env : m.sell_pipe;
-      if (pipe >= 6)
-        return pf ? cudaLaunchKernelEx(&cfg, sell_kernel<E, true, 6, true>, m, x, ea, sdist, xpf)
-                  : cudaLaunchKernelEx(&cfg, sell_kernel<E, false, 6, true>, m, x, ea, sdist, xpf);
-      if (pipe > 0)
-        return pf ? cudaLaunchKernelEx(&cfg, sell_kernel<E, true, 4, true>, m, x, ea, sdist, xpf)
-                  : cudaLaunchKernelEx(&cfg, sell_kernel<E, false, 4, true>, m, x, ea, sdist, xpf);
-      return pf ? cudaLaunchKernelEx(&cfg, sell_kernel<E, true, 8>, m, x, ea, sdist, xpf)
-                : cudaLaunchKernelEx(&cfg, sell_kernel<E, false, 8>, m, x, ea, sdist, xpf);
+      if (pipe >= 6) SMG_SELL_LAUNCH(6, true);
+      if (pipe > 0) SMG_SELL_LAUNCH(4, true);
+      SMG_SELL_LAUNCH(8, false);
     }
     const int sdist = g_sm_count * 8 * waves;
-    return pf ? cudaLaunchKernelEx(&cfg, sell_kernel<E, true, 4>, m, x, ea, sdist, xpf)
-              : cudaLaunchKernelEx(&cfg, sell_kernel<E, false, 4>, m, x, ea, sdist, xpf);
+    SMG_SELL_LAUNCH(4, false);
+#undef SMG_SELL_LAUNCH
   }
   if (m.fixed) {
     if (m.multichunk)

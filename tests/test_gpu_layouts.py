@@ -2,8 +2,8 @@
 
 The sweeps, residuals and transfers run on one of three layouts chosen per
 operator at upload (offset-table CSR tiles, fixed-capacity CSR tiles,
-SELL-32-sigma256 with a 4/8/16-deep loop, SELL-8x4 with 2/4 batches in
-flight).  The fixtures
+SELL-32-sigma256 with a 4/8/16-deep loop and int32 or 16-bit delta-coded
+columns, SELL-8x4 with 2/4 batches in flight).  The fixtures
 are small, so the automatic rule picks tiles for them; here each layout is
 forced with smg_operator_set_layout and checked against the reference's golden
 vectors and the oracle: bitwise for SpMV-type work and every smoother sweep,
@@ -18,7 +18,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 NAMES = ["crit7_adj", "c1s", "c2s", "c3s"]
-LAYOUTS = [(0, 0), (1, 0), (2, 4), (2, 8), (2, 16), (3, 2), (3, 4)]
+LAYOUTS = [(0, 0), (1, 0), (2, 4), (2, 8), (2, 16), (3, 2), (3, 4), (4, 4), (4, 8), (4, 16)]
 
 
 def fresh(m):
@@ -37,7 +37,7 @@ def forced(m, layout, unroll, with_transpose=False):
     lay, unr = ctypes.c_int(), ctypes.c_int()
     _lib.check(lib.smg_operator_layout(op.handle, ctypes.byref(lay), ctypes.byref(unr)))
     assert lay.value == layout
-    if layout in (2, 3):
+    if layout in (2, 3, 4):
         assert unr.value == unroll
     return op
 

@@ -65,7 +65,7 @@ def main():
         lay, unr = ctypes.c_int(), ctypes.c_int()
         _lib.check(lib.smg_operator_layout(op.handle, ctypes.byref(lay), ctypes.byref(unr)))
         levels.append({"level": l, "rows": n, "nnz": lvl.a.nnz,
-                       "layout": ["tiles", "tiles-fixed", "sell"][lay.value], "unroll": unr.value,
+                       "layout": ["tiles", "tiles-fixed", "sell", "sell4", "sell-d16"][lay.value], "unroll": unr.value,
                        "smooth_bitwise": ok_s, "residual_bitwise": ok_r})
     out["levels"] = levels
     transfers = []
