@@ -235,10 +235,10 @@ static int stages_env()
 }
 
 
-// symmetric-inverse ring geometry: a stage holds one chunk of 4 rows
-// (4 (nmax + 2) doubles), as many stages (2..8) as fit SMG_SYM_RING_KB
-// (default 66 KB: four stages and two CTAs per SM for 512-dof regions)
-constexpr int kSymRowsLayout = 4;   // rows per chunk of the symmetric-inverse ring (= kSymRows)
+// symmetric-inverse ring geometry: a stage holds one chunk of 8 rows
+// (8 (nmax + 2) doubles), as many stages (2..8) as fit SMG_SYM_RING_KB
+// (default 66 KB: two stages and two CTAs per SM for 512-dof regions)
+constexpr int kSymRowsLayout = 8;   // rows per chunk of the symmetric-inverse ring (= kSymRows)
 
 __host__ __device__ inline PatchSmem patch_smem_layout(int nmax, bool allow_stream = true,
                                                        int nst = kRingStages, bool sym = false,
@@ -501,24 +501,26 @@ __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_
 // ---------------------------------------------------------------------------
 // Symmetric-inverse correction: x = A[B,B]^{-1} r from the packed lower
 // triangle M of the inverse (row-major, row i = M[i][0..i]), read from HBM
-// once.  Chunks of kSymRows = 4 rows -- contiguous in the packed layout -- flow
-// HBM -> shared memory by 1D bulk copies through a ring of "full" (bytes
-// landed) and "empty" (all eight warps done) mbarriers; there is no CTA-wide
-// barrier per chunk, so warps drift and the copies stay ahead.  A chunk with
-// rows [i0, i0 + 4) is a strip of 32-column blocks; warp w owns the blocks
+// once.  Chunks of kSymRows = 8 rows -- contiguous in the packed layout -- flow
+// HBM -> shared memory by 1D bulk copies through a ring.  A chunk with rows
+// [i0, i0 + 8) is a strip of 32-column blocks; warp w owns the blocks
 // cb = w, w + 8, ... and lane l the column j = 32 cb + l of each:
 //   column part  y_j += sum_{i in chunk, i > j} M[i][j] r_i   (private to the lane;
 //                one running sum per column over the whole solve)
-//   row part     a_k += M[i0+k][j] r_j  for the 4 rows (j <= i), accumulated
-//                over the warp's blocks, then ONE 4-value butterfly per warp
-//                per chunk (6 exchanges instead of 4 x 5) leaves the warp's
-//                partial of row i0 + k on a lane.
-// Chunk c is closed by warp c mod 8: it waits for the chunk's "empty" phase,
-// adds the eight warps' row partials in warp order (z), and requests chunk
-// c + nst into the freed stage.  At the end x = y + z.  Nothing in a chunk
-// depends on another chunk's result: the ring is the only chain.  Fixed order
-// everywhere: deterministic, independent of the ring depth.
-constexpr int kSymRows = 4;
+//   row part     a_k += M[i0+k][j] r_j  for the 8 rows (j <= i), accumulated
+//                over the warp's blocks, then ONE 8-value butterfly per warp
+//                per chunk (9 exchanges instead of 8 x 5) leaves the warp's
+//                partial of row i0 + k on a lane; the eight warps' partials
+//                are added in warp order after the chunk's barrier.
+// At the end x = y + z.  Nothing in a chunk depends on another chunk's
+// result: the ring is the only chain.  Fixed order everywhere: deterministic,
+// independent of the ring depth.
+// Measured alternatives (profiles/r02/SUMMARY.md): variable-size chunks with a
+// warp per row and a thread per column (203 us on C5: ~3,800 cycles of
+// bookkeeping and shuffle chains per 16 KB chunk), and 4-row chunks with
+// full / empty mbarriers instead of the CTA barrier, each chunk closed by a
+// rotating warp (175 us: the per-chunk fixed costs double).
+constexpr int kSymRows = 8;
 static_assert(kSymRows == kSymRowsLayout, "ring stage size and chunk rows must agree");
 
 struct SymIssue {
@@ -529,155 +531,192 @@ struct SymIssue {
 // 32-bit triangle numbers (regions are far below 65k dofs)
 __device__ __forceinline__ int tri32(int i) { return (i * (i + 1)) >> 1; }
 
-__device__ __forceinline__ void sym_issue_next(const double* Mg, double* ring, int S, int nst,
+// the next chunk's copy, prepared ahead of the barrier that frees its stage
+struct SymCopy {
+  uint32_t dst = 0, bar = 0, bytes = 0;
+  const double* src = nullptr;
+};
+
+__device__ __forceinline__ SymCopy sym_prepare(const double* Mg, double* ring, int S, int nst,
                                                int n, SymIssue& si, uint64_t* bars)
 {
+  SymCopy cp;
   const int i1 = min(si.i0 + kSymRows, n);
   const int a = tri32(si.i0) & ~1;
   const int b = (tri32(i1) + 1) & ~1;
   SMG_DCHECK(b - a <= S && i1 > si.i0 && si.stage < nst);
-  uint64_t* bar = &bars[si.stage];
-  const uint32_t bytes = (uint32_t)(b - a) * 8u;
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(psmem_u32(bar)),
-               "r"(bytes)
+  cp.bar = psmem_u32(&bars[si.stage]);
+  cp.bytes = (uint32_t)(b - a) * 8u;
+  cp.dst = psmem_u32(ring + si.stage * S);
+  cp.src = Mg + a;
+  si.i0 = i1;
+  if (++si.stage == nst) si.stage = 0;
+  return cp;
+}
+
+__device__ __forceinline__ void sym_issue(const SymCopy& cp)
+{
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(cp.bar),
+               "r"(cp.bytes)
                : "memory");
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(psmem_u32(ring + si.stage * S)),
-      "l"(Mg + a), "r"(bytes), "r"(psmem_u32(bar))
+          "r"(cp.dst),
+      "l"(cp.src), "r"(cp.bytes), "r"(cp.bar)
       : "memory");
-  si.i0 = i1;
-  if (++si.stage == nst) si.stage = 0;
 }
 
 // thread 0, at kernel entry (the inverse is static data: before the
 // dependency wait, overlapping the residual): barriers + the first nst chunks
 __device__ __forceinline__ void sym_ring_start(const double* Mg, double* ring, int S, int nst,
-                                               int n, SymIssue& si, uint64_t* full, uint64_t* empty)
+                                               int n, SymIssue& si, uint64_t* bars)
 {
-  for (int q = 0; q < nst; ++q) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(psmem_u32(&full[q])) : "memory");
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(psmem_u32(&empty[q])),
-                 "r"(kSolveWarps)
-                 : "memory");
-  }
+  for (int q = 0; q < nst; ++q)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(psmem_u32(&bars[q])) : "memory");
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  for (int q = 0; q < nst && si.i0 < n; ++q) sym_issue_next(Mg, ring, S, nst, n, si, full);
+  for (int q = 0; q < nst && si.i0 < n; ++q) sym_issue(sym_prepare(Mg, ring, S, nst, n, si, bars));
 }
 
 // s_x holds r on entry (visible to all threads) and x on return (after a
-// barrier).  part: nst x kSymRows x kSolveWarps doubles (per-warp row partials
-// of the chunks in flight).
+// barrier).  part: 2 x kSymRows x kSolveWarps doubles (per-warp row partials,
+// double-buffered by chunk parity).
 __device__ void sym_apply(const double* __restrict__ Mg, double* ring, int S, int nst, int n,
-                          double* s_x, double* s_y, double* s_z, double* part, uint64_t* full,
-                          uint64_t* empty)
+                          double* s_x, double* s_y, double* s_z, double* part, uint64_t* bars,
+                          SymIssue& si)
 {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   // this lane's columns are 32 (warp + 8 q) + lane: zero their running sums
   for (int j = warp * 32 + lane; j < n; j += kSolveThreads) s_y[j] = 0.0;
-  const int nchunks = (n + kSymRows - 1) / kSymRows;
-  int stg = 0, closer = 0;
+  int stg = 0, buf = 0;
   uint32_t phase = 0;
-  for (int c = 0; c < nchunks; ++c) {
-    const int i0 = c * kSymRows;
+  for (int i0 = 0; i0 < n; i0 += kSymRows) {
+    const long long t0 = PTRACE_CLK();
     const int crows = min(kSymRows, n - i0);
-    ring_wait(&full[stg], phase);
+    // thread 0: the refill of this stage, ready to go right after the barrier
+    SymCopy next;
+    const bool refill = threadIdx.x == 0 && si.i0 < n;
+    if (refill) next = sym_prepare(Mg, ring, S, nst, n, si, bars);
+    ring_wait(&bars[stg], phase);
+    const long long t2 = PTRACE_CLK();
+    PTRACE_ACC(9, t2 - t0);
+    const int last = i0 + crows - 1;   // last column any row of the chunk reaches
+    // warps whose first block lies right of the chunk's last column have no
+    // entry of it: they only keep the barrier (short rows: most warps)
+    if (warp * 32 <= last) {
     // M[i0 + k][j] = base[roff[k] + j]
-    const double* base = ring + stg * S - (tri32(i0) & ~1);
+    const int t0r = tri32(i0);
+    const double* base = ring + stg * S - (t0r & ~1);
     int roff[kSymRows];
     double ri[kSymRows], a[kSymRows];
+    roff[0] = t0r;
 #pragma unroll
-    for (int k = 0; k < kSymRows; ++k) {
-      roff[k] = tri32(i0 + k);
-      ri[k] = k < crows ? s_x[i0 + k] : 0.0;
-      a[k] = 0.0;
+    for (int k = 1; k < kSymRows; ++k) roff[k] = roff[k - 1] + i0 + k;
+    if (crows == kSymRows) {
+#pragma unroll
+      for (int k = 0; k < kSymRows; ++k) ri[k] = s_x[i0 + k];
+    } else {
+#pragma unroll
+      for (int k = 0; k < kSymRows; ++k) ri[k] = k < crows ? s_x[i0 + k] : 0.0;
     }
-    const int last = i0 + crows - 1;   // last column any row of the chunk reaches
+#pragma unroll
+    for (int k = 0; k < kSymRows; ++k) a[k] = 0.0;
     for (int c0 = warp * 32; c0 <= last; c0 += kSolveWarps * 32) {
       const int j = c0 + lane;
       double m[kSymRows];
-      if (c0 + 31 < i0) {
+      if (c0 + 31 < i0 && crows == kSymRows) {
         // the block lies strictly left of every row's diagonal: no predicates
 #pragma unroll
-        for (int k = 0; k < kSymRows; ++k) m[k] = k < crows ? base[roff[k] + j] : 0.0;
+        for (int k = 0; k < kSymRows; ++k) m[k] = base[roff[k] + j];
         const double rj = s_x[j];
-        double y = s_y[j];
+        // two interleaved chains per column sum (even / odd rows of the chunk)
+        double y0 = s_y[j], y1 = 0.0;
 #pragma unroll
-        for (int k = 0; k < kSymRows; ++k) {
+        for (int k = 0; k < kSymRows; k += 2) {
           a[k] += m[k] * rj;
-          y += m[k] * ri[k];
+          a[k + 1] += m[k + 1] * rj;
+          y0 += m[k] * ri[k];
+          y1 += m[k + 1] * ri[k + 1];
         }
-        s_y[j] = y;
+        s_y[j] = y0 + y1;
       } else {
-        // block crossing the diagonal: row part j <= i, column part j < i
+        // block crossing the diagonal (or the last, partial chunk): row part
+        // j <= i, column part j < i
 #pragma unroll
         for (int k = 0; k < kSymRows; ++k)
           m[k] = (k < crows && j <= i0 + k) ? base[roff[k] + j] : 0.0;
         const double rj = j < n ? s_x[j] : 0.0;
-        double y = j < n ? s_y[j] : 0.0;
+        double y0 = j < n ? s_y[j] : 0.0, y1 = 0.0;
 #pragma unroll
-        for (int k = 0; k < kSymRows; ++k) {
+        for (int k = 0; k < kSymRows; k += 2) {
           a[k] += m[k] * rj;
-          if (j < i0 + k) y += m[k] * ri[k];
+          a[k + 1] += m[k + 1] * rj;
+          if (j < i0 + k) y0 += m[k] * ri[k];
+          if (j < i0 + k + 1) y1 += m[k + 1] * ri[k + 1];
         }
-        if (j < n) s_y[j] = y;
+        if (j < n) s_y[j] = y0 + y1;
       }
     }
-    // 4-value butterfly: after it the lanes with (lane & 7) == 0 hold the
-    // warp's partial of row i0 + 2 b4 + b3 (b = bits of the lane)
+    const long long t3 = PTRACE_CLK();
+    PTRACE_ACC(10, t3 - t2);
+    // 8-value butterfly: after it the lanes with (lane & 3) == 0 hold the
+    // warp's partial of row i0 + 4 b4 + 2 b3 + b2 (b = bits of the lane)
     {
       const bool u16 = (lane & 16) != 0;
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const double send = u16 ? a[k] : a[k + 2];
-        const double keep = u16 ? a[k + 2] : a[k];
+      for (int k = 0; k < 4; ++k) {
+        const double send = u16 ? a[k] : a[k + 4];
+        const double keep = u16 ? a[k + 4] : a[k];
         a[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
       }
       const bool u8 = (lane & 8) != 0;
-      const double send = u8 ? a[0] : a[1];
-      const double keep = u8 ? a[1] : a[0];
-      double v = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-      v += __shfl_xor_sync(0xffffffffu, v, 4);
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const double send = u8 ? a[k] : a[k + 2];
+        const double keep = u8 ? a[k + 2] : a[k];
+        a[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+      }
+      const bool u4 = (lane & 4) != 0;
+      const double send = u4 ? a[0] : a[1];
+      const double keep = u4 ? a[1] : a[0];
+      double v = keep + __shfl_xor_sync(0xffffffffu, send, 4);
       v += __shfl_xor_sync(0xffffffffu, v, 2);
       v += __shfl_xor_sync(0xffffffffu, v, 1);
-      if ((lane & 7) == 0) {
-        const int row = ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
-        part[(stg * kSymRows + row) * kSolveWarps + warp] = v;
+      if ((lane & 3) == 0) {
+        const int row = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+        part[(buf * kSymRows + row) * kSolveWarps + warp] = v;
       }
     }
-    // this warp is done with the stage (its reads and its partials are
-    // ordered before the arrival: release)
-    __syncwarp();
-    if (lane == 0)
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(psmem_u32(&empty[stg]))
-                   : "memory");
-    if (warp == closer) {
-      // close the chunk: every warp has arrived (acquire) -> z, then the refill
-      ring_wait(&empty[stg], phase);
-      if (lane < crows) {
-        const double* pp = part + (stg * kSymRows + lane) * kSolveWarps;
-        double z = 0.0;
+    PTRACE_ACC(11, PTRACE_CLK() - t3);
+    }   // active warp
+    const long long t4 = PTRACE_CLK();
+    __syncthreads();   // the stage is free; the partials are visible
+    const long long t5 = PTRACE_CLK();
+    if (refill) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      sym_issue(next);
+    }
+    // (the other buffer is rewritten only after the next barrier)
+    if (threadIdx.x >= 32 && threadIdx.x < 32 + crows) {
+      const int k = threadIdx.x - 32;
+      const double* pp = part + (buf * kSymRows + k) * kSolveWarps;
+      const int nact = min(kSolveWarps, (last >> 5) + 1);   // warps that had a block
+      double z = 0.0;
 #pragma unroll
-        for (int w = 0; w < kSolveWarps; ++w) z += pp[w];
-        s_z[i0 + lane] = z;
-      }
-      __syncwarp();
-      if (lane == 0 && c + nst < nchunks) {
-        SymIssue si;
-        si.i0 = (c + nst) * kSymRows;
-        si.stage = stg;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        sym_issue_next(Mg, ring, S, nst, n, si, full);
-      }
+      for (int w = 0; w < kSolveWarps; ++w)
+        if (w < nact) z += pp[w];
+      s_z[i0 + k] = z;
     }
-    if (++closer == kSolveWarps) closer = 0;
+    PTRACE_ACC(12, t5 - t4);
+    PTRACE_ACC(13, PTRACE_CLK() - t5);
+    PTRACE_ACC(14, 1);
+    buf ^= 1;
     if (++stg == nst) {
       stg = 0;
       phase ^= 1u;
     }
   }
-  __syncthreads();   // every chunk closed: z complete, y owned per lane
+  __syncthreads();   // z of the last chunk
   for (int j = threadIdx.x; j < n; j += kSolveThreads) s_x[j] = s_z[j] + s_y[j];
   __syncthreads();
 }
@@ -707,7 +746,6 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   __shared__ uint64_t s_bar;
   __shared__ uint64_t s_ring_bar[kMaxRingStages];
   __shared__ uint64_t s_dinv_bar[2];
-  __shared__ uint64_t s_sym_empty[kMaxRingStages];
   const bool sym_on = (flags & kFlagSym) != 0;
   const PatchSmem L_ = patch_smem_layout(nmax, allow_stream, (flags >> kFlagStagesShift) & 15, sym_on,
                                          (int64_t)((unsigned)flags >> kFlagSymStageShift) * 2,
@@ -748,7 +786,7 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   // symmetric-inverse region: the first chunks of the inverse are requested now
   SymIssue sym_iss;
   if (is_sym && threadIdx.x == 0)
-    sym_ring_start(Lg, s_L, (int)L_.stage, L_.nst, n, sym_iss, s_ring_bar, s_sym_empty);
+    sym_ring_start(Lg, s_L, (int)L_.stage, L_.nst, n, sym_iss, s_ring_bar);
   // a factor streamed through the ring: pull all of it towards L2 now, so the
   // ring's dependent copies hit L2 instead of paying HBM latency one chunk at
   // a time (the slot is contiguous, 16-byte aligned, even length)
@@ -961,7 +999,7 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   if (is_sym) {
     // (the residual's product buffer is free now: per-warp row partials)
     sym_apply(Lg, s_L, (int)L_.stage, L_.nst, n, s_x, reinterpret_cast<double*>(psm + L_.y_off),
-              reinterpret_cast<double*>(psm + L_.z_off), s_prod, s_ring_bar, s_sym_empty);
+              reinterpret_cast<double*>(psm + L_.z_off), s_prod, s_ring_bar, sym_iss);
   } else if (blk == 2 * kPanel) {
     // x = L^{-T} (L^{-1} r): two GEMVs with the stored inverse
     gemv_inv<2 * kPanel>(L + patch_tri_even(n), s_x, n, false, s_prod);
