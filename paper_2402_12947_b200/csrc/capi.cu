@@ -1012,6 +1012,7 @@ int smg_operator_create(int64_t nrows, int64_t ncols, const int64_t* rowptr, con
         return fail("column indices must be strictly increasing within rows");
     }
   }
+  configure_l2_persist();
   auto* op = new smg_operator();
   Operator& o = op->o;
   int rc = build_devcsr(o.allocs, o.device_bytes, nrows, ncols, rowptr, col, val, &o.a);

@@ -503,8 +503,8 @@ __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_
 // triangle M of the inverse (row-major, row i = M[i][0..i]), read from HBM
 // once.  Chunks of kSymRows = 8 rows -- contiguous in the packed layout -- flow
 // HBM -> shared memory by 1D bulk copies through a ring.  A chunk with rows
-// [i0, i0 + 8) is a strip of 32-column blocks; warp w owns the blocks
-// cb = w, w + 8, ... and lane l the column j = 32 cb + l of each:
+// [i0, i0 + 8) is a strip of 32-column blocks; warp w owns the block pairs
+// 2w, 2w + 1, then 2(w + 8), ... and lane l one column of each block:
 //   column part  y_j += sum_{i in chunk, i > j} M[i][j] r_i   (private to the lane;
 //                one running sum per column over the whole solve)
 //   row part     a_k += M[i0+k][j] r_j  for the 8 rows (j <= i), accumulated
@@ -520,6 +520,9 @@ __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_
 // bookkeeping and shuffle chains per 16 KB chunk), and 4-row chunks with
 // full / empty mbarriers instead of the CTA barrier, each chunk closed by a
 // rotating warp (175 us: the per-chunk fixed costs double).
+// columns per warp and pass: two adjacent 32-column blocks (short rows then
+// occupy half as many warps, each paying the per-chunk fixed costs once)
+constexpr int kSymGroup = 64;
 constexpr int kSymRows = 8;
 static_assert(kSymRows == kSymRowsLayout, "ring stage size and chunk rows must agree");
 
@@ -587,7 +590,10 @@ __device__ void sym_apply(const double* __restrict__ Mg, double* ring, int S, in
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   // this lane's columns are 32 (warp + 8 q) + lane: zero their running sums
-  for (int j = warp * 32 + lane; j < n; j += kSolveThreads) s_y[j] = 0.0;
+  for (int g = warp * kSymGroup; g < n; g += kSolveWarps * kSymGroup)
+#pragma unroll
+    for (int h = 0; h < kSymGroup; h += 32)
+      if (g + h + lane < n) s_y[g + h + lane] = 0.0;
   int stg = 0, buf = 0;
   uint32_t phase = 0;
   for (int i0 = 0; i0 < n; i0 += kSymRows) {
@@ -603,7 +609,7 @@ __device__ void sym_apply(const double* __restrict__ Mg, double* ring, int S, in
     const int last = i0 + crows - 1;   // last column any row of the chunk reaches
     // warps whose first block lies right of the chunk's last column have no
     // entry of it: they only keep the barrier (short rows: most warps)
-    if (warp * 32 <= last) {
+    if (warp * kSymGroup <= last) {
     // M[i0 + k][j] = base[roff[k] + j]
     const int t0r = tri32(i0);
     const double* base = ring + stg * S - (t0r & ~1);
@@ -621,7 +627,7 @@ __device__ void sym_apply(const double* __restrict__ Mg, double* ring, int S, in
     }
 #pragma unroll
     for (int k = 0; k < kSymRows; ++k) a[k] = 0.0;
-    for (int c0 = warp * 32; c0 <= last; c0 += kSolveWarps * 32) {
+    auto do_block = [&](int c0) {
       const int j = c0 + lane;
       double m[kSymRows];
       if (c0 + 31 < i0 && crows == kSymRows) {
@@ -656,6 +662,11 @@ __device__ void sym_apply(const double* __restrict__ Mg, double* ring, int S, in
         }
         if (j < n) s_y[j] = y0 + y1;
       }
+    };
+    for (int g = warp * kSymGroup; g <= last; g += kSolveWarps * kSymGroup) {
+#pragma unroll
+      for (int h = 0; h < kSymGroup; h += 32)
+        if (g + h <= last) do_block(g + h);
     }
     const long long t3 = PTRACE_CLK();
     PTRACE_ACC(10, t3 - t2);
@@ -700,7 +711,7 @@ __device__ void sym_apply(const double* __restrict__ Mg, double* ring, int S, in
     if (threadIdx.x >= 32 && threadIdx.x < 32 + crows) {
       const int k = threadIdx.x - 32;
       const double* pp = part + (buf * kSymRows + k) * kSolveWarps;
-      const int nact = min(kSolveWarps, (last >> 5) + 1);   // warps that had a block
+      const int nact = min(kSolveWarps, last / kSymGroup + 1);   // warps that had a block
       double z = 0.0;
 #pragma unroll
       for (int w = 0; w < kSolveWarps; ++w)
@@ -723,8 +734,11 @@ __device__ void sym_apply(const double* __restrict__ Mg, double* ring, int S, in
 
 __host__ __device__ __forceinline__ int nmax_ring(const FollowArgs& fa) { return fa.ring_max; }
 
-template <int kMode>
-__global__ void __launch_bounds__(kSolveThreads, 2)
+// kSym: the correction has symmetric-inverse regions (more than 128 dofs):
+// its own instantiation (128 registers, two CTAs per SM), so corrections of
+// small regions keep the lean kernel (C1-C3: 64 registers)
+template <int kMode, bool kSym>
+__global__ void __launch_bounds__(kSolveThreads, kSym ? 2 : 0)
 patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
              const double* __restrict__ pval, const int32_t* __restrict__ pptr,
              const int32_t* __restrict__ dofs,
@@ -746,7 +760,7 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   __shared__ uint64_t s_bar;
   __shared__ uint64_t s_ring_bar[kMaxRingStages];
   __shared__ uint64_t s_dinv_bar[2];
-  const bool sym_on = (flags & kFlagSym) != 0;
+  const bool sym_on = kSym && (flags & kFlagSym) != 0;
   const PatchSmem L_ = patch_smem_layout(nmax, allow_stream, (flags >> kFlagStagesShift) & 15, sym_on,
                                          (int64_t)((unsigned)flags >> kFlagSymStageShift) * 2,
                                          (flags >> kFlagStagesShift) & 15);
@@ -764,7 +778,7 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int64_t nslot = patch_slot_doubles(n, nmax, sym_on);
-  const bool is_sym = kMode != kResidualOnly && patch_is_sym(n, nmax, sym_on);
+  const bool is_sym = kSym && kMode != kResidualOnly && patch_is_sym(n, nmax, sym_on);
   const bool staged = kMode != kResidualOnly && !is_sym && nslot <= L_.tri_cap;
   SMG_DCHECK(L_.bytes <= (int64_t)227 * 1024);
   const double* __restrict__ Lg = lfac + foff[p];
@@ -1167,6 +1181,9 @@ struct PatchGeom {
   PatchSmem L;
 };
 
+// corrections whose larger regions hold packed inverses run the kSym kernels
+static bool patch_has_sym(const Correction& c) { return c.sym && c.max_dofs > 4 * kPanel; }
+
 static PatchGeom patch_geom(const Correction& c)
 {
   static const int l2pf = patch_env("SMG_PATCH_L2PF", 0);  // measured slower on C5 (222 vs 240 us)
@@ -1203,7 +1220,8 @@ static cudaError_t launch_patch(const Correction& c, size_t smem, const double* 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   static const int lpt = patch_env("SMG_PATCH_LPT", 1);
-  return cudaLaunchKernelEx(&cfg, patch_kernel<kMode>, c.prow, c.pcol, c.pval, c.pptr, c.dofs,
+  auto fn = patch_has_sym(c) ? patch_kernel<kMode, true> : patch_kernel<kMode, false>;
+  return cudaLaunchKernelEx(&cfg, fn, c.prow, c.pcol, c.pval, c.pptr, c.dofs,
                             c.foff, c.lfac, b, u_res, c.rbuf, tgt, add, c.max_dofs, flags,
                             lpt ? c.order : (const int32_t*)nullptr, FollowArgs(),
                             (const int32_t*)nullptr, (const int32_t*)nullptr,
@@ -1236,7 +1254,8 @@ cudaError_t launch_patch_follow(const Correction& c, const FollowArgs& fa, cudaS
   static const int lpt = patch_env("SMG_PATCH_LPT", 1);
   FollowArgs f = fa;
   f.ring_max = c.ring_max;
-  return cudaLaunchKernelEx(&cfg, patch_kernel<kFollow>, c.prow, c.pcol, c.pval, c.pptr, c.dofs,
+  auto fn = patch_has_sym(c) ? patch_kernel<kFollow, true> : patch_kernel<kFollow, false>;
+  return cudaLaunchKernelEx(&cfg, fn, c.prow, c.pcol, c.pval, c.pptr, c.dofs,
                             c.foff, c.lfac, fa.b, (const double*)nullptr, c.rbuf, fa.out, 1,
                             c.max_dofs, patch_geom(c).flags,
                             lpt ? c.order : (const int32_t*)nullptr, f, c.ring_ptr, c.ring_rows,
@@ -1283,21 +1302,32 @@ cudaError_t launch_patch_solve(const Correction& c, const double* b, const doubl
 // launch size).
 cudaError_t configure_patch_solve_smem(const Correction& c)
 {
-  static int cur[4] = {0, 0, 0, 0};
+  static int cur[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const PatchSmem L = patch_geom(c).L;
+  const bool sym = patch_has_sym(c);
   const int bytes = (int)(L.bytes + smem_pad());
   cudaError_t e = cudaSuccess;
   auto grow = [&](int mode, auto fn, int need) {
-    if (e == cudaSuccess && need > cur[mode]) {
+    const int slot = mode + (sym ? 4 : 0);
+    if (e == cudaSuccess && need > cur[slot]) {
       e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, need);
-      if (e == cudaSuccess) cur[mode] = need;
+      if (e == cudaSuccess) cur[slot] = need;
     }
   };
-  grow(kAddResidualSolve, patch_kernel<kAddResidualSolve>, bytes);
-  grow(kSolveFromBuf, patch_kernel<kSolveFromBuf>, bytes);
-  grow(kResidualOnly, patch_kernel<kResidualOnly>, (int)(L.sym ? L.y_off : L.l_off));
-  if (c.has_ring && patch_follow_fits(c))
-    grow(kFollow, patch_kernel<kFollow>, (int)follow_smem(c));
+  const int rbytes = (int)(L.sym ? L.y_off : L.l_off);
+  if (sym) {
+    grow(kAddResidualSolve, patch_kernel<kAddResidualSolve, true>, bytes);
+    grow(kSolveFromBuf, patch_kernel<kSolveFromBuf, true>, bytes);
+    grow(kResidualOnly, patch_kernel<kResidualOnly, true>, rbytes);
+    if (c.has_ring && patch_follow_fits(c))
+      grow(kFollow, patch_kernel<kFollow, true>, (int)follow_smem(c));
+  } else {
+    grow(kAddResidualSolve, patch_kernel<kAddResidualSolve, false>, bytes);
+    grow(kSolveFromBuf, patch_kernel<kSolveFromBuf, false>, bytes);
+    grow(kResidualOnly, patch_kernel<kResidualOnly, false>, rbytes);
+    if (c.has_ring && patch_follow_fits(c))
+      grow(kFollow, patch_kernel<kFollow, false>, (int)follow_smem(c));
+  }
   return e;
 }
 

@@ -270,6 +270,7 @@ struct FollowArgs {
 
 cudaError_t launch_csr_stream(const DevCsr& m, const double* x, Epi epi, const EpiArgs& ea,
                               cudaStream_t s);
+void configure_l2_persist();   // SMG_L2_PERSIST_MB carve-out (call outside stream capture)
 
 // patch kernels (patch_kernels.cu)
 cudaError_t launch_patch_residual(const DevCsr& a, const Correction& c, const double* b,

@@ -544,6 +544,37 @@ static bool env_flag(int& cache, const char* name, int dflt)
   return cache != 0;
 }
 
+// SMG_L2_PERSIST_MB (default 0 = off): a persisting-L2 carve-out of that size;
+// the sweeps of streamed operators then mark their gathered vector x with a
+// persisting access-policy window (and everything else they touch keeps its
+// normal / evict-first treatment), so the operator stream cannot displace x
+// between the gathers of neighbouring rows.  Set up outside any stream
+// capture (operator creation calls configure_l2_persist).
+static size_t g_persist_bytes = 0;
+static size_t g_persist_window = 0;
+
+void configure_l2_persist()
+{
+  static bool done = false;
+  if (done) return;
+  done = true;
+  const char* v = getenv("SMG_L2_PERSIST_MB");
+  const long mb = v ? atol(v) : 0;
+  if (mb <= 0) return;
+  int dev = 0, maxp = 0, maxw = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+  cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+  size_t want = (size_t)mb << 20;
+  if (want > (size_t)maxp) want = (size_t)maxp;
+  if (want == 0 || cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  g_persist_bytes = want;
+  g_persist_window = (size_t)maxw;
+}
+
 template <Epi E>
 static cudaError_t launch_t_sell(const DevCsr& m, const double* x, const EpiArgs& ea,
                                  cudaLaunchConfig_t cfg, bool pf, int waves);
@@ -563,11 +594,23 @@ static cudaError_t launch_t(const DevCsr& m, const double* x, const EpiArgs& ea,
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = env_flag(g_pdl, "SMG_PDL", 1) ? 1 : 0;
+  if (g_persist_bytes > 0 && m.streaming && m.ncols > 0) {
+    size_t bytes = (size_t)m.ncols * 8;
+    if (bytes > g_persist_window) bytes = g_persist_window;
+    cudaLaunchAttribute& a = attr[cfg.numAttrs++];
+    a.id = cudaLaunchAttributeAccessPolicyWindow;
+    a.val.accessPolicyWindow.base_ptr = const_cast<double*>(x);
+    a.val.accessPolicyWindow.num_bytes = bytes;
+    a.val.accessPolicyWindow.hitRatio =
+        bytes <= g_persist_bytes ? 1.0f : (float)((double)g_persist_bytes / (double)bytes);
+    a.val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    a.val.accessPolicyWindow.missProp = cudaAccessPropertyNormal;
+  }
   static const int waves = [] {
     const char* v = getenv("SMG_PF_WAVES");
     const int w = v ? atoi(v) : 1;
