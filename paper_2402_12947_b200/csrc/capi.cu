@@ -1844,7 +1844,7 @@ int smg_correction_create(const smg_operator* a, int64_t n_regions, const int64_
     max_dofs = std::max<int32_t>(max_dofs, (int32_t)(roff[r + 1] - roff[r]));
   // SMG_PATCH_SYM=0: keep the factor (panel substitution) for the larger regions
   const char* sym_env = getenv("SMG_PATCH_SYM");
-  const bool sym = !(sym_env && sym_env[0] == '0');
+  const bool sym = !(sym_env && sym_env[0] == '0') && max_dofs <= kPatchSymMaxDofs;
   for (int64_t r = 0; r < n_regions; ++r) {
     const int64_t nd = roff[r + 1] - roff[r];
     if (nd <= 0) return fail("region " + std::to_string(r) + " is empty");

@@ -160,7 +160,6 @@ enum PatchMode : int { kAddResidualSolve = 0, kSolveFromBuf = 1, kResidualOnly =
 constexpr int kFlagStream = 1;      // factors larger than shared memory stream through a ring
 constexpr int kFlagL2Prefetch = 2;  // ... after an L2 prefetch of the whole factor
 constexpr int kFlagSym = 4;         // the correction holds packed A[B,B]^{-1} for its larger regions
-constexpr int kFlagSymStageShift = 12;  // launch flags bits 12..30: symmetric ring stage, in pairs of doubles
 
 // Phase timestamps (SM clock) of the first 256 CTAs, compiled in only for the
 // tools/trace_patch.py build (-DSMG_PATCH_TRACE); no cost otherwise.
@@ -206,6 +205,7 @@ struct PatchSmem {
   int nst;
   int64_t y_off, z_off;   // symmetric-inverse path: column sums / row dots (double[n2] each)
   bool sym;               // ring carries packed A^{-1} rows (sym_apply), not factor rows
+  int sym_rows;           // rows per chunk of the symmetric-inverse rings (1 or 2)
 };
 
 #ifndef SMG_CHUNK_ROWS
@@ -235,10 +235,12 @@ static int stages_env()
 }
 
 
-// symmetric-inverse ring geometry: a stage holds one chunk of 8 rows
-// (8 (nmax + 2) doubles), as many stages (2..8) as fit SMG_SYM_RING_KB
-// (default 66 KB: two stages and two CTAs per SM for 512-dof regions)
-constexpr int kSymRowsLayout = 8;   // rows per chunk of the symmetric-inverse ring (= kSymRows)
+// symmetric-inverse ring geometry: every warp has its own ring of nst (2..4)
+// stages, a stage holds one chunk of sym_rows (2, or 1 for very large
+// regions) rows: sym_rows (nmax + 2) doubles
+constexpr int kSymMaxRows = 2;
+constexpr int kSymWarps = 8;        // = kSolveWarps (defined below)
+constexpr int kSymMaxStages = 4;
 
 __host__ __device__ inline PatchSmem patch_smem_layout(int nmax, bool allow_stream = true,
                                                        int nst = kRingStages, bool sym = false,
@@ -256,17 +258,27 @@ __host__ __device__ inline PatchSmem patch_smem_layout(int nmax, bool allow_stre
   p.y_off = p.z_off = 0;
   p.sym = sym && nmax > 4 * kPanel;
   p.stage = 0;
+  p.sym_rows = 0;
   if (p.sym) {
     // regions of more than 128 dofs (and 65..128 beside them) stream the packed
-    // lower triangle of their inverse through the ring; smaller ones are staged
+    // lower triangle of their inverse through per-warp rings; smaller ones are
+    // staged whole in the same area.  y: one column-sum vector per warp.
     p.y_off = p.l_off;
-    p.z_off = p.y_off + 8 * n2;
+    p.z_off = p.y_off + 8 * n2 * kSymWarps;
     p.l_off = p.z_off + 8 * n2;
     (void)sym_stage;
-    p.stage = ((int64_t)kSymRowsLayout * (nmax + 2) + 1) & ~int64_t(1);
-    p.nst = sym_nst < 2 ? 2 : (sym_nst > kMaxRingStages ? kMaxRingStages : sym_nst);
+    p.nst = sym_nst < 2 ? 2 : (sym_nst > kSymMaxStages ? kSymMaxStages : sym_nst);
+    p.sym_rows = kSymMaxRows;
+    for (;;) {
+      p.stage = ((int64_t)p.sym_rows * (nmax + 2) + 1) & ~int64_t(1);
+      if (p.l_off + 8 * kSymWarps * p.nst * p.stage <= kSmemBudget) break;
+      if (p.nst > 2) --p.nst;
+      else if (p.sym_rows > 1) --p.sym_rows;
+      else break;
+    }
     const int64_t need = patch_slot_max(nmax, true);
-    p.tri_cap = p.nst * p.stage > need ? p.nst * p.stage : need;
+    const int64_t ring = (int64_t)kSymWarps * p.nst * p.stage;
+    p.tri_cap = ring > need ? ring : need;
     p.bytes = p.l_off + 8 * p.tri_cap;
     return p;
   }
@@ -501,234 +513,178 @@ __device__ void stream_solve(const double* __restrict__ Lg, double* ring, int64_
 // ---------------------------------------------------------------------------
 // Symmetric-inverse correction: x = A[B,B]^{-1} r from the packed lower
 // triangle M of the inverse (row-major, row i = M[i][0..i]), read from HBM
-// once.  Chunks of kSymRows = 8 rows -- contiguous in the packed layout -- flow
-// HBM -> shared memory by 1D bulk copies through a ring.  A chunk with rows
-// [i0, i0 + 8) is a strip of 32-column blocks; warp w owns the block pairs
-// 2w, 2w + 1, then 2(w + 8), ... and lane l one column of each block:
-//   column part  y_j += sum_{i in chunk, i > j} M[i][j] r_i   (private to the lane;
-//                one running sum per column over the whole solve)
-//   row part     a_k += M[i0+k][j] r_j  for the 8 rows (j <= i), accumulated
-//                over the warp's blocks, then ONE 8-value butterfly per warp
-//                per chunk (9 exchanges instead of 8 x 5) leaves the warp's
-//                partial of row i0 + k on a lane; the eight warps' partials
-//                are added in warp order after the chunk's barrier.
-// At the end x = y + z.  Nothing in a chunk depends on another chunk's
-// result: the ring is the only chain.  Fixed order everywhere: deterministic,
-// independent of the ring depth.
-// Measured alternatives (profiles/r02/SUMMARY.md): variable-size chunks with a
-// warp per row and a thread per column (203 us on C5: ~3,800 cycles of
-// bookkeeping and shuffle chains per 16 KB chunk), and 4-row chunks with
-// full / empty mbarriers instead of the CTA barrier, each chunk closed by a
-// rotating warp (175 us: the per-chunk fixed costs double).
-// columns per warp and pass: two adjacent 32-column blocks (short rows then
-// occupy half as many warps, each paying the per-chunk fixed costs once)
-constexpr int kSymGroup = 64;
-constexpr int kSymRows = 8;
-static_assert(kSymRows == kSymRowsLayout, "ring stage size and chunk rows must agree");
-
-struct SymIssue {
-  int i0 = 0;      // first row of the next chunk to request
-  int stage = 0;   // ring stage it goes into
-};
+// once.  The rows are cut into chunks of R (2, or 1) consecutive rows --
+// contiguous in the packed layout -- and chunk c belongs to warp c mod 8
+// alone: every warp runs its own bulk-copy ring (its lane 0 requests, the
+// warp waits on its own mbarriers), so the stream loop has no CTA barrier and
+// no exchange between warps.  For a chunk with rows [i0, i0 + R) the warp
+// walks the 32-column blocks, lane l on column j = c0 + l:
+//   row part     a_k += M[i0+k][j] r_j   (j <= i), summed over the blocks, then
+//                one butterfly per chunk leaves z_{i0+k} on a lane;
+//   column part  y_w[j] += sum_k M[i0+k][j] r_{i0+k}   (j < i), the warp's own
+//                column-sum vector in shared memory.
+// At the end x = z + sum_w y_w (warp order).  Nothing in a chunk depends on
+// another chunk's result.  Fixed order everywhere: deterministic, independent
+// of the ring depth.
+// Measured alternatives (profiles/r02/SUMMARY.md): chunks shared by all eight
+// warps (column blocks split over the warps, per-warp partial row sums
+// combined after a CTA barrier per chunk: 119-125 us on C5 against 75 here --
+// the per-chunk fixed costs, ~240 instructions per warp, were three times the
+// arithmetic); variable-size byte chunks with a warp per row and a thread per
+// column (203 us); 4-row chunks with full / empty mbarriers and a rotating
+// closing warp (175 us).
 
 // 32-bit triangle numbers (regions are far below 65k dofs)
 __device__ __forceinline__ int tri32(int i) { return (i * (i + 1)) >> 1; }
 
-// the next chunk's copy, prepared ahead of the barrier that frees its stage
-struct SymCopy {
-  uint32_t dst = 0, bar = 0, bytes = 0;
-  const double* src = nullptr;
-};
-
-__device__ __forceinline__ SymCopy sym_prepare(const double* Mg, double* ring, int S, int nst,
-                                               int n, SymIssue& si, uint64_t* bars)
+// lane 0 of a warp: request chunk c (rows [c R, c R + R)) into `dst`
+__device__ __forceinline__ void sym_issue(const double* Mg, double* dst, int R, int n, int c,
+                                          uint64_t* bar)
 {
-  SymCopy cp;
-  const int i1 = min(si.i0 + kSymRows, n);
-  const int a = tri32(si.i0) & ~1;
+  const int i0 = c * R;
+  const int i1 = min(i0 + R, n);
+  const int a = tri32(i0) & ~1;
   const int b = (tri32(i1) + 1) & ~1;
-  SMG_DCHECK(b - a <= S && i1 > si.i0 && si.stage < nst);
-  cp.bar = psmem_u32(&bars[si.stage]);
-  cp.bytes = (uint32_t)(b - a) * 8u;
-  cp.dst = psmem_u32(ring + si.stage * S);
-  cp.src = Mg + a;
-  si.i0 = i1;
-  if (++si.stage == nst) si.stage = 0;
-  return cp;
-}
-
-__device__ __forceinline__ void sym_issue(const SymCopy& cp)
-{
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(cp.bar),
-               "r"(cp.bytes)
+  const uint32_t bytes = (uint32_t)(b - a) * 8u;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(psmem_u32(bar)),
+               "r"(bytes)
                : "memory");
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(cp.dst),
-      "l"(cp.src), "r"(cp.bytes), "r"(cp.bar)
+          "r"(psmem_u32(dst)),
+      "l"(Mg + a), "r"(bytes), "r"(psmem_u32(bar))
       : "memory");
 }
 
-// thread 0, at kernel entry (the inverse is static data: before the
-// dependency wait, overlapping the residual): barriers + the first nst chunks
-__device__ __forceinline__ void sym_ring_start(const double* Mg, double* ring, int S, int nst,
-                                               int n, SymIssue& si, uint64_t* bars)
+// thread 0, at kernel entry: the warps' ring barriers (kSymWarps x nst)
+__device__ __forceinline__ void sym_ring_init(int nst, uint64_t* bars)
 {
-  for (int q = 0; q < nst; ++q)
+  for (int q = 0; q < kSymWarps * nst; ++q)
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(psmem_u32(&bars[q])) : "memory");
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  for (int q = 0; q < nst && si.i0 < n; ++q) sym_issue(sym_prepare(Mg, ring, S, nst, n, si, bars));
+}
+
+// every warp's lane 0, after the barrier that publishes the initialised
+// mbarriers (the inverse is static data: before the dependency wait,
+// overlapping the residual): the warp's first nst chunks
+__device__ __forceinline__ void sym_ring_start(const double* Mg, double* ring, int S, int nst, int R,
+                                               int n, uint64_t* bars)
+{
+  const int warp = threadIdx.x >> 5;
+  const int nchunks = (n + R - 1) / R;
+  for (int q = 0; q < nst; ++q) {
+    const int c = warp + q * kSymWarps;
+    if (c < nchunks)
+      sym_issue(Mg, ring + (warp * nst + q) * S, R, n, c, &bars[warp * nst + q]);
+  }
 }
 
 // s_x holds r on entry (visible to all threads) and x on return (after a
-// barrier).  part: 2 x kSymRows x kSolveWarps doubles (per-warp row partials,
-// double-buffered by chunk parity).
-__device__ void sym_apply(const double* __restrict__ Mg, double* ring, int S, int nst, int n,
-                          double* s_x, double* s_y, double* s_z, double* part, uint64_t* bars,
-                          SymIssue& si)
+// barrier).  s_y: kSymWarps vectors of n2 doubles.
+__device__ void sym_apply(const double* __restrict__ Mg, double* ring, int S, int nst, int R, int n,
+                          int n2, double* s_x, double* s_y, double* s_z, uint64_t* bars)
 {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  // this lane's columns are 32 (warp + 8 q) + lane: zero their running sums
-  for (int g = warp * kSymGroup; g < n; g += kSolveWarps * kSymGroup)
-#pragma unroll
-    for (int h = 0; h < kSymGroup; h += 32)
-      if (g + h + lane < n) s_y[g + h + lane] = 0.0;
-  int stg = 0, buf = 0;
+  double* __restrict__ yw = s_y + warp * n2;
+  const double* __restrict__ xr = s_x;   // r: read-only until the final combine
+  for (int j = lane; j < n; j += 32) yw[j] = 0.0;
+  __syncwarp();
+  const int nchunks = (n + R - 1) / R;
+  double* ringw = ring + warp * nst * S;
+  uint64_t* barw = bars + warp * nst;
+  int stg = 0;
   uint32_t phase = 0;
-  for (int i0 = 0; i0 < n; i0 += kSymRows) {
-    const long long t0 = PTRACE_CLK();
-    const int crows = min(kSymRows, n - i0);
-    // thread 0: the refill of this stage, ready to go right after the barrier
-    SymCopy next;
-    const bool refill = threadIdx.x == 0 && si.i0 < n;
-    if (refill) next = sym_prepare(Mg, ring, S, nst, n, si, bars);
-    ring_wait(&bars[stg], phase);
-    const long long t2 = PTRACE_CLK();
-    PTRACE_ACC(9, t2 - t0);
-    const int last = i0 + crows - 1;   // last column any row of the chunk reaches
-    // warps whose first block lies right of the chunk's last column have no
-    // entry of it: they only keep the barrier (short rows: most warps)
-    if (warp * kSymGroup <= last) {
-    // M[i0 + k][j] = base[roff[k] + j]
-    const int t0r = tri32(i0);
-    const double* base = ring + stg * S - (t0r & ~1);
-    int roff[kSymRows];
-    double ri[kSymRows], a[kSymRows];
-    roff[0] = t0r;
-#pragma unroll
-    for (int k = 1; k < kSymRows; ++k) roff[k] = roff[k - 1] + i0 + k;
-    if (crows == kSymRows) {
-#pragma unroll
-      for (int k = 0; k < kSymRows; ++k) ri[k] = s_x[i0 + k];
-    } else {
-#pragma unroll
-      for (int k = 0; k < kSymRows; ++k) ri[k] = k < crows ? s_x[i0 + k] : 0.0;
-    }
-#pragma unroll
-    for (int k = 0; k < kSymRows; ++k) a[k] = 0.0;
-    auto do_block = [&](int c0) {
+  for (int c = warp; c < nchunks; c += kSymWarps) {
+    const int i0 = c * R;
+    const bool two = R == 2 && i0 + 1 < n;      // the chunk has a second row
+    ring_wait(&barw[stg], phase);
+    const int t0 = tri32(i0);
+    const double* __restrict__ row0 = ringw + stg * S - (t0 & ~1) + t0;   // M[i0][j] = row0[j]
+    const double* __restrict__ row1 = row0 + i0 + 1;                      // M[i0 + 1][j] = row1[j]
+    const double r0 = xr[i0];
+    const double r1 = two ? xr[i0 + 1] : 0.0;
+    double a0 = 0.0, a1 = 0.0;
+    // blocks strictly left of the diagonal: no predicates; four per pass with
+    // all sixteen loads ahead of the arithmetic (two warps per scheduler: the
+    // shared-memory latency has to be covered inside the warp)
+    int c0 = 0;
+    for (; c0 + 127 < i0; c0 += 128) {
       const int j = c0 + lane;
-      double m[kSymRows];
-      if (c0 + 31 < i0 && crows == kSymRows) {
-        // the block lies strictly left of every row's diagonal: no predicates
+      double m0[4], m1[4], xv[4], yv[4];
 #pragma unroll
-        for (int k = 0; k < kSymRows; ++k) m[k] = base[roff[k] + j];
-        const double rj = s_x[j];
-        // two interleaved chains per column sum (even / odd rows of the chunk)
-        double y0 = s_y[j], y1 = 0.0;
-#pragma unroll
-        for (int k = 0; k < kSymRows; k += 2) {
-          a[k] += m[k] * rj;
-          a[k + 1] += m[k + 1] * rj;
-          y0 += m[k] * ri[k];
-          y1 += m[k + 1] * ri[k + 1];
-        }
-        s_y[j] = y0 + y1;
-      } else {
-        // block crossing the diagonal (or the last, partial chunk): row part
-        // j <= i, column part j < i
-#pragma unroll
-        for (int k = 0; k < kSymRows; ++k)
-          m[k] = (k < crows && j <= i0 + k) ? base[roff[k] + j] : 0.0;
-        const double rj = j < n ? s_x[j] : 0.0;
-        double y0 = j < n ? s_y[j] : 0.0, y1 = 0.0;
-#pragma unroll
-        for (int k = 0; k < kSymRows; k += 2) {
-          a[k] += m[k] * rj;
-          a[k + 1] += m[k + 1] * rj;
-          if (j < i0 + k) y0 += m[k] * ri[k];
-          if (j < i0 + k + 1) y1 += m[k + 1] * ri[k + 1];
-        }
-        if (j < n) s_y[j] = y0 + y1;
+      for (int q = 0; q < 4; ++q) {
+        m0[q] = row0[j + 32 * q];
+        m1[q] = two ? row1[j + 32 * q] : 0.0;
+        xv[q] = xr[j + 32 * q];
+        yv[q] = yw[j + 32 * q];
       }
-    };
-    for (int g = warp * kSymGroup; g <= last; g += kSolveWarps * kSymGroup) {
 #pragma unroll
-      for (int h = 0; h < kSymGroup; h += 32)
-        if (g + h <= last) do_block(g + h);
+      for (int q = 0; q < 4; ++q) {
+        a0 += m0[q] * xv[q];
+        a1 += m1[q] * xv[q];
+        yv[q] = (yv[q] + m0[q] * r0) + m1[q] * r1;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) yw[j + 32 * q] = yv[q];
     }
-    const long long t3 = PTRACE_CLK();
-    PTRACE_ACC(10, t3 - t2);
-    // 8-value butterfly: after it the lanes with (lane & 3) == 0 hold the
-    // warp's partial of row i0 + 4 b4 + 2 b3 + b2 (b = bits of the lane)
+    for (; c0 + 31 < i0; c0 += 32) {
+      const int j = c0 + lane;
+      const double m00 = row0[j];
+      const double m10 = two ? row1[j] : 0.0;
+      const double x0 = xr[j];
+      a0 += m00 * x0;
+      a1 += m10 * x0;
+      yw[j] = (yw[j] + m00 * r0) + m10 * r1;
+    }
+    // blocks crossing the diagonal: row part j <= i, column part j < i
+    const int last = two ? i0 + 1 : i0;
+    for (; c0 <= last; c0 += 32) {
+      const int j = c0 + lane;
+      const double m00 = j <= i0 ? row0[j] : 0.0;
+      const double m10 = (two && j <= i0 + 1) ? row1[j] : 0.0;
+      const double x0 = j < n ? xr[j] : 0.0;
+      a0 += m00 * x0;
+      a1 += m10 * x0;
+      if (j < last) {
+        double y = yw[j];
+        if (j < i0) y += m00 * r0;
+        if (two) y += m10 * r1;   // j < i0 + 1 = last
+        yw[j] = y;
+      }
+    }
+    // 2-value butterfly: lane 0 ends with z_{i0}, lane 16 with z_{i0+1}
     {
-      const bool u16 = (lane & 16) != 0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const double send = u16 ? a[k] : a[k + 4];
-        const double keep = u16 ? a[k + 4] : a[k];
-        a[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-      }
-      const bool u8 = (lane & 8) != 0;
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const double send = u8 ? a[k] : a[k + 2];
-        const double keep = u8 ? a[k + 2] : a[k];
-        a[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-      }
-      const bool u4 = (lane & 4) != 0;
-      const double send = u4 ? a[0] : a[1];
-      const double keep = u4 ? a[1] : a[0];
-      double v = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+      const bool up = (lane & 16) != 0;
+      const double send = up ? a0 : a1;
+      const double keep = up ? a1 : a0;
+      double v = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
       v += __shfl_xor_sync(0xffffffffu, v, 2);
       v += __shfl_xor_sync(0xffffffffu, v, 1);
-      if ((lane & 3) == 0) {
-        const int row = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-        part[(buf * kSymRows + row) * kSolveWarps + warp] = v;
-      }
+      if (lane == 0) s_z[i0] = v;
+      if (lane == 16 && two) s_z[i0 + 1] = v;
     }
-    PTRACE_ACC(11, PTRACE_CLK() - t3);
-    }   // active warp
-    const long long t4 = PTRACE_CLK();
-    __syncthreads();   // the stage is free; the partials are visible
-    const long long t5 = PTRACE_CLK();
-    if (refill) {
+    // the stage is free once every lane has read it: refill with this warp's
+    // chunk nst rounds ahead
+    __syncwarp();
+    if (lane == 0 && c + nst * kSymWarps < nchunks) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      sym_issue(next);
+      sym_issue(Mg, ringw + stg * S, R, n, c + nst * kSymWarps, &barw[stg]);
     }
-    // (the other buffer is rewritten only after the next barrier)
-    if (threadIdx.x >= 32 && threadIdx.x < 32 + crows) {
-      const int k = threadIdx.x - 32;
-      const double* pp = part + (buf * kSymRows + k) * kSolveWarps;
-      const int nact = min(kSolveWarps, last / kSymGroup + 1);   // warps that had a block
-      double z = 0.0;
-#pragma unroll
-      for (int w = 0; w < kSolveWarps; ++w)
-        if (w < nact) z += pp[w];
-      s_z[i0 + k] = z;
-    }
-    PTRACE_ACC(12, t5 - t4);
-    PTRACE_ACC(13, PTRACE_CLK() - t5);
-    PTRACE_ACC(14, 1);
-    buf ^= 1;
     if (++stg == nst) {
       stg = 0;
       phase ^= 1u;
     }
   }
-  __syncthreads();   // z of the last chunk
-  for (int j = threadIdx.x; j < n; j += kSolveThreads) s_x[j] = s_z[j] + s_y[j];
+  __syncthreads();   // every warp's z rows and column sums
+  for (int j = threadIdx.x; j < n; j += kSolveThreads) {
+    double y = s_y[j];
+#pragma unroll
+    for (int w = 1; w < kSymWarps; ++w) y += s_y[w * n2 + j];
+    s_x[j] = s_z[j] + y;
+  }
   __syncthreads();
 }
 
@@ -759,11 +715,11 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   __shared__ double s_red[kSolveWarps][32];
   __shared__ uint64_t s_bar;
   __shared__ uint64_t s_ring_bar[kMaxRingStages];
+  __shared__ uint64_t s_sym_bar[kSymWarps * kSymMaxStages];
   __shared__ uint64_t s_dinv_bar[2];
   const bool sym_on = kSym && (flags & kFlagSym) != 0;
   const PatchSmem L_ = patch_smem_layout(nmax, allow_stream, (flags >> kFlagStagesShift) & 15, sym_on,
-                                         (int64_t)((unsigned)flags >> kFlagSymStageShift) * 2,
-                                         (flags >> kFlagStagesShift) & 15);
+                                         0, (flags >> kFlagStagesShift) & 15);
   double* s_x = reinterpret_cast<double*>(psm + L_.x_off);
   int32_t* s_off = reinterpret_cast<int32_t*>(psm + L_.off_off);
   double* s_prod = reinterpret_cast<double*>(psm + L_.prod_off);
@@ -798,9 +754,8 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   if (staged && threadIdx.x == 0)
     factor_bulk_load(s_L, Lg, (uint32_t)(nslot * 8), &s_bar);
   // symmetric-inverse region: the first chunks of the inverse are requested now
-  SymIssue sym_iss;
-  if (is_sym && threadIdx.x == 0)
-    sym_ring_start(Lg, s_L, (int)L_.stage, L_.nst, n, sym_iss, s_ring_bar);
+  // (the warps' own first chunks are requested right after the barrier below)
+  if (is_sym && threadIdx.x == 0) sym_ring_init(L_.nst, s_sym_bar);
   // a factor streamed through the ring: pull all of it towards L2 now, so the
   // ring's dependent copies hit L2 instead of paying HBM latency one chunk at
   // a time (the slot is contiguous, 16-byte aligned, even length)
@@ -818,6 +773,8 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   }
   // every thread may only wait on the barrier after thread 0 has initialised it
   __syncthreads();
+  if (is_sym && lane == 0)
+    sym_ring_start(Lg, s_L, (int)L_.stage, L_.nst, L_.sym_rows, n, s_sym_bar);
 
   if (kMode == kFollow) {
     // ---- follow mode: this kernel was launched (programmatic dependent
@@ -1011,9 +968,9 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
 
   const int blk = patch_block(n, nmax);
   if (is_sym) {
-    // (the residual's product buffer is free now: per-warp row partials)
-    sym_apply(Lg, s_L, (int)L_.stage, L_.nst, n, s_x, reinterpret_cast<double*>(psm + L_.y_off),
-              reinterpret_cast<double*>(psm + L_.z_off), s_prod, s_ring_bar, sym_iss);
+    sym_apply(Lg, s_L, (int)L_.stage, L_.nst, L_.sym_rows, n, (nmax + 2) & ~1, s_x,
+              reinterpret_cast<double*>(psm + L_.y_off), reinterpret_cast<double*>(psm + L_.z_off),
+              s_sym_bar);
   } else if (blk == 2 * kPanel) {
     // x = L^{-T} (L^{-1} r): two GEMVs with the stored inverse
     gemv_inv<2 * kPanel>(L + patch_tri_even(n), s_x, n, false, s_prod);
@@ -1188,19 +1145,14 @@ static PatchGeom patch_geom(const Correction& c)
 {
   static const int l2pf = patch_env("SMG_PATCH_L2PF", 0);  // measured slower on C5 (222 vs 240 us)
   // read per launch (tests vary it); a graph bakes the value of its capture
-  const int sym_ring_kb = patch_env("SMG_SYM_RING_KB", 66);
+  const int sym_stages = patch_env("SMG_SYM_STAGES", 2);
   const bool st = !nostream_env();
   int nst = stages_env();
-  int64_t S = 0;
-  if (c.sym && c.max_dofs > 4 * kPanel) {
-    S = ((int64_t)kSymRowsLayout * (c.max_dofs + 2) + 1) & ~int64_t(1);
-    int64_t q = (int64_t)sym_ring_kb * 1024 / (8 * S);
-    nst = (int)(q < 2 ? 2 : (q > kMaxRingStages ? kMaxRingStages : q));
-  }
+  if (patch_has_sym(c)) nst = sym_stages < 2 ? 2 : (sym_stages > kSymMaxStages ? kSymMaxStages : sym_stages);
   PatchGeom g;
   g.flags = (st ? kFlagStream : 0) | (l2pf ? kFlagL2Prefetch : 0) | (nst << kFlagStagesShift) |
-            (c.sym ? kFlagSym : 0) | (int)((S / 2) << kFlagSymStageShift);
-  g.L = patch_smem_layout(c.max_dofs, st, nst, c.sym, S, nst);
+            (c.sym ? kFlagSym : 0);
+  g.L = patch_smem_layout(c.max_dofs, st, nst, c.sym, 0, nst);
   return g;
 }
 

@@ -187,6 +187,9 @@ __host__ __device__ inline int patch_block(int64_t nd, int64_t nmax)
 // whole-L^{-1} block) stores the packed lower triangle of A[B,B]^{-1} =
 // L^{-T} L^{-1} instead of L: the correction is one symmetric matrix-vector
 // product streamed from HBM once, with no serial panel chain.
+// (corrections with a region of more than kPatchSymMaxDofs dofs keep the
+// substitution path: the per-warp rings would not fit shared memory)
+constexpr int kPatchSymMaxDofs = 896;
 __host__ __device__ inline bool patch_is_sym(int64_t nd, int64_t nmax, bool sym)
 {
   return sym && nd > kPanel && patch_block(nd, nmax) == 0;

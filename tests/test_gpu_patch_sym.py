@@ -54,15 +54,15 @@ def test_c5p_blocks_both_paths(P, sym, monkeypatch):
     assert rel(out, z["lc_apply"]) <= 1e-13
 
 
-@pytest.mark.parametrize("ring_kb", ["10", "100", "140", "190"])
-def test_ring_geometry_does_not_change_bits(P, ring_kb, monkeypatch):
-    """The ring depth (2..5 stages here) only changes when rows arrive, never
-    the order of a sum: every depth gives the default depth's bits."""
+@pytest.mark.parametrize("stages", ["2", "3", "4"])
+def test_ring_geometry_does_not_change_bits(P, stages, monkeypatch):
+    """The depth of the warps' rings only changes when rows arrive, never the
+    order of a sum: every depth gives the default depth's bits."""
     from tests.test_oracle_golden import load_c5p
     z, lc = load_c5p()
     a = _c5p_operator(z)
     base, _ = _fresh_apply(lc, a, z["r"])
-    monkeypatch.setenv("SMG_SYM_RING_KB", ring_kb)
+    monkeypatch.setenv("SMG_SYM_STAGES", stages)
     out, _ = _fresh_apply(lc, a, z["r"])
     assert np.array_equal(out, base)
     assert rel(out, z["lc_apply"]) <= 1e-13
@@ -77,7 +77,7 @@ def test_many_sizes_vs_lapack(P):
     from paper_2402_12947_b200.sparse import CsrMatrix, DenseFactor
     rng = np.random.default_rng(12947)
     sizes = [1, 2, 31, 32, 33, 63, 64, 65, 66, 90, 127, 128, 129, 130, 191, 255, 256, 257, 300,
-             383, 511, 513, 640]
+             383, 511, 513, 640, 895]
     n = int(sum(sizes)) + 100
     perm = rng.permutation(n)
     regions, start, blocks = [], 0, []
@@ -102,6 +102,32 @@ def test_many_sizes_vs_lapack(P):
     for idx, _ in blocks:
         untouched[idx] = False
     assert not out[untouched].any()
+
+
+def test_very_large_region_keeps_the_substitution(P):
+    """A correction with a region past the symmetric path's size limit (its
+    per-warp rings would not fit shared memory) runs the streamed substitution
+    for all its regions; same bar."""
+    import scipy.linalg as sl
+    from paper_2402_12947_b200.smoothers import LocalCorrection
+    from paper_2402_12947_b200.sparse import CsrMatrix, DenseFactor
+    rng = np.random.default_rng(7)
+    sizes = [1000, 300, 40]
+    n = sum(sizes) + 10
+    perm = rng.permutation(n)
+    regions, blocks, start = [], [], 0
+    for nd in sizes:
+        idx = np.sort(perm[start:start + nd])
+        start += nd
+        q, _ = np.linalg.qr(rng.standard_normal((nd, nd)))
+        blk = (q * np.logspace(0, -3, nd)) @ q.T
+        c = sl.cho_factor(0.5 * (blk + blk.T), lower=True)
+        regions.append((idx.astype(np.int64), DenseFactor("cholesky", c, nd)))
+        blocks.append((idx, c))
+    r = rng.standard_normal(n)
+    out, _ = _fresh_apply(LocalCorrection(tuple(regions), n), CsrMatrix.identity(n), r)
+    for idx, c in blocks:
+        assert rel(out[idx], sl.cho_solve(c, r[idx])) <= 1e-12, f"region of {len(idx)} dofs"
 
 
 @pytest.mark.parametrize("name", ["c4s", "c2s", "cpl_p2"])
