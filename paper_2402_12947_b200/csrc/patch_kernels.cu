@@ -160,6 +160,7 @@ enum PatchMode : int { kAddResidualSolve = 0, kSolveFromBuf = 1, kResidualOnly =
 constexpr int kFlagStream = 1;      // factors larger than shared memory stream through a ring
 constexpr int kFlagL2Prefetch = 2;  // ... after an L2 prefetch of the whole factor
 constexpr int kFlagSym = 4;         // the correction holds packed A[B,B]^{-1} for its larger regions
+constexpr int kFlagSymPfShift = 12; // launch flags bits 12..16: L2 prefetch distance of the symmetric rings (rounds)
 
 // Phase timestamps (SM clock) of the first 256 CTAs, compiled in only for the
 // tools/trace_patch.py build (-DSMG_PATCH_TRACE); no cost otherwise.
@@ -556,6 +557,19 @@ __device__ __forceinline__ void sym_issue(const double* Mg, double* dst, int R, 
       : "memory");
 }
 
+// lane 0 of a warp: pull chunk c towards L2 (fire and forget: no shared
+// memory, so the bytes in flight are not limited by the ring)
+__device__ __forceinline__ void sym_prefetch(const double* Mg, int R, int n, int c)
+{
+  const int i0 = c * R;
+  const int i1 = min(i0 + R, n);
+  const int a = tri32(i0) & ~1;
+  const int b = (tri32(i1) + 1) & ~1;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Mg + a),
+               "r"((uint32_t)(b - a) * 8u)
+               : "memory");
+}
+
 // thread 0, at kernel entry: the warps' ring barriers (kSymWarps x nst)
 __device__ __forceinline__ void sym_ring_init(int nst, uint64_t* bars)
 {
@@ -568,7 +582,7 @@ __device__ __forceinline__ void sym_ring_init(int nst, uint64_t* bars)
 // mbarriers (the inverse is static data: before the dependency wait,
 // overlapping the residual): the warp's first nst chunks
 __device__ __forceinline__ void sym_ring_start(const double* Mg, double* ring, int S, int nst, int R,
-                                               int n, uint64_t* bars)
+                                               int n, uint64_t* bars, int pf)
 {
   const int warp = threadIdx.x >> 5;
   const int nchunks = (n + R - 1) / R;
@@ -577,12 +591,17 @@ __device__ __forceinline__ void sym_ring_start(const double* Mg, double* ring, i
     if (c < nchunks)
       sym_issue(Mg, ring + (warp * nst + q) * S, R, n, c, &bars[warp * nst + q]);
   }
+  // the next pf rounds of this warp's chunks go towards L2 meanwhile
+  for (int q = nst; q < nst + pf; ++q) {
+    const int c = warp + q * kSymWarps;
+    if (c < nchunks) sym_prefetch(Mg, R, n, c);
+  }
 }
 
 // s_x holds r on entry (visible to all threads) and x on return (after a
 // barrier).  s_y: kSymWarps vectors of n2 doubles.
 __device__ void sym_apply(const double* __restrict__ Mg, double* ring, int S, int nst, int R, int n,
-                          int n2, double* s_x, double* s_y, double* s_z, uint64_t* bars)
+                          int n2, double* s_x, double* s_y, double* s_z, uint64_t* bars, int pf)
 {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -672,6 +691,8 @@ __device__ void sym_apply(const double* __restrict__ Mg, double* ring, int S, in
     if (lane == 0 && c + nst * kSymWarps < nchunks) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       sym_issue(Mg, ringw + stg * S, R, n, c + nst * kSymWarps, &barw[stg]);
+      if (pf > 0 && c + (nst + pf) * kSymWarps < nchunks)
+        sym_prefetch(Mg, R, n, c + (nst + pf) * kSymWarps);
     }
     if (++stg == nst) {
       stg = 0;
@@ -774,7 +795,8 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   // every thread may only wait on the barrier after thread 0 has initialised it
   __syncthreads();
   if (is_sym && lane == 0)
-    sym_ring_start(Lg, s_L, (int)L_.stage, L_.nst, L_.sym_rows, n, s_sym_bar);
+    sym_ring_start(Lg, s_L, (int)L_.stage, L_.nst, L_.sym_rows, n, s_sym_bar,
+                   (flags >> kFlagSymPfShift) & 31);
 
   if (kMode == kFollow) {
     // ---- follow mode: this kernel was launched (programmatic dependent
@@ -970,7 +992,7 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   if (is_sym) {
     sym_apply(Lg, s_L, (int)L_.stage, L_.nst, L_.sym_rows, n, (nmax + 2) & ~1, s_x,
               reinterpret_cast<double*>(psm + L_.y_off), reinterpret_cast<double*>(psm + L_.z_off),
-              s_sym_bar);
+              s_sym_bar, (flags >> kFlagSymPfShift) & 31);
   } else if (blk == 2 * kPanel) {
     // x = L^{-T} (L^{-1} r): two GEMVs with the stored inverse
     gemv_inv<2 * kPanel>(L + patch_tri_even(n), s_x, n, false, s_prod);
@@ -1146,12 +1168,15 @@ static PatchGeom patch_geom(const Correction& c)
   static const int l2pf = patch_env("SMG_PATCH_L2PF", 0);  // measured slower on C5 (222 vs 240 us)
   // read per launch (tests vary it); a graph bakes the value of its capture
   const int sym_stages = patch_env("SMG_SYM_STAGES", 2);
+  // SMG_SYM_L2PF: rounds (of eight chunks) pulled towards L2 ahead of the rings
+  int sym_pf = patch_env("SMG_SYM_L2PF", 0);
+  sym_pf = sym_pf < 0 ? 0 : (sym_pf > 31 ? 31 : sym_pf);
   const bool st = !nostream_env();
   int nst = stages_env();
   if (patch_has_sym(c)) nst = sym_stages < 2 ? 2 : (sym_stages > kSymMaxStages ? kSymMaxStages : sym_stages);
   PatchGeom g;
   g.flags = (st ? kFlagStream : 0) | (l2pf ? kFlagL2Prefetch : 0) | (nst << kFlagStagesShift) |
-            (c.sym ? kFlagSym : 0);
+            (c.sym ? kFlagSym : 0) | (sym_pf << kFlagSymPfShift);
   g.L = patch_smem_layout(c.max_dofs, st, nst, c.sym, 0, nst);
   return g;
 }

@@ -242,6 +242,190 @@ csr_tile_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, 
   if (write) epilogue<E>(ea, grow, sum, inv, bv, uv, dv, ov);
 }
 
+// Warp-specialised tile kernel for long-row operators on offset-table tiles
+// (SMG_TILE_WS=1; C2 levels 2-3, C3 level 1, C4 level 2: L2-resident,
+// latency-bound).  In csr_tile_kernel every thread first forms products and
+// then the few row owners sum them while the other threads wait at the
+// barrier; here six loader warps stream (value, column) chunks, gather x and
+// fill a ring of three product buffers, while two summer warps add each
+// row's products in column order as the chunks arrive (row r of the tile
+// belongs to summer thread r mod 64, which keeps its running sum across
+// chunks).  "full" / "empty" mbarriers per buffer, one arrival per warp; no
+// CTA barrier after the start.  Same products, same order: bit-identical.
+constexpr int kWsLoaders = 192;
+constexpr int kWsSummers = kThreads - kWsLoaders;   // 64
+constexpr int kWsSlots = 3;
+constexpr int kWsItems = (kTileNnz + kWsLoaders - 1) / kWsLoaders;   // 11
+constexpr int kWsRows = kRowsPerTile / kWsSummers;                   // 4 rows per summer thread
+
+__device__ __forceinline__ uint32_t ws_smem_u32(const void* p)
+{
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void ws_wait(uint64_t* bar, uint32_t parity)
+{
+  asm volatile(
+      "{\n.reg .pred p;\nWS_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WS_%=;\n}\n" ::"r"(ws_smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void ws_arrive(uint64_t* bar)
+{
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ws_smem_u32(bar)) : "memory");
+}
+
+template <Epi E, bool kPf>
+__global__ void __launch_bounds__(kThreads, 4)
+csr_ws_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, int pf_dist)
+{
+  using T = EpiTraits<E>;
+  // dynamic: 3 x 16 KB of products (+ barriers) is past the 48 KB static limit
+  extern __shared__ __align__(16) unsigned char ws_smem[];
+  double(*s_prod)[kTileNnz] = reinterpret_cast<double(*)[kTileNnz]>(ws_smem);
+  uint64_t* s_full = reinterpret_cast<uint64_t*>(ws_smem + sizeof(double) * kWsSlots * kTileNnz);
+  uint64_t* s_empty = s_full + kWsSlots;
+  const int t = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int64_t e0 = m.tile_nz[t];
+  const int cnt = (int)(m.tile_nz[t + 1] - e0);
+  const int nq = (cnt + kTileNnz - 1) / kTileNnz;
+  if (tid == 0) {
+    for (int s = 0; s < kWsSlots; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(ws_smem_u32(&s_full[s])),
+                   "r"(kWsLoaders / 32)
+                   : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(ws_smem_u32(&s_empty[s])),
+                   "r"(kWsSummers / 32)
+                   : "memory");
+    }
+  }
+  if (tid < kWsLoaders) {
+    // ---- loaders: operator data before the dependency wait
+    int32_t c[kWsItems];
+    double v[kWsItems];
+    auto load_chunk = [&](int q0) {
+#pragma unroll
+      for (int i = 0; i < kWsItems; ++i) {
+        const int k = q0 + i * kWsLoaders + tid;
+        c[i] = 0;
+        v[i] = 0.0;
+        if (k < cnt && k < q0 + kTileNnz) {
+          if (m.streaming) {
+            c[i] = __ldcs(m.col + e0 + k);
+            v[i] = __ldcs(m.val + e0 + k);
+          } else {
+            c[i] = __ldg(m.col + e0 + k);
+            v[i] = __ldg(m.val + e0 + k);
+          }
+        }
+      }
+    };
+    load_chunk(0);
+    if constexpr (kPf) {
+      if (tid == 0) {
+        const int tp = t + pf_dist;
+        if (tp < m.ntiles) {
+          const int64_t p0 = m.tile_nz[tp], p1 = m.tile_nz[tp + 1];
+          if (p1 - p0 <= kTileNnz * kMaxTileChunks && p1 > p0) {
+            const int64_t va = p0 & ~int64_t(1), vb = (p1 + 1) & ~int64_t(1);
+            const int64_t ca = p0 & ~int64_t(3), cb = (p1 + 3) & ~int64_t(3);
+            prefetch_l2(m.val + va, (uint32_t)((vb - va) * 8), m.streaming);
+            prefetch_l2(m.col + ca, (uint32_t)((cb - ca) * 4), m.streaming);
+          }
+        }
+      }
+    }
+    __syncthreads();   // barriers initialised
+    pdl_wait();
+    pdl_trigger();
+    int slot = 0;
+    uint32_t eph = 1;   // parity of the "empty" phase a refill waits for (first round: free)
+    for (int q = 0; q < nq; ++q) {
+      const int q0 = q * kTileNnz;
+      const int qn = min(kTileNnz, cnt - q0);
+      if (q >= kWsSlots) ws_wait(&s_empty[slot], eph);
+      double* buf = s_prod[slot];
+#pragma unroll
+      for (int i = 0; i < kWsItems; ++i) {
+        const int k = i * kWsLoaders + tid;
+        if (k < qn) buf[k] = __dmul_rn(v[i], __ldg(x + c[i]));
+      }
+      if (q + 1 < nq) load_chunk(q0 + kTileNnz);
+      __syncwarp();
+      if (lane == 0) ws_arrive(&s_full[slot]);
+      if (++slot == kWsSlots) {
+        slot = 0;
+        if (q >= kWsSlots - 1) eph ^= 1u;
+      }
+    }
+    return;
+  }
+  // ---- summers: rows r0 + s + 64 j
+  const int sidx = tid - kWsLoaders;
+  const int32_t r0 = m.tile_row[t];
+  const int32_t r1 = m.tile_row[t + 1];
+  int lo[kWsRows], hi[kWsRows];
+#pragma unroll
+  for (int j = 0; j < kWsRows; ++j) {
+    const int32_t row = r0 + sidx + kWsSummers * j;
+    lo[j] = hi[j] = 0;
+    if (row < r1) {
+      lo[j] = (int)(m.rowptr[row] - e0);
+      hi[j] = (int)(m.rowptr[row + 1] - e0);
+    }
+  }
+  __syncthreads();   // barriers initialised
+  pdl_wait();
+  pdl_trigger();
+  double bv[kWsRows], uv[kWsRows], dv[kWsRows], ov[kWsRows], inv[kWsRows], sum[kWsRows];
+  int32_t grow[kWsRows];
+  bool write[kWsRows];
+#pragma unroll
+  for (int j = 0; j < kWsRows; ++j) {
+    const int32_t row = r0 + sidx + kWsSummers * j;
+    const bool has_row = row < r1;
+    grow[j] = (has_row && m.row_map) ? m.row_map[row] : row;
+    write[j] = has_row && !(ea.skip_rows && ea.skip_rows[grow[j]]);
+    bv[j] = uv[j] = dv[j] = ov[j] = inv[j] = 0.0;
+    sum[j] = 0.0;
+    if (write[j]) {
+      if constexpr (T::kB) bv[j] = ea.b[grow[j]];
+      if constexpr (T::kU) uv[j] = ea.u_in[grow[j]];
+      if constexpr (T::kD) dv[j] = ea.d[grow[j]];
+      if constexpr (T::kOut) ov[j] = (ea.u_in ? ea.u_in : ea.out)[grow[j]];
+      if constexpr (T::kDiag) inv[j] = m.inv_diag[grow[j]];
+      if constexpr (T::kDiagVec) inv[j] = ea.inv_diag[grow[j]];
+    }
+  }
+  int slot = 0;
+  uint32_t fph = 0;
+  for (int q = 0; q < nq; ++q) {
+    const int q0 = q * kTileNnz;
+    const int qn = min(kTileNnz, cnt - q0);
+    ws_wait(&s_full[slot], fph);
+    const double* buf = s_prod[slot];
+#pragma unroll
+    for (int j = 0; j < kWsRows; ++j) {
+      const int j0 = max(lo[j], q0), j1 = min(hi[j], q0 + qn);
+      double sacc = sum[j];
+      for (int e = j0; e < j1; ++e) sacc = __dadd_rn(sacc, buf[e - q0]);
+      sum[j] = sacc;
+    }
+    __syncwarp();
+    if (lane == 0) ws_arrive(&s_empty[slot]);
+    if (++slot == kWsSlots) {
+      slot = 0;
+      fph ^= 1u;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kWsRows; ++j)
+    if (write[j]) epilogue<E>(ea, grow[j], sum[j], inv[j], bv[j], uv[j], dv[j], ov[j]);
+}
+
 // SELL-32-sigma256 (DevCsr::sell): one CTA per window of 256 rows, warp k =
 // slice k, lane = slot.  Each thread streams its own row -- entry j of the 32
 // slots is contiguous, so every load is coalesced -- and adds the products in
@@ -697,9 +881,29 @@ static cudaError_t launch_t_sell(const DevCsr& m, const double* x, const EpiArgs
     return pf ? cudaLaunchKernelEx(&cfg, csr_tile_kernel<E, true, false, true>, m, x, ea, dist)
               : cudaLaunchKernelEx(&cfg, csr_tile_kernel<E, false, false, true>, m, x, ea, dist);
   }
-  if (m.multichunk)
+  if (m.multichunk) {
+    static const int ws = [] {
+      const char* v = getenv("SMG_TILE_WS");
+      return v ? atoi(v) : 0;
+    }();
+    if (ws) {
+      constexpr int kWsSmem = (int)(sizeof(double) * kWsSlots * kTileNnz + 2 * kWsSlots * sizeof(uint64_t));
+      static const cudaError_t attr_rc = [] {
+        cudaError_t e = cudaFuncSetAttribute(csr_ws_kernel<E, true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kWsSmem);
+        if (e == cudaSuccess)
+          e = cudaFuncSetAttribute(csr_ws_kernel<E, false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kWsSmem);
+        return e;
+      }();
+      if (attr_rc != cudaSuccess) return attr_rc;
+      cfg.dynamicSmemBytes = kWsSmem;
+      return pf ? cudaLaunchKernelEx(&cfg, csr_ws_kernel<E, true>, m, x, ea, dist)
+                : cudaLaunchKernelEx(&cfg, csr_ws_kernel<E, false>, m, x, ea, dist);
+    }
     return pf ? cudaLaunchKernelEx(&cfg, csr_tile_kernel<E, true, true, false>, m, x, ea, dist)
               : cudaLaunchKernelEx(&cfg, csr_tile_kernel<E, false, true, false>, m, x, ea, dist);
+  }
   return pf ? cudaLaunchKernelEx(&cfg, csr_tile_kernel<E, true, false, false>, m, x, ea, dist)
             : cudaLaunchKernelEx(&cfg, csr_tile_kernel<E, false, false, false>, m, x, ea, dist);
 }
