@@ -331,6 +331,8 @@ def _layout(lib, op) -> str:
         return f"sell_kernel (SELL-32-sigma256, 16-bit delta-coded columns, {unr.value}-deep)"
     if lay.value == 3:
         return f"sell4_kernel (SELL-8x4, 4 lanes per row, {unr.value} batches)"
+    if lay.value == 5:
+        return f"csr_stage_kernel (offset-table tiles staged whole in shared memory, {unr.value} load batch(es))"
     kind = "fixed-capacity" if lay.value == 1 else "offset-table"
     return f"csr_tile_kernel ({kind} tiles, {unr.value} chunk(s))"
 

@@ -83,12 +83,17 @@ SMG_API int smg_operator_info(const smg_operator *op, int64_t *nrows, int64_t *n
  *                           (10 instead of 12 bytes per entry; same sums);
  *                           chosen by the rule for SELL operators whose rows
  *                           need at most two escapes
+ *   SMG_LAYOUT_TILES_STAGED offset-table tiles staged whole in shared memory
+ *                           (csr_stage_kernel: one barrier, every row of the
+ *                           tile sums at once); chosen for long-row operators
+ *                           that stay L2-resident; *unroll = load batches per tile
  * For tiles *unroll is the chunks per tile (1, or 4 for long-row operators). */
 #define SMG_LAYOUT_TILES 0
 #define SMG_LAYOUT_TILES_FIXED 1
 #define SMG_LAYOUT_SELL 2
 #define SMG_LAYOUT_SELL4 3
 #define SMG_LAYOUT_SELL_D16 4
+#define SMG_LAYOUT_TILES_STAGED 5
 SMG_API int smg_operator_layout(const smg_operator *op, int *layout, int *unroll);
 /* Force a layout (and SELL loop depth 4/8/16; 0 = by the rule) for the
  * operator and its stored transpose -- for tests and A/B runs; results are

@@ -450,6 +450,36 @@ static int build_devcsr(std::vector<void*>& allocs, int64_t& bytes, int64_t nrow
     d.pval = dpv;
     d.rel_end = drel;
   }
+  // Whole-tile staging (csr_stage_kernel, SMG_LAYOUT_TILES_STAGED): long-row
+  // operators that stay in L2 and keep the offset-table tiles get tiles sized
+  // so that the operator is one resident wave of kStageCtas CTAs per SM (at
+  // most kStageMaxNnz nonzeros each), staged whole in shared memory.
+  // SMG_TILE_STAGE=0 keeps the chunked tile kernel.
+  static const int stage_mode = env_int("SMG_TILE_STAGE", 1);
+  bool stage = stage_mode != 0 && nrows > 0 && !d.sell && !d.fixed &&
+               nnz * 12 <= kStreamBytes && long_rows(nnz, nrows);
+  if (forced_layout >= 0) stage = forced_layout == SMG_LAYOUT_TILES_STAGED && nrows > 0;
+  if (stage) {
+    const int64_t slots = (int64_t)(148 * kStageCtas * 95) / 100;
+    int64_t scap = ((nnz + slots - 1) / slots + 255) & ~int64_t(255);
+    if (scap < 1024) scap = 1024;
+    if (scap > kStageMaxNnz) scap = kStageMaxNnz;
+    std::vector<int32_t> st = make_tiles(nrows, rowptr, scap);
+    std::vector<int64_t> sz(st.size());
+    for (size_t i = 0; i < st.size(); ++i) sz[i] = rowptr[st[i]];
+    for (size_t i = 0; stage && i + 1 < st.size(); ++i)
+      if (sz[i + 1] - sz[i] > scap) stage = false;   // a single row longer than the capacity
+    if (stage) {
+      int32_t* str = nullptr;
+      int64_t* stz = nullptr;
+      SMG_TRY(dev_upload(allocs, bytes, st.data(), st.size(), &str));
+      SMG_TRY(dev_upload(allocs, bytes, sz.data(), sz.size(), &stz));
+      d.tile_row = str;
+      d.tile_nz = stz;
+      d.ntiles = (int32_t)(st.size() - 1);
+      d.stage_cap = (int32_t)scap;
+    }
+  }
   *out = d;
   return SMG_OK;
 }
@@ -1126,7 +1156,7 @@ static int relayout(Operator& o, DevCsr& m, int layout, int unroll)
 int smg_operator_set_layout(smg_operator* op, int layout, int unroll)
 {
   if (!op) return fail("operator is NULL");
-  if (layout < SMG_LAYOUT_TILES || layout > SMG_LAYOUT_SELL_D16) return fail("unknown layout");
+  if (layout < SMG_LAYOUT_TILES || layout > SMG_LAYOUT_TILES_STAGED) return fail("unknown layout");
   SMG_CUDA(cudaDeviceSynchronize());
   SMG_TRY(relayout(op->o, op->o.a, layout, unroll));
   if (op->o.has_t) SMG_TRY(relayout(op->o, op->o.t, layout, unroll));
@@ -1140,8 +1170,12 @@ int smg_operator_layout(const smg_operator* op, int* layout, int* unroll)
   if (layout)
     *layout = m.sell ? (m.sell_lanes == 4 ? SMG_LAYOUT_SELL4
                                           : (m.sell_delta ? SMG_LAYOUT_SELL_D16 : SMG_LAYOUT_SELL))
-                     : (m.fixed ? SMG_LAYOUT_TILES_FIXED : SMG_LAYOUT_TILES);
-  if (unroll) *unroll = m.sell ? m.sell_unroll : (m.multichunk ? kMaxTileChunks : 1);
+                     : (m.stage_cap > 0 ? SMG_LAYOUT_TILES_STAGED
+                                        : (m.fixed ? SMG_LAYOUT_TILES_FIXED : SMG_LAYOUT_TILES));
+  if (unroll)
+    *unroll = m.sell ? m.sell_unroll
+                     : (m.stage_cap > 0 ? (m.stage_cap + kTileNnz - 1) / kTileNnz
+                                        : (m.multichunk ? kMaxTileChunks : 1));
   return SMG_OK;
 }
 

@@ -50,6 +50,10 @@ constexpr int kItems = kTileNnz / kThreads;
 // and each chunk's loads overlap the previous chunk's sums
 constexpr int kMaxTileChunks = 4;
 constexpr int64_t kStreamBytes = 64ll << 20;   // operators above this are streamed evict-first
+// whole-tile staging (csr_stage_kernel): the tile's products live in dynamic
+// shared memory (8 B each), kStageCtas CTAs per SM
+constexpr int kStageCtas = 3;
+constexpr int kStageMaxNnz = 9216;   // 72 KB per CTA, 3 x 73 KB <= 227 KB per SM
 
 struct DevCsr {
   int64_t nrows = 0, ncols = 0, nnz = 0;
@@ -63,6 +67,7 @@ struct DevCsr {
   int32_t ntiles = 0;
   bool streaming = false;            // val+col exceed kStreamBytes: evict-first reads
   bool multichunk = false;           // long rows: tiles of up to kMaxTileChunks chunks
+  int32_t stage_cap = 0;             // > 0: tiles of at most stage_cap nonzeros, staged whole (csr_stage_kernel)
   // fixed-capacity layout: tile t's nonzeros sit at [t*cap, (t+1)*cap) of the
   // padded arrays (zero values / column 0 after the last row), so a CTA can
   // issue its value/column loads without first loading its tile offset;

@@ -426,6 +426,129 @@ csr_ws_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, in
     if (write[j]) epilogue<E>(ea, grow[j], sum[j], inv[j], bv[j], uv[j], dv[j], ov[j]);
 }
 
+// Whole-tile staging for L2-resident long-row operators (DevCsr::stage_cap > 0,
+// SMG_LAYOUT_TILES_STAGED; C2 levels 2-3, C3 levels 1-2).  csr_tile_kernel
+// walks such a tile in 2048-product chunks and, after every chunk, the ~34
+// row owners add their 60 products one after the other while the rest of the
+// CTA waits at the barrier: four serial rounds of (gather latency + add chain)
+// per tile.  Here the tile (up to kStageMaxNnz products, sized at upload so
+// the operator is one resident wave of 3 CTAs per SM) is staged whole: the
+// loads of batch q+1 are in flight during the x gathers of batch q, there is
+// ONE barrier, and then every row of the tile sums at once.  Same products,
+// same order per row: bit-identical.
+template <Epi E, bool kPf>
+__global__ void __launch_bounds__(kThreads, kStageCtas)
+csr_stage_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea, int pf_dist)
+{
+  using T = EpiTraits<E>;
+  extern __shared__ __align__(16) double st_prod[];
+  const int t = blockIdx.x;
+  const int tid = threadIdx.x;
+  // ---- operator data (never written by any kernel): before the dependency wait
+  const int64_t e0 = m.tile_nz[t];
+  const int cnt = (int)(m.tile_nz[t + 1] - e0);
+  const int32_t* __restrict__ colp = m.col + e0;
+  const double* __restrict__ valp = m.val + e0;
+  int32_t c[kItems];
+  double v[kItems];
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) {
+    const int k = i * kThreads + tid;
+    c[i] = 0;
+    v[i] = 0.0;
+    if (k < cnt) {
+      c[i] = __ldg(colp + k);
+      v[i] = __ldg(valp + k);
+    }
+  }
+  const int32_t r0 = m.tile_row[t];
+  const int32_t r1 = m.tile_row[t + 1];
+  const int32_t row = r0 + tid;
+  const bool has_row = row < r1;
+  int a = 0, bnd = 0;   // this row's tile-relative range
+  if (has_row) {
+    a = (int)(m.rowptr[row] - e0);
+    bnd = (int)(m.rowptr[row + 1] - e0);
+  }
+  if constexpr (kPf) {
+    if (tid == 0) {
+      const int tp = t + pf_dist;
+      if (tp < m.ntiles) {
+        const int64_t p0 = m.tile_nz[tp], p1 = m.tile_nz[tp + 1];
+        if (p1 > p0 && p1 - p0 <= kStageMaxNnz) {
+          const int64_t va = p0 & ~int64_t(1), vb = (p1 + 1) & ~int64_t(1);
+          const int64_t ca = p0 & ~int64_t(3), cb = (p1 + 3) & ~int64_t(3);
+          prefetch_l2(m.val + va, (uint32_t)((vb - va) * 8), false);
+          prefetch_l2(m.col + ca, (uint32_t)((cb - ca) * 4), false);
+        }
+      }
+    }
+  }
+  // ---- vectors produced by earlier kernels: after the dependency wait
+  pdl_wait();
+  pdl_trigger();
+  const int32_t grow = (has_row && m.row_map) ? m.row_map[row] : row;
+  SMG_DCHECK(!has_row || (grow >= 0 && (m.row_map || grow < m.nrows)));
+  const bool write = has_row && !(ea.skip_rows && ea.skip_rows[grow]);
+  double bv = 0.0, uv = 0.0, dv = 0.0, ov = 0.0, inv = 0.0;
+  if (write) {
+    if constexpr (T::kB) bv = ea.b[grow];
+    if constexpr (T::kU) uv = ea.u_in[grow];
+    if constexpr (T::kD) dv = ea.d[grow];
+    if constexpr (T::kOut) ov = (ea.u_in ? ea.u_in : ea.out)[grow];
+    if constexpr (T::kDiag) inv = m.inv_diag[grow];
+    if constexpr (T::kDiagVec) inv = ea.inv_diag[grow];
+  }
+  for (int q0 = 0; q0 < cnt; q0 += kTileNnz) {
+    double xv[kItems];
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+      SMG_DCHECK(c[i] >= 0 && c[i] < m.ncols);
+      xv[i] = __ldg(x + c[i]);   // c = 0 past the end: a valid address, product unused
+    }
+    // the next batch's values and columns are requested before this batch's
+    // gathers are consumed
+    int32_t cn[kItems];
+    double vn[kItems];
+    const int qn = q0 + kTileNnz;
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+      const int k = qn + i * kThreads + tid;
+      cn[i] = 0;
+      vn[i] = 0.0;
+      if (k < cnt) {
+        cn[i] = __ldg(colp + k);
+        vn[i] = __ldg(valp + k);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+      const int k = q0 + i * kThreads + tid;
+      if (k < cnt) st_prod[k] = __dmul_rn(v[i], xv[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+      c[i] = cn[i];
+      v[i] = vn[i];
+    }
+  }
+  __syncthreads();
+  double sum = 0.0;
+  if (has_row) {
+    SMG_DCHECK(a >= 0 && a <= bnd && bnd <= cnt);
+    int j = a;
+    for (; j + 8 <= bnd; j += 8) {
+      double p[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) p[i] = st_prod[j + i];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) sum = __dadd_rn(sum, p[i]);
+    }
+    for (; j < bnd; ++j) sum = __dadd_rn(sum, st_prod[j]);
+  }
+  if (write) epilogue<E>(ea, grow, sum, inv, bv, uv, dv, ov);
+}
+
 // SELL-32-sigma256 (DevCsr::sell): one CTA per window of 256 rows, warp k =
 // slice k, lane = slot.  Each thread streams its own row -- entry j of the 32
 // slots is contiguous, so every load is coalesced -- and adds the products in
@@ -873,6 +996,23 @@ static cudaError_t launch_t_sell(const DevCsr& m, const double* x, const EpiArgs
     const int sdist = g_sm_count * 8 * waves;
     SMG_SELL_LAUNCH(4, false);
 #undef SMG_SELL_LAUNCH
+  }
+  if (m.stage_cap > 0) {
+    const int smem = (int)sizeof(double) * m.stage_cap;
+    static const cudaError_t attr_rc = [] {
+      const int cap = (int)sizeof(double) * kStageMaxNnz;
+      cudaError_t e = cudaFuncSetAttribute(csr_stage_kernel<E, true>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(csr_stage_kernel<E, false>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+      return e;
+    }();
+    if (attr_rc != cudaSuccess) return attr_rc;
+    cfg.dynamicSmemBytes = (size_t)smem;
+    const int sdist = g_sm_count * kStageCtas * waves;
+    return pf ? cudaLaunchKernelEx(&cfg, csr_stage_kernel<E, true>, m, x, ea, sdist)
+              : cudaLaunchKernelEx(&cfg, csr_stage_kernel<E, false>, m, x, ea, sdist);
   }
   if (m.fixed) {
     if (m.multichunk)

@@ -18,7 +18,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 NAMES = ["crit7_adj", "c1s", "c2s", "c3s"]
-LAYOUTS = [(0, 0), (1, 0), (2, 4), (2, 8), (2, 16), (3, 2), (3, 4), (4, 4), (4, 8), (4, 16)]
+LAYOUTS = [(0, 0), (1, 0), (2, 4), (2, 8), (2, 16), (3, 2), (3, 4), (4, 4), (4, 8), (4, 16), (5, 0)]
 
 
 def fresh(m):
