@@ -161,6 +161,7 @@ constexpr int kFlagStream = 1;      // factors larger than shared memory stream 
 constexpr int kFlagL2Prefetch = 2;  // ... after an L2 prefetch of the whole factor
 constexpr int kFlagSym = 4;         // the correction holds packed A[B,B]^{-1} for its larger regions
 constexpr int kFlagSymPfShift = 12; // launch flags bits 12..16: L2 prefetch distance of the symmetric rings (rounds)
+constexpr int kFlagSymFold = 1 << 17; // symmetric rings carry folded chunks: rows {c, n-1-c}, (n + 1) entries each
 
 // Phase timestamps (SM clock) of the first 256 CTAs, compiled in only for the
 // tools/trace_patch.py build (-DSMG_PATCH_TRACE); no cost otherwise.
@@ -241,7 +242,7 @@ static int stages_env()
 // regions) rows: sym_rows (nmax + 2) doubles
 constexpr int kSymMaxRows = 2;
 constexpr int kSymWarps = 8;        // = kSolveWarps (defined below)
-constexpr int kSymMaxStages = 4;
+constexpr int kSymMaxStages = 6;
 
 __host__ __device__ inline PatchSmem patch_smem_layout(int nmax, bool allow_stream = true,
                                                        int nst = kRingStages, bool sym = false,
@@ -267,15 +268,22 @@ __host__ __device__ inline PatchSmem patch_smem_layout(int nmax, bool allow_stre
     p.y_off = p.l_off;
     p.z_off = p.y_off + 8 * n2 * kSymWarps;
     p.l_off = p.z_off + 8 * n2;
-    (void)sym_stage;
     p.nst = sym_nst < 2 ? 2 : (sym_nst > kSymMaxStages ? kSymMaxStages : sym_nst);
     p.sym_rows = kSymMaxRows;
-    for (;;) {
-      p.stage = ((int64_t)p.sym_rows * (nmax + 2) + 1) & ~int64_t(1);
-      if (p.l_off + 8 * kSymWarps * p.nst * p.stage <= kSmemBudget) break;
-      if (p.nst > 2) --p.nst;
-      else if (p.sym_rows > 1) --p.sym_rows;
-      else break;
+    if (sym_stage != 0) {
+      // folded chunks (rows c and n-1-c, two 16-byte aligned copies): n + 1
+      // entries plus alignment slack, whatever c
+      p.sym_rows = 0;
+      p.stage = ((int64_t)nmax + 6) & ~int64_t(1);
+      while (p.nst > 2 && p.l_off + 8 * kSymWarps * p.nst * p.stage > kSmemBudget) --p.nst;
+    } else {
+      for (;;) {
+        p.stage = ((int64_t)p.sym_rows * (nmax + 2) + 1) & ~int64_t(1);
+        if (p.l_off + 8 * kSymWarps * p.nst * p.stage <= kSmemBudget) break;
+        if (p.nst > 2) --p.nst;
+        else if (p.sym_rows > 1) --p.sym_rows;
+        else break;
+      }
     }
     const int64_t need = patch_slot_max(nmax, true);
     const int64_t ring = (int64_t)kSymWarps * p.nst * p.stage;
@@ -570,6 +578,37 @@ __device__ __forceinline__ void sym_prefetch(const double* Mg, int R, int n, int
                : "memory");
 }
 
+// folded chunks (R == 0): chunk c = rows {c, n - 1 - c} -- n + 1 entries for
+// every c, so each ring stage carries the same bytes and the bytes in flight
+// per CTA are the ring's capacity (with consecutive row pairs the first
+// chunks are a few hundred bytes and the ring is half empty on average).
+// Two copies per chunk (the rows are not adjacent in the packed layout), one
+// mbarrier.
+__device__ __forceinline__ void sym_issue_fold(const double* Mg, double* dst, int n, int c,
+                                               uint64_t* bar)
+{
+  const int ia = c, ib = n - 1 - c;
+  const int a0 = tri32(ia) & ~1, a1 = (tri32(ia + 1) + 1) & ~1;
+  const int b0 = tri32(ib) & ~1, b1 = (tri32(ib + 1) + 1) & ~1;
+  const bool two = ib > ia;
+  const uint32_t bytes_a = (uint32_t)(a1 - a0) * 8u;
+  const uint32_t bytes_b = two ? (uint32_t)(b1 - b0) * 8u : 0u;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(psmem_u32(bar)),
+               "r"(bytes_a + bytes_b)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(psmem_u32(dst)),
+      "l"(Mg + a0), "r"(bytes_a), "r"(psmem_u32(bar))
+      : "memory");
+  if (two)
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(psmem_u32(dst + (a1 - a0))),
+        "l"(Mg + b0), "r"(bytes_b), "r"(psmem_u32(bar))
+        : "memory");
+}
+
 // thread 0, at kernel entry: the warps' ring barriers (kSymWarps x nst)
 __device__ __forceinline__ void sym_ring_init(int nst, uint64_t* bars)
 {
@@ -585,6 +624,14 @@ __device__ __forceinline__ void sym_ring_start(const double* Mg, double* ring, i
                                                int n, uint64_t* bars, int pf)
 {
   const int warp = threadIdx.x >> 5;
+  if (R == 0) {   // folded chunks
+    const int nch = (n + 1) >> 1;
+    for (int q = 0; q < nst; ++q) {
+      const int c = warp + q * kSymWarps;
+      if (c < nch) sym_issue_fold(Mg, ring + (warp * nst + q) * S, n, c, &bars[warp * nst + q]);
+    }
+    return;
+  }
   const int nchunks = (n + R - 1) / R;
   for (int q = 0; q < nst; ++q) {
     const int c = warp + q * kSymWarps;
@@ -596,6 +643,149 @@ __device__ __forceinline__ void sym_ring_start(const double* Mg, double* ring, i
     const int c = warp + q * kSymWarps;
     if (c < nchunks) sym_prefetch(Mg, R, n, c);
   }
+}
+
+// Folded-chunk version of sym_apply (below): chunk c = rows ia = c and
+// ib = n - 1 - c.  Blocks left of ia's diagonal take both rows, the block on
+// ia's diagonal is predicated, the blocks between the two diagonals take row
+// ib alone.  Same row / column parts, same final combine.
+__device__ void sym_apply_fold(const double* __restrict__ Mg, double* ring, int S, int nst, int n,
+                               int n2, double* s_x, double* s_y, double* s_z, uint64_t* bars)
+{
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  double* __restrict__ yw = s_y + warp * n2;
+  const double* __restrict__ xr = s_x;
+  for (int j = lane; j < n; j += 32) yw[j] = 0.0;
+  __syncwarp();
+  const int nch = (n + 1) >> 1;
+  double* ringw = ring + warp * nst * S;
+  uint64_t* barw = bars + warp * nst;
+  int stg = 0;
+  uint32_t phase = 0;
+  for (int c = warp; c < nch; c += kSymWarps) {
+    const int ia = c, ib = n - 1 - c;
+    const bool two = ib > ia;
+    ring_wait(&barw[stg], phase);
+    const double* base = ringw + stg * S;
+    const int ta = tri32(ia);
+    const int len_a = ((tri32(ia + 1) + 1) & ~1) - (ta & ~1);
+    const int tb = tri32(ib);
+    const double* __restrict__ rowa = base - (ta & ~1) + ta;            // M[ia][j] = rowa[j]
+    const double* __restrict__ rowb = base + len_a - (tb & ~1) + tb;    // M[ib][j] = rowb[j]
+    const double ra = xr[ia];
+    const double rb = two ? xr[ib] : 0.0;
+    double aa = 0.0, ab = 0.0;
+    int c0 = 0;
+    // both rows, blocks strictly left of ia's diagonal
+    for (; c0 + 127 < ia; c0 += 128) {
+      const int j = c0 + lane;
+      double m0[4], m1[4], xv[4], yv[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        m0[q] = rowa[j + 32 * q];
+        m1[q] = two ? rowb[j + 32 * q] : 0.0;   // (the middle row of an odd region is alone)
+        xv[q] = xr[j + 32 * q];
+        yv[q] = yw[j + 32 * q];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        aa += m0[q] * xv[q];
+        ab += m1[q] * xv[q];
+        yv[q] = (yv[q] + m0[q] * ra) + m1[q] * rb;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) yw[j + 32 * q] = yv[q];
+    }
+    for (; c0 + 31 < ia; c0 += 32) {
+      const int j = c0 + lane;
+      const double m00 = rowa[j];
+      const double m10 = two ? rowb[j] : 0.0;
+      const double x0 = xr[j];
+      aa += m00 * x0;
+      ab += m10 * x0;
+      yw[j] = (yw[j] + m00 * ra) + m10 * rb;
+    }
+    // the block on ia's diagonal (c0 <= ia < c0 + 32)
+    {
+      const int j = c0 + lane;
+      const double m00 = j <= ia ? rowa[j] : 0.0;
+      const double m10 = (two && j <= ib) ? rowb[j] : 0.0;
+      const double x0 = j < n ? xr[j] : 0.0;
+      aa += m00 * x0;
+      ab += m10 * x0;
+      if (j < ib) {   // j < ia implies j < ib
+        double y = yw[j];
+        if (j < ia) y += m00 * ra;
+        if (two) y += m10 * rb;
+        yw[j] = y;
+      }
+      c0 += 32;
+    }
+    // row ib alone, up to its diagonal
+    if (two) {
+      for (; c0 + 127 < ib; c0 += 128) {
+        const int j = c0 + lane;
+        double m1[4], xv[4], yv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          m1[q] = rowb[j + 32 * q];
+          xv[q] = xr[j + 32 * q];
+          yv[q] = yw[j + 32 * q];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          ab += m1[q] * xv[q];
+          yv[q] += m1[q] * rb;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) yw[j + 32 * q] = yv[q];
+      }
+      for (; c0 + 31 < ib; c0 += 32) {
+        const int j = c0 + lane;
+        const double m10 = rowb[j];
+        ab += m10 * xr[j];
+        yw[j] += m10 * rb;
+      }
+      for (; c0 <= ib; c0 += 32) {
+        const int j = c0 + lane;
+        const double m10 = j <= ib ? rowb[j] : 0.0;
+        const double x0 = j < n ? xr[j] : 0.0;
+        ab += m10 * x0;
+        if (j < ib) yw[j] += m10 * rb;
+      }
+    }
+    // 2-value butterfly: lane 0 ends with z_ia, lane 16 with z_ib
+    {
+      const bool up = (lane & 16) != 0;
+      const double send = up ? aa : ab;
+      const double keep = up ? ab : aa;
+      double v = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      if (lane == 0) s_z[ia] = v;
+      if (lane == 16 && two) s_z[ib] = v;
+    }
+    __syncwarp();
+    if (lane == 0 && c + nst * kSymWarps < nch) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      sym_issue_fold(Mg, ringw + stg * S, n, c + nst * kSymWarps, &barw[stg]);
+    }
+    if (++stg == nst) {
+      stg = 0;
+      phase ^= 1u;
+    }
+  }
+  __syncthreads();   // every warp's z rows and column sums
+  for (int j = threadIdx.x; j < n; j += kSolveThreads) {
+    double y = s_y[j];
+#pragma unroll
+    for (int w = 1; w < kSymWarps; ++w) y += s_y[w * n2 + j];
+    s_x[j] = s_z[j] + y;
+  }
+  __syncthreads();
 }
 
 // s_x holds r on entry (visible to all threads) and x on return (after a
@@ -740,7 +930,8 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   __shared__ uint64_t s_dinv_bar[2];
   const bool sym_on = kSym && (flags & kFlagSym) != 0;
   const PatchSmem L_ = patch_smem_layout(nmax, allow_stream, (flags >> kFlagStagesShift) & 15, sym_on,
-                                         0, (flags >> kFlagStagesShift) & 15);
+                                         (flags & kFlagSymFold) ? 1 : 0,
+                                         (flags >> kFlagStagesShift) & 15);
   double* s_x = reinterpret_cast<double*>(psm + L_.x_off);
   int32_t* s_off = reinterpret_cast<int32_t*>(psm + L_.off_off);
   double* s_prod = reinterpret_cast<double*>(psm + L_.prod_off);
@@ -989,7 +1180,11 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   const double* Dinv = L + patch_tri_even(n);   // inverted diagonal blocks, row stride 33
 
   const int blk = patch_block(n, nmax);
-  if (is_sym) {
+  if (is_sym && L_.sym_rows == 0) {
+    sym_apply_fold(Lg, s_L, (int)L_.stage, L_.nst, n, (nmax + 2) & ~1, s_x,
+                   reinterpret_cast<double*>(psm + L_.y_off),
+                   reinterpret_cast<double*>(psm + L_.z_off), s_sym_bar);
+  } else if (is_sym) {
     sym_apply(Lg, s_L, (int)L_.stage, L_.nst, L_.sym_rows, n, (nmax + 2) & ~1, s_x,
               reinterpret_cast<double*>(psm + L_.y_off), reinterpret_cast<double*>(psm + L_.z_off),
               s_sym_bar, (flags >> kFlagSymPfShift) & 31);
@@ -1167,7 +1362,10 @@ static PatchGeom patch_geom(const Correction& c)
 {
   static const int l2pf = patch_env("SMG_PATCH_L2PF", 0);  // measured slower on C5 (222 vs 240 us)
   // read per launch (tests vary it); a graph bakes the value of its capture
-  const int sym_stages = patch_env("SMG_SYM_STAGES", 2);
+  // SMG_SYM_FOLD (default 1): folded chunks (rows c and n-1-c), ring depth
+  // SMG_SYM_STAGES (default 4 folded, 2 with consecutive row pairs)
+  const int sym_fold = patch_env("SMG_SYM_FOLD", 1);
+  const int sym_stages = patch_env("SMG_SYM_STAGES", sym_fold ? 4 : 2);
   // SMG_SYM_L2PF: rounds (of eight chunks) pulled towards L2 ahead of the rings
   int sym_pf = patch_env("SMG_SYM_L2PF", 0);
   sym_pf = sym_pf < 0 ? 0 : (sym_pf > 31 ? 31 : sym_pf);
@@ -1176,8 +1374,9 @@ static PatchGeom patch_geom(const Correction& c)
   if (patch_has_sym(c)) nst = sym_stages < 2 ? 2 : (sym_stages > kSymMaxStages ? kSymMaxStages : sym_stages);
   PatchGeom g;
   g.flags = (st ? kFlagStream : 0) | (l2pf ? kFlagL2Prefetch : 0) | (nst << kFlagStagesShift) |
-            (c.sym ? kFlagSym : 0) | (sym_pf << kFlagSymPfShift);
-  g.L = patch_smem_layout(c.max_dofs, st, nst, c.sym, 0, nst);
+            (c.sym ? kFlagSym : 0) | (sym_pf << kFlagSymPfShift) |
+            ((c.sym && sym_fold) ? kFlagSymFold : 0);
+  g.L = patch_smem_layout(c.max_dofs, st, nst, c.sym, (c.sym && sym_fold) ? 1 : 0, nst);
   return g;
 }
 

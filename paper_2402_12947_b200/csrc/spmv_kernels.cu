@@ -901,11 +901,25 @@ static cudaError_t launch_t(const DevCsr& m, const double* x, const EpiArgs& ea,
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[3];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = env_flag(g_pdl, "SMG_PDL", 1) ? 1 : 0;
+  // L1 / shared-memory split per launch (SMG_CARVEOUT: 0 = driver's choice,
+  // 1 = SELL kernels, which use no shared memory, ask for the largest L1, so
+  // the x gathers do not inherit the small L1 a shared-memory-heavy kernel
+  // (patch_kernel, csr_stage_kernel) left on the SM; 2 = also the tile
+  // kernels ask for just their own 4 CTAs' worth)
+  static const int carve = [] {
+    const char* v = getenv("SMG_CARVEOUT");
+    return v ? atoi(v) : 1;
+  }();
+  if (carve >= 1 && (m.sell || (carve >= 2 && m.stage_cap == 0))) {
+    cudaLaunchAttribute& a = attr[cfg.numAttrs++];
+    a.id = cudaLaunchAttributePreferredSharedMemoryCarveout;
+    a.val.sharedMemCarveout = m.sell ? 0u : (m.multichunk ? 60u : 30u);
+  }
   if (g_persist_bytes > 0 && m.streaming && m.ncols > 0) {
     size_t bytes = (size_t)m.ncols * 8;
     if (bytes > g_persist_window) bytes = g_persist_window;

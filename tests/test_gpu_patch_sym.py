@@ -54,13 +54,16 @@ def test_c5p_blocks_both_paths(P, sym, monkeypatch):
     assert rel(out, z["lc_apply"]) <= 1e-13
 
 
-@pytest.mark.parametrize("stages", ["2", "3", "4"])
-def test_ring_geometry_does_not_change_bits(P, stages, monkeypatch):
+@pytest.mark.parametrize("fold", ["1", "0"])
+@pytest.mark.parametrize("stages", ["2", "3", "4", "6"])
+def test_ring_geometry_does_not_change_bits(P, stages, fold, monkeypatch):
     """The depth of the warps' rings only changes when rows arrive, never the
-    order of a sum: every depth gives the default depth's bits."""
+    order of a sum: every depth gives the default depth's bits -- with folded
+    chunks (rows c and n-1-c, the default) and with consecutive row pairs."""
     from tests.test_oracle_golden import load_c5p
     z, lc = load_c5p()
     a = _c5p_operator(z)
+    monkeypatch.setenv("SMG_SYM_FOLD", fold)
     base, _ = _fresh_apply(lc, a, z["r"])
     monkeypatch.setenv("SMG_SYM_STAGES", stages)
     out, _ = _fresh_apply(lc, a, z["r"])
@@ -68,13 +71,15 @@ def test_ring_geometry_does_not_change_bits(P, stages, monkeypatch):
     assert rel(out, z["lc_apply"]) <= 1e-13
 
 
-def test_many_sizes_vs_lapack(P):
+@pytest.mark.parametrize("fold", ["1", "0"])
+def test_many_sizes_vs_lapack(P, fold, monkeypatch):
     """Every region size class at once (<= 32: panel, 33..64: L^{-1} block,
     65..: symmetric inverse, including sizes around the chunk boundaries and
     odd sizes) against scipy's cho_solve on cond-1e4 blocks."""
     import scipy.linalg as sl
     from paper_2402_12947_b200.smoothers import LocalCorrection
     from paper_2402_12947_b200.sparse import CsrMatrix, DenseFactor
+    monkeypatch.setenv("SMG_SYM_FOLD", fold)
     rng = np.random.default_rng(12947)
     sizes = [1, 2, 31, 32, 33, 63, 64, 65, 66, 90, 127, 128, 129, 130, 191, 255, 256, 257, 300,
              383, 511, 513, 640, 895]
