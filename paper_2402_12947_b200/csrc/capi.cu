@@ -464,12 +464,14 @@ static int build_devcsr(std::vector<void*>& allocs, int64_t& bytes, int64_t nrow
     int64_t scap = ((nnz + slots - 1) / slots + 255) & ~int64_t(255);
     if (scap < 1024) scap = 1024;
     // by the rule only operators whose one-wave tiles stay small
-    // (SMG_STAGE_MAX_CAP nonzeros, default 4096 = 32 KB per CTA): with 72 KB
-    // tiles (C2 level 2) the kernel alone is faster (13.8 -> 12.2 us) but the
+    // (SMG_STAGE_MAX_CAP nonzeros, default 6144 = 48 KB per CTA; measured
+    // gains up to 4,608: C2 level 3 and C3 levels 1-2): with 72 KB tiles
+    // (C2 level 2) the kernel alone is faster (13.8 -> 12.2 us) but the
     // V-cycle is not -- three such CTAs leave the SM 28 KB of L1 for the x
-    // gathers and no room for the next kernel's programmatic early launch
-    // (profiles/r02/SUMMARY.md, session 5)
-    static const int stage_max_cap = env_int("SMG_STAGE_MAX_CAP", 4096);
+    // gathers and no room for the next kernel's programmatic early launch,
+    // and level 1's sweeps next to it lose 8 us (profiles/r02/SUMMARY.md,
+    // session 5)
+    static const int stage_max_cap = env_int("SMG_STAGE_MAX_CAP", 6144);
     if (forced_layout < 0 && scap > stage_max_cap) stage = false;
     if (scap > kStageMaxNnz) scap = kStageMaxNnz;
     std::vector<int32_t> st;

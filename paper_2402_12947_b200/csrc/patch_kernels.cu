@@ -161,6 +161,7 @@ constexpr int kFlagStream = 1;      // factors larger than shared memory stream 
 constexpr int kFlagL2Prefetch = 2;  // ... after an L2 prefetch of the whole factor
 constexpr int kFlagSym = 4;         // the correction holds packed A[B,B]^{-1} for its larger regions
 constexpr int kFlagSymPfShift = 12; // launch flags bits 12..16: L2 prefetch distance of the symmetric rings (rounds)
+constexpr int kFlagSymNoFence = 1 << 18; // A/B: no fence.proxy.async before a ring refill (SMG_SYM_NOFENCE=1)
 constexpr int kFlagSymFold = 1 << 17; // symmetric rings carry folded chunks: rows {c, n-1-c}, (n + 1) entries each
 
 // Phase timestamps (SM clock) of the first 256 CTAs, compiled in only for the
@@ -791,7 +792,8 @@ __device__ void sym_apply_fold(const double* __restrict__ Mg, double* ring, int 
 // s_x holds r on entry (visible to all threads) and x on return (after a
 // barrier).  s_y: kSymWarps vectors of n2 doubles.
 __device__ void sym_apply(const double* __restrict__ Mg, double* ring, int S, int nst, int R, int n,
-                          int n2, double* s_x, double* s_y, double* s_z, uint64_t* bars, int pf)
+                          int n2, double* s_x, double* s_y, double* s_z, uint64_t* bars, int pf,
+                          bool fence)
 {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -807,7 +809,10 @@ __device__ void sym_apply(const double* __restrict__ Mg, double* ring, int S, in
   for (int c = warp; c < nchunks; c += kSymWarps) {
     const int i0 = c * R;
     const bool two = R == 2 && i0 + 1 < n;      // the chunk has a second row
+    const long long tr0 = PTRACE_CLK();
     ring_wait(&barw[stg], phase);
+    const long long tr1 = PTRACE_CLK();
+    PTRACE_ACC(9, tr1 - tr0);
     const int t0 = tri32(i0);
     const double* __restrict__ row0 = ringw + stg * S - (t0 & ~1) + t0;   // M[i0][j] = row0[j]
     const double* __restrict__ row1 = row0 + i0 + 1;                      // M[i0 + 1][j] = row1[j]
@@ -862,6 +867,8 @@ __device__ void sym_apply(const double* __restrict__ Mg, double* ring, int S, in
         yw[j] = y;
       }
     }
+    const long long tr2 = PTRACE_CLK();
+    PTRACE_ACC(10, tr2 - tr1);
     // 2-value butterfly: lane 0 ends with z_{i0}, lane 16 with z_{i0+1}
     {
       const bool up = (lane & 16) != 0;
@@ -877,13 +884,17 @@ __device__ void sym_apply(const double* __restrict__ Mg, double* ring, int S, in
     }
     // the stage is free once every lane has read it: refill with this warp's
     // chunk nst rounds ahead
+    const long long tr3 = PTRACE_CLK();
+    PTRACE_ACC(11, tr3 - tr2);
     __syncwarp();
     if (lane == 0 && c + nst * kSymWarps < nchunks) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (fence) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       sym_issue(Mg, ringw + stg * S, R, n, c + nst * kSymWarps, &barw[stg]);
       if (pf > 0 && c + (nst + pf) * kSymWarps < nchunks)
         sym_prefetch(Mg, R, n, c + (nst + pf) * kSymWarps);
     }
+    PTRACE_ACC(13, PTRACE_CLK() - tr3);
+    PTRACE_ACC(14, 1);
     if (++stg == nst) {
       stg = 0;
       phase ^= 1u;
@@ -1187,7 +1198,7 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
   } else if (is_sym) {
     sym_apply(Lg, s_L, (int)L_.stage, L_.nst, L_.sym_rows, n, (nmax + 2) & ~1, s_x,
               reinterpret_cast<double*>(psm + L_.y_off), reinterpret_cast<double*>(psm + L_.z_off),
-              s_sym_bar, (flags >> kFlagSymPfShift) & 31);
+              s_sym_bar, (flags >> kFlagSymPfShift) & 31, (flags & kFlagSymNoFence) == 0);
   } else if (blk == 2 * kPanel) {
     // x = L^{-T} (L^{-1} r): two GEMVs with the stored inverse
     gemv_inv<2 * kPanel>(L + patch_tri_even(n), s_x, n, false, s_prod);
@@ -1362,9 +1373,13 @@ static PatchGeom patch_geom(const Correction& c)
 {
   static const int l2pf = patch_env("SMG_PATCH_L2PF", 0);  // measured slower on C5 (222 vs 240 us)
   // read per launch (tests vary it); a graph bakes the value of its capture
-  // SMG_SYM_FOLD (default 1): folded chunks (rows c and n-1-c), ring depth
-  // SMG_SYM_STAGES (default 4 folded, 2 with consecutive row pairs)
-  const int sym_fold = patch_env("SMG_SYM_FOLD", 1);
+  // SMG_SYM_FOLD (default 0): folded chunks (rows c and n-1-c), ring depth
+  // SMG_SYM_STAGES (default 4 folded, 2 with consecutive row pairs).  Measured
+  // slower at every depth (C5 129 -> 152 us, 512 x1 39.5 -> 45.7 us, the same
+  // for 2 / 3 / 4 / 6 stages; profiles/r02/SUMMARY.md session 5): the rings
+  // are not waiting for bytes, and the folded chunk's three block phases cost
+  // more instructions per chunk
+  const int sym_fold = patch_env("SMG_SYM_FOLD", 0);
   const int sym_stages = patch_env("SMG_SYM_STAGES", sym_fold ? 4 : 2);
   // SMG_SYM_L2PF: rounds (of eight chunks) pulled towards L2 ahead of the rings
   int sym_pf = patch_env("SMG_SYM_L2PF", 0);
@@ -1375,7 +1390,8 @@ static PatchGeom patch_geom(const Correction& c)
   PatchGeom g;
   g.flags = (st ? kFlagStream : 0) | (l2pf ? kFlagL2Prefetch : 0) | (nst << kFlagStagesShift) |
             (c.sym ? kFlagSym : 0) | (sym_pf << kFlagSymPfShift) |
-            ((c.sym && sym_fold) ? kFlagSymFold : 0);
+            ((c.sym && sym_fold) ? kFlagSymFold : 0) |
+            (patch_env("SMG_SYM_NOFENCE", 0) ? kFlagSymNoFence : 0);
   g.L = patch_smem_layout(c.max_dofs, st, nst, c.sym, (c.sym && sym_fold) ? 1 : 0, nst);
   return g;
 }
