@@ -472,6 +472,13 @@ static int build_devcsr(std::vector<void*>& allocs, int64_t& bytes, int64_t nrow
     // and level 1's sweeps next to it lose 8 us (profiles/r02/SUMMARY.md,
     // session 5)
     static const int stage_max_cap = env_int("SMG_STAGE_MAX_CAP", 6144);
+    // SMG_STAGE_WAVES (default 1): operators whose one-wave tiles are too
+    // large may be staged as that many resident waves of smaller tiles
+    static const int stage_waves = env_int("SMG_STAGE_WAVES", 1);
+    for (int w = 2; forced_layout < 0 && scap > stage_max_cap && w <= stage_waves; ++w) {
+      scap = ((nnz + slots * w - 1) / (slots * w) + 255) & ~int64_t(255);
+      if (scap < 1024) scap = 1024;
+    }
     if (forced_layout < 0 && scap > stage_max_cap) stage = false;
     if (scap > kStageMaxNnz) scap = kStageMaxNnz;
     std::vector<int32_t> st;

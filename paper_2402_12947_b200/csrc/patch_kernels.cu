@@ -162,6 +162,7 @@ constexpr int kFlagL2Prefetch = 2;  // ... after an L2 prefetch of the whole fac
 constexpr int kFlagSym = 4;         // the correction holds packed A[B,B]^{-1} for its larger regions
 constexpr int kFlagSymPfShift = 12; // launch flags bits 12..16: L2 prefetch distance of the symmetric rings (rounds)
 constexpr int kFlagSymNoFence = 1 << 18; // A/B: no fence.proxy.async before a ring refill (SMG_SYM_NOFENCE=1)
+constexpr int kFlagSymReg = 1 << 19;     // register-resident column sums (sym_apply_reg; SMG_SYM_REG, default 1)
 constexpr int kFlagSymFold = 1 << 17; // symmetric rings carry folded chunks: rows {c, n-1-c}, (n + 1) entries each
 
 // Phase timestamps (SM clock) of the first 256 CTAs, compiled in only for the
@@ -789,6 +790,180 @@ __device__ void sym_apply_fold(const double* __restrict__ Mg, double* ring, int 
   __syncthreads();
 }
 
+// Register-resident version of sym_apply (below) for regions of at most
+// 32 NB dofs, consecutive row pairs (R = 2).  The phase trace of sym_apply
+// (profiles/r02/SUMMARY.md, session 5: per chunk 850 cycles in the blocks,
+// 430 in the butterfly, 300 in the refill, 95 waiting for the ring) showed
+// the warps bound by their own instruction latencies, not by the copies:
+//   * lane l owns columns l, l + 32, ...: its r_j and its column sums y_j
+//     stay in registers (NB of each), so a block left of the diagonal costs
+//     two shared-memory loads (the two matrix rows) instead of four loads
+//     and a store; four blocks are loaded ahead of their arithmetic;
+//   * the block(s) on the diagonal keep the predicated shared-memory path
+//     (the warp's own column-sum vector yw), added to the registers' sums in
+//     the final combine;
+//   * the row sums of four consecutive chunks of the warp (eight values) are
+//     reduced by ONE transposed butterfly (nine shuffles, depth five) instead
+//     of four 2-value butterflies.
+// Fixed order everywhere: deterministic, independent of the ring depth.
+template <int NB>
+__device__ void sym_apply_reg(const double* __restrict__ Mg, double* ring, int S, int nst, int n,
+                              int n2, double* s_x, double* s_y, double* s_z, uint64_t* bars,
+                              bool fence)
+{
+  constexpr int R = 2;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  double* __restrict__ yw = s_y + warp * n2;
+  double xr[NB], y[NB];
+#pragma unroll
+  for (int k = 0; k < NB; ++k) {
+    const int j = 32 * k + lane;
+    xr[k] = j < n ? s_x[j] : 0.0;
+    y[k] = 0.0;
+  }
+  for (int j = lane; j < n; j += 32) yw[j] = 0.0;
+  __syncwarp();
+  const int nchunks = (n + R - 1) / R;
+  double* ringw = ring + warp * nst * S;
+  uint64_t* barw = bars + warp * nst;
+  int stg = 0;
+  uint32_t phase = 0;
+  double acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.0;
+  int q = 0;            // chunks in the current group of four
+  int cg = warp;        // first chunk of the group
+  for (int c = warp; c < nchunks; c += kSymWarps) {
+    const int i0 = c * R;
+    const bool two = i0 + 1 < n;
+    ring_wait(&barw[stg], phase);
+    const int t0 = tri32(i0);
+    const double* __restrict__ row0 = ringw + stg * S - (t0 & ~1) + t0;   // M[i0][j] = row0[j]
+    const double* __restrict__ row1 = row0 + i0 + 1;                      // M[i0 + 1][j] = row1[j]
+    const double r0 = s_x[i0];
+    const double r1 = two ? s_x[i0 + 1] : 0.0;
+    double a0 = 0.0, a1 = 0.0;
+    const int kd = i0 >> 5;   // blocks k < kd lie strictly left of the diagonal
+#pragma unroll
+    for (int kk = 0; kk < NB; kk += 4) {
+      if (kk + 3 < kd) {
+        double m0[4], m1[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          m0[t] = row0[32 * (kk + t) + lane];
+          m1[t] = two ? row1[32 * (kk + t) + lane] : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          a0 += m0[t] * xr[kk + t];
+          a1 += m1[t] * xr[kk + t];
+          y[kk + t] = (y[kk + t] + m0[t] * r0) + m1[t] * r1;
+        }
+      } else if (kk < kd) {
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+          if (kk + t < kd) {
+            const double m00 = row0[32 * (kk + t) + lane];
+            const double m10 = two ? row1[32 * (kk + t) + lane] : 0.0;
+            a0 += m00 * xr[kk + t];
+            a1 += m10 * xr[kk + t];
+            y[kk + t] = (y[kk + t] + m00 * r0) + m10 * r1;
+          }
+        }
+      }
+    }
+    // blocks crossing the diagonal: row part j <= i, column part j < i
+    const int last = two ? i0 + 1 : i0;
+    for (int c0 = kd << 5; c0 <= last; c0 += 32) {
+      const int j = c0 + lane;
+      const double m00 = j <= i0 ? row0[j] : 0.0;
+      const double m10 = (two && j <= i0 + 1) ? row1[j] : 0.0;
+      const double x0 = j < n ? s_x[j] : 0.0;
+      a0 += m00 * x0;
+      a1 += m10 * x0;
+      if (j < last) {
+        double yy = yw[j];
+        if (j < i0) yy += m00 * r0;
+        if (two) yy += m10 * r1;   // j < i0 + 1 = last
+        yw[j] = yy;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (q == i) {
+        acc[2 * i] = a0;
+        acc[2 * i + 1] = a1;
+      }
+    // the stage is free once every lane has read it: refill with this warp's
+    // chunk nst rounds ahead
+    __syncwarp();
+    if (lane == 0 && c + nst * kSymWarps < nchunks) {
+      if (fence) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      sym_issue(Mg, ringw + stg * S, R, n, c + nst * kSymWarps, &barw[stg]);
+    }
+    if (++stg == nst) {
+      stg = 0;
+      phase ^= 1u;
+    }
+    ++q;
+    if (q == 4 || c + kSymWarps >= nchunks) {
+      // transposed butterfly: value i (row 2 (cg + 8 (i / 2)) + (i & 1)) ends on lane 4 i
+      double w4[4], w2[2];
+      {
+        const bool up = (lane & 16) != 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const double send = up ? acc[i] : acc[4 + i];
+          const double keep = up ? acc[4 + i] : acc[i];
+          w4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+        }
+      }
+      {
+        const bool up = (lane & 8) != 0;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const double send = up ? w4[i] : w4[2 + i];
+          const double keep = up ? w4[2 + i] : w4[i];
+          w2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        }
+      }
+      double v;
+      {
+        const bool up = (lane & 4) != 0;
+        const double send = up ? w2[0] : w2[1];
+        const double keep = up ? w2[1] : w2[0];
+        v = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+      }
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      if ((lane & 3) == 0) {
+        const int i = lane >> 2;                       // value index 0..7
+        const int row = R * (cg + kSymWarps * (i >> 1)) + (i & 1);
+        if ((i >> 1) < q && row < n) s_z[row] = v;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = 0.0;
+      q = 0;
+      cg = c + kSymWarps;
+    }
+  }
+  // the registers' column sums join the diagonal blocks' in the warp's vector
+#pragma unroll
+  for (int k = 0; k < NB; ++k) {
+    const int j = 32 * k + lane;
+    if (j < n) yw[j] += y[k];
+  }
+  __syncthreads();   // every warp's z rows and column sums
+  for (int j = threadIdx.x; j < n; j += kSolveThreads) {
+    double yy = s_y[j];
+#pragma unroll
+    for (int w = 1; w < kSymWarps; ++w) yy += s_y[w * n2 + j];
+    s_x[j] = s_z[j] + yy;
+  }
+  __syncthreads();
+}
+
 // s_x holds r on entry (visible to all threads) and x on return (after a
 // barrier).  s_y: kSymWarps vectors of n2 doubles.
 __device__ void sym_apply(const double* __restrict__ Mg, double* ring, int S, int nst, int R, int n,
@@ -1195,6 +1370,16 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
     sym_apply_fold(Lg, s_L, (int)L_.stage, L_.nst, n, (nmax + 2) & ~1, s_x,
                    reinterpret_cast<double*>(psm + L_.y_off),
                    reinterpret_cast<double*>(psm + L_.z_off), s_sym_bar);
+  } else if (is_sym && L_.sym_rows == 2 && n <= 256 && (flags & kFlagSymReg)) {
+    sym_apply_reg<8>(Lg, s_L, (int)L_.stage, L_.nst, n, (nmax + 2) & ~1, s_x,
+                     reinterpret_cast<double*>(psm + L_.y_off),
+                     reinterpret_cast<double*>(psm + L_.z_off), s_sym_bar,
+                     (flags & kFlagSymNoFence) == 0);
+  } else if (is_sym && L_.sym_rows == 2 && n <= 512 && (flags & kFlagSymReg)) {
+    sym_apply_reg<16>(Lg, s_L, (int)L_.stage, L_.nst, n, (nmax + 2) & ~1, s_x,
+                      reinterpret_cast<double*>(psm + L_.y_off),
+                      reinterpret_cast<double*>(psm + L_.z_off), s_sym_bar,
+                      (flags & kFlagSymNoFence) == 0);
   } else if (is_sym) {
     sym_apply(Lg, s_L, (int)L_.stage, L_.nst, L_.sym_rows, n, (nmax + 2) & ~1, s_x,
               reinterpret_cast<double*>(psm + L_.y_off), reinterpret_cast<double*>(psm + L_.z_off),
@@ -1391,7 +1576,8 @@ static PatchGeom patch_geom(const Correction& c)
   g.flags = (st ? kFlagStream : 0) | (l2pf ? kFlagL2Prefetch : 0) | (nst << kFlagStagesShift) |
             (c.sym ? kFlagSym : 0) | (sym_pf << kFlagSymPfShift) |
             ((c.sym && sym_fold) ? kFlagSymFold : 0) |
-            (patch_env("SMG_SYM_NOFENCE", 0) ? kFlagSymNoFence : 0);
+            (patch_env("SMG_SYM_NOFENCE", 0) ? kFlagSymNoFence : 0) |
+            (patch_env("SMG_SYM_REG", 1) ? kFlagSymReg : 0);
   g.L = patch_smem_layout(c.max_dofs, st, nst, c.sym, (c.sym && sym_fold) ? 1 : 0, nst);
   return g;
 }
