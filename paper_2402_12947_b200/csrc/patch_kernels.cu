@@ -791,7 +791,8 @@ __device__ void sym_apply_fold(const double* __restrict__ Mg, double* ring, int 
 }
 
 // Register-resident version of sym_apply (below) for regions of at most
-// 32 NB dofs, consecutive row pairs (R = 2).  The phase trace of sym_apply
+// 32 NB dofs, consecutive row pairs (R = 2); used for regions of <= 256 dofs
+// (NB = 8: 192 x1000 61.5 -> 56.7 us, 256 x1000 81.3 -> 74.2 us).  The phase trace of sym_apply
 // (profiles/r02/SUMMARY.md, session 5: per chunk 850 cycles in the blocks,
 // 430 in the butterfly, 300 in the refill, 95 waiting for the ring) showed
 // the warps bound by their own instruction latencies, not by the copies:
@@ -1375,12 +1376,10 @@ patch_kernel(const int64_t* __restrict__ prow, const int32_t* __restrict__ pcol,
                      reinterpret_cast<double*>(psm + L_.y_off),
                      reinterpret_cast<double*>(psm + L_.z_off), s_sym_bar,
                      (flags & kFlagSymNoFence) == 0);
-  } else if (is_sym && L_.sym_rows == 2 && n <= 512 && (flags & kFlagSymReg)) {
-    sym_apply_reg<16>(Lg, s_L, (int)L_.stage, L_.nst, n, (nmax + 2) & ~1, s_x,
-                      reinterpret_cast<double*>(psm + L_.y_off),
-                      reinterpret_cast<double*>(psm + L_.z_off), s_sym_bar,
-                      (flags & kFlagSymNoFence) == 0);
   } else if (is_sym) {
+    // (larger regions keep the shared-memory column sums: sym_apply_reg<16>
+    // measured slower for 257..512 dofs -- 512 x1000 244 -> 261 us, 384 x1000
+    // 176 -> 194 us; profiles/r02/SUMMARY.md session 5)
     sym_apply(Lg, s_L, (int)L_.stage, L_.nst, L_.sym_rows, n, (nmax + 2) & ~1, s_x,
               reinterpret_cast<double*>(psm + L_.y_off), reinterpret_cast<double*>(psm + L_.z_off),
               s_sym_bar, (flags >> kFlagSymPfShift) & 31, (flags & kFlagSymNoFence) == 0);
