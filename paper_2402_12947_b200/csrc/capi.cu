@@ -424,6 +424,18 @@ static int build_devcsr(std::vector<void*>& allocs, int64_t& bytes, int64_t nrow
     d.sell_col = dsc;
     d.sell_val = dsv;
   }
+  // Streamed operators with very long rows that are too small for SELL (C4
+  // level 2: 117,649 rows x 335 nonzeros): single-chunk tiles hold six rows,
+  // whose owners add 335 products each while 250 threads wait (0.49 of HBM in
+  // every layout, profiles/r02/af/).  Staged whole in 9,216-product tiles
+  // (27 rows summing at once, three CTAs per SM, several resident waves)
+  // instead; SMG_STAGE_STREAM_MIN_ROW (default 128, 0 = off).
+  static const int stage_stream_min_row = env_int("SMG_STAGE_STREAM_MIN_ROW", 128);
+  const bool stage_stream = forced_layout < 0 && env_int("SMG_TILE_STAGE", 1) != 0 &&
+                            stage_stream_min_row > 0 && nrows > 0 && !d.sell &&
+                            nnz * 12 > kStreamBytes &&
+                            nnz >= (int64_t)stage_stream_min_row * nrows;
+  if (stage_stream) fixed = false;
   if (fixed) {
     const size_t nt = tiles.size() - 1;
     std::vector<int32_t> pc(nt * (size_t)cap + 4, 0);
@@ -459,10 +471,12 @@ static int build_devcsr(std::vector<void*>& allocs, int64_t& bytes, int64_t nrow
   bool stage = stage_mode != 0 && nrows > 0 && !d.sell && !d.fixed &&
                nnz * 12 <= kStreamBytes && long_rows(nnz, nrows);
   if (forced_layout >= 0) stage = forced_layout == SMG_LAYOUT_TILES_STAGED && nrows > 0;
+  if (stage_stream) stage = true;
   if (stage) {
     const int64_t slots = (int64_t)(148 * kStageCtas * 95) / 100;
     int64_t scap = ((nnz + slots - 1) / slots + 255) & ~int64_t(255);
     if (scap < 1024) scap = 1024;
+    if (stage_stream) scap = kStageMaxNnz;   // several resident waves of the largest tiles
     // by the rule only operators whose one-wave tiles stay small
     // (SMG_STAGE_MAX_CAP nonzeros, default 6144 = 48 KB per CTA; measured
     // gains up to 4,608: C2 level 3 and C3 levels 1-2): with 72 KB tiles
@@ -475,11 +489,11 @@ static int build_devcsr(std::vector<void*>& allocs, int64_t& bytes, int64_t nrow
     // SMG_STAGE_WAVES (default 1): operators whose one-wave tiles are too
     // large may be staged as that many resident waves of smaller tiles
     static const int stage_waves = env_int("SMG_STAGE_WAVES", 1);
-    for (int w = 2; forced_layout < 0 && scap > stage_max_cap && w <= stage_waves; ++w) {
+    for (int w = 2; forced_layout < 0 && !stage_stream && scap > stage_max_cap && w <= stage_waves; ++w) {
       scap = ((nnz + slots * w - 1) / (slots * w) + 255) & ~int64_t(255);
       if (scap < 1024) scap = 1024;
     }
-    if (forced_layout < 0 && scap > stage_max_cap) stage = false;
+    if (forced_layout < 0 && !stage_stream && scap > stage_max_cap) stage = false;
     if (scap > kStageMaxNnz) scap = kStageMaxNnz;
     std::vector<int32_t> st;
     if (stage) st = make_tiles(nrows, rowptr, scap);

@@ -457,8 +457,13 @@ csr_stage_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea,
     c[i] = 0;
     v[i] = 0.0;
     if (k < cnt) {
-      c[i] = __ldg(colp + k);
-      v[i] = __ldg(valp + k);
+      if (m.streaming) {   // several waves of an operator larger than L2: evict-first
+        c[i] = __ldcs(colp + k);
+        v[i] = __ldcs(valp + k);
+      } else {
+        c[i] = __ldg(colp + k);
+        v[i] = __ldg(valp + k);
+      }
     }
   }
   const int32_t r0 = m.tile_row[t];
@@ -478,8 +483,8 @@ csr_stage_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea,
         if (p1 > p0 && p1 - p0 <= kStageMaxNnz) {
           const int64_t va = p0 & ~int64_t(1), vb = (p1 + 1) & ~int64_t(1);
           const int64_t ca = p0 & ~int64_t(3), cb = (p1 + 3) & ~int64_t(3);
-          prefetch_l2(m.val + va, (uint32_t)((vb - va) * 8), false);
-          prefetch_l2(m.col + ca, (uint32_t)((cb - ca) * 4), false);
+          prefetch_l2(m.val + va, (uint32_t)((vb - va) * 8), m.streaming);
+          prefetch_l2(m.col + ca, (uint32_t)((cb - ca) * 4), m.streaming);
         }
       }
     }
@@ -517,8 +522,13 @@ csr_stage_kernel(const DevCsr m, const double* __restrict__ x, const EpiArgs ea,
       cn[i] = 0;
       vn[i] = 0.0;
       if (k < cnt) {
-        cn[i] = __ldg(colp + k);
-        vn[i] = __ldg(valp + k);
+        if (m.streaming) {
+          cn[i] = __ldcs(colp + k);
+          vn[i] = __ldcs(valp + k);
+        } else {
+          cn[i] = __ldg(colp + k);
+          vn[i] = __ldg(valp + k);
+        }
       }
     }
 #pragma unroll
