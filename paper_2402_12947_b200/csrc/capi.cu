@@ -428,9 +428,11 @@ static int build_devcsr(std::vector<void*>& allocs, int64_t& bytes, int64_t nrow
   // level 2: 117,649 rows x 335 nonzeros): single-chunk tiles hold six rows,
   // whose owners add 335 products each while 250 threads wait (0.49 of HBM in
   // every layout, profiles/r02/af/).  Staged whole in 9,216-product tiles
-  // (27 rows summing at once, three CTAs per SM, several resident waves)
-  // instead; SMG_STAGE_STREAM_MIN_ROW (default 128, 0 = off).
-  static const int stage_stream_min_row = env_int("SMG_STAGE_STREAM_MIN_ROW", 128);
+  // (27 rows summing at once, three CTAs per SM, several resident waves) they
+  // measured SLOWER (146 -> 158 us per step, C4 197.9 -> 194.8 V-cycles/s;
+  // bit-identical, profiles/r02/ah/), so this is opt-in:
+  // SMG_STAGE_STREAM_MIN_ROW = least average row length (default 0 = off).
+  static const int stage_stream_min_row = env_int("SMG_STAGE_STREAM_MIN_ROW", 0);
   const bool stage_stream = forced_layout < 0 && env_int("SMG_TILE_STAGE", 1) != 0 &&
                             stage_stream_min_row > 0 && nrows > 0 && !d.sell &&
                             nnz * 12 > kStreamBytes &&
