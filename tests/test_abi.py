@@ -48,7 +48,9 @@ def test_sass_is_sm100a_and_parity_kernels_have_no_fma():
         assert names, f"csr_tile_kernel<{epi}> missing"
         sell = [f for f in funcs if f.startswith(f"_ZN3smg11sell_kernelILNS_3EpiE{epi}E")]
         assert sell, f"sell_kernel<{epi}> missing"
-        for name in names + sell:  # every layout, with and without the L2 prefetch
+        stage = [f for f in funcs if f.startswith(f"_ZN3smg16csr_stage_kernelILNS_3EpiE{epi}E")]
+        assert stage, f"csr_stage_kernel<{epi}> missing"
+        for name in names + sell + stage:  # every layout, with and without the L2 prefetch
             body = "\n".join(funcs[name])
             assert "DFMA" not in body, f"{name} contains DFMA"
             assert "DMUL" in body and "DADD" in body
