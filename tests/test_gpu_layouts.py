@@ -137,3 +137,35 @@ def test_renumbered_levels_are_bitwise(name, mask, monkeypatch):
     assert np.array_equal(res[0], res[3]) and np.array_equal(res[1], res[4])
     assert np.array_equal(res[2], res[5])
     assert np.linalg.norm(res[3] - z["g/vcycle2"]) <= 1e-12 * np.linalg.norm(z["g/vcycle2"])
+
+
+@pytest.mark.parametrize("nrows,per_row,want", [
+    (30_000, 40, 5),     # L2-resident long rows, one-wave tiles of 3,072 products: staged by the rule
+    (30_000, 8, 1),      # short rows: fixed-capacity tiles
+    (120_000, 40, 0),    # one-wave tiles of 11.5k products: past SMG_STAGE_MAX_CAP, chunked offset-table tiles
+])
+def test_rule_picks_the_staged_layout_for_small_long_row_operators(nrows, per_row, want):
+    """The upload rule (capi.cu build_devcsr): long-row operators that stay in
+    L2 and fit one resident wave of small tiles run csr_stage_kernel; the result
+    is the oracle's bit for bit whatever the rule picks."""
+    import paper_2402_12947_b200 as P
+    from oracle import oracle as O
+    from paper_2402_12947_b200 import _lib
+    from paper_2402_12947_b200 import device as D
+    from paper_2402_12947_b200.sparse import CsrMatrix
+    rng = np.random.default_rng(nrows + per_row)
+    counts = rng.integers(per_row - per_row // 4, per_row + per_row // 4 + 1, size=nrows)
+    rp = np.zeros(nrows + 1, dtype=np.int64)
+    np.cumsum(counts, out=rp[1:])
+    cols = np.empty(rp[-1], dtype=np.int64)
+    for r in range(nrows):   # sorted unique columns near the diagonal
+        lo = max(0, min(r - counts[r], nrows - 2 * counts[r] - 1))
+        cols[rp[r]:rp[r + 1]] = lo + np.sort(rng.choice(2 * counts[r], size=counts[r], replace=False))
+    a = CsrMatrix(nrows, nrows, rp, cols, rng.standard_normal(rp[-1]))
+    op = D.device_operator(a)
+    lib = _lib.load()
+    lay, unr = ctypes.c_int(), ctypes.c_int()
+    _lib.check(lib.smg_operator_layout(op.handle, ctypes.byref(lay), ctypes.byref(unr)))
+    assert lay.value == want
+    x = rng.standard_normal(nrows)
+    assert np.array_equal(P.spmv(a, x), O.spmv(a, x))
